@@ -1,0 +1,177 @@
+/*
+ * dm_moe.h — C ABI of the B200 (sm_100a) DisagMoE MoE hot path.
+ *
+ * The reference (arxiv/paper_2605_11005, package `afpipe`) ships no kernel and
+ * no FFI: the hot path exists there only as durations and byte counts. Each
+ * entry point below replaces the reference quantity that *models* that stage
+ * (citations relative to /root/reference):
+ *
+ *   router / dispatch  (dm_router_*, dm_expert_scan, dm_permute,
+ *                       dm_route_and_dispatch)
+ *       replaces: m2n_comm_bytes V = e*b*s*k*H   pkg/src/afpipe/costs.py:95-103
+ *                 A->F M2NSend/M2NRecv twins      pkg/src/afpipe/taskgraph.py:331-332
+ *                 gating semantics
+ *   expert FFN fwd     (dm_grouped_w13_swiglu_fwd, dm_grouped_w2_fwd)
+ *       replaces: ffn_flops C_f = 4*b*k*s*H*D_e   pkg/src/afpipe/costs.py:90-92
+ *                 F FwdCompute task duration       pkg/src/afpipe/taskgraph.py:333-334, :152
+ *   expert FFN bwd     (dm_grouped_w2_dgrad_swiglu_bwd, dm_grouped_w13_dgrad,
+ *                       dm_grouped_wgrad)
+ *       replaces: backward_scale (2x fwd)          pkg/src/afpipe/costs.py:146-150
+ *                 F BwdCompute task               pkg/src/afpipe/taskgraph.py:346-347
+ *   combine fwd/bwd    (dm_combine_fwd, dm_combine_bwd, dm_permute_bwd,
+ *                       dm_router_wgrad)
+ *       replaces: F->A transfer + weighted sum     pkg/src/afpipe/taskgraph.py:335-339
+ *                 backward chain                   pkg/src/afpipe/taskgraph.py:343-356
+ *
+ * Conventions (no exceptions cross this boundary):
+ *   - The caller owns all memory; pointers are device pointers; nothing here
+ *     allocates, frees or synchronises. `stream` is a cudaStream_t (NULL = legacy).
+ *   - Return 0 on success, >0 = cudaError_t of a failing launch, <0 = DM_ERR_*.
+ *     dm_last_error_string() gives the thread-local message.
+ *   - bf16 row-major tensors; H (hidden) rows must be 16-byte aligned.
+ *   - Permuted buffers are expert-contiguous with every expert block padded to
+ *     DM_ROW_ALIGN rows (zero-filled); pad_off[E+1] holds the block offsets and
+ *     dm_capacity_rows() bounds their total, so no host sync is ever needed.
+ *   - W13 is [E, 2*D_e, H] with gate/up rows interleaved in blocks of 128
+ *     (rows 256b..256b+127 = gate rows 128b.., next 128 = up rows 128b..);
+ *     W2 is [E, H, D_e]; router weight W_g is fp32 [E, H].
+ */
+#ifndef DM_MOE_H_
+#define DM_MOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define DM_API __attribute__((visibility("default")))
+#else
+#define DM_API
+#endif
+
+#define DM_OK 0
+#define DM_ERR_SHAPE (-1)
+#define DM_ERR_DTYPE (-2)
+#define DM_ERR_ALIGN (-3)
+#define DM_ERR_ARG (-4)
+#define DM_ERR_DRIVER (-5)
+
+#define DM_ABI_VERSION 1
+#define DM_CHUNK_TOKENS 32      /* tokens per histogram chunk (stable sort unit) */
+#define DM_ROW_ALIGN 128        /* expert block alignment in permuted buffers   */
+#define DM_MAX_TOPK 16
+#define DM_MAX_EXPERTS 1024
+#define DM_WGRAD_TOKEN_BLOCK 512
+
+static inline int dm_num_chunks(int T) { return (T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS; }
+
+/* Upper bound on sum_e roundup(count_e, DM_ROW_ALIGN) for T tokens, top-k. */
+static inline int dm_capacity_rows(int T, int E, int k) {
+  long long r = (long long)T * k + (long long)E * (DM_ROW_ALIGN - 1);
+  return (int)((r + DM_ROW_ALIGN - 1) / DM_ROW_ALIGN * DM_ROW_ALIGN);
+}
+
+typedef struct dm_route_ws {
+  float* logits;        /* [T, E] fp32 */
+  int32_t* chunk_hist;  /* [nchunk, E] */
+  int32_t* chunk_base;  /* [nchunk, E] */
+} dm_route_ws;
+
+static inline size_t dm_align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static inline size_t dm_route_workspace_size(int T, int H, int E, int k) {
+  (void)H; (void)k;
+  size_t nchunk = (size_t)dm_num_chunks(T);
+  return dm_align256((size_t)T * E * 4) + 2 * dm_align256(nchunk * E * 4);
+}
+
+static inline void dm_route_workspace_layout(int T, int H, int E, int k, void* ws, dm_route_ws* out) {
+  (void)H; (void)k;
+  char* p = (char*)ws;
+  size_t nchunk = (size_t)dm_num_chunks(T);
+  out->logits = (float*)p;
+  p += dm_align256((size_t)T * E * 4);
+  out->chunk_hist = (int32_t*)p;
+  p += dm_align256(nchunk * E * 4);
+  out->chunk_base = (int32_t*)p;
+}
+
+static inline size_t dm_router_wgrad_workspace_size(int T, int H, int E) {
+  size_t ntb = (size_t)((T + DM_WGRAD_TOKEN_BLOCK - 1) / DM_WGRAD_TOKEN_BLOCK);
+  return ntb * (size_t)E * (size_t)H * 4;
+}
+
+/* ---- library ---------------------------------------------------------- */
+DM_API int dm_version(void);
+DM_API const char* dm_last_error_string(void);
+DM_API int dm_num_sms(int device);
+/* Kernel launches issued through this ABI since load (evidence for benches). */
+DM_API long long dm_launch_count(void);
+/* Exported copies of the inline sizing helpers (for FFI users without a C compiler). */
+DM_API int dm_capacity_rows_fn(int T, int E, int k);
+DM_API size_t dm_route_workspace_size_fn(int T, int H, int E, int k);
+DM_API size_t dm_router_wgrad_workspace_size_fn(int T, int H, int E);
+
+/* ---- dispatch (A side) ------------------------------------------------ */
+/* logits[T,E] = x[T,H] (bf16) . W_g[E,H]^T (fp32) in the canonical fixed order. */
+DM_API int dm_router_logits(const void* x, const float* wg, float* logits, int T, int H, int E, void* stream);
+/* top-k by logit (ties -> lower expert id); w = softmax over the selected logits;
+ * chunk_hist[nchunk, E] per-chunk expert counts. */
+DM_API int dm_router_topk(const float* logits, int T, int E, int k, int32_t* idx, float* w,
+                   int32_t* chunk_hist, void* stream);
+/* counts[E], pad_off[E+1] (DM_ROW_ALIGN-padded block offsets), chunk_base[nchunk, E]. */
+DM_API int dm_expert_scan(const int32_t* chunk_hist, int T, int E, int32_t* counts, int32_t* pad_off,
+                   int32_t* chunk_base, void* stream);
+/* Stable counting sort: row_map[t*k+j] = position of (t,j); src_token[pos] = t
+ * (-1 for padding); x_perm[pos] = x[t]; padding rows zeroed. */
+DM_API int dm_permute(const void* x, const int32_t* idx, const int32_t* chunk_base, const int32_t* counts,
+               const int32_t* pad_off, int T, int H, int E, int k, int32_t* row_map,
+               int32_t* src_token, void* x_perm, void* stream);
+/* logits -> topk -> scan -> permute; workspace of dm_route_workspace_size bytes. */
+DM_API int dm_route_and_dispatch(const void* x, const float* wg, int T, int H, int E, int k, void* workspace,
+                          int32_t* idx, float* w, int32_t* counts, int32_t* pad_off,
+                          int32_t* row_map, int32_t* src_token, void* x_perm, void* stream);
+
+/* ---- expert FFN (F side), grouped over experts by pad_off --------------- */
+/* h13[r, :] = x_perm[r, :] . W13_e^T ; act = silu(gate) * up.  h13 [cap, 2*D_e], act [cap, D_e]. */
+DM_API int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t* pad_off, int E,
+                              int cap_rows, int H, int De, void* h13, void* act, void* stream);
+/* y_perm[r, :] = act[r, :] . W2_e^T */
+DM_API int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* pad_off, int E, int cap_rows,
+                      int H, int De, void* y_perm, void* stream);
+/* d_act = dy_perm . W2_e ; dh13 = SwiGLU'(h13) (.) d_act  (same interleaved layout as h13). */
+DM_API int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const void* h13,
+                                   const int32_t* pad_off, int E, int cap_rows, int H, int De,
+                                   void* dh13, void* stream);
+/* dx_perm = dh13 . W13_e */
+DM_API int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* pad_off, int E,
+                         int cap_rows, int H, int De, void* dx_perm, void* stream);
+/* dW[e] (fp32 [M, N]) = a_tok[rows_e, :M]^T . b_tok[rows_e, :N] + beta * dW[e].
+ * dW2 = wgrad(dy_perm, M=H, act, N=D_e); dW13 = wgrad(dh13, M=2*D_e, x_perm, N=H). */
+DM_API int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* pad_off,
+                     int E, int cap_rows, float* dW, float beta, void* stream);
+
+/* ---- combine (A side) ------------------------------------------------- */
+DM_API int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,
+                   void* y, void* stream);
+/* dy_perm = w * dy scattered (padding zeroed); dw = <dy, y_perm>;
+ * dlogit[t,j] = w_j (dw_j - sum_i w_i dw_i). */
+DM_API int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_map, const float* w,
+                   const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
+                   void* dy_perm, float* dw, float* dlogit, void* stream);
+/* dx = sum_j dx_perm[row_map] + sum_j dlogit * W_g[idx]  (dlogit may be NULL). */
+DM_API int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* idx,
+                   const float* dlogit, const float* wg, int T, int H, int k, void* dx, void* stream);
+/* dW_g[E,H] = sum_{t,j} dlogit[t,j] x[t] at row idx[t,j] (+ beta * dW_g);
+ * partial_ws of dm_router_wgrad_workspace_size bytes. */
+DM_API int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int T, int H, int E,
+                    int k, float* partial_ws, float* dwg, float beta, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DM_MOE_H_ */

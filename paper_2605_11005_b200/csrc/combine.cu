@@ -1,0 +1,266 @@
+// Combine side of the MoE hot path (A ranks): gate-weighted unpermute-reduce
+// (fwd), its backward (scatter of weighted grads + gate-weight grads, fused
+// with the top-k softmax Jacobian), the permutation backward (gather-reduce,
+// fused with the router's dx term) and the router weight gradient.
+//
+// Reference counterpart: "outputs ... reduced by a weighted sum";
+// the F->A transfer task of _build_afpipe (pkg/src/afpipe/taskgraph.py:335-339)
+// and the backward chain taskgraph.py:343-356 are the reference's stand-ins.
+// All kernels are HBM-bound row gathers/scatters: warp per token, 128-bit
+// vectors, fp32 accumulation in a fixed j order, no atomics.
+#include "dm_common.cuh"
+#include "dm_internal.h"
+
+namespace dm {
+
+__device__ __forceinline__ void unpack8(const int4& v, float (&f)[8]) {
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { f[2 * i] = bf16lo(p[i]); f[2 * i + 1] = bf16hi(p[i]); }
+}
+__device__ __forceinline__ int4 pack8(const float (&f)[8]) {
+  int4 v;
+  uint32_t* p = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) p[i] = pack_bf16(f[2 * i], f[2 * i + 1]);
+  return v;
+}
+
+// y[t] = sum_j w[t,j] * y_perm[row_map[t,j]]
+__global__ void __launch_bounds__(256)
+combine_fwd_kernel(const __nv_bfloat16* __restrict__ y_perm, const int32_t* __restrict__ row_map,
+                   const float* __restrict__ w, int T, int H, int k, __nv_bfloat16* __restrict__ y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nvec = H >> 3;
+  for (int t = warp; t < T; t += nwarps) {
+    int pos[DM_MAX_TOPK];
+    float wt[DM_MAX_TOPK];
+    for (int j = 0; j < k; ++j) { pos[j] = row_map[(size_t)t * k + j]; wt[j] = w[(size_t)t * k + j]; }
+    for (int ch = lane; ch < nvec; ch += 32) {
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+      for (int j = 0; j < k; ++j) {
+        float f[8];
+        unpack8(ld_nc_v4(y_perm + (size_t)pos[j] * H + ch * 8), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(wt[j], f[i], acc[i]);
+      }
+      st_v4(y + (size_t)t * H + ch * 8, pack8(acc));
+    }
+  }
+}
+
+// dy_perm[row_map[t,j]] = w[t,j] * dy[t];  dw[t,j] = <dy[t], y_perm[row_map[t,j]]>;
+// dlogit[t,j] = w_j * (dw_j - sum_i w_i dw_i)   (softmax over the selected logits).
+__global__ void __launch_bounds__(256)
+combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ y_perm,
+                   const int32_t* __restrict__ row_map, const float* __restrict__ w,
+                   const int32_t* __restrict__ counts, const int32_t* __restrict__ pad_off,
+                   int T, int H, int E, int k, __nv_bfloat16* __restrict__ dy_perm,
+                   float* __restrict__ dw, float* __restrict__ dlogit) {
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nvec = H >> 3;
+  for (int t = gwarp; t < T; t += nwarps) {
+    int pos[DM_MAX_TOPK];
+    float wt[DM_MAX_TOPK], part[DM_MAX_TOPK];
+    for (int j = 0; j < k; ++j) {
+      pos[j] = row_map[(size_t)t * k + j];
+      wt[j] = w[(size_t)t * k + j];
+      part[j] = 0.0f;
+    }
+    for (int ch = lane; ch < nvec; ch += 32) {
+      float g[8];
+      unpack8(ld_nc_v4(dy + (size_t)t * H + ch * 8), g);
+      for (int j = 0; j < k; ++j) {
+        float f[8], o[8];
+        unpack8(ld_nc_v4(y_perm + (size_t)pos[j] * H + ch * 8), f);
+        float p = part[j];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { p = __fmaf_rn(g[i], f[i], p); o[i] = wt[j] * g[i]; }
+        part[j] = p;
+        st_v4(dy_perm + (size_t)pos[j] * H + ch * 8, pack8(o));
+      }
+    }
+    float s = 0.0f;
+    for (int j = 0; j < k; ++j) {
+      part[j] = warp_sum_butterfly(part[j]);
+      s = __fmaf_rn(wt[j], part[j], s);
+    }
+    if (lane == 0) {
+      for (int j = 0; j < k; ++j) {
+        dw[(size_t)t * k + j] = part[j];
+        dlogit[(size_t)t * k + j] = wt[j] * (part[j] - s);
+      }
+    }
+  }
+  // zero padding rows of dy_perm so the ragged-K wgrad sees exact zeros
+  const int4 z = make_int4(0, 0, 0, 0);
+  for (int e = 0; e < E; ++e) {
+    const int beg = pad_off[e] + counts[e], end = pad_off[e + 1];
+    for (int r = beg + gwarp; r < end; r += nwarps)
+      for (int ch = lane; ch < nvec; ch += 32) st_v4(dy_perm + (size_t)r * H + ch * 8, z);
+  }
+}
+
+// dx[t] = sum_j dx_perm[row_map[t,j]] + sum_j dlogit[t,j] * W_g[idx[t,j], :]
+__global__ void __launch_bounds__(256)
+permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_map,
+                   const int32_t* __restrict__ idx, const float* __restrict__ dlogit,
+                   const float* __restrict__ wg, int T, int H, int k, __nv_bfloat16* __restrict__ dx) {
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nvec = H >> 3;
+  for (int t = gwarp; t < T; t += nwarps) {
+    int pos[DM_MAX_TOPK], ex[DM_MAX_TOPK];
+    float dl[DM_MAX_TOPK];
+    for (int j = 0; j < k; ++j) {
+      pos[j] = row_map[(size_t)t * k + j];
+      ex[j] = idx[(size_t)t * k + j];
+      dl[j] = dlogit ? dlogit[(size_t)t * k + j] : 0.0f;
+    }
+    for (int ch = lane; ch < nvec; ch += 32) {
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+      for (int j = 0; j < k; ++j) {
+        float f[8];
+        unpack8(ld_nc_v4(dx_perm + (size_t)pos[j] * H + ch * 8), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += f[i];
+      }
+      if (dlogit) {
+        for (int j = 0; j < k; ++j) {
+          const float4* wr = reinterpret_cast<const float4*>(wg + (size_t)ex[j] * H + ch * 8);
+          const float4 a = wr[0], b = wr[1];
+          acc[0] = __fmaf_rn(dl[j], a.x, acc[0]); acc[1] = __fmaf_rn(dl[j], a.y, acc[1]);
+          acc[2] = __fmaf_rn(dl[j], a.z, acc[2]); acc[3] = __fmaf_rn(dl[j], a.w, acc[3]);
+          acc[4] = __fmaf_rn(dl[j], b.x, acc[4]); acc[5] = __fmaf_rn(dl[j], b.y, acc[5]);
+          acc[6] = __fmaf_rn(dl[j], b.z, acc[6]); acc[7] = __fmaf_rn(dl[j], b.w, acc[7]);
+        }
+      }
+      st_v4(dx + (size_t)t * H + ch * 8, pack8(acc));
+    }
+  }
+}
+
+// Router weight gradient, stage 1: partial[tb][e][h] = sum over the token
+// block's (t, j) with idx == e of dlogit[t,j] * x[t,h]; thread per column.
+__global__ void router_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
+                                            const int32_t* __restrict__ idx,
+                                            const float* __restrict__ dlogit, int T, int H, int E,
+                                            int k, float* __restrict__ partial) {
+  extern __shared__ float s_acc[];  // [E][blockDim.x]
+  const int cw = blockDim.x;
+  const int h = blockIdx.x * cw + threadIdx.x;
+  const int tb = blockIdx.y;
+  const int t_beg = tb * DM_WGRAD_TOKEN_BLOCK, t_end = min(T, t_beg + DM_WGRAD_TOKEN_BLOCK);
+  for (int e = 0; e < E; ++e) s_acc[e * cw + threadIdx.x] = 0.0f;
+  if (h < H) {
+    for (int t = t_beg; t < t_end; ++t) {
+      const float xv = __bfloat162float(x[(size_t)t * H + h]);
+      for (int j = 0; j < k; ++j) {
+        const int e = idx[(size_t)t * k + j];
+        float* a = &s_acc[e * cw + threadIdx.x];
+        *a = __fmaf_rn(dlogit[(size_t)t * k + j], xv, *a);
+      }
+    }
+    for (int e = 0; e < E; ++e) partial[((size_t)tb * E + e) * H + h] = s_acc[e * cw + threadIdx.x];
+  }
+}
+
+__global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, int ntb, size_t EH,
+                                           float* __restrict__ dwg, float beta) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < EH; i += (size_t)gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int tb = 0; tb < ntb; ++tb) s += partial[(size_t)tb * EH + i];
+    dwg[i] = beta != 0.0f ? s + beta * dwg[i] : s;
+  }
+}
+
+static int token_grid(int T) {
+  int blocks = (T + 7) / 8;  // 8 warps (tokens) per 256-thread block
+  const int cap = num_sms_current() * 8;
+  return blocks < cap ? blocks : cap;
+}
+
+}  // namespace dm
+
+using namespace dm;
+
+extern "C" {
+
+int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,
+                   void* y, void* stream) {
+  if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK) return set_error(DM_ERR_SHAPE, "combine_fwd bad shape");
+  combine_fwd_kernel<<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k,
+      reinterpret_cast<__nv_bfloat16*>(y));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "combine_fwd launch");
+  note_launch();
+  return DM_OK;
+}
+
+int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_map, const float* w,
+                   const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
+                   void* dy_perm, float* dw, float* dlogit, void* stream) {
+  if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK || E < 1) return set_error(DM_ERR_SHAPE, "combine_bwd bad shape");
+  combine_bwd_kernel<<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm),
+      row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "combine_bwd launch");
+  note_launch();
+  return DM_OK;
+}
+
+int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* idx,
+                   const float* dlogit, const float* wg, int T, int H, int k, void* dx, void* stream) {
+  if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK) return set_error(DM_ERR_SHAPE, "permute_bwd bad shape");
+  permute_bwd_kernel<<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k,
+      reinterpret_cast<__nv_bfloat16*>(dx));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "permute_bwd launch");
+  note_launch();
+  return DM_OK;
+}
+
+int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int T, int H, int E,
+                    int k, float* partial_ws, float* dwg, float beta, void* stream) {
+  if (T < 1 || H % 8 || E < 1 || E > DM_MAX_EXPERTS || k < 1 || k > DM_MAX_TOPK)
+    return set_error(DM_ERR_SHAPE, "router_wgrad bad shape");
+  int cw = 128;
+  while (cw > 32 && (size_t)E * cw * sizeof(float) > 96 * 1024) cw >>= 1;
+  const size_t smem = (size_t)E * cw * sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(router_wgrad_partial_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router_wgrad)");
+    configured = true;
+  }
+  const int ntb = (T + DM_WGRAD_TOKEN_BLOCK - 1) / DM_WGRAD_TOKEN_BLOCK;
+  dim3 grid((H + cw - 1) / cw, ntb);
+  router_wgrad_partial_kernel<<<grid, cw, smem, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit, T, H, E, k, partial_ws);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_partial launch");
+  note_launch();
+  const size_t EH = (size_t)E * H;
+  int rblocks = (int)((EH + 255) / 256);
+  if (rblocks > num_sms_current() * 4) rblocks = num_sms_current() * 4;
+  router_wgrad_reduce_kernel<<<rblocks, 256, 0, (cudaStream_t)stream>>>(partial_ws, ntb, EH, dwg, beta);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_reduce launch");
+  note_launch();
+  return DM_OK;
+}
+
+}  // extern "C"

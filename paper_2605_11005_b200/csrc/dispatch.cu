@@ -1,0 +1,357 @@
+// Dispatch side of the MoE hot path (attention/A ranks): router logits with a
+// fixed, documented fp32 reduction order, top-k gating, per-chunk expert
+// histograms, a deterministic scan to 128-aligned expert offsets, and the
+// stable counting-sort permutation into expert-contiguous buffers.
+//
+// Reference counterpart: none in code. The semantics come from the paper's
+// gating sentence ("trainable gate network to select the top-k
+// experts"); the reference only models this stage's exchange volume,
+// m2n_comm_bytes V = e*b*s*k*H (pkg/src/afpipe/costs.py:95-103). The CPU oracle
+// (oracle/moe_oracle.c) restates the exact same order, so expert ids,
+// permutation indices and counts are bit-exact.
+//
+// Canonical logit order (shared with oracle/moe_oracle.c:dm_oracle_router):
+//   partial[p], p in [0,32): fmaf chain over 8-element chunks c with c % 32 == p,
+//   c ascending, elements ascending; then an xor butterfly 16,8,4,2,1 with
+//   round-to-nearest fp32 adds.
+#include "dm_common.cuh"
+#include "dm_internal.h"
+
+namespace dm {
+
+constexpr int ROUTER_NT = 4;        // tokens per warp per pass
+constexpr int ROUTER_WARPS = 8;
+constexpr int ROUTER_ER = 8;        // experts per register tile
+constexpr int ROUTER_SMEM_BUDGET = 160 * 1024;
+
+__global__ void __launch_bounds__(ROUTER_WARPS * 32)
+router_logits_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg,
+                     float* __restrict__ logits, int T, int H, int E, int ec) {
+  extern __shared__ float4 sw4[];
+  float* sw = reinterpret_cast<float*>(sw4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = H >> 3;
+  for (int e0 = 0; e0 < E; e0 += ec) {
+    const int ecur = min(ec, E - e0);
+    __syncthreads();
+    const float4* src = reinterpret_cast<const float4*>(wg + (size_t)e0 * H);
+    for (int i = threadIdx.x; i < ecur * H / 4; i += blockDim.x) sw4[i] = src[i];
+    __syncthreads();
+    for (int tg = (blockIdx.x * ROUTER_WARPS + warp) * ROUTER_NT; tg < T;
+         tg += gridDim.x * ROUTER_WARPS * ROUTER_NT) {
+      for (int er = 0; er < ecur; er += ROUTER_ER) {
+        float acc[ROUTER_NT][ROUTER_ER];
+#pragma unroll
+        for (int t = 0; t < ROUTER_NT; ++t)
+#pragma unroll
+          for (int e = 0; e < ROUTER_ER; ++e) acc[t][e] = 0.0f;
+        for (int c = lane; c < nch; c += 32) {
+          int4 xv[ROUTER_NT];
+#pragma unroll
+          for (int t = 0; t < ROUTER_NT; ++t)
+            xv[t] = (tg + t < T) ? ld_nc_v4(x + (size_t)(tg + t) * H + c * 8) : make_int4(0, 0, 0, 0);
+#pragma unroll
+          for (int e = 0; e < ROUTER_ER; ++e) {
+            if (er + e < ecur) {
+              const float4* wp = reinterpret_cast<const float4*>(sw + (size_t)(er + e) * H + c * 8);
+              const float4 w0 = wp[0], w1 = wp[1];
+#pragma unroll
+              for (int t = 0; t < ROUTER_NT; ++t) {
+                const uint32_t* xp = reinterpret_cast<const uint32_t*>(&xv[t]);
+                float a = acc[t][e];
+                a = __fmaf_rn(bf16lo(xp[0]), w0.x, a);
+                a = __fmaf_rn(bf16hi(xp[0]), w0.y, a);
+                a = __fmaf_rn(bf16lo(xp[1]), w0.z, a);
+                a = __fmaf_rn(bf16hi(xp[1]), w0.w, a);
+                a = __fmaf_rn(bf16lo(xp[2]), w1.x, a);
+                a = __fmaf_rn(bf16hi(xp[2]), w1.y, a);
+                a = __fmaf_rn(bf16lo(xp[3]), w1.z, a);
+                a = __fmaf_rn(bf16hi(xp[3]), w1.w, a);
+                acc[t][e] = a;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < ROUTER_NT; ++t) {
+#pragma unroll
+          for (int e = 0; e < ROUTER_ER; ++e) {
+            const float v = warp_sum_butterfly(acc[t][e]);
+            if (lane == e && er + e < ecur && tg + t < T)
+              logits[(size_t)(tg + t) * E + e0 + er + e] = v;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Warp per token: top-k by logit (ties -> lower expert id), weights = softmax
+// over the selected logits (== softmax then renormalise over the top-k).
+__global__ void __launch_bounds__(256)
+router_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int32_t* __restrict__ idx,
+                   float* __restrict__ w, int32_t* __restrict__ chunk_hist) {
+  extern __shared__ int shist[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) shist[i] = 0;
+  __syncthreads();
+  const int t0 = blockIdx.x * DM_CHUNK_TOKENS;
+  for (int tt = warp; tt < DM_CHUNK_TOKENS; tt += nwarps) {
+    const int t = t0 + tt;
+    if (t >= T) break;
+    const float* row = logits + (size_t)t * E;
+    int sel_e[DM_MAX_TOPK];
+    float sel_v[DM_MAX_TOPK];
+    for (int j = 0; j < k; ++j) {
+      float bv = -INFINITY;
+      int be = 0x7fffffff;
+      for (int e = lane; e < E; e += 32) {
+        bool taken = false;
+        for (int q = 0; q < j; ++q) taken |= (sel_e[q] == e);
+        const float v = row[e];
+        if (!taken && (v > bv || (v == bv && e < be))) { bv = v; be = e; }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+      }
+      sel_e[j] = be;
+      sel_v[j] = bv;
+    }
+    float s = 0.0f;
+    for (int j = 0; j < k; ++j) s += expf(sel_v[j] - sel_v[0]);
+    if (lane == 0) {
+      for (int j = 0; j < k; ++j) {
+        idx[(size_t)t * k + j] = sel_e[j];
+        w[(size_t)t * k + j] = expf(sel_v[j] - sel_v[0]) / s;
+        atomicAdd(&shist[sel_e[j]], 1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) chunk_hist[(size_t)blockIdx.x * E + i] = shist[i];
+}
+
+// One CTA: per-expert running sums over chunks (fixed chunk order), padded
+// offsets (each expert's block rounded up to DM_ROW_ALIGN rows), chunk bases.
+__global__ void __launch_bounds__(1024)
+expert_scan_kernel(const int32_t* __restrict__ hist, int nchunk, int E, int32_t* __restrict__ counts,
+                   int32_t* __restrict__ pad_off, int32_t* __restrict__ chunk_base) {
+  __shared__ int s_off[DM_MAX_EXPERTS + 1];
+  __shared__ int s_cnt[DM_MAX_EXPERTS];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+    for (int c = 0; c < nchunk; ++c) {
+      chunk_base[(size_t)c * E + e] = run;
+      run += hist[(size_t)c * E + e];
+    }
+    s_cnt[e] = run;
+    counts[e] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      s_off[e] = acc;
+      acc += (s_cnt[e] + DM_ROW_ALIGN - 1) / DM_ROW_ALIGN * DM_ROW_ALIGN;
+    }
+    s_off[E] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) pad_off[e] = s_off[e];
+  for (int i = threadIdx.x; i < nchunk * E; i += blockDim.x) chunk_base[i] += s_off[i % E];
+}
+
+// Zero rows [pad_off[e] + counts[e], pad_off[e+1]) of a permuted buffer; the
+// caller's grid strides over them so padding never feeds NaN into wgrad.
+__device__ __forceinline__ void zero_padding_rows(__nv_bfloat16* buf, const int32_t* counts,
+                                                  const int32_t* pad_off, int E, int H,
+                                                  int worker, int nworkers, int lane) {
+  const int4 z = make_int4(0, 0, 0, 0);
+  for (int e = 0; e < E; ++e) {
+    const int beg = pad_off[e] + counts[e];
+    const int end = pad_off[e + 1];
+    for (int r = beg + worker; r < end; r += nworkers) {
+      __nv_bfloat16* row = buf + (size_t)r * H;
+      for (int c = lane; c < (H >> 3); c += 32) st_v4(row + c * 8, z);
+    }
+  }
+}
+
+// CTA per chunk of DM_CHUNK_TOKENS tokens. Warp 0 assigns stable positions
+// (token-major (t, j) order within each expert, chunk bases from the scan);
+// then every warp copies whole token rows to their k destinations with
+// 128-bit loads/stores (x is read once, x_perm written once).
+__global__ void __launch_bounds__(128)
+permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
+               const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ counts,
+               const int32_t* __restrict__ pad_off, int T, int H, int E, int k,
+               int32_t* __restrict__ row_map, int32_t* __restrict__ src_token,
+               __nv_bfloat16* __restrict__ x_perm) {
+  extern __shared__ int s_perm[];
+  int* run = s_perm;               // [E]
+  int* spos = s_perm + E;          // [DM_CHUNK_TOKENS * k]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int c = blockIdx.x;
+  const int t0 = c * DM_CHUNK_TOKENS;
+  const int nt = min(DM_CHUNK_TOKENS, T - t0);
+  const int nslots = nt * k;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) run[i] = 0;
+  __syncthreads();
+  if (warp == 0) {
+    for (int base = 0; base < nslots; base += 32) {
+      const int s = base + lane;
+      const bool valid = s < nslots;
+      const int e = valid ? idx[(size_t)t0 * k + s] : -1 - lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, e);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      const int prior = valid ? run[e] : 0;
+      __syncwarp();
+      if (valid) {
+        const int pos = chunk_base[(size_t)c * E + e] + prior + rank;
+        spos[s] = pos;
+        row_map[(size_t)t0 * k + s] = pos;
+        src_token[pos] = t0 + s / k;
+        if (rank == 0) run[e] = prior + __popc(peers);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  const int nvec = H >> 3;
+  for (int tt = warp; tt < nt; tt += nwarps) {
+    const __nv_bfloat16* src = x + (size_t)(t0 + tt) * H;
+    int p[DM_MAX_TOPK];
+    for (int j = 0; j < k; ++j) p[j] = spos[tt * k + j];
+    int ch = lane;
+    for (; ch + 96 < nvec; ch += 128) {
+      int4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = ld_nc_v4(src + (ch + 32 * u) * 8);
+      for (int j = 0; j < k; ++j) {
+        __nv_bfloat16* dst = x_perm + (size_t)p[j] * H;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) st_v4(dst + (ch + 32 * u) * 8, v[u]);
+      }
+    }
+    for (; ch < nvec; ch += 32) {
+      const int4 v = ld_nc_v4(src + ch * 8);
+      for (int j = 0; j < k; ++j) st_v4(x_perm + (size_t)p[j] * H + ch * 8, v);
+    }
+  }
+  zero_padding_rows(x_perm, counts, pad_off, E, H, c * nwarps + warp, gridDim.x * nwarps, lane);
+  // padding rows carry no token
+  for (int e = 0; e < E; ++e) {
+    for (int r = pad_off[e] + counts[e] + c * blockDim.x + threadIdx.x; r < pad_off[e + 1];
+         r += gridDim.x * blockDim.x)
+      src_token[r] = -1;
+  }
+}
+
+int router_logits_launch(const void* x, const float* wg, float* logits, int T, int H, int E,
+                         cudaStream_t stream) {
+  const size_t row_bytes = (size_t)H * sizeof(float);
+  int ec = (int)(ROUTER_SMEM_BUDGET / row_bytes);
+  if (ec < 1) return set_error(DM_ERR_SHAPE, "router: hidden %d too large for one smem row", H);
+  if (ec > E) ec = E;
+  const size_t smem = (size_t)ec * row_bytes;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(router_logits_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ROUTER_SMEM_BUDGET);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router)");
+    configured = true;
+  }
+  const int per_cta = ROUTER_WARPS * ROUTER_NT;
+  int grid = (T + per_cta - 1) / per_cta;
+  const int cap = num_sms_current();
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  router_logits_kernel<<<grid, ROUTER_WARPS * 32, smem, stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), wg, logits, T, H, E, ec);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "router_logits launch");
+  note_launch();
+  return DM_OK;
+}
+
+}  // namespace dm
+
+using namespace dm;
+
+static int check_route_shape(int T, int H, int E, int k) {
+  if (T < 1 || H < 8 || E < 1 || k < 1) return set_error(DM_ERR_SHAPE, "bad shape T=%d H=%d E=%d k=%d", T, H, E, k);
+  if (H % 8) return set_error(DM_ERR_ALIGN, "hidden %d must be a multiple of 8 (128-bit rows)", H);
+  if (E > DM_MAX_EXPERTS) return set_error(DM_ERR_SHAPE, "experts %d > %d", E, DM_MAX_EXPERTS);
+  if (k > DM_MAX_TOPK || k > E) return set_error(DM_ERR_SHAPE, "topk %d invalid (max %d, E=%d)", k, DM_MAX_TOPK, E);
+  return DM_OK;
+}
+
+extern "C" {
+
+int dm_router_logits(const void* x, const float* wg, float* logits, int T, int H, int E, void* stream) {
+  int rc = check_route_shape(T, H, E, 1);
+  if (rc) return rc;
+  if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(wg) & 15)
+    return set_error(DM_ERR_ALIGN, "router operands must be 16-byte aligned");
+  return router_logits_launch(x, wg, logits, T, H, E, (cudaStream_t)stream);
+}
+
+int dm_router_topk(const float* logits, int T, int E, int k, int32_t* idx, float* w,
+                   int32_t* chunk_hist, void* stream) {
+  int rc = check_route_shape(T, 8, E, k);
+  if (rc) return rc;
+  const int nchunk = dm_num_chunks(T);
+  router_topk_kernel<<<nchunk, 256, E * sizeof(int), (cudaStream_t)stream>>>(logits, T, E, k, idx, w, chunk_hist);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "router_topk launch");
+  note_launch();
+  return DM_OK;
+}
+
+int dm_expert_scan(const int32_t* chunk_hist, int T, int E, int32_t* counts, int32_t* pad_off,
+                   int32_t* chunk_base, void* stream) {
+  int rc = check_route_shape(T, 8, E, 1);
+  if (rc) return rc;
+  const int nchunk = dm_num_chunks(T);
+  expert_scan_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(chunk_hist, nchunk, E, counts, pad_off, chunk_base);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "expert_scan launch");
+  note_launch();
+  return DM_OK;
+}
+
+int dm_permute(const void* x, const int32_t* idx, const int32_t* chunk_base, const int32_t* counts,
+               const int32_t* pad_off, int T, int H, int E, int k, int32_t* row_map,
+               int32_t* src_token, void* x_perm, void* stream) {
+  int rc = check_route_shape(T, H, E, k);
+  if (rc) return rc;
+  if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(x_perm) & 15)
+    return set_error(DM_ERR_ALIGN, "permute rows must be 16-byte aligned");
+  const int nchunk = dm_num_chunks(T);
+  const size_t smem = (E + DM_CHUNK_TOKENS * k) * sizeof(int);
+  permute_kernel<<<nchunk, 128, smem, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), idx, chunk_base, counts, pad_off, T, H, E, k,
+      row_map, src_token, reinterpret_cast<__nv_bfloat16*>(x_perm));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "permute launch");
+  note_launch();
+  return DM_OK;
+}
+
+int dm_route_and_dispatch(const void* x, const float* wg, int T, int H, int E, int k, void* workspace,
+                          int32_t* idx, float* w, int32_t* counts, int32_t* pad_off,
+                          int32_t* row_map, int32_t* src_token, void* x_perm, void* stream) {
+  int rc = check_route_shape(T, H, E, k);
+  if (rc) return rc;
+  dm_route_ws ws;
+  dm_route_workspace_layout(T, H, E, k, workspace, &ws);
+  if ((rc = dm_router_logits(x, wg, ws.logits, T, H, E, stream))) return rc;
+  if ((rc = dm_router_topk(ws.logits, T, E, k, idx, w, ws.chunk_hist, stream))) return rc;
+  if ((rc = dm_expert_scan(ws.chunk_hist, T, E, counts, pad_off, ws.chunk_base, stream))) return rc;
+  return dm_permute(x, idx, ws.chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, x_perm, stream);
+}
+
+}  // extern "C"

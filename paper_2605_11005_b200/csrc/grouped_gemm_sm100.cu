@@ -1,0 +1,468 @@
+// Grouped (per-expert) bf16 GEMMs for the SwiGLU expert FFN, fwd + bwd, on
+// 5th-gen tensor cores: TMA -> 4-stage smem ring -> tcgen05.mma (one thread)
+// -> fp32 accumulators in TMEM (2 x 128x256 tiles, double buffered) -> fused
+// epilogue warps (SwiGLU fwd / SwiGLU bwd / bf16 store / fp32 store+accumulate).
+//
+// Reference counterpart: the reference only *costs* this stage —
+// ffn_flops C_f = 4*b*k*s*H*D_e (pkg/src/afpipe/costs.py:90-92, two GEMMs) and
+// backward_scale 2x (costs.py:146-150); the F-side FwdCompute/BwdCompute tasks
+// of _build_afpipe (taskgraph.py:333-347) stand for what this file computes.
+//
+// Two grouping modes, both driven by the 128-aligned per-expert row offsets
+// `group_off` produced on device by the dispatch scan (no host sync):
+//   ragged-M  (fwd, dgrad): C[rows_e, N] = A[rows_e, K] * B_e^T, tiles over
+//             (expert, 128-row m-tile, 256-col n-tile), m fastest so the 8
+//             m-tiles of one expert reuse each weight n-tile from L2.
+//   ragged-K  (wgrad):      C_e[M, N] = A_tok[rows_e, M]^T * B_tok[rows_e, N],
+//             K loop over the expert's (zero-padded) token rows.
+#include "dm_common.cuh"
+#include "dm_internal.h"
+
+namespace dm {
+
+constexpr int GBM = 128, GBN = 256, GBK = 64, GSTAGES = 4;
+constexpr uint32_t GA_BYTES = GBM * GBK * 2;   // 16 KiB
+constexpr uint32_t GB_BYTES = GBN * GBK * 2;   // 32 KiB
+constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_MAX_GROUPS = 1024;
+constexpr size_t GEMM_SMEM_BYTES =
+    1024 /*align slack*/ + GSTAGES * (GA_BYTES + GB_BYTES) + 256 /*barriers*/ +
+    2 * (GEMM_MAX_GROUPS + 1) * sizeof(int);
+
+enum { EPI_BF16 = 0, EPI_SWIGLU_FWD = 1, EPI_SWIGLU_BWD = 2, EPI_F32 = 3 };
+
+struct GemmArgs {
+  int num_groups;
+  const int* group_off;          // [G+1], 128-aligned, device
+  int M;                         // ragged-K: rows of C per group (multiple of 128)
+  int N;                         // multiple of 256
+  int K;                         // ragged-M: reduction length (multiple of 64)
+  int b_group_rows;              // ragged-M: rows of the B tensor owned by one group
+  void* C;
+  long long ldc;
+  long long c_group_stride;      // ragged-K: elements between groups' C blocks
+  __nv_bfloat16* aux;            // SwiGLU fwd: h13 out; SwiGLU bwd: dh13 out
+  long long ld_aux;
+  const __nv_bfloat16* aux_in;   // SwiGLU bwd: h13 in
+  long long ld_aux_in;
+  float beta;                    // EPI_F32: C = acc + beta * C
+};
+
+struct TileInfo {
+  int g, m0, n0, kb_count, row_base;
+};
+
+template <int RAGGED_K>
+__device__ __forceinline__ TileInfo decode_tile(int t, const int* tile_start, const int* off,
+                                                int G, const GemmArgs& a) {
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_start[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  TileInfo ti;
+  ti.g = lo;
+  const int local = t - tile_start[lo];
+  const int row_off = off[lo];
+  const int rows = off[lo + 1] - row_off;
+  ti.row_base = row_off;
+  if (!RAGGED_K) {
+    const int mt = rows / GBM;
+    ti.m0 = row_off + (local % mt) * GBM;
+    ti.n0 = (local / mt) * GBN;
+    ti.kb_count = a.K / GBK;
+  } else {
+    const int mt = a.M / GBM;
+    ti.m0 = (local % mt) * GBM;
+    ti.n0 = (local / mt) * GBN;
+    ti.kb_count = rows / GBK;
+  }
+  return ti;
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+// One thread owns one accumulator row (TMEM lane) of the 128x256 tile.
+template <int EPI>
+__device__ __forceinline__ void epilogue_row(const TileInfo& ti, uint32_t trow, int r,
+                                             const GemmArgs& a) {
+  if constexpr (EPI == EPI_BF16) {
+    const long long row = ti.m0 + r;
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.C) + row * a.ldc + ti.n0;
+#pragma unroll 1
+    for (int c = 0; c < GBN; c += 32) {
+      uint32_t v0[16], v1[16];
+      tmem_ld16(trow + c, v0);
+      tmem_ld16(trow + c + 16, v1);
+      tmem_wait_ld();
+      int4 o[4];
+      uint32_t* op = reinterpret_cast<uint32_t*>(o);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) op[i] = pack_bf16(__uint_as_float(v0[2 * i]), __uint_as_float(v0[2 * i + 1]));
+#pragma unroll
+      for (int i = 0; i < 8; ++i) op[8 + i] = pack_bf16(__uint_as_float(v1[2 * i]), __uint_as_float(v1[2 * i + 1]));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) st_v4(out + c + 8 * i, o[i]);
+    }
+  } else if constexpr (EPI == EPI_SWIGLU_FWD) {
+    // Tile columns [0,128) are gate rows of W13, [128,256) the matching up rows.
+    const long long row = ti.m0 + r;
+    __nv_bfloat16* hout = a.aux + row * a.ld_aux + ti.n0;
+    __nv_bfloat16* aout = reinterpret_cast<__nv_bfloat16*>(a.C) + row * a.ldc + (ti.n0 >> 1);
+#pragma unroll 1
+    for (int c = 0; c < GBN / 2; c += 16) {
+      uint32_t g[16], u[16];
+      tmem_ld16(trow + c, g);
+      tmem_ld16(trow + 128 + c, u);
+      tmem_wait_ld();
+      int4 hg[2], hu[2], ao[2];
+      uint32_t* hgp = reinterpret_cast<uint32_t*>(hg);
+      uint32_t* hup = reinterpret_cast<uint32_t*>(hu);
+      uint32_t* aop = reinterpret_cast<uint32_t*>(ao);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
+        const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+        hgp[i] = pack_bf16(g0, g1);
+        hup[i] = pack_bf16(u0, u1);
+        aop[i] = pack_bf16(silu_f(g0) * u0, silu_f(g1) * u1);
+      }
+      st_v4(hout + c, hg[0]);       st_v4(hout + c + 8, hg[1]);
+      st_v4(hout + 128 + c, hu[0]); st_v4(hout + 128 + c + 8, hu[1]);
+      st_v4(aout + c, ao[0]);       st_v4(aout + c + 8, ao[1]);
+    }
+  } else if constexpr (EPI == EPI_SWIGLU_BWD) {
+    // Accumulator = d_act for D_e columns [n0, n0+256); gate/up live in the
+    // 128-block-interleaved h13 layout: d -> (d/128)*256 + d%128 (+128 for up).
+    const long long row = ti.m0 + r;
+    const __nv_bfloat16* hin = a.aux_in + row * a.ld_aux_in;
+    __nv_bfloat16* dhout = a.aux + row * a.ld_aux;
+#pragma unroll 1
+    for (int c = 0; c < GBN; c += 16) {
+      uint32_t d[16];
+      tmem_ld16(trow + c, d);
+      const int dcol = ti.n0 + c;
+      const long long gcol = (long long)(dcol >> 7) * 256 + (dcol & 127);
+      int4 gv[2], uv[2];
+      gv[0] = ld_v4(hin + gcol);       gv[1] = ld_v4(hin + gcol + 8);
+      uv[0] = ld_v4(hin + gcol + 128); uv[1] = ld_v4(hin + gcol + 136);
+      tmem_wait_ld();
+      const uint32_t* gp = reinterpret_cast<const uint32_t*>(gv);
+      const uint32_t* up = reinterpret_cast<const uint32_t*>(uv);
+      int4 dg[2], du[2];
+      uint32_t* dgp = reinterpret_cast<uint32_t*>(dg);
+      uint32_t* dup = reinterpret_cast<uint32_t*>(du);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float gg[2] = {bf16lo(gp[i]), bf16hi(gp[i])};
+        float uu[2] = {bf16lo(up[i]), bf16hi(up[i])};
+        float da[2] = {__uint_as_float(d[2 * i]), __uint_as_float(d[2 * i + 1])};
+        float rg[2], ru[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float sg = 1.0f / (1.0f + __expf(-gg[h]));
+          const float sl = gg[h] * sg;
+          ru[h] = da[h] * sl;
+          rg[h] = da[h] * uu[h] * sg * (1.0f + gg[h] * (1.0f - sg));
+        }
+        dgp[i] = pack_bf16(rg[0], rg[1]);
+        dup[i] = pack_bf16(ru[0], ru[1]);
+      }
+      st_v4(dhout + gcol, dg[0]);       st_v4(dhout + gcol + 8, dg[1]);
+      st_v4(dhout + gcol + 128, du[0]); st_v4(dhout + gcol + 136, du[1]);
+    }
+  } else {  // EPI_F32 (wgrad): C_g[m, n] = acc + beta * C_g[m, n]
+    float* out = reinterpret_cast<float*>(a.C) + (long long)ti.g * a.c_group_stride +
+                 (long long)(ti.m0 + r) * a.ldc + ti.n0;
+    const bool empty = ti.kb_count == 0;
+#pragma unroll 1
+    for (int c = 0; c < GBN; c += 16) {
+      uint32_t v[16];
+      if (!empty) {
+        tmem_ld16(trow + c, v);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0u;
+      }
+      float4* o4 = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float4 f = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                               __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        if (a.beta != 0.0f) {
+          const float4 old = o4[i];
+          f.x += a.beta * old.x; f.y += a.beta * old.y; f.z += a.beta * old.z; f.w += a.beta * old.w;
+        }
+        o4[i] = f;
+      }
+    }
+  }
+}
+
+template <int A_MN, int B_MN, int RAGGED_K, int EPI>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                    const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + GSTAGES * GA_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + GSTAGES * GB_BYTES);
+  uint64_t* empty = full + GSTAGES;
+  uint64_t* tfull = empty + GSTAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_tile = reinterpret_cast<int*>(smem + GSTAGES * (GA_BYTES + GB_BYTES) + 256);
+  int* s_off = s_tile + (GEMM_MAX_GROUPS + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int G = args.num_groups;
+
+  for (int i = threadIdx.x; i <= G; i += GEMM_THREADS) s_off[i] = args.group_off[i];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < GSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  __syncthreads();
+  if (threadIdx.x == 32 * 3) {
+    int acc = 0;
+    for (int g = 0; g < G; ++g) {
+      s_tile[g] = acc;
+      const int rows = s_off[g + 1] - s_off[g];
+      acc += RAGGED_K ? (args.M / GBM) * (args.N / GBN) : (rows / GBM) * (args.N / GBN);
+    }
+    s_tile[G] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = s_tile[G];
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const TileInfo ti = decode_tile<RAGGED_K>(t, s_tile, s_off, G, args);
+        const int b_gofs = RAGGED_K ? 0 : ti.g * args.b_group_rows;
+        for (int kb = 0; kb < ti.kb_count; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], GA_BYTES + GB_BYTES);
+          uint8_t* a_dst = sA + stage * GA_BYTES;
+          uint8_t* b_dst = sB + stage * GB_BYTES;
+          const int kcoord = RAGGED_K ? ti.row_base + kb * GBK : kb * GBK;
+          if (!A_MN) {
+            tma_load_2d(a_dst, &tmA, &full[stage], kcoord, ti.m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < GBM / 64; ++j)
+              tma_load_2d(a_dst + j * 8192, &tmA, &full[stage], ti.m0 + 64 * j, kcoord);
+          }
+          if (!B_MN) {
+            tma_load_2d(b_dst, &tmB, &full[stage], kcoord, b_gofs + ti.n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < GBN / 64; ++j)
+              tma_load_2d(b_dst + j * 8192, &tmB, &full[stage], ti.n0 + 64 * j, b_gofs + kcoord);
+          }
+          if (++stage == GSTAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(GBM, GBN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+        const TileInfo ti = decode_tile<RAGGED_K>(t, s_tile, s_off, G, args);
+        const int as = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * GBN;
+        for (int kb = 0; kb < ti.kb_count; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * GA_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * GB_BYTES);
+#pragma unroll
+          for (int k = 0; k < GBK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sdesc_sw128(a_addr + k * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc_sw128(b_addr + k * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(b_addr + k * 32, 16, 1024);
+            umma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == GSTAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[as]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // --------------------------------------------------------- epilogue warps
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++it) {
+      const TileInfo ti = decode_tile<RAGGED_K>(t, s_tile, s_off, G, args);
+      const int as = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * GBN;
+      epilogue_row<EPI>(ti, trow, q * 32 + lane, args);
+      tc_fence_before();
+      mbar_arrive(&tempty[as]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+// ------------------------------------------------------------------- host side
+
+static int make_tmap_bf16_2d(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer,
+                             uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled entry point unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((row_stride_elems * 2) & 15))
+    return set_error(DM_ERR_ALIGN, "TMA operand base/stride not 16-byte aligned");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DM_OK;
+}
+
+template <int A_MN, int B_MN, int RAGGED_K, int EPI>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args,
+                       cudaStream_t stream) {
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)GEMM_SMEM_BYTES);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm smem)");
+    configured = true;
+  }
+  const int grid = num_sms_current();
+  kern<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(ta, tb, args);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm launch");
+  note_launch();
+  return DM_OK;
+}
+
+static int check_groups(int E, int cap_rows) {
+  if (E < 1 || E > GEMM_MAX_GROUPS) return set_error(DM_ERR_SHAPE, "expert count %d outside [1, %d]", E, GEMM_MAX_GROUPS);
+  if (cap_rows < 0 || (cap_rows % GBM)) return set_error(DM_ERR_SHAPE, "cap_rows %d must be a multiple of %d", cap_rows, GBM);
+  return DM_OK;
+}
+
+}  // namespace dm
+
+using namespace dm;
+
+extern "C" {
+
+int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t* pad_off, int E,
+                              int cap_rows, int H, int De, void* h13, void* act, void* stream) {
+  int rc = check_groups(E, cap_rows);
+  if (rc) return rc;
+  if (H % GBK || H < GBK || De % 128 || De < 128)
+    return set_error(DM_ERR_SHAPE, "w13 fwd needs H %% 64 == 0 and D_e %% 128 == 0 (H=%d, D_e=%d)", H, De);
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap_bf16_2d(&ta, x_perm, H, cap_rows, H, 64, 128))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, w13, H, (uint64_t)E * 2 * De, H, 64, 256))) return rc;
+  GemmArgs a{};
+  a.num_groups = E; a.group_off = pad_off; a.N = 2 * De; a.K = H; a.b_group_rows = 2 * De;
+  a.C = act; a.ldc = De; a.aux = reinterpret_cast<__nv_bfloat16*>(h13); a.ld_aux = 2 * De;
+  return launch_gemm<0, 0, 0, EPI_SWIGLU_FWD>(ta, tb, a, (cudaStream_t)stream);
+}
+
+int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* pad_off, int E, int cap_rows,
+                      int H, int De, void* y_perm, void* stream) {
+  int rc = check_groups(E, cap_rows);
+  if (rc) return rc;
+  if (H % GBN || De % GBK)
+    return set_error(DM_ERR_SHAPE, "w2 fwd needs H %% 256 == 0 and D_e %% 64 == 0 (H=%d, D_e=%d)", H, De);
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap_bf16_2d(&ta, act, De, cap_rows, De, 64, 128))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, w2, De, (uint64_t)E * H, De, 64, 256))) return rc;
+  GemmArgs a{};
+  a.num_groups = E; a.group_off = pad_off; a.N = H; a.K = De; a.b_group_rows = H;
+  a.C = y_perm; a.ldc = H;
+  return launch_gemm<0, 0, 0, EPI_BF16>(ta, tb, a, (cudaStream_t)stream);
+}
+
+int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const void* h13,
+                                   const int32_t* pad_off, int E, int cap_rows, int H, int De,
+                                   void* dh13, void* stream) {
+  int rc = check_groups(E, cap_rows);
+  if (rc) return rc;
+  if (H % GBK || De % GBN)
+    return set_error(DM_ERR_SHAPE, "w2 dgrad needs H %% 64 == 0 and D_e %% 256 == 0 (H=%d, D_e=%d)", H, De);
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap_bf16_2d(&ta, dy_perm, H, cap_rows, H, 64, 128))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, w2, De, (uint64_t)E * H, De, 64, 64))) return rc;
+  GemmArgs a{};
+  a.num_groups = E; a.group_off = pad_off; a.N = De; a.K = H; a.b_group_rows = H;
+  a.aux = reinterpret_cast<__nv_bfloat16*>(dh13); a.ld_aux = 2 * De;
+  a.aux_in = reinterpret_cast<const __nv_bfloat16*>(h13); a.ld_aux_in = 2 * De;
+  return launch_gemm<0, 1, 0, EPI_SWIGLU_BWD>(ta, tb, a, (cudaStream_t)stream);
+}
+
+int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* pad_off, int E,
+                         int cap_rows, int H, int De, void* dx_perm, void* stream) {
+  int rc = check_groups(E, cap_rows);
+  if (rc) return rc;
+  if (H % GBN || De % 128)
+    return set_error(DM_ERR_SHAPE, "w13 dgrad needs H %% 256 == 0 and D_e %% 128 == 0 (H=%d, D_e=%d)", H, De);
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap_bf16_2d(&ta, dh13, 2 * De, cap_rows, 2 * De, 64, 128))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, w13, H, (uint64_t)E * 2 * De, H, 64, 64))) return rc;
+  GemmArgs a{};
+  a.num_groups = E; a.group_off = pad_off; a.N = H; a.K = 2 * De; a.b_group_rows = 2 * De;
+  a.C = dx_perm; a.ldc = H;
+  return launch_gemm<0, 1, 0, EPI_BF16>(ta, tb, a, (cudaStream_t)stream);
+}
+
+int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* pad_off,
+                     int E, int cap_rows, float* dW, float beta, void* stream) {
+  int rc = check_groups(E, cap_rows);
+  if (rc) return rc;
+  if (M % GBM || N % GBN || M <= 0 || N <= 0)
+    return set_error(DM_ERR_SHAPE, "wgrad needs M %% 128 == 0 and N %% 256 == 0 (M=%d, N=%d)", M, N);
+  if (reinterpret_cast<uintptr_t>(dW) & 15) return set_error(DM_ERR_ALIGN, "dW not 16-byte aligned");
+  CUtensorMap ta, tb;
+  if ((rc = make_tmap_bf16_2d(&ta, a_tok, M, cap_rows, M, 64, 64))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, b_tok, N, cap_rows, N, 64, 64))) return rc;
+  GemmArgs a{};
+  a.num_groups = E; a.group_off = pad_off; a.M = M; a.N = N;
+  a.C = dW; a.ldc = N; a.c_group_stride = (long long)M * N; a.beta = beta;
+  return launch_gemm<1, 1, 1, EPI_F32>(ta, tb, a, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+"""Thin torch-tensor wrappers over the dm_* C ABI (one function per entry point).
+
+Tensors must already live on the current CUDA device; the calls are
+stream-ordered on torch's current stream and never synchronise. Shapes and
+dtypes are checked here so misuse fails loudly before reaching the ABI.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+BF16 = torch.bfloat16
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("dm kernels need CUDA tensors (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("dm kernels need contiguous tensors")
+    return t.data_ptr()
+
+
+def _stream(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _check(t: torch.Tensor, dtype: torch.dtype, shape: tuple, name: str) -> None:
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+# ------------------------------------------------------------------ dispatch
+def router_logits(x, wg, logits, stream=None):
+    T, H = x.shape
+    E = wg.shape[0]
+    _check(x, BF16, (T, H), "x"); _check(wg, torch.float32, (E, H), "wg")
+    _check(logits, torch.float32, (T, E), "logits")
+    _lib.call("dm_router_logits", _ptr(x), _ptr(wg), _ptr(logits), T, H, E, _stream(stream))
+
+
+def router_topk(logits, k, idx, w, chunk_hist, stream=None):
+    T, E = logits.shape
+    _check(idx, torch.int32, (T, k), "idx"); _check(w, torch.float32, (T, k), "w")
+    _check(chunk_hist, torch.int32, (_lib.num_chunks(T), E), "chunk_hist")
+    _lib.call("dm_router_topk", _ptr(logits), T, E, k, _ptr(idx), _ptr(w), _ptr(chunk_hist), _stream(stream))
+
+
+def expert_scan(chunk_hist, T, counts, pad_off, chunk_base, stream=None):
+    nch, E = chunk_hist.shape
+    _check(counts, torch.int32, (E,), "counts"); _check(pad_off, torch.int32, (E + 1,), "pad_off")
+    _check(chunk_base, torch.int32, (nch, E), "chunk_base")
+    _lib.call("dm_expert_scan", _ptr(chunk_hist), T, E, _ptr(counts), _ptr(pad_off), _ptr(chunk_base),
+              _stream(stream))
+
+
+def permute(x, idx, chunk_base, counts, pad_off, row_map, src_token, x_perm, stream=None):
+    T, H = x.shape
+    k = idx.shape[1]
+    E = counts.shape[0]
+    _check(row_map, torch.int32, (T, k), "row_map")
+    if x_perm.dtype != BF16 or x_perm.shape[1] != H:
+        raise ValueError("x_perm must be bf16 [cap, H]")
+    _lib.call("dm_permute", _ptr(x), _ptr(idx), _ptr(chunk_base), _ptr(counts), _ptr(pad_off), T, H, E, k,
+              _ptr(row_map), _ptr(src_token), _ptr(x_perm), _stream(stream))
+
+
+def route_and_dispatch(x, wg, k, workspace, idx, w, counts, pad_off, row_map, src_token, x_perm, stream=None):
+    T, H = x.shape
+    E = wg.shape[0]
+    _check(x, BF16, (T, H), "x"); _check(wg, torch.float32, (E, H), "wg")
+    need = _lib.route_workspace_size(T, H, E, k)
+    if workspace.numel() * workspace.element_size() < need:
+        raise ValueError(f"route workspace too small ({need} bytes needed)")
+    _lib.call("dm_route_and_dispatch", _ptr(x), _ptr(wg), T, H, E, k, _ptr(workspace), _ptr(idx), _ptr(w),
+              _ptr(counts), _ptr(pad_off), _ptr(row_map), _ptr(src_token), _ptr(x_perm), _stream(stream))
+
+
+# --------------------------------------------------------------- expert FFN
+def w13_swiglu_fwd(x_perm, w13, pad_off, h13, act, stream=None):
+    cap, H = x_perm.shape
+    E, two_de, _ = w13.shape
+    De = two_de // 2
+    _check(h13, BF16, (cap, 2 * De), "h13"); _check(act, BF16, (cap, De), "act")
+    _lib.call("dm_grouped_w13_swiglu_fwd", _ptr(x_perm), _ptr(w13), _ptr(pad_off), E, cap, H, De,
+              _ptr(h13), _ptr(act), _stream(stream))
+
+
+def w2_fwd(act, w2, pad_off, y_perm, stream=None):
+    cap, De = act.shape
+    E, H, _ = w2.shape
+    _check(y_perm, BF16, (cap, H), "y_perm")
+    _lib.call("dm_grouped_w2_fwd", _ptr(act), _ptr(w2), _ptr(pad_off), E, cap, H, De, _ptr(y_perm),
+              _stream(stream))
+
+
+def w2_dgrad_swiglu_bwd(dy_perm, w2, h13, pad_off, dh13, stream=None):
+    cap, H = dy_perm.shape
+    E, _, De = w2.shape
+    _check(dh13, BF16, (cap, 2 * De), "dh13")
+    _lib.call("dm_grouped_w2_dgrad_swiglu_bwd", _ptr(dy_perm), _ptr(w2), _ptr(h13), _ptr(pad_off), E, cap,
+              H, De, _ptr(dh13), _stream(stream))
+
+
+def w13_dgrad(dh13, w13, pad_off, dx_perm, stream=None):
+    cap, two_de = dh13.shape
+    E, _, H = w13.shape
+    _check(dx_perm, BF16, (cap, H), "dx_perm")
+    _lib.call("dm_grouped_w13_dgrad", _ptr(dh13), _ptr(w13), _ptr(pad_off), E, cap, H, two_de // 2,
+              _ptr(dx_perm), _stream(stream))
+
+
+def wgrad(a_tok, b_tok, pad_off, dW, beta=0.0, stream=None):
+    cap, M = a_tok.shape
+    _, N = b_tok.shape
+    E = pad_off.shape[0] - 1
+    _check(dW, torch.float32, (E, M, N), "dW")
+    _lib.call("dm_grouped_wgrad", _ptr(a_tok), M, _ptr(b_tok), N, _ptr(pad_off), E, cap, _ptr(dW),
+              float(beta), _stream(stream))
+
+
+# ------------------------------------------------------------------ combine
+def combine_fwd(y_perm, row_map, w, y, stream=None):
+    T, k = row_map.shape
+    H = y_perm.shape[1]
+    _check(y, BF16, (T, H), "y")
+    _lib.call("dm_combine_fwd", _ptr(y_perm), _ptr(row_map), _ptr(w), T, H, k, _ptr(y), _stream(stream))
+
+
+def combine_bwd(dy, y_perm, row_map, w, counts, pad_off, dy_perm, dw, dlogit, stream=None):
+    T, H = dy.shape
+    k = row_map.shape[1]
+    E = counts.shape[0]
+    _lib.call("dm_combine_bwd", _ptr(dy), _ptr(y_perm), _ptr(row_map), _ptr(w), _ptr(counts), _ptr(pad_off),
+              T, H, E, k, _ptr(dy_perm), _ptr(dw), _ptr(dlogit), _stream(stream))
+
+
+def permute_bwd(dx_perm, row_map, idx, dlogit, wg, dx, stream=None):
+    T, k = row_map.shape
+    H = dx.shape[1]
+    _lib.call("dm_permute_bwd", _ptr(dx_perm), _ptr(row_map), _ptr(idx), _ptr(dlogit), _ptr(wg), T, H, k,
+              _ptr(dx), _stream(stream))
+
+
+def router_wgrad(x, idx, dlogit, partial_ws, dwg, beta=0.0, stream=None):
+    T, H = x.shape
+    k = idx.shape[1]
+    E = dwg.shape[0]
+    need = _lib.router_wgrad_workspace_size(T, H, E)
+    if partial_ws.numel() * partial_ws.element_size() < need:
+        raise ValueError(f"router wgrad workspace too small ({need} bytes needed)")
+    _lib.call("dm_router_wgrad", _ptr(x), _ptr(idx), _ptr(dlogit), T, H, E, k, _ptr(partial_ws), _ptr(dwg),
+              float(beta), _stream(stream))
