@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark: MoE layer fwd+bwd tokens/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config configs/mixtral_layer.yaml]
+                    [--impl ours|reference]
+
+A step = one iteration of the layer over `num_microbatches` micro-batches of
+T = seq_len * micro_batch synthetic tokens (fwd + bwd each, weight gradients
+accumulated across micro-batches, fp32). N=1 runs the fused single-device path
+(A and F stages on one GPU) on BASELINE configs[1] (Mixtral-8x7B layer).
+N>1 runs the AF-Pipe runtime split into attention:FFN groups when it is
+available, otherwise independent replicas (weak scaling), as stated in the
+JSON line's config.parallelism.
+
+`--impl reference` times the CPU oracle port (oracle/, the reference has no
+MoE arithmetic to run — DESIGN.md §3) on the host cores on a bounded token
+sample of the same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE fwd+bwd tokens/s at 1/2/4/8 B200; exposed A2F comm %; roofline %"
+UNIT = "tokens/s"
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: int | None = None):
+    """Time the oracle port (numpy fp32 BLAS, all host threads) on a bounded token sample."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    threads = O.cpu_threads()
+    H, E, k, De = shape.H, shape.E, shape.k, shape.De
+    rng = np.random.default_rng(7)
+    if layer is not None:
+        from paper_2605_11005_b200.moe import split_w13
+
+        w1t, w3t = split_w13(layer.experts.w13)
+        w1 = w1t.float().cpu().numpy()
+        w3 = w3t.float().cpu().numpy()
+        w2 = layer.experts.w2.float().cpu().numpy()
+        wg = layer.router.wg.float().cpu().numpy()
+    else:
+        w1 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02)
+        w3 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02)
+        w2 = (rng.standard_normal((E, H, De), dtype=np.float32) * 0.02)
+        wg = (rng.standard_normal((E, H), dtype=np.float32) * 0.02)
+    T = 64
+    best = None
+    while True:
+        x = O.f32_to_bf16_bits(rng.standard_normal((T, H), dtype=np.float32))
+        dy = O.round_bf16(rng.standard_normal((T, H), dtype=np.float32))
+        t0 = time.perf_counter()
+        f = O.moe_forward(x, wg, w1, w3, w2, k, dtype=np.float32)
+        O.moe_backward(f, x, wg, w1, w3, w2, dy, dtype=np.float32)
+        dt = time.perf_counter() - t0
+        best = (T, dt)
+        if dt > tokens_budget_s / 4 or T >= (max_tokens or shape.T) or T * 2 > shape.T:
+            break
+        T *= 2
+    T, dt = best
+    return {"value": T / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{T} tokens of the {shape.T}-token micro-batch, full layer fwd+bwd "
+                      f"(H={H}, E={E}, k={k}, D_e={De}), numpy fp32 BLAS oracle, {dt:.2f} s"}
+
+
+def run_reference(args, shape, exp):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    steps, warm = args.steps, args.warmup
+    samples = []
+    for i in range(warm + steps):
+        r = cpu_baseline(shape, tokens_budget_s=8.0, max_tokens=256)
+        if i >= warm:
+            samples.append(r)
+    value = statistics.median(s["value"] for s in samples)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E,
+                   "k": shape.k, "D_e": shape.De, "microbatches": exp.workload.num_microbatches},
+        "cpu_baseline": {**samples[-1], "value": value},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, shape, exp):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_11005_b200 import _lib
+    from paper_2605_11005_b200.moe import MoELayer, a_combine, a_combine_bwd, a_dispatch, a_dispatch_bwd, \
+        f_backward, f_forward
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    mb = exp.workload.num_microbatches
+    layer = MoELayer.random(shape, device=dev, seed=1234 + rank, num_buffers=2)
+    stream = torch.cuda.current_stream(dev)
+    for b in layer.buffers:
+        b.x.normal_()
+        b.dy.normal_()
+
+    # per-stage CUDA events: GEMM (F) time and HBM-kernel (A) time inside the timed region
+    class Ev:
+        def __init__(self):
+            self.pairs = {"gemm": [], "dispatch": [], "combine_fwd": [], "combine_bwd": [], "permute_bwd": []}
+
+        def mark(self, name, fn):
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            fn()
+            e.record(stream)
+            self.pairs[name].append((s, e))
+
+        def total_ms(self, name):
+            return sum(s.elapsed_time(e) for s, e in self.pairs[name])
+
+    def step(ev=None):
+        for i in range(mb):
+            buf = layer.buffers[i % 2]
+            acc = i > 0
+            if ev is None:
+                layer.forward_backward(buf, accumulate=acc)
+                continue
+            ev.mark("dispatch", lambda: a_dispatch(buf, layer.router))
+            ev.mark("gemm", lambda: f_forward(buf, layer.experts))
+            ev.mark("combine_fwd", lambda: a_combine(buf))
+            ev.mark("combine_bwd", lambda: a_combine_bwd(buf))
+            ev.mark("gemm", lambda: f_backward(buf, layer.experts, acc))
+            ev.mark("permute_bwd", lambda: a_dispatch_bwd(buf, layer.router, acc))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(dev.index) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    ev = Ev()
+    launches0 = _lib.launch_count()
+    t_s = torch.cuda.Event(enable_timing=True)
+    t_e = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t_s.record(stream)
+    for _ in range(args.steps):
+        step(ev)
+    t_e.record(stream)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    ms = t_s.elapsed_time(t_e)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = tt.item()
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+
+    # ---- e2e: public API with pinned host buffers, copies inside the timed region
+    e2e = run_e2e(args, layer, shape, mb, dev, world)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    peaks, peak_kind = _peaks()
+    tokens = args.steps * mb * shape.T * world
+    value = tokens / (ms / 1e3)
+    gemm_ms = ev.total_ms("gemm")
+    gemm_flops = args.steps * mb * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd())
+    achieved_tf = gemm_flops / (gemm_ms / 1e3) / 1e12
+    peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    hb = shape.hbm_bytes()
+    hbm = {}
+    for name in ("dispatch", "combine_fwd", "combine_bwd", "permute_bwd"):
+        t = ev.total_ms(name) / (args.steps * mb)
+        gbs = hb[name] / (t / 1e3) / 1e9
+        hbm[name] = {"ms": round(t, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 3)}
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_gemm_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("bytes_per_microbatch")
+        except (ValueError, OSError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {
+            "workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E, "k": shape.k,
+            "D_e": shape.De, "microbatches": mb, "tokens_per_step": mb * shape.T * world,
+            "parallelism": "fused single-device (A+F on one GPU)" if world == 1 else f"replicas x{world}",
+            "weights": "random-init", "l2": "inputs+weights (2.8 GB) larger than L2 (126 MB)",
+            "wgrad": "fp32, accumulated across micro-batches",
+        },
+        "roofline": {
+            "bound": "tensor", "kernel": "grouped expert GEMMs (K4/K5/K8, 6 launches per micro-batch)",
+            "achieved": round(achieved_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
+            "peak_kind": f"{peak_kind} sustained bf16 (MEASURED_PEAKS.json)",
+            "gemm_ms_per_microbatch": round(gemm_ms / (args.steps * mb), 4),
+            "frac_of_burst": round(achieved_tf / peaks["bf16_tflops"], 4),
+        },
+        "roofline_hbm": {"peak_GB/s": peaks["hbm_gbs"], **hbm},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(shape, layer=layer)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, layer, shape, mb, dev, world):
+    """Same metric through the public API with host buffers: per micro-batch H2D of
+    x and dy from pinned memory and D2H of y and dx, overlapped on a copy stream."""
+    import torch
+    import torch.distributed as dist
+
+    T, H = shape.T, shape.H
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    hx = [torch.randn(T, H).to(torch.bfloat16).pin_memory() for _ in range(mb)]
+    hdy = [torch.randn(T, H).to(torch.bfloat16).pin_memory() for _ in range(mb)]
+    hy = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(mb)]
+    hdx = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(mb)]
+    bufs = layer.buffers
+
+    def step():
+        loaded = [torch.cuda.Event() for _ in range(mb)]
+        done = [torch.cuda.Event() for _ in range(mb)]
+        freed = [torch.cuda.Event() for _ in range(mb)]
+        with torch.cuda.stream(copy):
+            for i in range(min(2, mb)):
+                bufs[i % 2].x.copy_(hx[i], non_blocking=True)
+                bufs[i % 2].dy.copy_(hdy[i], non_blocking=True)
+                loaded[i].record(copy)
+        for i in range(mb):
+            b = bufs[i % 2]
+            comp.wait_event(loaded[i])
+            layer.forward_backward(b, accumulate=i > 0)
+            done[i].record(comp)
+            with torch.cuda.stream(copy):
+                copy.wait_event(done[i])
+                hy[i].copy_(b.y, non_blocking=True)
+                hdx[i].copy_(b.dx, non_blocking=True)
+                freed[i].record(copy)
+                if i + 2 < mb:
+                    bufs[i % 2].x.copy_(hx[i + 2], non_blocking=True)
+                    bufs[i % 2].dy.copy_(hdy[i + 2], non_blocking=True)
+                    loaded[i + 2].record(copy)
+        comp.wait_stream(copy)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(comp)
+    for _ in range(args.steps):
+        step()
+    t1.record(comp)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = tt.item()
+    per = T * H * 2
+    return {"value": round(args.steps * mb * T * world / (ms / 1e3), 1), "unit": UNIT,
+            "h2d_bytes_per_step": 2 * per * mb, "d2h_bytes_per_step": 2 * per * mb,
+            "ms_per_step": round(ms / args.steps, 3),
+            "path": "MoELayer.forward_backward with pinned host x/dy in, y/dx out (copy stream overlapped)"}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=str(ROOT / "configs" / "mixtral_layer.yaml"))
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    from paper_2605_11005_b200.config import load_experiment
+    from paper_2605_11005_b200.moe import MoEShape
+
+    exp = load_experiment(args.config)
+    shape = MoEShape.from_experiment(exp)
+    if args.impl == "reference":
+        return run_reference(args, shape, exp)
+    return run_ours(args, shape, exp)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

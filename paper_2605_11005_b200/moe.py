@@ -1,0 +1,285 @@
+"""The MoE layer hot path on B200: dispatch -> SwiGLU experts -> combine, fwd + bwd.
+
+Stage split follows the AF-Pipe task boundaries of the reference DAG
+(/root/reference/pkg/src/afpipe/taskgraph.py:307-356):
+
+    A side (attention ranks)           F side (FFN ranks)
+    a_dispatch      (A FwdCompute tail) f_forward   (F FwdCompute, :333-334)
+    a_combine       (A FwdCompute head of the next visit, fed by the N2M recv :335-339)
+    a_combine_bwd   (A BwdCompute)      f_backward  (F BwdCompute, :346-347)
+    a_dispatch_bwd  (A BwdCompute, after the recv of :348-349)
+
+Every stage is a fixed sequence of dm_* kernel launches on one CUDA stream
+with no host synchronisation: per-expert sizes stay on the device (pad_off),
+buffers are pre-sized to dm_capacity_rows(). There is no CPU fallback — a
+missing libdm_moe.so raises at construction.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from . import kernels as K
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+I32 = torch.int32
+
+
+@dataclass(frozen=True)
+class MoEShape:
+    """T tokens per micro-batch, hidden H, E experts, top-k, expert hidden D_e."""
+
+    T: int
+    H: int
+    E: int
+    k: int
+    De: int
+
+    @property
+    def R(self) -> int:
+        return self.T * self.k
+
+    @property
+    def cap(self) -> int:
+        return _lib.capacity_rows(self.T, self.E, self.k)
+
+    def validate(self) -> None:
+        if self.H % 256 or self.De % 256:
+            raise ValueError(f"hidden ({self.H}) and moe_hidden ({self.De}) must be multiples of 256")
+        if not (1 <= self.k <= min(self.E, _lib.DM_MAX_TOPK)):
+            raise ValueError(f"topk {self.k} out of range for E={self.E}")
+        if self.E > _lib.DM_MAX_EXPERTS:
+            raise ValueError(f"experts {self.E} > {_lib.DM_MAX_EXPERTS}")
+
+    # Algorithmic work: GEMM FLOPs and HBM bytes per micro-batch.
+    def gemm_flops_fwd(self) -> int:
+        return 6 * self.R * self.H * self.De
+
+    def gemm_flops_bwd(self) -> int:
+        return 12 * self.R * self.H * self.De
+
+    def hbm_bytes(self) -> dict[str, int]:
+        T, H, R, e = self.T, self.H, self.R, 2
+        return {
+            "dispatch": T * H * e + R * H * e + 8 * R,
+            "combine_fwd": R * H * e + 4 * R + T * H * e,
+            "combine_bwd": T * H * e + 2 * R * H * e + 4 * R,
+            "permute_bwd": R * H * e + T * H * e,
+        }
+
+    @classmethod
+    def from_experiment(cls, exp) -> "MoEShape":
+        m = exp.model
+        return cls(T=exp.workload.seq_len * exp.workload.micro_batch, H=m.hidden, E=m.experts,
+                   k=m.topk, De=m.moe_hidden)
+
+
+def interleave_w13(w1: torch.Tensor, w3: torch.Tensor, block: int = 128) -> torch.Tensor:
+    """[E, D_e, H] gate + up -> [E, 2*D_e, H] with 128-row gate/up blocks (dm_moe.h)."""
+    E, De, H = w1.shape
+    out = torch.empty(E, 2 * De, H, dtype=w1.dtype, device=w1.device)
+    v = out.view(E, De // block, 2, block, H)
+    v[:, :, 0] = w1.view(E, De // block, block, H)
+    v[:, :, 1] = w3.view(E, De // block, block, H)
+    return out
+
+
+def split_w13(w13: torch.Tensor, block: int = 128) -> tuple[torch.Tensor, torch.Tensor]:
+    E, two_de, H = w13.shape
+    v = w13.view(E, two_de // (2 * block), 2, block, H)
+    return v[:, :, 0].reshape(E, two_de // 2, H), v[:, :, 1].reshape(E, two_de // 2, H)
+
+
+class RouterParams:
+    """A-side parameters: W_g fp32 [E, H] and its gradient."""
+
+    def __init__(self, wg: torch.Tensor):
+        self.wg = wg.contiguous()
+        self.dwg = torch.zeros_like(self.wg)
+
+
+class ExpertParams:
+    """F-side parameters for a block of experts: W13 [E,2D_e,H], W2 [E,H,D_e] bf16,
+    fp32 gradients dW13 / dW2 (accumulated across micro-batches with beta=1)."""
+
+    def __init__(self, w13: torch.Tensor, w2: torch.Tensor):
+        self.w13 = w13.contiguous()
+        self.w2 = w2.contiguous()
+        self.dw13 = torch.zeros(self.w13.shape, dtype=F32, device=w13.device)
+        self.dw2 = torch.zeros(self.w2.shape, dtype=F32, device=w2.device)
+
+    @property
+    def num_experts(self) -> int:
+        return self.w13.shape[0]
+
+
+class MicroBatchBuffers:
+    """Device buffers of one in-flight micro-batch (both sides on the fused path)."""
+
+    def __init__(self, shape: MoEShape, device, a_side: bool = True, f_side: bool = True,
+                 f_experts: int | None = None, f_rows: int | None = None):
+        s = shape
+        dev = torch.device(device)
+        cap = s.cap if f_rows is None else f_rows
+        z = lambda *sh, dt=BF16: torch.empty(*sh, dtype=dt, device=dev)  # noqa: E731
+        self.shape = s
+        self.cap = cap
+        E = s.E
+        # routing metadata (A produces, both use)
+        self.counts = z(E, dt=I32)
+        self.pad_off = z(E + 1, dt=I32)
+        if a_side:
+            self.x = z(s.T, s.H)
+            self.idx = z(s.T, s.k, dt=I32)
+            self.w = z(s.T, s.k, dt=F32)
+            self.row_map = z(s.T, s.k, dt=I32)
+            self.src = z(s.cap, dt=I32)
+            self.route_ws = z(_lib.route_workspace_size(s.T, s.H, s.E, s.k), dt=torch.uint8)
+            self.wgrad_ws = z(_lib.router_wgrad_workspace_size(s.T, s.H, s.E) // 4, dt=F32)
+            self.y = z(s.T, s.H)
+            self.dy = z(s.T, s.H)
+            self.dw = z(s.T, s.k, dt=F32)
+            self.dlogit = z(s.T, s.k, dt=F32)
+            self.dx = z(s.T, s.H)
+        # permuted rows: x_perm / y_perm / dy_perm / dx_perm exist on both sides
+        self.x_perm = z(cap, s.H)
+        self.y_perm = z(cap, s.H)
+        self.dy_perm = z(cap, s.H)
+        self.dx_perm = z(cap, s.H)
+        if f_side:
+            self.h13 = z(cap, 2 * s.De)
+            self.act = z(cap, s.De)
+            self.dh13 = z(cap, 2 * s.De)
+            if f_experts is not None and f_experts != E:
+                self.f_pad_off = z(f_experts + 1, dt=I32)
+
+
+# ---------------------------------------------------------------- stages
+def a_dispatch(buf: MicroBatchBuffers, router: RouterParams, stream=None) -> None:
+    s = buf.shape
+    K.route_and_dispatch(buf.x, router.wg, s.k, buf.route_ws, buf.idx, buf.w, buf.counts, buf.pad_off,
+                         buf.row_map, buf.src, buf.x_perm, stream)
+
+
+def f_forward(buf: MicroBatchBuffers, experts: ExpertParams, pad_off=None, stream=None) -> None:
+    po = buf.pad_off if pad_off is None else pad_off
+    K.w13_swiglu_fwd(buf.x_perm, experts.w13, po, buf.h13, buf.act, stream)
+    K.w2_fwd(buf.act, experts.w2, po, buf.y_perm, stream)
+
+
+def a_combine(buf: MicroBatchBuffers, stream=None) -> None:
+    K.combine_fwd(buf.y_perm, buf.row_map, buf.w, buf.y, stream)
+
+
+def a_combine_bwd(buf: MicroBatchBuffers, stream=None) -> None:
+    K.combine_bwd(buf.dy, buf.y_perm, buf.row_map, buf.w, buf.counts, buf.pad_off, buf.dy_perm, buf.dw,
+                  buf.dlogit, stream)
+
+
+def f_backward(buf: MicroBatchBuffers, experts: ExpertParams, accumulate: bool, pad_off=None,
+               stream=None) -> None:
+    po = buf.pad_off if pad_off is None else pad_off
+    beta = 1.0 if accumulate else 0.0
+    K.w2_dgrad_swiglu_bwd(buf.dy_perm, experts.w2, buf.h13, po, buf.dh13, stream)
+    K.w13_dgrad(buf.dh13, experts.w13, po, buf.dx_perm, stream)
+    K.wgrad(buf.dy_perm, buf.act, po, experts.dw2, beta, stream)
+    K.wgrad(buf.dh13, buf.x_perm, po, experts.dw13, beta, stream)
+
+
+def a_dispatch_bwd(buf: MicroBatchBuffers, router: RouterParams, accumulate: bool, stream=None) -> None:
+    K.permute_bwd(buf.dx_perm, buf.row_map, buf.idx, buf.dlogit, router.wg, buf.dx, stream)
+    K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws, router.dwg, 1.0 if accumulate else 0.0, stream)
+
+
+class MoELayer:
+    """Fused single-device MoE layer (1 GPU: A and F stages on one device).
+
+    `forward_backward(x, dy, accumulate)` runs one micro-batch fwd + bwd and
+    leaves y / dx in the buffers and gradients in the parameter objects.
+    """
+
+    def __init__(self, shape: MoEShape, wg: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor,
+                 device="cuda", num_buffers: int = 1):
+        shape.validate()
+        _lib.load()  # fail loudly if the sm_100a library is absent
+        self.shape = shape
+        self.device = torch.device(device)
+        self.router = RouterParams(wg.to(self.device, F32))
+        self.experts = ExpertParams(w13.to(self.device, BF16), w2.to(self.device, BF16))
+        self.buffers = [MicroBatchBuffers(shape, self.device) for _ in range(num_buffers)]
+
+    @classmethod
+    def random(cls, shape: MoEShape, device="cuda", seed: int = 0, num_buffers: int = 1) -> "MoELayer":
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        wg = torch.randn(shape.E, shape.H, generator=g) * 0.02
+        dev = torch.device(device)
+        w13 = torch.empty(shape.E, 2 * shape.De, shape.H, dtype=BF16, device=dev)
+        w2 = torch.empty(shape.E, shape.H, shape.De, dtype=BF16, device=dev)
+        gd = torch.Generator(device=dev).manual_seed(seed + 1)
+        w13.normal_(0.0, 0.02, generator=gd)
+        w2.normal_(0.0, 0.02, generator=gd)
+        return cls(shape, wg, w13, w2, device, num_buffers)
+
+    def forward(self, buf: MicroBatchBuffers, stream=None) -> None:
+        a_dispatch(buf, self.router, stream)
+        f_forward(buf, self.experts, stream=stream)
+        a_combine(buf, stream)
+
+    def backward(self, buf: MicroBatchBuffers, accumulate: bool, stream=None) -> None:
+        a_combine_bwd(buf, stream)
+        f_backward(buf, self.experts, accumulate, stream=stream)
+        a_dispatch_bwd(buf, self.router, accumulate, stream)
+
+    def forward_backward(self, buf: MicroBatchBuffers, accumulate: bool = False, stream=None) -> None:
+        self.forward(buf, stream)
+        self.backward(buf, accumulate, stream)
+
+    def zero_grad(self) -> None:
+        self.router.dwg.zero_()
+        self.experts.dw13.zero_()
+        self.experts.dw2.zero_()
+
+    launches_per_microbatch = 15  # 4 dispatch + 2 fwd GEMM + 1 combine + 1 combine_bwd + 4 bwd GEMM + 3
+
+
+class MoEFunction(torch.autograd.Function):
+    """autograd entry point: y = MoE(x; W_g, W13, W2) on one device.
+
+    Gradients: dx (bf16), dW_g / dW13 / dW2 (fp32, same shapes as the weights).
+    """
+
+    @staticmethod
+    def forward(ctx, x, wg, w13, w2, k: int):
+        T, H = x.shape
+        E, two_de, _ = w13.shape
+        shape = MoEShape(T=T, H=H, E=E, k=k, De=two_de // 2)
+        shape.validate()
+        buf = MicroBatchBuffers(shape, x.device)
+        buf.x.copy_(x)
+        router = RouterParams(wg.detach().float().contiguous())
+        experts = ExpertParams.__new__(ExpertParams)
+        experts.w13, experts.w2 = w13.detach().contiguous(), w2.detach().contiguous()
+        a_dispatch(buf, router)
+        f_forward(buf, experts)
+        a_combine(buf)
+        ctx.buf, ctx.router, ctx.experts = buf, router, experts
+        return buf.y.clone()
+
+    @staticmethod
+    def backward(ctx, dy):
+        buf, router, experts = ctx.buf, ctx.router, ctx.experts
+        experts.dw13 = torch.empty(experts.w13.shape, dtype=F32, device=dy.device)
+        experts.dw2 = torch.empty(experts.w2.shape, dtype=F32, device=dy.device)
+        buf.dy.copy_(dy.to(BF16))
+        a_combine_bwd(buf)
+        f_backward(buf, experts, accumulate=False)
+        a_dispatch_bwd(buf, router, accumulate=False)
+        return buf.dx.clone(), router.dwg, experts.dw13, experts.dw2, None
+
+
+def moe(x: torch.Tensor, wg: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor, k: int) -> torch.Tensor:
+    return MoEFunction.apply(x, wg, w13, w2, k)
