@@ -189,7 +189,7 @@ def run_ours(args, shape, exp):
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     mb = exp.workload.num_microbatches
-    layer = MoELayer.random(shape, device=dev, seed=1234 + rank, num_buffers=2)
+    layer = MoELayer.random(shape, device=dev, seed=1234 + rank, num_buffers=mb)
     stream = torch.cuda.current_stream(dev)
     for b in layer.buffers:
         b.x.normal_()
@@ -212,18 +212,19 @@ def run_ours(args, shape, exp):
             return sum(s.elapsed_time(e) for s, e in self.pairs[name])
 
     def step(ev=None):
+        if ev is None:
+            layer.iteration(mb)
+            return
         for i in range(mb):
-            buf = layer.buffers[i % 2]
+            buf = layer.buffers[i]
             acc = i > 0
-            if ev is None:
-                layer.forward_backward(buf, accumulate=acc)
-                continue
             ev.mark("dispatch", lambda: a_dispatch(buf, layer.router))
             ev.mark("gemm", lambda: f_forward(buf, layer.experts))
             ev.mark("combine_fwd", lambda: a_combine(buf))
             ev.mark("combine_bwd", lambda: a_combine_bwd(buf))
-            ev.mark("gemm", lambda: f_backward(buf, layer.experts, acc))
+            ev.mark("gemm", lambda: f_backward(buf, layer.experts, acc, defer_wgrad=True))
             ev.mark("permute_bwd", lambda: a_dispatch_bwd(buf, layer.router, acc))
+        ev.mark("gemm", lambda: layer.wgrad(mb))
 
     for _ in range(args.warmup):
         step()
@@ -288,7 +289,7 @@ def run_ours(args, shape, exp):
             "D_e": shape.De, "microbatches": mb, "tokens_per_step": mb * shape.T * world,
             "parallelism": "fused single-device (A+F on one GPU)" if world == 1 else f"replicas x{world}",
             "weights": "random-init", "l2": "inputs+weights (2.8 GB) larger than L2 (126 MB)",
-            "wgrad": "fp32, accumulated across micro-batches",
+            "wgrad": "fp32, deferred: one grouped GEMM per iteration over all micro-batches (K = mb*T*k rows)",
         },
         "roofline": {
             "bound": "tensor", "kernel": "grouped expert GEMMs (K4/K5/K8, 6 launches per micro-batch)",
@@ -329,26 +330,22 @@ def run_e2e(args, layer, shape, mb, dev, world):
     def step():
         loaded = [torch.cuda.Event() for _ in range(mb)]
         done = [torch.cuda.Event() for _ in range(mb)]
-        freed = [torch.cuda.Event() for _ in range(mb)]
+        copy.wait_stream(comp)  # previous step finished with the input buffers
         with torch.cuda.stream(copy):
-            for i in range(min(2, mb)):
-                bufs[i % 2].x.copy_(hx[i], non_blocking=True)
-                bufs[i % 2].dy.copy_(hdy[i], non_blocking=True)
+            for i in range(mb):
+                bufs[i].x.copy_(hx[i], non_blocking=True)
+                bufs[i].dy.copy_(hdy[i], non_blocking=True)
                 loaded[i].record(copy)
         for i in range(mb):
-            b = bufs[i % 2]
+            b = bufs[i]
             comp.wait_event(loaded[i])
-            layer.forward_backward(b, accumulate=i > 0)
+            layer.forward_backward(b, accumulate=i > 0, defer_wgrad=True)
             done[i].record(comp)
             with torch.cuda.stream(copy):
                 copy.wait_event(done[i])
                 hy[i].copy_(b.y, non_blocking=True)
                 hdx[i].copy_(b.dx, non_blocking=True)
-                freed[i].record(copy)
-                if i + 2 < mb:
-                    bufs[i % 2].x.copy_(hx[i + 2], non_blocking=True)
-                    bufs[i % 2].dy.copy_(hdy[i + 2], non_blocking=True)
-                    loaded[i + 2].record(copy)
+        layer.wgrad(mb)
         comp.wait_stream(copy)
 
     for _ in range(max(1, args.warmup)):

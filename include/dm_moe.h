@@ -64,7 +64,6 @@ extern "C" {
 #define DM_ROW_ALIGN 128        /* expert block alignment in permuted buffers   */
 #define DM_MAX_TOPK 16
 #define DM_MAX_EXPERTS 1024
-#define DM_WGRAD_TOKEN_BLOCK 512
 
 static inline int dm_num_chunks(int T) { return (T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS; }
 
@@ -99,8 +98,13 @@ static inline void dm_route_workspace_layout(int T, int H, int E, int k, void* w
   out->chunk_base = (int32_t*)p;
 }
 
+/* Tokens per router-wgrad partial block: small blocks (more parallelism) when the
+ * per-block partials are small, i.e. for few experts. */
+static inline int dm_router_wgrad_token_block(int E) { return E <= 16 ? 64 : 512; }
+
 static inline size_t dm_router_wgrad_workspace_size(int T, int H, int E) {
-  size_t ntb = (size_t)((T + DM_WGRAD_TOKEN_BLOCK - 1) / DM_WGRAD_TOKEN_BLOCK);
+  int tb = dm_router_wgrad_token_block(E);
+  size_t ntb = (size_t)((T + tb - 1) / tb);
   return ntb * (size_t)E * (size_t)H * 4;
 }
 
@@ -149,10 +153,15 @@ DM_API int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, c
 /* dx_perm = dh13 . W13_e */
 DM_API int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* pad_off, int E,
                          int cap_rows, int H, int De, void* dx_perm, void* stream);
-/* dW[e] (fp32 [M, N]) = a_tok[rows_e, :M]^T . b_tok[rows_e, :N] + beta * dW[e].
- * dW2 = wgrad(dy_perm, M=H, act, N=D_e); dW13 = wgrad(dh13, M=2*D_e, x_perm, N=H). */
-DM_API int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* pad_off,
-                     int E, int cap_rows, float* dW, float beta, void* stream);
+/* dW[e] (fp32 [M, N]) = sum over segments i < nseg of
+ *   a_tok[rows_{i,e}, :M]^T . b_tok[rows_{i,e}, :N]   (+ beta * dW[e]),
+ * rows_{i,e} = i*seg_rows + [seg_off[i*(E+1)+e], seg_off[i*(E+1)+e+1]).
+ * a_tok / b_tok hold nseg stacked per-micro-batch buffers of seg_rows rows each,
+ * so one launch reduces an expert's gradient over every micro-batch of an
+ * iteration (deferred weight-gradient pass). dW2 = wgrad(dy_perm, M=H, act, N=D_e);
+ * dW13 = wgrad(dh13, M=2*D_e, x_perm, N=H). */
+DM_API int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* seg_off,
+                            int nseg, int E, int seg_rows, float* dW, float beta, void* stream);
 
 /* ---- combine (A side) ------------------------------------------------- */
 DM_API int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,

@@ -18,7 +18,6 @@ DM_CHUNK_TOKENS = 32
 DM_ROW_ALIGN = 128
 DM_MAX_TOPK = 16
 DM_MAX_EXPERTS = 1024
-DM_WGRAD_TOKEN_BLOCK = 512
 
 
 class DMError(RuntimeError):
@@ -59,7 +58,7 @@ SIGNATURES: dict[str, tuple] = {
     "dm_grouped_w2_fwd": (_i, [_vp, _vp, _i32p, _i, _i, _i, _i, _vp, _vp]),
     "dm_grouped_w2_dgrad_swiglu_bwd": (_i, [_vp, _vp, _vp, _i32p, _i, _i, _i, _i, _vp, _vp]),
     "dm_grouped_w13_dgrad": (_i, [_vp, _vp, _i32p, _i, _i, _i, _i, _vp, _vp]),
-    "dm_grouped_wgrad": (_i, [_vp, _i, _vp, _i, _i32p, _i, _i, _f32p, _f, _vp]),
+    "dm_grouped_wgrad": (_i, [_vp, _i, _vp, _i, _i32p, _i, _i, _i, _f32p, _f, _vp]),
     "dm_combine_fwd": (_i, [_vp, _i32p, _f32p, _i, _i, _i, _vp, _vp]),
     "dm_combine_bwd": (_i, [_vp, _vp, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _i, _vp, _f32p,
                             _f32p, _vp]),
@@ -124,6 +123,11 @@ def route_workspace_size(T: int, H: int, E: int, k: int) -> int:
     return a(T * E * 4) + 2 * a(nch * E * 4)
 
 
+def router_wgrad_token_block(E: int) -> int:
+    return 64 if E <= 16 else 512
+
+
 def router_wgrad_workspace_size(T: int, H: int, E: int) -> int:
-    ntb = (T + DM_WGRAD_TOKEN_BLOCK - 1) // DM_WGRAD_TOKEN_BLOCK
+    tb = router_wgrad_token_block(E)
+    ntb = (T + tb - 1) // tb
     return ntb * E * H * 4

@@ -149,17 +149,60 @@ permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __r
   }
 }
 
-// Router weight gradient, stage 1: partial[tb][e][h] = sum over the token
-// block's (t, j) with idx == e of dlogit[t,j] * x[t,h]; thread per column.
+// Router weight gradient, stage 1 (E <= 16): warp per (256-column chunk, token
+// block); each lane owns 8 columns and keeps acc[E][8] in registers, reading x
+// with 128-bit loads. gw[e] = dlogit[t,j] when idx[t,j] == e (each expert appears
+// at most once per token), accumulated over the block's tokens in ascending order.
+template <int EM>
+__global__ void __launch_bounds__(256)
+router_wgrad_reg_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
+                        const float* __restrict__ dlogit, int T, int H, int E, int k, int tb_tokens,
+                        float* __restrict__ partial) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = ((blockIdx.x * (blockDim.x >> 5) + warp) * 32 + lane) * 8;
+  if (col >= H) return;
+  const int tb = blockIdx.y;
+  const int t_beg = tb * tb_tokens, t_end = min(T, t_beg + tb_tokens);
+  float acc[EM][8];
+#pragma unroll
+  for (int e = 0; e < EM; ++e)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[e][i] = 0.0f;
+#pragma unroll 4
+  for (int t = t_beg; t < t_end; ++t) {
+    float xf[8];
+    unpack8(ld_nc_v4(x + (size_t)t * H + col), xf);
+    float gw[EM];
+#pragma unroll
+    for (int e = 0; e < EM; ++e) gw[e] = 0.0f;
+    for (int j = 0; j < k; ++j) {
+      const int ej = idx[(size_t)t * k + j];
+      const float dl = dlogit[(size_t)t * k + j];
+#pragma unroll
+      for (int e = 0; e < EM; ++e) gw[e] = (ej == e) ? dl : gw[e];
+    }
+#pragma unroll
+    for (int e = 0; e < EM; ++e)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[e][i] = __fmaf_rn(gw[e], xf[i], acc[e][i]);
+  }
+  for (int e = 0; e < E && e < EM; ++e) {
+    float4* o = reinterpret_cast<float4*>(partial + ((size_t)tb * E + e) * H + col);
+    o[0] = make_float4(acc[e][0], acc[e][1], acc[e][2], acc[e][3]);
+    o[1] = make_float4(acc[e][4], acc[e][5], acc[e][6], acc[e][7]);
+  }
+}
+
+// Router weight gradient, stage 1 (any E): thread per column, accumulators in smem.
 __global__ void router_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
                                             const int32_t* __restrict__ idx,
                                             const float* __restrict__ dlogit, int T, int H, int E,
-                                            int k, float* __restrict__ partial) {
+                                            int k, int tb_tokens, float* __restrict__ partial) {
   extern __shared__ float s_acc[];  // [E][blockDim.x]
   const int cw = blockDim.x;
   const int h = blockIdx.x * cw + threadIdx.x;
   const int tb = blockIdx.y;
-  const int t_beg = tb * DM_WGRAD_TOKEN_BLOCK, t_end = min(T, t_beg + DM_WGRAD_TOKEN_BLOCK);
+  const int t_beg = tb * tb_tokens, t_end = min(T, t_beg + tb_tokens);
   for (int e = 0; e < E; ++e) s_acc[e * cw + threadIdx.x] = 0.0f;
   if (h < H) {
     for (int t = t_beg; t < t_end; ++t) {
@@ -176,10 +219,19 @@ __global__ void router_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
 
 __global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, int ntb, size_t EH,
                                            float* __restrict__ dwg, float beta) {
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < EH; i += (size_t)gridDim.x * blockDim.x) {
-    float s = 0.0f;
-    for (int tb = 0; tb < ntb; ++tb) s += partial[(size_t)tb * EH + i];
-    dwg[i] = beta != 0.0f ? s + beta * dwg[i] : s;
+  for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < EH;
+       i += (size_t)gridDim.x * blockDim.x * 4) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int tb = 0; tb < ntb; ++tb) {
+      const float4 v = *reinterpret_cast<const float4*>(partial + (size_t)tb * EH + i);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    float4* o = reinterpret_cast<float4*>(dwg + i);
+    if (beta != 0.0f) {
+      const float4 old = *o;
+      s.x += beta * old.x; s.y += beta * old.y; s.z += beta * old.z; s.w += beta * old.w;
+    }
+    *o = s;
   }
 }
 
@@ -236,27 +288,41 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
                     int k, float* partial_ws, float* dwg, float beta, void* stream) {
   if (T < 1 || H % 8 || E < 1 || E > DM_MAX_EXPERTS || k < 1 || k > DM_MAX_TOPK)
     return set_error(DM_ERR_SHAPE, "router_wgrad bad shape");
-  int cw = 128;
-  while (cw > 32 && (size_t)E * cw * sizeof(float) > 96 * 1024) cw >>= 1;
-  const size_t smem = (size_t)E * cw * sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(router_wgrad_partial_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router_wgrad)");
-    configured = true;
+  if (((size_t)E * H) % 4 || reinterpret_cast<uintptr_t>(dwg) & 15 || reinterpret_cast<uintptr_t>(partial_ws) & 15)
+    return set_error(DM_ERR_ALIGN, "router_wgrad needs 16-byte aligned fp32 buffers");
+  const int tbt = dm_router_wgrad_token_block(E);
+  const int ntb = (T + tbt - 1) / tbt;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (E <= 16) {
+    dim3 grid((H / 8 + 255) / 256, ntb);
+    if (E <= 8)
+      router_wgrad_reg_kernel<8><<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
+                                                       T, H, E, k, tbt, partial_ws);
+    else
+      router_wgrad_reg_kernel<16><<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
+                                                        T, H, E, k, tbt, partial_ws);
+  } else {
+    int cw = 128;
+    while (cw > 32 && (size_t)E * cw * sizeof(float) > 96 * 1024) cw >>= 1;
+    const size_t smem = (size_t)E * cw * sizeof(float);
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(router_wgrad_partial_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router_wgrad)");
+      configured = true;
+    }
+    dim3 grid((H + cw - 1) / cw, ntb);
+    router_wgrad_partial_kernel<<<grid, cw, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
+                                                       T, H, E, k, tbt, partial_ws);
   }
-  const int ntb = (T + DM_WGRAD_TOKEN_BLOCK - 1) / DM_WGRAD_TOKEN_BLOCK;
-  dim3 grid((H + cw - 1) / cw, ntb);
-  router_wgrad_partial_kernel<<<grid, cw, smem, (cudaStream_t)stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit, T, H, E, k, partial_ws);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_partial launch");
   note_launch();
   const size_t EH = (size_t)E * H;
-  int rblocks = (int)((EH + 255) / 256);
+  int rblocks = (int)((EH / 4 + 255) / 256);
   if (rblocks > num_sms_current() * 4) rblocks = num_sms_current() * 4;
-  router_wgrad_reduce_kernel<<<rblocks, 256, 0, (cudaStream_t)stream>>>(partial_ws, ntb, EH, dwg, beta);
+  router_wgrad_reduce_kernel<<<rblocks, 256, 0, st>>>(partial_ws, ntb, EH, dwg, beta);
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_reduce launch");
   note_launch();

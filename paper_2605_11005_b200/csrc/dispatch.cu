@@ -134,21 +134,21 @@ router_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int32_
   for (int i = threadIdx.x; i < E; i += blockDim.x) chunk_hist[(size_t)blockIdx.x * E + i] = shist[i];
 }
 
-// One CTA: per-expert running sums over chunks (fixed chunk order), padded
-// offsets (each expert's block rounded up to DM_ROW_ALIGN rows), chunk bases.
+// One CTA, warp per expert: pass 1 sums the expert's chunk counts, thread 0
+// turns the totals into DM_ROW_ALIGN-padded block offsets, pass 2 writes the
+// exclusive per-chunk bases (warp shuffle scan, chunks in ascending order).
 __global__ void __launch_bounds__(1024)
 expert_scan_kernel(const int32_t* __restrict__ hist, int nchunk, int E, int32_t* __restrict__ counts,
                    int32_t* __restrict__ pad_off, int32_t* __restrict__ chunk_base) {
   __shared__ int s_off[DM_MAX_EXPERTS + 1];
   __shared__ int s_cnt[DM_MAX_EXPERTS];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int run = 0;
-    for (int c = 0; c < nchunk; ++c) {
-      chunk_base[(size_t)c * E + e] = run;
-      run += hist[(size_t)c * E + e];
-    }
-    s_cnt[e] = run;
-    counts[e] = run;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int e = warp; e < E; e += nwarps) {
+    int tot = 0;
+    for (int c = lane; c < nchunk; c += 32) tot += hist[(size_t)c * E + e];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+    if (lane == 0) { s_cnt[e] = tot; counts[e] = tot; }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -161,7 +161,21 @@ expert_scan_kernel(const int32_t* __restrict__ hist, int nchunk, int E, int32_t*
   }
   __syncthreads();
   for (int e = threadIdx.x; e <= E; e += blockDim.x) pad_off[e] = s_off[e];
-  for (int i = threadIdx.x; i < nchunk * E; i += blockDim.x) chunk_base[i] += s_off[i % E];
+  for (int e = warp; e < E; e += nwarps) {
+    int run = s_off[e];
+    for (int c0 = 0; c0 < nchunk; c0 += 32) {
+      const int c = c0 + lane;
+      const int v = c < nchunk ? hist[(size_t)c * E + e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+      }
+      if (c < nchunk) chunk_base[(size_t)c * E + e] = run + incl - v;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
 }
 
 // Zero rows [pad_off[e] + counts[e], pad_off[e+1]) of a permuted buffer; the

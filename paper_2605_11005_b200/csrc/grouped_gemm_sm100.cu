@@ -46,6 +46,11 @@ struct GemmArgs {
   const __nv_bfloat16* aux_in;   // SwiGLU bwd: h13 in
   long long ld_aux_in;
   float beta;                    // EPI_F32: C = acc + beta * C
+  // ragged-K: group g's K rows are the union over segments i < nseg of
+  // [i*seg_stride_rows + seg_off[i*(G+1)+g], i*seg_stride_rows + seg_off[i*(G+1)+g+1])
+  const int* seg_off;
+  int nseg;
+  int seg_stride_rows;
 };
 
 struct TileInfo {
@@ -63,8 +68,8 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* tile_start, co
   TileInfo ti;
   ti.g = lo;
   const int local = t - tile_start[lo];
-  const int row_off = off[lo];
-  const int rows = off[lo + 1] - row_off;
+  const int row_off = RAGGED_K ? 0 : off[lo];
+  const int rows = RAGGED_K ? 0 : off[lo + 1] - row_off;
   ti.row_base = row_off;
   if (!RAGGED_K) {
     const int mt = rows / GBM;
@@ -75,7 +80,10 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* tile_start, co
     const int mt = a.M / GBM;
     ti.m0 = (local % mt) * GBM;
     ti.n0 = (local / mt) * GBN;
-    ti.kb_count = rows / GBK;
+    int kb = 0;
+    for (int i = 0; i < a.nseg; ++i)
+      kb += (a.seg_off[i * (G + 1) + lo + 1] - a.seg_off[i * (G + 1) + lo]) / GBK;
+    ti.kb_count = kb;
   }
   return ti;
 }
@@ -221,7 +229,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
   const int lane = threadIdx.x & 31;
   const int G = args.num_groups;
 
-  for (int i = threadIdx.x; i <= G; i += GEMM_THREADS) s_off[i] = args.group_off[i];
+  if (!RAGGED_K)
+    for (int i = threadIdx.x; i <= G; i += GEMM_THREADS) s_off[i] = args.group_off[i];
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < GSTAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -236,7 +245,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
     int acc = 0;
     for (int g = 0; g < G; ++g) {
       s_tile[g] = acc;
-      const int rows = s_off[g + 1] - s_off[g];
+      const int rows = RAGGED_K ? 0 : s_off[g + 1] - s_off[g];
       acc += RAGGED_K ? (args.M / GBM) * (args.N / GBN) : (rows / GBM) * (args.N / GBN);
     }
     s_tile[G] = acc;
@@ -255,12 +264,26 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         const TileInfo ti = decode_tile<RAGGED_K>(t, s_tile, s_off, G, args);
         const int b_gofs = RAGGED_K ? 0 : ti.g * args.b_group_rows;
+        int seg = 0, seg_kb = 0, seg_nkb = 0, seg_row0 = 0;
         for (int kb = 0; kb < ti.kb_count; ++kb) {
+          int kcoord;
+          if (RAGGED_K) {
+            while (seg_kb == seg_nkb) {  // advance to the next non-empty segment
+              const int* so = args.seg_off + seg * (G + 1) + ti.g;
+              seg_row0 = seg * args.seg_stride_rows + so[0];
+              seg_nkb = (so[1] - so[0]) / GBK;
+              seg_kb = 0;
+              ++seg;
+            }
+            kcoord = seg_row0 + seg_kb * GBK;
+            ++seg_kb;
+          } else {
+            kcoord = kb * GBK;
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], GA_BYTES + GB_BYTES);
           uint8_t* a_dst = sA + stage * GA_BYTES;
           uint8_t* b_dst = sB + stage * GB_BYTES;
-          const int kcoord = RAGGED_K ? ti.row_base + kb * GBK : kb * GBK;
           if (!A_MN) {
             tma_load_2d(a_dst, &tmA, &full[stage], kcoord, ti.m0);
           } else {
@@ -449,19 +472,22 @@ int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* pad_o
   return launch_gemm<0, 1, 0, EPI_BF16>(ta, tb, a, (cudaStream_t)stream);
 }
 
-int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* pad_off,
-                     int E, int cap_rows, float* dW, float beta, void* stream) {
-  int rc = check_groups(E, cap_rows);
+int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* seg_off,
+                     int nseg, int E, int seg_rows, float* dW, float beta, void* stream) {
+  int rc = check_groups(E, seg_rows);
   if (rc) return rc;
   if (M % GBM || N % GBN || M <= 0 || N <= 0)
     return set_error(DM_ERR_SHAPE, "wgrad needs M %% 128 == 0 and N %% 256 == 0 (M=%d, N=%d)", M, N);
+  if (nseg < 1 || nseg > 64) return set_error(DM_ERR_SHAPE, "wgrad segments %d outside [1, 64]", nseg);
   if (reinterpret_cast<uintptr_t>(dW) & 15) return set_error(DM_ERR_ALIGN, "dW not 16-byte aligned");
   CUtensorMap ta, tb;
-  if ((rc = make_tmap_bf16_2d(&ta, a_tok, M, cap_rows, M, 64, 64))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, b_tok, N, cap_rows, N, 64, 64))) return rc;
+  const uint64_t rows = (uint64_t)nseg * seg_rows;
+  if ((rc = make_tmap_bf16_2d(&ta, a_tok, M, rows, M, 64, 64))) return rc;
+  if ((rc = make_tmap_bf16_2d(&tb, b_tok, N, rows, N, 64, 64))) return rc;
   GemmArgs a{};
-  a.num_groups = E; a.group_off = pad_off; a.M = M; a.N = N;
+  a.num_groups = E; a.group_off = seg_off; a.M = M; a.N = N;
   a.C = dW; a.ldc = N; a.c_group_stride = (long long)M * N; a.beta = beta;
+  a.seg_off = seg_off; a.nseg = nseg; a.seg_stride_rows = seg_rows;
   return launch_gemm<1, 1, 1, EPI_F32>(ta, tb, a, (cudaStream_t)stream);
 }
 

@@ -116,12 +116,20 @@ def w13_dgrad(dh13, w13, pad_off, dx_perm, stream=None):
               _ptr(dx_perm), _stream(stream))
 
 
-def wgrad(a_tok, b_tok, pad_off, dW, beta=0.0, stream=None):
-    cap, M = a_tok.shape
+def wgrad(a_tok, b_tok, seg_off, dW, beta=0.0, stream=None):
+    """dW[e] = sum over segments of a_tok[rows]^T b_tok[rows]; seg_off is [E+1] (one
+    segment) or [nseg, E+1] with a_tok / b_tok stacking nseg equal row blocks."""
+    rows, M = a_tok.shape
     _, N = b_tok.shape
-    E = pad_off.shape[0] - 1
+    so = seg_off if seg_off.dim() == 2 else seg_off.view(1, -1)
+    nseg, E1 = so.shape
+    E = E1 - 1
+    if rows % nseg:
+        raise ValueError("token buffers must stack nseg equal blocks")
+    if not so.is_contiguous():
+        raise ValueError("seg_off must be contiguous")
     _check(dW, torch.float32, (E, M, N), "dW")
-    _lib.call("dm_grouped_wgrad", _ptr(a_tok), M, _ptr(b_tok), N, _ptr(pad_off), E, cap, _ptr(dW),
+    _lib.call("dm_grouped_wgrad", _ptr(a_tok), M, _ptr(b_tok), N, _ptr(so), nseg, E, rows // nseg, _ptr(dW),
               float(beta), _stream(stream))
 
 

@@ -117,27 +117,58 @@ class ExpertParams:
         return self.w13.shape[0]
 
 
-class MicroBatchBuffers:
-    """Device buffers of one in-flight micro-batch (both sides on the fused path)."""
+class ActivationSlab:
+    """F-side activations of `n` micro-batches stacked in contiguous [n*cap, .] slabs.
 
-    def __init__(self, shape: MoEShape, device, a_side: bool = True, f_side: bool = True,
-                 f_experts: int | None = None, f_rows: int | None = None):
+    Micro-batch i owns rows [i*cap, (i+1)*cap) of every slab, and row i of the
+    [n, E+1] offset slab. Keeping a whole iteration resident (HBM is 180 GB) lets
+    the weight-gradient GEMM run once per iteration with K = all of its tokens
+    (dm_grouped_wgrad with nseg = n), instead of a fp32 read-modify-write of
+    dW per micro-batch.
+    """
+
+    def __init__(self, shape: MoEShape, n: int, device, rows: int | None = None, f_side: bool = True):
         s = shape
         dev = torch.device(device)
-        cap = s.cap if f_rows is None else f_rows
+        self.n = n
+        self.cap = s.cap if rows is None else rows
+        R = n * self.cap
+        e = lambda *sh, dt=BF16: torch.empty(*sh, dtype=dt, device=dev)  # noqa: E731
+        self.pad_off = torch.zeros(n, s.E + 1, dtype=I32, device=dev)
+        self.x_perm = e(R, s.H)
+        self.y_perm = e(R, s.H)
+        self.dy_perm = e(R, s.H)
+        self.dx_perm = e(R, s.H)
+        if f_side:
+            self.h13 = e(R, 2 * s.De)
+            self.act = e(R, s.De)
+            self.dh13 = e(R, 2 * s.De)
+
+    def rows(self, i: int) -> slice:
+        return slice(i * self.cap, (i + 1) * self.cap)
+
+
+class MicroBatchBuffers:
+    """Device buffers of one in-flight micro-batch; permuted/F-side tensors are
+    views into an ActivationSlab (both sides live on one device on the fused path)."""
+
+    def __init__(self, shape: MoEShape, device, slab: ActivationSlab, index: int, a_side: bool = True):
+        s = shape
+        dev = torch.device(device)
         z = lambda *sh, dt=BF16: torch.empty(*sh, dtype=dt, device=dev)  # noqa: E731
         self.shape = s
-        self.cap = cap
-        E = s.E
-        # routing metadata (A produces, both use)
-        self.counts = z(E, dt=I32)
-        self.pad_off = z(E + 1, dt=I32)
+        self.slab = slab
+        self.index = index
+        self.cap = slab.cap
+        rows = slab.rows(index)
+        self.counts = z(s.E, dt=I32)
+        self.pad_off = slab.pad_off[index]
         if a_side:
             self.x = z(s.T, s.H)
             self.idx = z(s.T, s.k, dt=I32)
             self.w = z(s.T, s.k, dt=F32)
             self.row_map = z(s.T, s.k, dt=I32)
-            self.src = z(s.cap, dt=I32)
+            self.src = z(slab.cap, dt=I32)
             self.route_ws = z(_lib.route_workspace_size(s.T, s.H, s.E, s.k), dt=torch.uint8)
             self.wgrad_ws = z(_lib.router_wgrad_workspace_size(s.T, s.H, s.E) // 4, dt=F32)
             self.y = z(s.T, s.H)
@@ -145,17 +176,14 @@ class MicroBatchBuffers:
             self.dw = z(s.T, s.k, dt=F32)
             self.dlogit = z(s.T, s.k, dt=F32)
             self.dx = z(s.T, s.H)
-        # permuted rows: x_perm / y_perm / dy_perm / dx_perm exist on both sides
-        self.x_perm = z(cap, s.H)
-        self.y_perm = z(cap, s.H)
-        self.dy_perm = z(cap, s.H)
-        self.dx_perm = z(cap, s.H)
-        if f_side:
-            self.h13 = z(cap, 2 * s.De)
-            self.act = z(cap, s.De)
-            self.dh13 = z(cap, 2 * s.De)
-            if f_experts is not None and f_experts != E:
-                self.f_pad_off = z(f_experts + 1, dt=I32)
+        self.x_perm = slab.x_perm[rows]
+        self.y_perm = slab.y_perm[rows]
+        self.dy_perm = slab.dy_perm[rows]
+        self.dx_perm = slab.dx_perm[rows]
+        if hasattr(slab, "h13"):
+            self.h13 = slab.h13[rows]
+            self.act = slab.act[rows]
+            self.dh13 = slab.dh13[rows]
 
 
 # ---------------------------------------------------------------- stages
@@ -181,13 +209,24 @@ def a_combine_bwd(buf: MicroBatchBuffers, stream=None) -> None:
 
 
 def f_backward(buf: MicroBatchBuffers, experts: ExpertParams, accumulate: bool, pad_off=None,
-               stream=None) -> None:
+               stream=None, defer_wgrad: bool = False) -> None:
+    """dgrad (always) and, unless deferred to f_wgrad, this micro-batch's wgrad."""
     po = buf.pad_off if pad_off is None else pad_off
-    beta = 1.0 if accumulate else 0.0
     K.w2_dgrad_swiglu_bwd(buf.dy_perm, experts.w2, buf.h13, po, buf.dh13, stream)
     K.w13_dgrad(buf.dh13, experts.w13, po, buf.dx_perm, stream)
-    K.wgrad(buf.dy_perm, buf.act, po, experts.dw2, beta, stream)
-    K.wgrad(buf.dh13, buf.x_perm, po, experts.dw13, beta, stream)
+    if not defer_wgrad:
+        beta = 1.0 if accumulate else 0.0
+        K.wgrad(buf.dy_perm, buf.act, po, experts.dw2, beta, stream)
+        K.wgrad(buf.dh13, buf.x_perm, po, experts.dw13, beta, stream)
+
+
+def f_wgrad(slab: ActivationSlab, n: int, experts: ExpertParams, accumulate: bool, stream=None) -> None:
+    """Deferred weight-gradient pass over micro-batches 0..n-1 of the slab."""
+    beta = 1.0 if accumulate else 0.0
+    rows = slice(0, n * slab.cap)
+    so = slab.pad_off[:n]
+    K.wgrad(slab.dy_perm[rows], slab.act[rows], so, experts.dw2, beta, stream)
+    K.wgrad(slab.dh13[rows], slab.x_perm[rows], so, experts.dw13, beta, stream)
 
 
 def a_dispatch_bwd(buf: MicroBatchBuffers, router: RouterParams, accumulate: bool, stream=None) -> None:
@@ -198,8 +237,9 @@ def a_dispatch_bwd(buf: MicroBatchBuffers, router: RouterParams, accumulate: boo
 class MoELayer:
     """Fused single-device MoE layer (1 GPU: A and F stages on one device).
 
-    `forward_backward(x, dy, accumulate)` runs one micro-batch fwd + bwd and
-    leaves y / dx in the buffers and gradients in the parameter objects.
+    `iteration(n)` runs micro-batches 0..n-1 fwd + bwd (dgrad) and then one
+    deferred weight-gradient pass; `forward_backward(buf)` is the one-micro-batch
+    form with the wgrad inline.
     """
 
     def __init__(self, shape: MoEShape, wg: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor,
@@ -210,7 +250,8 @@ class MoELayer:
         self.device = torch.device(device)
         self.router = RouterParams(wg.to(self.device, F32))
         self.experts = ExpertParams(w13.to(self.device, BF16), w2.to(self.device, BF16))
-        self.buffers = [MicroBatchBuffers(shape, self.device) for _ in range(num_buffers)]
+        self.slab = ActivationSlab(shape, num_buffers, self.device)
+        self.buffers = [MicroBatchBuffers(shape, self.device, self.slab, i) for i in range(num_buffers)]
 
     @classmethod
     def random(cls, shape: MoEShape, device="cuda", seed: int = 0, num_buffers: int = 1) -> "MoELayer":
@@ -229,21 +270,36 @@ class MoELayer:
         f_forward(buf, self.experts, stream=stream)
         a_combine(buf, stream)
 
-    def backward(self, buf: MicroBatchBuffers, accumulate: bool, stream=None) -> None:
+    def backward(self, buf: MicroBatchBuffers, accumulate: bool, stream=None, defer_wgrad: bool = False) -> None:
         a_combine_bwd(buf, stream)
-        f_backward(buf, self.experts, accumulate, stream=stream)
+        f_backward(buf, self.experts, accumulate, stream=stream, defer_wgrad=defer_wgrad)
         a_dispatch_bwd(buf, self.router, accumulate, stream)
 
-    def forward_backward(self, buf: MicroBatchBuffers, accumulate: bool = False, stream=None) -> None:
+    def forward_backward(self, buf: MicroBatchBuffers, accumulate: bool = False, stream=None,
+                         defer_wgrad: bool = False) -> None:
         self.forward(buf, stream)
-        self.backward(buf, accumulate, stream)
+        self.backward(buf, accumulate, stream, defer_wgrad)
+
+    def wgrad(self, n: int | None = None, accumulate: bool = False, stream=None) -> None:
+        f_wgrad(self.slab, len(self.buffers) if n is None else n, self.experts, accumulate, stream)
+
+    def iteration(self, n: int | None = None, accumulate: bool = False, stream=None) -> None:
+        """Micro-batches 0..n-1 (inputs already in buffers[i].x / .dy), then the W pass."""
+        n = len(self.buffers) if n is None else n
+        for i in range(n):
+            self.forward_backward(self.buffers[i], accumulate=accumulate or i > 0, stream=stream,
+                                  defer_wgrad=True)
+        self.wgrad(n, accumulate, stream)
 
     def zero_grad(self) -> None:
         self.router.dwg.zero_()
         self.experts.dw13.zero_()
         self.experts.dw2.zero_()
 
-    launches_per_microbatch = 15  # 4 dispatch + 2 fwd GEMM + 1 combine + 1 combine_bwd + 4 bwd GEMM + 3
+    # dispatch 4 + expert fwd 2 + combine 1 + combine_bwd 1 + dgrad 2 + permute_bwd 1 + router wgrad 2
+    launches_per_microbatch_deferred = 13
+    launches_per_microbatch = 15          # + 2 inline wgrad launches
+    launches_per_wgrad_pass = 2
 
 
 class MoEFunction(torch.autograd.Function):
@@ -258,7 +314,7 @@ class MoEFunction(torch.autograd.Function):
         E, two_de, _ = w13.shape
         shape = MoEShape(T=T, H=H, E=E, k=k, De=two_de // 2)
         shape.validate()
-        buf = MicroBatchBuffers(shape, x.device)
+        buf = MicroBatchBuffers(shape, x.device, ActivationSlab(shape, 1, x.device), 0)
         buf.x.copy_(x)
         router = RouterParams(wg.detach().float().contiguous())
         experts = ExpertParams.__new__(ExpertParams)

@@ -1,0 +1,28 @@
+"""One warm-up + N profiled steps of the fused Mixtral layer (for ncu launch lists)."""
+import argparse
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2605_11005_b200.config import load_experiment  # noqa: E402
+from paper_2605_11005_b200.moe import MoELayer, MoEShape  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="configs/mixtral_layer.yaml")
+ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--warmup", type=int, default=1)
+a = ap.parse_args()
+exp = load_experiment(a.config)
+shape = MoEShape.from_experiment(exp)
+layer = MoELayer.random(shape, device="cuda", seed=1, num_buffers=2)
+for b in layer.buffers:
+    b.x.normal_()
+    b.dy.normal_()
+mb = exp.workload.num_microbatches
+for s in range(a.warmup + a.steps):
+    for i in range(mb):
+        layer.forward_backward(layer.buffers[i % 2], accumulate=i > 0)
+torch.cuda.synchronize()
+print("ok")

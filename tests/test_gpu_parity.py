@@ -27,7 +27,7 @@ def to_dev_bf16(vals: np.ndarray, dev) -> torch.Tensor:
 
 
 def f32(t: torch.Tensor) -> np.ndarray:
-    return t.float().cpu().numpy()
+    return t.detach().float().cpu().numpy()
 
 
 def run_layer(dev, x, wg, w1, w3, w2, dy, k):
@@ -228,3 +228,49 @@ def test_launch_counter_moves(cuda):
     layer.forward_backward(layer.buffers[0])
     torch.cuda.synchronize()
     assert _lib.launch_count() - before == MoELayer.launches_per_microbatch
+    before = _lib.launch_count()
+    layer.iteration()
+    torch.cuda.synchronize()
+    assert _lib.launch_count() - before == MoELayer.launches_per_microbatch_deferred + MoELayer.launches_per_wgrad_pass
+
+
+def test_deferred_wgrad_equals_inline_accumulation(cuda):
+    """One W pass over a 3-micro-batch slab == per-micro-batch wgrad with beta=1."""
+    from paper_2605_11005_b200.moe import MoELayer, MoEShape
+
+    shape = MoEShape(T=300, H=512, E=8, k=2, De=256)
+    layer = MoELayer.random(shape, device=cuda, seed=3, num_buffers=3)
+    for b in layer.buffers:
+        b.x.normal_()
+        b.dy.normal_()
+    for i, b in enumerate(layer.buffers):
+        layer.forward_backward(b, accumulate=i > 0)
+    inline = (layer.experts.dw13.clone(), layer.experts.dw2.clone(), layer.router.dwg.clone())
+    layer.zero_grad()
+    layer.iteration()
+    torch.cuda.synchronize()
+    for a, b_ in zip(inline, (layer.experts.dw13, layer.experts.dw2, layer.router.dwg)):
+        assert O.normwise_rel_err(f32(b_), f32(a)) < 1e-5
+
+
+def test_iteration_matches_oracle_sum_over_microbatches(cuda):
+    from paper_2605_11005_b200.moe import MoELayer, MoEShape, interleave_w13, split_w13
+
+    T, H, E, k, De = 128, 256, 8, 2, 256
+    ins = [O.make_inputs(T, H, E, k, De, seed=40 + i) for i in range(2)]
+    x0, wg, w1, w3, w2, _ = ins[0]
+    layer = MoELayer(MoEShape(T, H, E, k, De), torch.from_numpy(wg),
+                     interleave_w13(to_dev_bf16(w1, cuda), to_dev_bf16(w3, cuda)), to_dev_bf16(w2, cuda),
+                     cuda, num_buffers=2)
+    dw1 = dw2 = 0
+    for i, (x, _, _, _, _, dy) in enumerate(ins):
+        layer.buffers[i].x.copy_(to_dev_bf16_bits(x, cuda))
+        layer.buffers[i].dy.copy_(to_dev_bf16(dy, cuda))
+        f = O.moe_forward(x, wg, w1, w3, w2, k)
+        b = O.moe_backward(f, x, wg, w1, w3, w2, dy)
+        dw1, dw2 = dw1 + b.dw1, dw2 + b.dw2
+    layer.iteration()
+    torch.cuda.synchronize()
+    g1, _ = split_w13(layer.experts.dw13)
+    assert O.normwise_rel_err(f32(g1), dw1) < TOL_BF16
+    assert O.normwise_rel_err(f32(layer.experts.dw2), dw2) < TOL_BF16
