@@ -360,7 +360,224 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
   if (warp == 2) tmem_dealloc(tmem_base, 512);
 }
 
+// ==================================================================== 2-SM path
+// CTA pair (cluster of 2) computing 256x256 output tiles with
+// tcgen05.mma.cta_group::2 (UMMA M=256): each CTA stages its 128 rows of A and
+// its 128 rows (N half) of B per k-block, so per-SM smem operand traffic is
+// 32 KiB per 256x256x64 step instead of 48 KiB per 128x256x64 step of the
+// 1-SM kernel. The leader (rank 0) issues all MMAs; both CTAs' TMEM hold their
+// 128 accumulator rows; each CTA's epilogue drains its own half.
+constexpr int G2_STAGES = 6;
+constexpr uint32_t G2_A_BYTES = 128 * GBK * 2;   // 16 KiB (this CTA's M half)
+constexpr uint32_t G2_B_BYTES = 128 * GBK * 2;   // 16 KiB (this CTA's N half)
+constexpr size_t GEMM2_SMEM_BYTES =
+    1024 + G2_STAGES * (G2_A_BYTES + G2_B_BYTES) + 256 + 2 * (GEMM_MAX_GROUPS + 1) * sizeof(int);
+
+template <int RAGGED_K>
+__device__ __forceinline__ TileInfo decode_tile_2sm(int t, const int* tile_start, const int* off, int G,
+                                                    const GemmArgs& a, uint32_t rank, bool& active) {
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_start[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  TileInfo ti;
+  ti.g = lo;
+  const int local = t - tile_start[lo];
+  if (!RAGGED_K) {
+    const int row_off = off[lo];
+    const int rows = off[lo + 1] - row_off;
+    const int mt = (rows + 255) / 256;
+    ti.m0 = row_off + (local % mt) * 256 + 128 * rank;   // this CTA's first row
+    ti.n0 = (local / mt) * GBN;
+    ti.kb_count = a.K / GBK;
+    ti.row_base = row_off;
+    active = ti.m0 < row_off + rows;
+  } else {
+    const int mt = a.M / 256;
+    ti.m0 = (local % mt) * 256 + 128 * rank;
+    ti.n0 = (local / mt) * GBN;
+    int kb = 0;
+    for (int i = 0; i < a.nseg; ++i)
+      kb += (a.seg_off[i * (G + 1) + lo + 1] - a.seg_off[i * (G + 1) + lo]) / GBK;
+    ti.kb_count = kb;
+    ti.row_base = 0;
+    active = true;
+  }
+  return ti;
+}
+
+template <int A_MN, int B_MN, int RAGGED_K, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + G2_STAGES * G2_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + G2_STAGES * G2_B_BYTES);
+  uint64_t* empty = full + G2_STAGES;
+  uint64_t* tfull = empty + G2_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_tile = reinterpret_cast<int*>(smem + G2_STAGES * (G2_A_BYTES + G2_B_BYTES) + 256);
+  int* s_off = s_tile + (GEMM_MAX_GROUPS + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int G = args.num_groups;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1;
+  const int num_clusters = gridDim.x >> 1;
+
+  if (!RAGGED_K)
+    for (int i = threadIdx.x; i <= G; i += GEMM_THREADS) s_off[i] = args.group_off[i];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < G2_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * 128); }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  __syncthreads();
+  if (threadIdx.x == 32 * 3) {
+    int acc = 0;
+    for (int g = 0; g < G; ++g) {
+      s_tile[g] = acc;
+      const int rows = RAGGED_K ? 0 : s_off[g + 1] - s_off[g];
+      acc += RAGGED_K ? (args.M / 256) * (args.N / GBN) : ((rows + 255) / 256) * (args.N / GBN);
+    }
+    s_tile[G] = acc;
+  }
+  tc_fence_before();
+  cluster_sync_all();   // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = s_tile[G];
+
+  if (warp == 0) {
+    // ------------------------------------------- TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster_id; t < total_tiles; t += num_clusters) {
+        bool active;
+        const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, G, args, rank, active);
+        const int b_gofs = RAGGED_K ? 0 : ti.g * args.b_group_rows;
+        const int nb0 = ti.n0 + 128 * (int)rank;   // this CTA's half of the N tile
+        int seg = 0, seg_kb = 0, seg_nkb = 0, seg_row0 = 0;
+        for (int kb = 0; kb < ti.kb_count; ++kb) {
+          int kcoord;
+          if (RAGGED_K) {
+            while (seg_kb == seg_nkb) {
+              const int* so = args.seg_off + seg * (G + 1) + ti.g;
+              seg_row0 = seg * args.seg_stride_rows + so[0];
+              seg_nkb = (so[1] - so[0]) / GBK;
+              seg_kb = 0;
+              ++seg;
+            }
+            kcoord = seg_row0 + seg_kb * GBK;
+            ++seg_kb;
+          } else {
+            kcoord = kb * GBK;
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], 2 * (G2_A_BYTES + G2_B_BYTES));
+          uint8_t* a_dst = sA + stage * G2_A_BYTES;
+          uint8_t* b_dst = sB + stage * G2_B_BYTES;
+          if (!A_MN) {
+            tma_load_2d_2sm(a_dst, &tmA, &full[stage], kcoord, ti.m0);
+          } else {
+            tma_load_2d_2sm(a_dst, &tmA, &full[stage], ti.m0, kcoord);
+            tma_load_2d_2sm(a_dst + 8192, &tmA, &full[stage], ti.m0 + 64, kcoord);
+          }
+          if (!B_MN) {
+            tma_load_2d_2sm(b_dst, &tmB, &full[stage], kcoord, b_gofs + nb0);
+          } else {
+            tma_load_2d_2sm(b_dst, &tmB, &full[stage], nb0, b_gofs + kcoord);
+            tma_load_2d_2sm(b_dst + 8192, &tmB, &full[stage], nb0 + 64, b_gofs + kcoord);
+          }
+          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(256, GBN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+        bool active;
+        const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, G, args, rank, active);
+        const int as = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * GBN;
+        for (int kb = 0; kb < ti.kb_count; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * G2_A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * G2_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < GBK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_sdesc_sw128(a_addr + k * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_sdesc_sw128(b_addr + k * 2048, 8192, 1024)
+                                     : make_sdesc_sw128(b_addr + k * 32, 16, 1024);
+            umma_bf16_ss_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit_2sm_mc(&empty[stage]);
+          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_2sm_mc(&tfull[as]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------- epilogue warps (both CTAs)
+    const int q = warp & 3;
+    int it = 0;
+    for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
+      bool active;
+      const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, G, args, rank, active);
+      const int as = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      if (active) {
+        const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * GBN;
+        epilogue_row<EPI>(ti, trow, q * 32 + lane, args);
+      }
+      tc_fence_before();
+      if (leader) mbar_arrive(&tempty[as]);
+      else mbar_arrive_cluster(&tempty[as], 0);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm(tmem_base, 512);
+}
+
 // ------------------------------------------------------------------- host side
+
+static bool use_2sm() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DM_GEMM_1SM");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 static int make_tmap_bf16_2d(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer,
                              uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
@@ -379,19 +596,52 @@ static int make_tmap_bf16_2d(CUtensorMap* tm, const void* base, uint64_t inner, 
   return DM_OK;
 }
 
+// Builds both operand maps for the chosen path: the 2-SM kernel stages a
+// 128-row half of the N tile per CTA, the 1-SM kernel the full 256 rows.
+struct GemmOperand {
+  const void* base;
+  uint64_t inner, outer, ld;
+  bool mn_major;
+  bool is_b;
+};
+
+static int make_operand_map(CUtensorMap* tm, const GemmOperand& o, bool two_sm) {
+  if (o.mn_major) return make_tmap_bf16_2d(tm, o.base, o.inner, o.outer, o.ld, 64, 64);
+  const uint32_t rows = (o.is_b && !two_sm) ? 256 : 128;
+  return make_tmap_bf16_2d(tm, o.base, o.inner, o.outer, o.ld, 64, rows);
+}
+
 template <int A_MN, int B_MN, int RAGGED_K, int EPI>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args,
+static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const GemmArgs& args,
                        cudaStream_t stream) {
-  auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)GEMM_SMEM_BYTES);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm smem)");
-    configured = true;
+  const bool two = use_2sm();
+  CUtensorMap ta, tb;
+  int rc;
+  if ((rc = make_operand_map(&ta, oa, two))) return rc;
+  if ((rc = make_operand_map(&tb, ob, two))) return rc;
+  int grid = num_sms_current();
+  if (two) {
+    auto kern = grouped_gemm_2sm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)GEMM2_SMEM_BYTES);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm2 smem)");
+      configured = true;
+    }
+    grid &= ~1;
+    kern<<<grid, GEMM_THREADS, GEMM2_SMEM_BYTES, stream>>>(ta, tb, args);
+  } else {
+    auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)GEMM_SMEM_BYTES);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm smem)");
+      configured = true;
+    }
+    kern<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(ta, tb, args);
   }
-  const int grid = num_sms_current();
-  kern<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(ta, tb, args);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm launch");
   note_launch();
@@ -416,13 +666,12 @@ int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t
   if (rc) return rc;
   if (H % GBK || H < GBK || De % 128 || De < 128)
     return set_error(DM_ERR_SHAPE, "w13 fwd needs H %% 64 == 0 and D_e %% 128 == 0 (H=%d, D_e=%d)", H, De);
-  CUtensorMap ta, tb;
-  if ((rc = make_tmap_bf16_2d(&ta, x_perm, H, cap_rows, H, 64, 128))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, w13, H, (uint64_t)E * 2 * De, H, 64, 256))) return rc;
+  const GemmOperand A{x_perm, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H, false, false};
+  const GemmOperand B{w13, (uint64_t)H, (uint64_t)E * 2 * De, (uint64_t)H, false, true};
   GemmArgs a{};
   a.num_groups = E; a.group_off = pad_off; a.N = 2 * De; a.K = H; a.b_group_rows = 2 * De;
   a.C = act; a.ldc = De; a.aux = reinterpret_cast<__nv_bfloat16*>(h13); a.ld_aux = 2 * De;
-  return launch_gemm<0, 0, 0, EPI_SWIGLU_FWD>(ta, tb, a, (cudaStream_t)stream);
+  return launch_gemm<0, 0, 0, EPI_SWIGLU_FWD>(A, B, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* pad_off, int E, int cap_rows,
@@ -431,13 +680,12 @@ int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* pad_off, i
   if (rc) return rc;
   if (H % GBN || De % GBK)
     return set_error(DM_ERR_SHAPE, "w2 fwd needs H %% 256 == 0 and D_e %% 64 == 0 (H=%d, D_e=%d)", H, De);
-  CUtensorMap ta, tb;
-  if ((rc = make_tmap_bf16_2d(&ta, act, De, cap_rows, De, 64, 128))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, w2, De, (uint64_t)E * H, De, 64, 256))) return rc;
+  const GemmOperand A{act, (uint64_t)De, (uint64_t)cap_rows, (uint64_t)De, false, false};
+  const GemmOperand B{w2, (uint64_t)De, (uint64_t)E * H, (uint64_t)De, false, true};
   GemmArgs a{};
   a.num_groups = E; a.group_off = pad_off; a.N = H; a.K = De; a.b_group_rows = H;
   a.C = y_perm; a.ldc = H;
-  return launch_gemm<0, 0, 0, EPI_BF16>(ta, tb, a, (cudaStream_t)stream);
+  return launch_gemm<0, 0, 0, EPI_BF16>(A, B, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const void* h13,
@@ -447,14 +695,13 @@ int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const vo
   if (rc) return rc;
   if (H % GBK || De % GBN)
     return set_error(DM_ERR_SHAPE, "w2 dgrad needs H %% 64 == 0 and D_e %% 256 == 0 (H=%d, D_e=%d)", H, De);
-  CUtensorMap ta, tb;
-  if ((rc = make_tmap_bf16_2d(&ta, dy_perm, H, cap_rows, H, 64, 128))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, w2, De, (uint64_t)E * H, De, 64, 64))) return rc;
+  const GemmOperand A{dy_perm, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H, false, false};
+  const GemmOperand B{w2, (uint64_t)De, (uint64_t)E * H, (uint64_t)De, true, true};
   GemmArgs a{};
   a.num_groups = E; a.group_off = pad_off; a.N = De; a.K = H; a.b_group_rows = H;
   a.aux = reinterpret_cast<__nv_bfloat16*>(dh13); a.ld_aux = 2 * De;
   a.aux_in = reinterpret_cast<const __nv_bfloat16*>(h13); a.ld_aux_in = 2 * De;
-  return launch_gemm<0, 1, 0, EPI_SWIGLU_BWD>(ta, tb, a, (cudaStream_t)stream);
+  return launch_gemm<0, 1, 0, EPI_SWIGLU_BWD>(A, B, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* pad_off, int E,
@@ -463,32 +710,30 @@ int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* pad_o
   if (rc) return rc;
   if (H % GBN || De % 128)
     return set_error(DM_ERR_SHAPE, "w13 dgrad needs H %% 256 == 0 and D_e %% 128 == 0 (H=%d, D_e=%d)", H, De);
-  CUtensorMap ta, tb;
-  if ((rc = make_tmap_bf16_2d(&ta, dh13, 2 * De, cap_rows, 2 * De, 64, 128))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, w13, H, (uint64_t)E * 2 * De, H, 64, 64))) return rc;
+  const GemmOperand A{dh13, (uint64_t)2 * De, (uint64_t)cap_rows, (uint64_t)2 * De, false, false};
+  const GemmOperand B{w13, (uint64_t)H, (uint64_t)E * 2 * De, (uint64_t)H, true, true};
   GemmArgs a{};
   a.num_groups = E; a.group_off = pad_off; a.N = H; a.K = 2 * De; a.b_group_rows = 2 * De;
   a.C = dx_perm; a.ldc = H;
-  return launch_gemm<0, 1, 0, EPI_BF16>(ta, tb, a, (cudaStream_t)stream);
+  return launch_gemm<0, 1, 0, EPI_BF16>(A, B, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* seg_off,
                      int nseg, int E, int seg_rows, float* dW, float beta, void* stream) {
   int rc = check_groups(E, seg_rows);
   if (rc) return rc;
-  if (M % GBM || N % GBN || M <= 0 || N <= 0)
-    return set_error(DM_ERR_SHAPE, "wgrad needs M %% 128 == 0 and N %% 256 == 0 (M=%d, N=%d)", M, N);
+  if (M % 256 || N % GBN || M <= 0 || N <= 0)
+    return set_error(DM_ERR_SHAPE, "wgrad needs M %% 256 == 0 and N %% 256 == 0 (M=%d, N=%d)", M, N);
   if (nseg < 1 || nseg > 64) return set_error(DM_ERR_SHAPE, "wgrad segments %d outside [1, 64]", nseg);
   if (reinterpret_cast<uintptr_t>(dW) & 15) return set_error(DM_ERR_ALIGN, "dW not 16-byte aligned");
-  CUtensorMap ta, tb;
   const uint64_t rows = (uint64_t)nseg * seg_rows;
-  if ((rc = make_tmap_bf16_2d(&ta, a_tok, M, rows, M, 64, 64))) return rc;
-  if ((rc = make_tmap_bf16_2d(&tb, b_tok, N, rows, N, 64, 64))) return rc;
+  const GemmOperand A{a_tok, (uint64_t)M, rows, (uint64_t)M, true, false};
+  const GemmOperand B{b_tok, (uint64_t)N, rows, (uint64_t)N, true, true};
   GemmArgs a{};
   a.num_groups = E; a.group_off = seg_off; a.M = M; a.N = N;
   a.C = dW; a.ldc = N; a.c_group_stride = (long long)M * N; a.beta = beta;
   a.seg_off = seg_off; a.nseg = nseg; a.seg_stride_rows = seg_rows;
-  return launch_gemm<1, 1, 1, EPI_F32>(ta, tb, a, (cudaStream_t)stream);
+  return launch_gemm<1, 1, 1, EPI_F32>(A, B, a, (cudaStream_t)stream);
 }
 
 }  // extern "C"

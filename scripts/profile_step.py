@@ -16,13 +16,12 @@ ap.add_argument("--warmup", type=int, default=1)
 a = ap.parse_args()
 exp = load_experiment(a.config)
 shape = MoEShape.from_experiment(exp)
-layer = MoELayer.random(shape, device="cuda", seed=1, num_buffers=2)
+mb = exp.workload.num_microbatches
+layer = MoELayer.random(shape, device="cuda", seed=1, num_buffers=mb)
 for b in layer.buffers:
     b.x.normal_()
     b.dy.normal_()
-mb = exp.workload.num_microbatches
 for s in range(a.warmup + a.steps):
-    for i in range(mb):
-        layer.forward_backward(layer.buffers[i % 2], accumulate=i > 0)
+    layer.iteration(mb)
 torch.cuda.synchronize()
 print("ok")
