@@ -394,9 +394,17 @@ __device__ __forceinline__ TileInfo decode_tile_2sm(int t, const int* tile_start
     ti.row_base = row_off;
     active = ti.m0 < row_off + rows;
   } else {
-    const int mt = a.M / 256;
-    ti.m0 = (local % mt) * 256 + 128 * rank;
-    ti.n0 = (local / mt) * GBN;
+    // Rasterise along the smaller output dimension so concurrent tiles share the
+    // larger operand's tile (streamed once) while the smaller operand stays in L2:
+    // dW13 (M = 2*D_e >> N = H) goes n-fastest, dW2 (M = H < N = D_e) m-fastest.
+    const int mt = a.M / 256, nt = a.N / GBN;
+    if (a.M >= a.N) {
+      ti.m0 = (local / nt) * 256 + 128 * rank;
+      ti.n0 = (local % nt) * GBN;
+    } else {
+      ti.m0 = (local % mt) * 256 + 128 * rank;
+      ti.n0 = (local / mt) * GBN;
+    }
     int kb = 0;
     for (int i = 0; i < a.nseg; ++i)
       kb += (a.seg_off[i * (G + 1) + lo + 1] - a.seg_off[i * (G + 1) + lo]) / GBK;
