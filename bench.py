@@ -188,6 +188,8 @@ def run_ours(args, shape, exp):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
+    if world > 1 and not args.replicas:
+        return run_afpipe(args, shape, exp, world, rank, local, dev)
     mb = exp.workload.num_microbatches
     layer = MoELayer.random(shape, device=dev, seed=1234 + rank, num_buffers=mb)
     stream = torch.cuda.current_stream(dev)
@@ -312,6 +314,169 @@ def run_ours(args, shape, exp):
     return 0
 
 
+def _union(iv):
+    out = []
+    for s, e in sorted(iv):
+        if out and s <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], e)
+        else:
+            out.append([s, e])
+    return out
+
+
+def _uncovered(a, b):
+    """Length of union(a) not covered by union(b) (the reference's exposed_comm, sim.py:273-299)."""
+    a, b = _union(a), _union(b)
+    tot, j = 0.0, 0
+    for s, e in a:
+        cur = s
+        while cur < e:
+            while j < len(b) and b[j][1] <= cur:
+                j += 1
+            if j == len(b) or b[j][0] >= e:
+                tot += e - cur
+                break
+            if b[j][0] > cur:
+                tot += b[j][0] - cur
+            cur = min(b[j][1], e)
+    return tot
+
+
+def run_afpipe(args, shape, exp, world, rank, local, dev):
+    """N>1: A:F-split AF-Pipe runtime (one process per GPU, NCCL over NVLink)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_11005_b200 import _lib
+    from paper_2605_11005_b200.runtime import AFPipeRank, Topology, trace_intervals
+
+    mb = exp.workload.num_microbatches
+    topo = Topology.default(world, shape.E, args.n_attn)
+    r = AFPipeRank(shape, topo, rank, mb, dev, seed=1234)
+    r.init_groups()
+    if r.role == "A":
+        for b in r.bufs:
+            b.x.normal_()
+            b.dy.normal_()
+    for _ in range(args.warmup):
+        r.run_iteration()
+    torch.cuda.synchronize()
+    dist.barrier()
+    sampler = ClockSampler(dev.index) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    n0 = _lib.launch_count()
+    t_s, t_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t_s.record()
+    for _ in range(args.steps):
+        r.run_iteration()
+    t_e.record()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - n0
+    ms = t_s.elapsed_time(t_e)
+    tt = torch.tensor([ms, float(launches)], device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = tt[0].item()
+    lsum = torch.tensor([float(launches)], device=dev)
+    dist.all_reduce(lsum)
+    clocks = sampler.stop() if sampler else None
+
+    # one instrumented iteration: per-task CUDA-event intervals on every rank
+    r.record_events = True
+    torch.cuda.synchronize()
+    dist.barrier()
+    r.run_iteration()
+    torch.cuda.synchronize()
+    ivs = trace_intervals(r)
+    r.record_events = False
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object({"rank": rank, "role": r.role, "ivs": ivs}, gathered, dst=0)
+
+    # e2e: A ranks feed x/dy from pinned host memory and read y/dx back every micro-batch
+    T, H = shape.T, shape.H
+    if r.role == "A":
+        mk = lambda: torch.empty(T, H, dtype=torch.bfloat16).pin_memory()  # noqa: E731
+        xs = [torch.randn(T, H).to(torch.bfloat16).pin_memory() for _ in range(mb)]
+        dys = [torch.randn(T, H).to(torch.bfloat16).pin_memory() for _ in range(mb)]
+        r.set_host_io(xs, dys, [mk() for _ in range(mb)], [mk() for _ in range(mb)])
+    r.run_iteration()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        r.run_iteration()
+    e1.record()
+    torch.cuda.synchronize()
+    ems = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+    ems = ems.item()
+
+    if rank == 0:
+        peaks, peak_kind = _peaks()
+        tokens = args.steps * mb * shape.T * topo.n_attn
+        value = tokens / (ms / 1e3)
+        comp_all, comm_all, per_rank, it_end = [], [], {}, 0.0
+        gemm_ms, link = 0.0, []
+        for g in gathered:
+            comp = [(s, e) for n, i, lane, s, e, b in g["ivs"] if lane == "compute"]
+            comm = [(s, e) for n, i, lane, s, e, b in g["ivs"] if lane != "compute"]
+            comp_all += comp
+            comm_all += comm
+            it_end = max([it_end] + [e for _, e in comp + comm])
+            per_rank[g["rank"]] = _uncovered(comm, comp)
+            if g["role"] == "F":
+                gemm_ms += sum(e - s for n, i, lane, s, e, b in g["ivs"] if lane == "compute")
+            link += [b / ((e - s) / 1e3) / 1e9 for n, i, lane, s, e, b in g["ivs"]
+                     if lane != "compute" and e > s and b > 0]
+        exposed = _uncovered(comm_all, comp_all)
+        f_flops = mb * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd()) * topo.n_attn
+        achieved = f_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+        peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {
+                "workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E, "k": shape.k,
+                "D_e": shape.De, "microbatches": mb, "tokens_per_step": mb * shape.T * topo.n_attn,
+                "parallelism": f"AF-Pipe {topo.n_attn}A:{topo.n_ffn}F (A: DP routing/combine, F: EP experts)",
+                "transport": "NCCL send/recv (torch.distributed P2P) over NVLink",
+                "weights": "random-init", "l2": "inputs+weights larger than L2",
+                "wgrad": "fp32, deferred per iteration on F ranks",
+            },
+            "roofline": {
+                "bound": "tensor", "kernel": "grouped expert GEMMs on F ranks (F_f + F_b + W tasks)",
+                "achieved": round(achieved, 1) if achieved else None, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": round(achieved / peak_tf, 4) if achieved else None, "traffic": None,
+                "peak_kind": f"{peak_kind} sustained bf16, per F GPU (sum of F compute time over F ranks)",
+            },
+            "exposed_comm": {
+                "global_ms": round(exposed, 4), "global_pct": round(100 * exposed / it_end, 3) if it_end else None,
+                "per_rank_max_pct": round(100 * max(per_rank.values()) / it_end, 3) if it_end else None,
+                "iteration_ms_instrumented": round(it_end, 3),
+                "definition": "reference sim.exposed_comm: comm running while every compute engine idles; "
+                              "per-rank: comm not covered by that rank's own compute; send-side intervals",
+            },
+            "link": {"mean_GB/s": round(statistics.mean(link), 1) if link else None,
+                     "max_GB/s": round(max(link), 1) if link else None,
+                     "peak_GB/s": 900.0, "note": "bytes / (data ready -> send complete), per transfer group"},
+            "gpu_launches": int(lsum.item()),
+            "clocks": clocks,
+            "e2e": {"value": round(tokens / (ems / 1e3), 1), "unit": UNIT,
+                    "h2d_bytes_per_step": 2 * T * H * 2 * mb * topo.n_attn,
+                    "d2h_bytes_per_step": 2 * T * H * 2 * mb * topo.n_attn,
+                    "ms_per_step": round(ems / args.steps, 3),
+                    "path": "AFPipeRank.run_iteration with pinned host x/dy in, y/dx out per micro-batch"},
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def run_e2e(args, layer, shape, mb, dev, world):
     """Same metric through the public API with host buffers: per micro-batch H2D of
     x and dy from pinned memory and D2H of y and dx, overlapped on a copy stream."""
@@ -380,6 +545,8 @@ def main(argv=None):
     ap.add_argument("--config", default=str(ROOT / "configs" / "mixtral_layer.yaml"))
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n-attn", type=int, default=None, help="A ranks for N>1 (default N/2)")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent fused replicas instead of AF-Pipe")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -139,29 +139,35 @@ DM_API int dm_route_and_dispatch(const void* x, const float* wg, int T, int H, i
                           int32_t* idx, float* w, int32_t* counts, int32_t* pad_off,
                           int32_t* row_map, int32_t* src_token, void* x_perm, void* stream);
 
-/* ---- expert FFN (F side), grouped over experts by pad_off --------------- */
+/* ---- expert FFN (F side), grouped by 128-aligned row offsets ------------
+ * group_off[G+1] partitions the permuted rows into G groups (each a multiple
+ * of 128 rows); group g multiplies weight matrix g % E. On the fused path
+ * G = E (one group per expert, group_off = pad_off); an F rank of the AF-Pipe
+ * runtime passes G = n_attention_ranks * E_local groups ordered (A rank, expert). */
 /* h13[r, :] = x_perm[r, :] . W13_e^T ; act = silu(gate) * up.  h13 [cap, 2*D_e], act [cap, D_e]. */
-DM_API int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t* pad_off, int E,
-                              int cap_rows, int H, int De, void* h13, void* act, void* stream);
+DM_API int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t* group_off, int G,
+                                     int E, int cap_rows, int H, int De, void* h13, void* act, void* stream);
 /* y_perm[r, :] = act[r, :] . W2_e^T */
-DM_API int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* pad_off, int E, int cap_rows,
-                      int H, int De, void* y_perm, void* stream);
+DM_API int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* group_off, int G, int E,
+                             int cap_rows, int H, int De, void* y_perm, void* stream);
 /* d_act = dy_perm . W2_e ; dh13 = SwiGLU'(h13) (.) d_act  (same interleaved layout as h13). */
 DM_API int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const void* h13,
-                                   const int32_t* pad_off, int E, int cap_rows, int H, int De,
-                                   void* dh13, void* stream);
+                                          const int32_t* group_off, int G, int E, int cap_rows, int H,
+                                          int De, void* dh13, void* stream);
 /* dx_perm = dh13 . W13_e */
-DM_API int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* pad_off, int E,
-                         int cap_rows, int H, int De, void* dx_perm, void* stream);
+DM_API int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* group_off, int G, int E,
+                                int cap_rows, int H, int De, void* dx_perm, void* stream);
 /* dW[e] (fp32 [M, N]) = sum over segments i < nseg of
  *   a_tok[rows_{i,e}, :M]^T . b_tok[rows_{i,e}, :N]   (+ beta * dW[e]),
- * rows_{i,e} = i*seg_rows + [seg_off[i*(E+1)+e], seg_off[i*(E+1)+e+1]).
- * a_tok / b_tok hold nseg stacked per-micro-batch buffers of seg_rows rows each,
- * so one launch reduces an expert's gradient over every micro-batch of an
- * iteration (deferred weight-gradient pass). dW2 = wgrad(dy_perm, M=H, act, N=D_e);
- * dW13 = wgrad(dh13, M=2*D_e, x_perm, N=H). */
+ * rows_{i,e} = i*seg_stride_rows + [seg_off[i*(E+1)+e], seg_off[i*(E+1)+e+1]),
+ * a_tok / b_tok having total_rows rows. With seg_stride_rows = cap and one
+ * segment per micro-batch, one launch reduces an expert's gradient over every
+ * micro-batch of an iteration (deferred weight-gradient pass); seg_stride_rows = 0
+ * takes absolute offsets (F ranks: one segment per (micro-batch, A rank)).
+ * dW2 = wgrad(dy_perm, M=H, act, N=D_e); dW13 = wgrad(dh13, M=2*D_e, x_perm, N=H). */
 DM_API int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* seg_off,
-                            int nseg, int E, int seg_rows, float* dW, float beta, void* stream);
+                            int nseg, int E, int total_rows, int seg_stride_rows, float* dW, float beta,
+                            void* stream);
 
 /* ---- combine (A side) ------------------------------------------------- */
 DM_API int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,

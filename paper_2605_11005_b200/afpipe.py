@@ -199,6 +199,63 @@ def plan_afpipe(layers: int, depth: int, microbatches: int, d: StageDurations) -
     return schedule(build_dag(layers, depth, microbatches, d))
 
 
+# Task names of the single-MoE-layer runtime chain: with the
+# expert block sharded over several F ranks a token's k outputs live on different
+# ranks, so the combine (and the loss turnaround) runs on the A side. Per micro-batch:
+#   A_f -> M2N -> F_f -> N2M -> A_t -> M2N_b -> F_b -> N2M_b -> A_b
+# i.e. the reference's interior-layer pattern (taskgraph.py:335-339, :352-356)
+# with the A visit split in dispatch (A_f), turnaround (A_t) and dispatch-bwd (A_b).
+@dataclass(frozen=True)
+class LayerDurations:
+    a_fwd: int       # dispatch (routing + permute)
+    a_turn: int      # combine fwd + loss turnaround + combine bwd
+    a_bwd: int       # permute bwd + router grads
+    f_fwd: int       # expert GEMMs fwd
+    f_bwd: int       # expert dgrad GEMMs
+    m2n: int         # one exchange in either direction
+
+
+def build_layer_dag(microbatches: int, d: LayerDurations, a_credit: int = 2, f_credit: int = 2) -> Plan:
+    tasks: list[PlanTask] = []
+
+    def new(kind, owner, lane, dur, deps, mb, comp, direction, name):
+        t = PlanTask(len(tasks), kind, owner, lane, dur, tuple(deps), mb, 0, 0, comp, direction)
+        t.name = name  # type: ignore[attr-defined]
+        tasks.append(t)
+        return t.id
+
+    def exchange(src, dst, dep, mb, direction, name):
+        s = new("M2NSend", src, SEND, d.m2n, (dep,), mb, None, direction, name)
+        r = new("M2NRecv", dst, RECV, d.m2n, (dep,), mb, None, direction, name)
+        tasks[s].twin, tasks[r].twin = r, s
+        return r
+
+    for mb in range(microbatches):
+        af = new("FwdCompute", "A0", COMPUTE, d.a_fwd, (), mb, "A", FWD, "A_f")
+        r = exchange("A0", "F0", af, mb, FWD, "M2N")
+        ff = new("FwdCompute", "F0", COMPUTE, d.f_fwd, (r,), mb, "F", FWD, "F_f")
+        r = exchange("F0", "A0", ff, mb, FWD, "N2M")
+        at = new("BwdCompute", "A0", COMPUTE, d.a_turn, (r,), mb, "A", BWD, "A_t")
+        r = exchange("A0", "F0", at, mb, BWD, "M2N_b")
+        fb = new("BwdCompute", "F0", COMPUTE, d.f_bwd, (r,), mb, "F", BWD, "F_b")
+        r = exchange("F0", "A0", fb, mb, BWD, "N2M_b")
+        new("BwdCompute", "A0", COMPUTE, d.a_bwd, (r,), mb, "A", BWD, "A_b")
+    return Plan(tasks, {"A0": a_credit, "F0": f_credit})
+
+
+def plan_layer(microbatches: int, d: LayerDurations, a_credit: int = 2, f_credit: int = 2) -> Plan:
+    """Scheduled single-layer chain; every rank issues its tasks in planned-start order,
+    which keeps the per-pair send/recv order identical on both ends (twins share a start)."""
+    return schedule(build_layer_dag(microbatches, d, a_credit, f_credit))
+
+
+def issue_order(plan: Plan, owner: str) -> list[PlanTask]:
+    """The owner's tasks across all its lanes, by planned start (then compute < send < recv, id)."""
+    lane_rank = {COMPUTE: 0, SEND: 1, RECV: 2}
+    mine = [t for t in plan.tasks if t.owner == owner]
+    return sorted(mine, key=lambda t: (t.start_ns, lane_rank[t.lane], t.id))
+
+
 # ----------------------------------------------------------- trace metrics
 def _union(intervals):
     out: list[list[int]] = []

@@ -37,7 +37,8 @@ struct GemmArgs {
   int M;                         // ragged-K: rows of C per group (multiple of 128)
   int N;                         // multiple of 256
   int K;                         // ragged-M: reduction length (multiple of 64)
-  int b_group_rows;              // ragged-M: rows of the B tensor owned by one group
+  int b_group_rows;              // ragged-M: rows of the B tensor owned by one weight matrix
+  int b_groups;                  // ragged-M: group g multiplies weight matrix g % b_groups
   void* C;
   long long ldc;
   long long c_group_stride;      // ragged-K: elements between groups' C blocks
@@ -263,7 +264,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         const TileInfo ti = decode_tile<RAGGED_K>(t, s_tile, s_off, G, args);
-        const int b_gofs = RAGGED_K ? 0 : ti.g * args.b_group_rows;
+        const int b_gofs = RAGGED_K ? 0 : (ti.g % args.b_groups) * args.b_group_rows;
         int seg = 0, seg_kb = 0, seg_nkb = 0, seg_row0 = 0;
         for (int kb = 0; kb < ti.kb_count; ++kb) {
           int kcoord;
@@ -475,7 +476,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         bool active;
         const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, G, args, rank, active);
-        const int b_gofs = RAGGED_K ? 0 : ti.g * args.b_group_rows;
+        const int b_gofs = RAGGED_K ? 0 : (ti.g % args.b_groups) * args.b_group_rows;
         const int nb0 = ti.n0 + 128 * (int)rank;   // this CTA's half of the N tile
         int seg = 0, seg_kb = 0, seg_nkb = 0, seg_row0 = 0;
         for (int kb = 0; kb < ti.kb_count; ++kb) {
@@ -656,8 +657,9 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const GemmA
   return DM_OK;
 }
 
-static int check_groups(int E, int cap_rows) {
-  if (E < 1 || E > GEMM_MAX_GROUPS) return set_error(DM_ERR_SHAPE, "expert count %d outside [1, %d]", E, GEMM_MAX_GROUPS);
+static int check_groups(int G, int E, int cap_rows) {
+  if (G < 1 || G > GEMM_MAX_GROUPS) return set_error(DM_ERR_SHAPE, "group count %d outside [1, %d]", G, GEMM_MAX_GROUPS);
+  if (E < 1 || E > G) return set_error(DM_ERR_SHAPE, "weight count %d outside [1, G=%d]", E, G);
   if (cap_rows < 0 || (cap_rows % GBM)) return set_error(DM_ERR_SHAPE, "cap_rows %d must be a multiple of %d", cap_rows, GBM);
   return DM_OK;
 }
@@ -668,79 +670,81 @@ using namespace dm;
 
 extern "C" {
 
-int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t* pad_off, int E,
-                              int cap_rows, int H, int De, void* h13, void* act, void* stream) {
-  int rc = check_groups(E, cap_rows);
+int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t* group_off, int G,
+                              int E, int cap_rows, int H, int De, void* h13, void* act, void* stream) {
+  int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
   if (H % GBK || H < GBK || De % 128 || De < 128)
     return set_error(DM_ERR_SHAPE, "w13 fwd needs H %% 64 == 0 and D_e %% 128 == 0 (H=%d, D_e=%d)", H, De);
   const GemmOperand A{x_perm, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H, false, false};
   const GemmOperand B{w13, (uint64_t)H, (uint64_t)E * 2 * De, (uint64_t)H, false, true};
   GemmArgs a{};
-  a.num_groups = E; a.group_off = pad_off; a.N = 2 * De; a.K = H; a.b_group_rows = 2 * De;
+  a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = 2 * De; a.K = H; a.b_group_rows = 2 * De;
   a.C = act; a.ldc = De; a.aux = reinterpret_cast<__nv_bfloat16*>(h13); a.ld_aux = 2 * De;
   return launch_gemm<0, 0, 0, EPI_SWIGLU_FWD>(A, B, a, (cudaStream_t)stream);
 }
 
-int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* pad_off, int E, int cap_rows,
-                      int H, int De, void* y_perm, void* stream) {
-  int rc = check_groups(E, cap_rows);
+int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* group_off, int G, int E,
+                      int cap_rows, int H, int De, void* y_perm, void* stream) {
+  int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
   if (H % GBN || De % GBK)
     return set_error(DM_ERR_SHAPE, "w2 fwd needs H %% 256 == 0 and D_e %% 64 == 0 (H=%d, D_e=%d)", H, De);
   const GemmOperand A{act, (uint64_t)De, (uint64_t)cap_rows, (uint64_t)De, false, false};
   const GemmOperand B{w2, (uint64_t)De, (uint64_t)E * H, (uint64_t)De, false, true};
   GemmArgs a{};
-  a.num_groups = E; a.group_off = pad_off; a.N = H; a.K = De; a.b_group_rows = H;
+  a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = H; a.K = De; a.b_group_rows = H;
   a.C = y_perm; a.ldc = H;
   return launch_gemm<0, 0, 0, EPI_BF16>(A, B, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const void* h13,
-                                   const int32_t* pad_off, int E, int cap_rows, int H, int De,
+                                   const int32_t* group_off, int G, int E, int cap_rows, int H, int De,
                                    void* dh13, void* stream) {
-  int rc = check_groups(E, cap_rows);
+  int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
   if (H % GBK || De % GBN)
     return set_error(DM_ERR_SHAPE, "w2 dgrad needs H %% 64 == 0 and D_e %% 256 == 0 (H=%d, D_e=%d)", H, De);
   const GemmOperand A{dy_perm, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H, false, false};
   const GemmOperand B{w2, (uint64_t)De, (uint64_t)E * H, (uint64_t)De, true, true};
   GemmArgs a{};
-  a.num_groups = E; a.group_off = pad_off; a.N = De; a.K = H; a.b_group_rows = H;
+  a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = De; a.K = H; a.b_group_rows = H;
   a.aux = reinterpret_cast<__nv_bfloat16*>(dh13); a.ld_aux = 2 * De;
   a.aux_in = reinterpret_cast<const __nv_bfloat16*>(h13); a.ld_aux_in = 2 * De;
   return launch_gemm<0, 1, 0, EPI_SWIGLU_BWD>(A, B, a, (cudaStream_t)stream);
 }
 
-int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* pad_off, int E,
+int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* group_off, int G, int E,
                          int cap_rows, int H, int De, void* dx_perm, void* stream) {
-  int rc = check_groups(E, cap_rows);
+  int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
   if (H % GBN || De % 128)
     return set_error(DM_ERR_SHAPE, "w13 dgrad needs H %% 256 == 0 and D_e %% 128 == 0 (H=%d, D_e=%d)", H, De);
   const GemmOperand A{dh13, (uint64_t)2 * De, (uint64_t)cap_rows, (uint64_t)2 * De, false, false};
   const GemmOperand B{w13, (uint64_t)H, (uint64_t)E * 2 * De, (uint64_t)H, true, true};
   GemmArgs a{};
-  a.num_groups = E; a.group_off = pad_off; a.N = H; a.K = 2 * De; a.b_group_rows = 2 * De;
+  a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = H; a.K = 2 * De; a.b_group_rows = 2 * De;
   a.C = dx_perm; a.ldc = H;
   return launch_gemm<0, 1, 0, EPI_BF16>(A, B, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* seg_off,
-                     int nseg, int E, int seg_rows, float* dW, float beta, void* stream) {
-  int rc = check_groups(E, seg_rows);
+                     int nseg, int E, int total_rows, int seg_stride_rows, float* dW, float beta,
+                     void* stream) {
+  int rc = check_groups(E, E, total_rows);
   if (rc) return rc;
   if (M % 256 || N % GBN || M <= 0 || N <= 0)
     return set_error(DM_ERR_SHAPE, "wgrad needs M %% 256 == 0 and N %% 256 == 0 (M=%d, N=%d)", M, N);
   if (nseg < 1 || nseg > 64) return set_error(DM_ERR_SHAPE, "wgrad segments %d outside [1, 64]", nseg);
+  if (seg_stride_rows < 0 || (long long)(nseg - 1) * seg_stride_rows > total_rows)
+    return set_error(DM_ERR_SHAPE, "wgrad segment stride %d inconsistent with %d rows", seg_stride_rows, total_rows);
   if (reinterpret_cast<uintptr_t>(dW) & 15) return set_error(DM_ERR_ALIGN, "dW not 16-byte aligned");
-  const uint64_t rows = (uint64_t)nseg * seg_rows;
-  const GemmOperand A{a_tok, (uint64_t)M, rows, (uint64_t)M, true, false};
-  const GemmOperand B{b_tok, (uint64_t)N, rows, (uint64_t)N, true, true};
+  const GemmOperand A{a_tok, (uint64_t)M, (uint64_t)total_rows, (uint64_t)M, true, false};
+  const GemmOperand B{b_tok, (uint64_t)N, (uint64_t)total_rows, (uint64_t)N, true, true};
   GemmArgs a{};
   a.num_groups = E; a.group_off = seg_off; a.M = M; a.N = N;
   a.C = dW; a.ldc = N; a.c_group_stride = (long long)M * N; a.beta = beta;
-  a.seg_off = seg_off; a.nseg = nseg; a.seg_stride_rows = seg_rows;
+  a.seg_off = seg_off; a.nseg = nseg; a.seg_stride_rows = seg_stride_rows;
   return launch_gemm<1, 1, 1, EPI_F32>(A, B, a, (cudaStream_t)stream);
 }
 

@@ -83,54 +83,65 @@ def route_and_dispatch(x, wg, k, workspace, idx, w, counts, pad_off, row_map, sr
 
 
 # --------------------------------------------------------------- expert FFN
-def w13_swiglu_fwd(x_perm, w13, pad_off, h13, act, stream=None):
+# group_off: int32 [G+1] row offsets (128-aligned); group g uses weight matrix g % E.
+def _groups(group_off, E):
+    G = group_off.numel() - 1
+    if group_off.dtype != torch.int32 or G < E:
+        raise ValueError("group_off must be int32 [G+1] with G >= number of experts")
+    return G
+
+
+def w13_swiglu_fwd(x_perm, w13, group_off, h13, act, stream=None):
     cap, H = x_perm.shape
     E, two_de, _ = w13.shape
     De = two_de // 2
     _check(h13, BF16, (cap, 2 * De), "h13"); _check(act, BF16, (cap, De), "act")
-    _lib.call("dm_grouped_w13_swiglu_fwd", _ptr(x_perm), _ptr(w13), _ptr(pad_off), E, cap, H, De,
-              _ptr(h13), _ptr(act), _stream(stream))
+    _lib.call("dm_grouped_w13_swiglu_fwd", _ptr(x_perm), _ptr(w13), _ptr(group_off), _groups(group_off, E), E,
+              cap, H, De, _ptr(h13), _ptr(act), _stream(stream))
 
 
-def w2_fwd(act, w2, pad_off, y_perm, stream=None):
+def w2_fwd(act, w2, group_off, y_perm, stream=None):
     cap, De = act.shape
     E, H, _ = w2.shape
     _check(y_perm, BF16, (cap, H), "y_perm")
-    _lib.call("dm_grouped_w2_fwd", _ptr(act), _ptr(w2), _ptr(pad_off), E, cap, H, De, _ptr(y_perm),
-              _stream(stream))
+    _lib.call("dm_grouped_w2_fwd", _ptr(act), _ptr(w2), _ptr(group_off), _groups(group_off, E), E, cap, H, De,
+              _ptr(y_perm), _stream(stream))
 
 
-def w2_dgrad_swiglu_bwd(dy_perm, w2, h13, pad_off, dh13, stream=None):
+def w2_dgrad_swiglu_bwd(dy_perm, w2, h13, group_off, dh13, stream=None):
     cap, H = dy_perm.shape
     E, _, De = w2.shape
     _check(dh13, BF16, (cap, 2 * De), "dh13")
-    _lib.call("dm_grouped_w2_dgrad_swiglu_bwd", _ptr(dy_perm), _ptr(w2), _ptr(h13), _ptr(pad_off), E, cap,
-              H, De, _ptr(dh13), _stream(stream))
+    _lib.call("dm_grouped_w2_dgrad_swiglu_bwd", _ptr(dy_perm), _ptr(w2), _ptr(h13), _ptr(group_off),
+              _groups(group_off, E), E, cap, H, De, _ptr(dh13), _stream(stream))
 
 
-def w13_dgrad(dh13, w13, pad_off, dx_perm, stream=None):
+def w13_dgrad(dh13, w13, group_off, dx_perm, stream=None):
     cap, two_de = dh13.shape
     E, _, H = w13.shape
     _check(dx_perm, BF16, (cap, H), "dx_perm")
-    _lib.call("dm_grouped_w13_dgrad", _ptr(dh13), _ptr(w13), _ptr(pad_off), E, cap, H, two_de // 2,
-              _ptr(dx_perm), _stream(stream))
+    _lib.call("dm_grouped_w13_dgrad", _ptr(dh13), _ptr(w13), _ptr(group_off), _groups(group_off, E), E, cap,
+              H, two_de // 2, _ptr(dx_perm), _stream(stream))
 
 
-def wgrad(a_tok, b_tok, seg_off, dW, beta=0.0, stream=None):
-    """dW[e] = sum over segments of a_tok[rows]^T b_tok[rows]; seg_off is [E+1] (one
-    segment) or [nseg, E+1] with a_tok / b_tok stacking nseg equal row blocks."""
+def wgrad(a_tok, b_tok, seg_off, dW, beta=0.0, stream=None, seg_stride_rows=None):
+    """dW[e] = sum over segments of a_tok[rows]^T b_tok[rows]. seg_off is [E+1] (one
+    segment) or [nseg, E+1]; by default segment i starts at row i * rows/nseg (stacked
+    equal blocks); seg_stride_rows=0 means seg_off holds absolute row offsets."""
     rows, M = a_tok.shape
     _, N = b_tok.shape
     so = seg_off if seg_off.dim() == 2 else seg_off.view(1, -1)
     nseg, E1 = so.shape
     E = E1 - 1
-    if rows % nseg:
-        raise ValueError("token buffers must stack nseg equal blocks")
+    if seg_stride_rows is None:
+        if rows % nseg:
+            raise ValueError("token buffers must stack nseg equal blocks")
+        seg_stride_rows = rows // nseg
     if not so.is_contiguous():
         raise ValueError("seg_off must be contiguous")
     _check(dW, torch.float32, (E, M, N), "dW")
-    _lib.call("dm_grouped_wgrad", _ptr(a_tok), M, _ptr(b_tok), N, _ptr(so), nseg, E, rows // nseg, _ptr(dW),
-              float(beta), _stream(stream))
+    _lib.call("dm_grouped_wgrad", _ptr(a_tok), M, _ptr(b_tok), N, _ptr(so), nseg, E, rows, seg_stride_rows,
+              _ptr(dW), float(beta), _stream(stream))
 
 
 # ------------------------------------------------------------------ combine

@@ -1,0 +1,498 @@
+"""AF-Pipe runtime: attention (A) ranks and FFN (F) ranks of one node exchanging
+micro-batches of one MoE layer over NCCL (NVLink 5 / NVSwitch).
+
+One process per GPU (torchrun). Ranks [0, n_attn) are A ranks — data parallel,
+each routes its own micro-batches with a replicated router W_g; ranks
+[n_attn, world) are F ranks — expert parallel, F rank f owns the contiguous
+expert block of reference taskgraph._balanced_blocks (taskgraph.py:257-259).
+Per micro-batch i (afpipe.build_layer_dag):
+
+    A_f   route + permute x -> x_perm (expert blocks grouped by owning F rank)
+    M2N   A -> F: header pad_off[lo_f..hi_f] (E_loc+1 ints, fixed size) then the
+          contiguous x_perm slice [pad_off[lo_f], pad_off[hi_f]) (reference
+          M2NSend/M2NRecv twins, taskgraph.py:204-242, volume costs.py:95-103)
+    F_f   grouped SwiGLU GEMMs over (A rank, expert) groups
+    N2M   F -> A: y_perm rows back into the same slice (taskgraph.py:335-339)
+    A_t   combine (weighted sum), loss turnaround, combine bwd -> dy_perm
+    M2N_b A -> F: dy_perm slices;   F_b: dgrad GEMMs (wgrad deferred)
+    N2M_b F -> A: dx_perm slices;   A_b: permute bwd + router grads
+    end:  F: one wgrad pass over all (micro-batch, A rank) segments;
+          A: all-reduce of dW_g over the A group (the only DP collective).
+
+Message sizes are data dependent; the only host synchronisation is reading the
+128-aligned offsets once per micro-batch (A: its own pad_off after dispatch;
+F: the received headers) on a side copy stream, so the compute stream never
+drains. Every rank issues its tasks in the planned order of afpipe.plan_layer,
+which makes the per-pair send/recv sequences identical on both ends.
+
+Stage arithmetic comes from a `Stages` object: `GpuStages` (the sm_100a
+kernels through the C ABI) is the product. Tests inject a CPU restatement to
+exercise this file's protocol under gloo; there is no automatic fallback.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .afpipe import COMPUTE, RECV, SEND, LayerDurations, issue_order, plan_layer
+from .moe import ActivationSlab, ExpertParams, MicroBatchBuffers, MoEShape, RouterParams
+
+BF16, F32, I32 = torch.bfloat16, torch.float32, torch.int32
+
+
+# ------------------------------------------------------------------ topology
+def balanced_blocks(total: int, parts: int) -> list[int]:
+    """Sizes of `parts` contiguous blocks of `total` (reference taskgraph.py:257-259)."""
+    base, extra = divmod(total, parts)
+    return [base + (1 if i < extra else 0) for i in range(parts)]
+
+
+@dataclass(frozen=True)
+class Topology:
+    world: int
+    n_attn: int
+    experts: int
+
+    def __post_init__(self):
+        if not (1 <= self.n_attn < self.world):
+            raise ValueError(f"need 1 <= n_attn < world (n_attn={self.n_attn}, world={self.world})")
+        if self.n_ffn > self.experts:
+            raise ValueError(f"{self.n_ffn} FFN ranks for {self.experts} experts")
+
+    @property
+    def n_ffn(self) -> int:
+        return self.world - self.n_attn
+
+    def role(self, rank: int) -> tuple[str, int]:
+        return ("A", rank) if rank < self.n_attn else ("F", rank - self.n_attn)
+
+    def a_rank(self, a: int) -> int:
+        return a
+
+    def f_rank(self, f: int) -> int:
+        return self.n_attn + f
+
+    def expert_block(self, f: int) -> tuple[int, int]:
+        sizes = balanced_blocks(self.experts, self.n_ffn)
+        lo = sum(sizes[:f])
+        return lo, lo + sizes[f]
+
+    @classmethod
+    def default(cls, world: int, experts: int, n_attn: int | None = None) -> "Topology":
+        """A:F = n_attn : world-n_attn; default half/half (BASELINE configs[1]: 4 + 4)."""
+        if n_attn is None:
+            n_attn = max(1, world // 2)
+        return cls(world, n_attn, experts)
+
+
+# ------------------------------------------------------------------ streams
+class _Streams:
+    """compute / send / recv / copy streams on CUDA; no-ops on CPU (gloo tests)."""
+
+    def __init__(self, device: torch.device):
+        self.cuda = device.type == "cuda"
+        if self.cuda:
+            self.compute = torch.cuda.current_stream(device)
+            self.send = torch.cuda.Stream(device)
+            self.recv = torch.cuda.Stream(device)
+            self.copy = torch.cuda.Stream(device)
+
+    def ctx(self, which: str):
+        if not self.cuda:
+            return _Null()
+        return torch.cuda.stream(getattr(self, which))
+
+    def event(self, which: str = "compute"):
+        if not self.cuda:
+            return None
+        ev = torch.cuda.Event()
+        ev.record(getattr(self, which))
+        return ev
+
+    def wait(self, which: str, ev) -> None:
+        if self.cuda and ev is not None:
+            getattr(self, which).wait_event(ev)
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def _exchange(ops: list[tuple[str, torch.Tensor, int]]):
+    """One coalesced group of P2P ops on the current stream; returns the works."""
+    ops = [o for o in ops if o[1].numel() > 0]
+    if not ops:
+        return []
+    p2p = [dist.P2POp(dist.isend if k == "send" else dist.irecv, t, peer) for k, t, peer in ops]
+    return dist.batch_isend_irecv(p2p)
+
+
+# ------------------------------------------------------------------ stages
+class GpuStages:
+    """The product stage implementations: sm_100a kernels via the C ABI."""
+
+    def __init__(self):
+        _lib.load()
+
+    def a_dispatch(self, buf: MicroBatchBuffers, router: RouterParams):
+        from .moe import a_dispatch
+
+        a_dispatch(buf, router)
+
+    def a_turnaround(self, buf: MicroBatchBuffers):
+        from .moe import a_combine, a_combine_bwd
+
+        a_combine(buf)
+        a_combine_bwd(buf)
+
+    def a_backward(self, buf: MicroBatchBuffers, router: RouterParams, accumulate: bool):
+        from .moe import a_dispatch_bwd
+
+        a_dispatch_bwd(buf, router, accumulate)
+
+    def f_forward(self, fb, experts: ExpertParams, group_off: torch.Tensor):
+        from . import kernels as K
+
+        K.w13_swiglu_fwd(fb.x_perm, experts.w13, group_off, fb.h13, fb.act)
+        K.w2_fwd(fb.act, experts.w2, group_off, fb.y_perm)
+
+    def f_backward(self, fb, experts: ExpertParams, group_off: torch.Tensor):
+        from . import kernels as K
+
+        K.w2_dgrad_swiglu_bwd(fb.dy_perm, experts.w2, fb.h13, group_off, fb.dh13)
+        K.w13_dgrad(fb.dh13, experts.w13, group_off, fb.dx_perm)
+
+    def f_wgrad(self, slab: ActivationSlab, experts: ExpertParams, seg_off: torch.Tensor, accumulate: bool):
+        from . import kernels as K
+
+        beta = 1.0 if accumulate else 0.0
+        K.wgrad(slab.dy_perm, slab.act, seg_off, experts.dw2, beta, seg_stride_rows=0)
+        K.wgrad(slab.dh13, slab.x_perm, seg_off, experts.dw13, beta, seg_stride_rows=0)
+
+
+@dataclass
+class _FMicroBatch:
+    """F-side view of micro-batch i: a region of the F slab holding the n_attn
+    received slices back to back (rows [base, base + rows))."""
+
+    x_perm: torch.Tensor
+    y_perm: torch.Tensor
+    dy_perm: torch.Tensor
+    dx_perm: torch.Tensor
+    h13: torch.Tensor
+    act: torch.Tensor
+    dh13: torch.Tensor
+    headers: list[torch.Tensor] = field(default_factory=list)   # per A rank, [E_loc+1] int32
+    slices: list[tuple[int, int]] = field(default_factory=list)  # per A rank (row begin, rows) in region
+    group_off: torch.Tensor | None = None                        # [n_attn*E_loc + 1] (region-relative)
+    works: dict = field(default_factory=dict)
+
+
+@dataclass
+class IterationStats:
+    ms: float
+    events: list = field(default_factory=list)   # (task name, mb, lane, start_ms, end_ms) relative to t0
+
+
+class AFPipeRank:
+    """One rank of the AF-Pipe runtime for a single MoE layer."""
+
+    def __init__(self, shape: MoEShape, topo: Topology, rank: int, microbatches: int, device,
+                 stages=None, seed: int = 0, weights=None, durations: LayerDurations | None = None,
+                 record_events: bool = False):
+        shape.validate() if device.type == "cuda" else None
+        self.shape, self.topo, self.rank, self.mb = shape, topo, rank, microbatches
+        self.device = torch.device(device)
+        self.role, self.idx = topo.role(rank)
+        self.stages = stages if stages is not None else GpuStages()
+        self.st = _Streams(self.device)
+        self.record_events = record_events and self.st.cuda
+        d = durations or self._default_durations()
+        self.plan = plan_layer(microbatches, d)
+        self.order = issue_order(self.plan, "A0" if self.role == "A" else "F0")
+        s = shape
+        if self.role == "A":
+            if weights:
+                wg = weights["wg"]
+            else:
+                wg = torch.randn(s.E, s.H, generator=torch.Generator().manual_seed(seed)) * 0.02
+            self.router = RouterParams(wg.to(self.device, F32))
+            self.slab = ActivationSlab(s, microbatches, self.device, f_side=False)
+            self.bufs = [MicroBatchBuffers(s, self.device, self.slab, i) for i in range(microbatches)]
+            self.pad_host = [torch.empty(s.E + 1, dtype=I32, pin_memory=self.st.cuda) for _ in range(microbatches)]
+            self.pad_ready = [None] * microbatches
+            self.a_group = None
+        else:
+            lo, hi = topo.expert_block(self.idx)
+            self.lo, self.hi, self.E_loc = lo, hi, hi - lo
+            if weights:
+                w13, w2 = weights["w13"][lo:hi], weights["w2"][lo:hi]
+            else:
+                g = torch.Generator(device=self.device).manual_seed(seed + 1 + self.idx)
+                w13 = torch.empty(self.E_loc, 2 * s.De, s.H, dtype=BF16, device=self.device).normal_(0, 0.02, generator=g)
+                w2 = torch.empty(self.E_loc, s.H, s.De, dtype=BF16, device=self.device).normal_(0, 0.02, generator=g)
+            self.experts = ExpertParams(w13.to(self.device), w2.to(self.device))
+            # worst case: every routed row of every A rank lands on this F rank
+            self.cap_f = topo.n_attn * s.cap
+            self.slab = ActivationSlab(s, microbatches, self.device, rows=self.cap_f)
+            self.fmb = []
+            for i in range(microbatches):
+                r = self.slab.rows(i)
+                sl = self.slab
+                self.fmb.append(_FMicroBatch(sl.x_perm[r], sl.y_perm[r], sl.dy_perm[r], sl.dx_perm[r],
+                                             sl.h13[r], sl.act[r], sl.dh13[r]))
+                self.fmb[-1].headers = [torch.zeros(self.E_loc + 1, dtype=I32, device=self.device)
+                                        for _ in range(topo.n_attn)]
+            self.seg_off = torch.zeros(microbatches * topo.n_attn, self.E_loc + 1, dtype=I32, device=self.device)
+        self.trace: list = []
+        self.t0 = None
+        self.host_io = None
+
+    # ----------------------------------------------------------------- plan
+    def _default_durations(self) -> LayerDurations:
+        """Rough per-stage estimates (ns) to derive the issue order; only the order matters."""
+        s = self.shape
+        tflops = 1.0e15
+        per_f = max(1, self.topo.n_ffn)
+        f_fwd = int(6 * s.R * s.H * s.De * self.topo.n_attn / per_f / tflops * 1e9)
+        m2n = int(2 * s.R * s.H / max(1, min(self.topo.n_attn, per_f)) / 7.0e11 * 1e9)
+        a = int(sum(s.hbm_bytes().values()) / 4 / 5.0e12 * 1e9)
+        return LayerDurations(a_fwd=a, a_turn=2 * a, a_bwd=2 * a, f_fwd=f_fwd, f_bwd=2 * f_fwd, m2n=max(1, m2n))
+
+    # ------------------------------------------------------------ tracing
+    def _xchg(self, ops, name: str, i: int):
+        """Issue one P2P group on the current stream; when tracing, bracket sends with
+        events on the send stream ([data ready, transfer complete])."""
+        sending = any(k == "send" for k, _, _ in ops)
+        ev0 = self.st.event("send") if (self.record_events and sending) else None
+        works = _exchange(ops)
+        if ev0 is not None:
+            for w in works:
+                w.wait()
+            nbytes = sum(t.numel() * t.element_size() for k, t, _ in ops if k == "send")
+            self.trace.append((name, i, SEND, ev0, self.st.event("send"), nbytes))
+        return works
+
+    def _compute(self, name: str, i: int, fn):
+        ev0 = self.st.event("compute") if self.record_events else None
+        fn()
+        if ev0 is not None:
+            self.trace.append((name, i, COMPUTE, ev0, self.st.event("compute"), 0))
+
+    # ------------------------------------------------------------- A side
+    def _a_pad(self, i: int) -> list[int]:
+        ev = self.pad_ready[i]
+        if ev is not None:
+            ev.synchronize()
+        return self.pad_host[i].tolist()
+
+    def _a_slices(self, i: int, pad: list[int]):
+        out = []
+        for f in range(self.topo.n_ffn):
+            lo, hi = self.topo.expert_block(f)
+            out.append((f, pad[lo], pad[hi], lo, hi))
+        return out
+
+    def set_host_io(self, xs, dys, ys, dxs) -> None:
+        """Pinned host tensors per micro-batch: inputs copied in on the copy stream at
+        iteration start, y / dx copied back as each micro-batch finishes (e2e mode)."""
+        self.host_io = (xs, dys, ys, dxs)
+
+    def _h2d_inputs(self):
+        xs, dys, _, _ = self.host_io
+        self.h2d_ready = []
+        with self.st.ctx("copy"):
+            for b, x, dy in zip(self.bufs, xs, dys):
+                b.x.copy_(x, non_blocking=True)
+                b.dy.copy_(dy, non_blocking=True)
+                self.h2d_ready.append(self.st.event("copy"))
+
+    def a_task(self, name: str, i: int, accumulate: bool):
+        b = self.bufs[i]
+        if name == "A_f":
+            if self.host_io is not None:
+                self.st.wait("compute", self.h2d_ready[i])
+            self.stages.a_dispatch(b, self.router)
+            done = self.st.event("compute")
+            with self.st.ctx("copy"):
+                self.st.wait("copy", done)
+                self.pad_host[i].copy_(b.pad_off, non_blocking=self.st.cuda)
+                self.pad_ready[i] = self.st.event("copy")
+            b.fwd_done = done
+        elif name == "A_t":
+            self._wait_works(b, "N2M")
+            self.stages.a_turnaround(b)
+            b.turn_done = self.st.event("compute")
+        elif name == "A_b":
+            self._wait_works(b, "N2M_b")
+            self.stages.a_backward(b, self.router, accumulate)
+            if self.host_io is not None:
+                _, _, ys, dxs = self.host_io
+                done = self.st.event("compute")
+                with self.st.ctx("copy"):
+                    self.st.wait("copy", done)
+                    ys[i].copy_(b.y, non_blocking=True)
+                    dxs[i].copy_(b.dx, non_blocking=True)
+
+    def a_comm(self, name: str, i: int, lane: str):
+        b = self.bufs[i]
+        pad = self._a_pad(i)
+        ops = []
+        if name == "M2N":
+            with self.st.ctx("send"):
+                self.st.wait("send", b.fwd_done)
+                for f, r0, r1, lo, hi in self._a_slices(i, pad):
+                    peer = self.topo.f_rank(f)
+                    hdr = b.pad_off[lo:hi + 1]
+                    ops += [("send", hdr, peer), ("send", b.x_perm[r0:r1], peer)]
+                b.works_M2N = self._xchg(ops, name, i)
+        elif name == "M2N_b":
+            with self.st.ctx("send"):
+                self.st.wait("send", b.turn_done)
+                for f, r0, r1, lo, hi in self._a_slices(i, pad):
+                    ops.append(("send", b.dy_perm[r0:r1], self.topo.f_rank(f)))
+                b.works_M2N_b = self._xchg(ops, name, i)
+        elif name in ("N2M", "N2M_b"):
+            dst = b.y_perm if name == "N2M" else b.dx_perm
+            with self.st.ctx("recv"):
+                for f, r0, r1, lo, hi in self._a_slices(i, pad):
+                    ops.append(("recv", dst[r0:r1], self.topo.f_rank(f)))
+                setattr(b, "works_" + name, _exchange(ops))
+
+    def _wait_works(self, obj, name):
+        for w in getattr(obj, "works_" + name, []) or []:
+            w.wait()  # CUDA: the current (compute) stream waits on the NCCL stream
+
+    # ------------------------------------------------------------- F side
+    def f_comm(self, name: str, i: int):
+        fm = self.fmb[i]
+        n_a = self.topo.n_attn
+        if name == "M2N":
+            with self.st.ctx("recv"):
+                hw = _exchange([("recv", fm.headers[a], self.topo.a_rank(a)) for a in range(n_a)])
+                for w in hw:
+                    w.wait()
+            with self.st.ctx("copy"):
+                self.st.wait("copy", self.st.event("recv"))
+                host = torch.stack(fm.headers).to("cpu", non_blocking=False) if not self.st.cuda else None
+                if self.st.cuda:
+                    pinned = torch.empty(n_a, self.E_loc + 1, dtype=I32, pin_memory=True)
+                    pinned.copy_(torch.stack(fm.headers), non_blocking=True)
+                    ev = self.st.event("copy")
+                    ev.synchronize()
+                    host = pinned
+            hdr = host.tolist()
+            # region layout: A rank a's slice at rows [base_a, base_a + n_a_rows), back to back
+            fm.slices, base, offs = [], 0, [0]
+            for a in range(n_a):
+                rows = hdr[a][-1] - hdr[a][0]
+                fm.slices.append((base, rows))
+                for e in range(self.E_loc):
+                    offs.append(base + hdr[a][e + 1] - hdr[a][0])
+                base += rows
+            if base > self.cap_f:
+                raise RuntimeError(f"F rank {self.rank}: {base} rows exceed capacity {self.cap_f}")
+            go = torch.tensor(offs, dtype=I32)
+            seg = torch.tensor([[i * self.cap_f + fm.slices[a][0] + hdr[a][e] - hdr[a][0]
+                                 for e in range(self.E_loc + 1)] for a in range(n_a)], dtype=I32)
+            if self.st.cuda:
+                go, seg = go.pin_memory(), seg.pin_memory()
+            fm.group_off = torch.empty(len(offs), dtype=I32, device=self.device)
+            fm.group_off.copy_(go, non_blocking=self.st.cuda)
+            self.seg_off[i * n_a:(i + 1) * n_a].copy_(seg, non_blocking=self.st.cuda)
+            with self.st.ctx("recv"):
+                ops = [("recv", fm.x_perm[b0:b0 + r], self.topo.a_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
+                fm.works["M2N"] = _exchange(ops)
+        elif name == "M2N_b":
+            with self.st.ctx("recv"):
+                ops = [("recv", fm.dy_perm[b0:b0 + r], self.topo.a_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
+                fm.works["M2N_b"] = _exchange(ops)
+        elif name in ("N2M", "N2M_b"):
+            src = fm.y_perm if name == "N2M" else fm.dx_perm
+            ready = fm.works.get(name + "_ready")
+            with self.st.ctx("send"):
+                self.st.wait("send", ready)
+                ops = [("send", src[b0:b0 + r], self.topo.a_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
+                fm.works[name] = self._xchg(ops, name, i)
+
+    def f_task(self, name: str, i: int):
+        fm = self.fmb[i]
+        if name == "F_f":
+            for w in fm.works.get("M2N", []):
+                w.wait()
+            self.stages.f_forward(fm, self.experts, fm.group_off)
+            fm.works["N2M_ready"] = self.st.event("compute")
+        elif name == "F_b":
+            for w in fm.works.get("M2N_b", []):
+                w.wait()
+            self.stages.f_backward(fm, self.experts, fm.group_off)
+            fm.works["N2M_b_ready"] = self.st.event("compute")
+
+    # ------------------------------------------------------------ iteration
+    def run_iteration(self, accumulate: bool = False) -> None:
+        # comm/copy streams must not touch this iteration's buffers before the
+        # compute stream is done with the previous iteration's uses of them
+        start = self.st.event("compute")
+        for which in ("send", "recv", "copy"):
+            self.st.wait(which, start)
+        self.trace = []
+        self.t0 = self.st.event("compute")
+        if self.host_io is not None and self.role == "A":
+            self._h2d_inputs()
+        for t in self.order:
+            name, i = t.name, t.microbatch
+            if self.role == "A":
+                if t.lane == COMPUTE:
+                    self._compute(name, i, lambda: self.a_task(name, i, accumulate or i > 0))
+                else:
+                    self.a_comm(name, i, t.lane)
+            else:
+                if t.lane == COMPUTE:
+                    self._compute(name, i, lambda: self.f_task(name, i))
+                else:
+                    self.f_comm(name, i)
+        if self.role == "F":
+            self._compute("W", -1, lambda: self.stages.f_wgrad(self.slab, self.experts, self.seg_off, accumulate))
+        else:
+            for b in self.bufs:
+                self._wait_works(b, "M2N")
+                self._wait_works(b, "M2N_b")
+            if self.host_io is not None:
+                self.st.compute.wait_stream(self.st.copy) if self.st.cuda else None
+            if self.a_group is not None and self.topo.n_attn > 1:
+                dist.all_reduce(self.router.dwg, group=self.a_group)
+        if self.role == "F":
+            for fm in self.fmb:
+                for k in ("N2M", "N2M_b"):
+                    for w in fm.works.get(k, []):
+                        w.wait()
+
+    def init_groups(self):
+        """Create the A-group communicator (collective: every rank must call it)."""
+        ranks = list(range(self.topo.n_attn))
+        g = dist.new_group(ranks)
+        if self.role == "A":
+            self.a_group = g
+
+
+def trace_intervals(rank: "AFPipeRank") -> list[tuple[str, int, str, float, float, int]]:
+    """(task, micro-batch, lane, start_ms, end_ms, bytes) relative to the iteration's t0
+    event (call after the iteration's work has completed)."""
+    out = []
+    for name, i, lane, e0, e1, nbytes in rank.trace:
+        out.append((name, i, lane, rank.t0.elapsed_time(e0), rank.t0.elapsed_time(e1), nbytes))
+    return out
+
+
+def env_rank() -> tuple[int, int, int]:
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))

@@ -57,9 +57,9 @@ def test_shape_errors_are_negative_codes_without_gpu(lib):
     assert rc == -3 and "multiple of 8" in _lib.last_error()
     rc = lib.dm_router_topk(None, 16, 8, 17, None, None, None, None)
     assert rc == -1
-    rc = lib.dm_grouped_w13_swiglu_fwd(None, None, None, 8, 100, 4096, 14336, None, None, None)
+    rc = lib.dm_grouped_w13_swiglu_fwd(None, None, None, 8, 8, 100, 4096, 14336, None, None, None)
     assert rc == -1 and "cap_rows" in _lib.last_error()
-    rc = lib.dm_grouped_wgrad(None, 100, None, 256, None, 1, 8, 1024, None, ctypes.c_float(0.0), None)
+    rc = lib.dm_grouped_wgrad(None, 100, None, 256, None, 1, 8, 1024, 1024, None, ctypes.c_float(0.0), None)
     assert rc == -1
     with pytest.raises(_lib.DMShapeError):
         _lib.call("dm_combine_fwd", None, None, None, 4, 10, 2, None, None)
