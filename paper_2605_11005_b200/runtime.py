@@ -107,10 +107,10 @@ class _Streams:
             return _Null()
         return torch.cuda.stream(getattr(self, which))
 
-    def event(self, which: str = "compute"):
+    def event(self, which: str = "compute", timing: bool = False):
         if not self.cuda:
             return None
-        ev = torch.cuda.Event()
+        ev = torch.cuda.Event(enable_timing=timing)
         ev.record(getattr(self, which))
         return ev
 
@@ -273,20 +273,20 @@ class AFPipeRank:
         """Issue one P2P group on the current stream; when tracing, bracket sends with
         events on the send stream ([data ready, transfer complete])."""
         sending = any(k == "send" for k, _, _ in ops)
-        ev0 = self.st.event("send") if (self.record_events and sending) else None
+        ev0 = self.st.event("send", True) if (self.record_events and sending) else None
         works = _exchange(ops)
         if ev0 is not None:
             for w in works:
                 w.wait()
             nbytes = sum(t.numel() * t.element_size() for k, t, _ in ops if k == "send")
-            self.trace.append((name, i, SEND, ev0, self.st.event("send"), nbytes))
+            self.trace.append((name, i, SEND, ev0, self.st.event("send", True), nbytes))
         return works
 
     def _compute(self, name: str, i: int, fn):
-        ev0 = self.st.event("compute") if self.record_events else None
+        ev0 = self.st.event("compute", True) if self.record_events else None
         fn()
         if ev0 is not None:
-            self.trace.append((name, i, COMPUTE, ev0, self.st.event("compute"), 0))
+            self.trace.append((name, i, COMPUTE, ev0, self.st.event("compute", True), 0))
 
     # ------------------------------------------------------------- A side
     def _a_pad(self, i: int) -> list[int]:
@@ -445,7 +445,7 @@ class AFPipeRank:
         for which in ("send", "recv", "copy"):
             self.st.wait(which, start)
         self.trace = []
-        self.t0 = self.st.event("compute")
+        self.t0 = self.st.event("compute", self.record_events)
         if self.host_io is not None and self.role == "A":
             self._h2d_inputs()
         for t in self.order:
