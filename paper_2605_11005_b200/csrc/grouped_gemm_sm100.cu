@@ -367,12 +367,23 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
 // its 128 rows (N half) of B per k-block, so per-SM smem operand traffic is
 // 32 KiB per 256x256x64 step instead of 48 KiB per 128x256x64 step of the
 // 1-SM kernel. The leader (rank 0) issues all MMAs; both CTAs' TMEM hold their
-// 128 accumulator rows; each CTA's epilogue drains its own half.
-constexpr int G2_STAGES = 6;
+// 128 accumulator rows; each CTA's epilogue drains its own half through
+// SWIZZLE_128B smem boxes and TMA bulk stores (fp32 accumulation into dW uses
+// the TMA reduce-add, so no read-modify-write passes through the SMs).
 constexpr uint32_t G2_A_BYTES = 128 * GBK * 2;   // 16 KiB (this CTA's M half)
 constexpr uint32_t G2_B_BYTES = 128 * GBK * 2;   // 16 KiB (this CTA's N half)
-constexpr size_t GEMM2_SMEM_BYTES =
-    1024 + G2_STAGES * (G2_A_BYTES + G2_B_BYTES) + 256 + 2 * (GEMM_MAX_GROUPS + 1) * sizeof(int);
+constexpr uint32_t BOX_BYTES = 4096;             // one 32-row x 128-byte staging box
+
+template <int EPI> constexpr int g2_stages() { return EPI == EPI_SWIGLU_BWD ? 4 : 5; }
+// per-epilogue-warp staging: BF16/F32 2 boxes (double buffer); SwiGLU fwd gate/up/act;
+// SwiGLU bwd dg/du out + g/u in
+template <int EPI> constexpr uint32_t g2_stg_bytes() {
+  return EPI == EPI_SWIGLU_FWD ? 3 * BOX_BYTES : EPI == EPI_SWIGLU_BWD ? 4 * BOX_BYTES : 2 * BOX_BYTES;
+}
+template <int EPI> constexpr size_t g2_smem_bytes() {
+  return 1024 + g2_stages<EPI>() * (G2_A_BYTES + G2_B_BYTES) + 4 * g2_stg_bytes<EPI>() + 256 +
+         2 * (GEMM_MAX_GROUPS + 1) * sizeof(int);
+}
 
 template <int RAGGED_K>
 __device__ __forceinline__ TileInfo decode_tile_2sm(int t, const int* tile_start, const int* off, int G,
@@ -416,21 +427,205 @@ __device__ __forceinline__ TileInfo decode_tile_2sm(int t, const int* tile_start
   return ti;
 }
 
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t* r) {
+  tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(r));
+  tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t(*)[16]>(r + 16));
+  tmem_ld16(taddr + 32, *reinterpret_cast<uint32_t(*)[16]>(r + 32));
+  tmem_ld16(taddr + 48, *reinterpret_cast<uint32_t(*)[16]>(r + 48));
+}
+
+// Write one thread's 64 fp32 accumulators (as bf16) into its 128-byte row of a box.
+__device__ __forceinline__ void box_row_bf16(uint32_t box, int lane, const uint32_t* v) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    st_shared_v4(box + sw128(lane, j),
+                 pack_bf16(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1])),
+                 pack_bf16(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3])),
+                 pack_bf16(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5])),
+                 pack_bf16(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7])));
+}
+
+// Epilogue of one epilogue warp (TMEM lane quarter q = rows q*32 .. q*32+31 of
+// this CTA's 128-row half). `stg` is the warp's private staging area; only lane 0
+// issues TMA and owns the bulk groups.
+template <int EPI>
+__device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, int q, int lane,
+                                             const GemmArgs& a, const CUtensorMap* tmC,
+                                             const CUtensorMap* tmAux, const CUtensorMap* tmIn,
+                                             uint8_t* stg, uint64_t* ibar, uint32_t& iphase) {
+  const uint32_t s0 = smem_u32(stg);
+  if constexpr (EPI == EPI_BF16) {
+    const int row0 = ti.m0 + q * 32;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v[64];
+      tmem_ld64(tacc + c * 64, v);
+      tmem_wait_ld();
+      if (c >= 2) {
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+      }
+      box_row_bf16(s0 + (c & 1) * BOX_BYTES, lane, v);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmC, stg + (c & 1) * BOX_BYTES, ti.n0 + c * 64, row0);
+        bulk_commit();
+      }
+    }
+  } else if constexpr (EPI == EPI_SWIGLU_FWD) {
+    // accumulator columns [0,128) = gate rows of W13, [128,256) = the matching up rows
+    const int row0 = ti.m0 + q * 32;
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 64) {
+      uint32_t g[64], u[64];
+      tmem_ld64(tacc + c, g);
+      tmem_ld64(tacc + 128 + c, u);
+      tmem_wait_ld();
+      if (c > 0) {
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+      }
+      box_row_bf16(s0, lane, g);
+      box_row_bf16(s0 + BOX_BYTES, lane, u);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float gf = __uint_as_float(g[i]), uf = __uint_as_float(u[i]);
+        g[i] = __float_as_uint(silu_f(gf) * uf);
+      }
+      box_row_bf16(s0 + 2 * BOX_BYTES, lane, g);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmAux, stg, ti.n0 + c, row0);
+        tma_store_2d(tmAux, stg + BOX_BYTES, ti.n0 + 128 + c, row0);
+        tma_store_2d(tmC, stg + 2 * BOX_BYTES, (ti.n0 >> 1) + c, row0);
+        bulk_commit();
+      }
+    }
+  } else if constexpr (EPI == EPI_SWIGLU_BWD) {
+    // accumulator = d_act for D_e columns [n0, n0+256); g/u come from the
+    // 128-block-interleaved h13 (d -> (d/128)*256 + d%128, +128 for up)
+    const int row0 = ti.m0 + q * 32;
+    const uint32_t in_g = s0 + 2 * BOX_BYTES, in_u = s0 + 3 * BOX_BYTES;
+    auto gcol_of = [&](int c) {
+      const int dcol = ti.n0 + c * 64;
+      return (dcol >> 7) * 256 + (dcol & 127);
+    };
+    if (lane == 0) {
+      mbar_expect_tx(ibar, 2 * BOX_BYTES);
+      tma_load_2d(stg + 2 * BOX_BYTES, tmIn, ibar, gcol_of(0), row0);
+      tma_load_2d(stg + 3 * BOX_BYTES, tmIn, ibar, gcol_of(0) + 128, row0);
+    }
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      const int gcol = gcol_of(c);
+      uint32_t d[64];
+      tmem_ld64(tacc + c * 64, d);
+      mbar_wait(ibar, iphase);
+      iphase ^= 1;
+      uint32_t gu[32], uu[32];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int4 gv = ld_shared_v4(in_g + sw128(lane, j));
+        const int4 uv = ld_shared_v4(in_u + sw128(lane, j));
+        gu[4 * j] = gv.x; gu[4 * j + 1] = gv.y; gu[4 * j + 2] = gv.z; gu[4 * j + 3] = gv.w;
+        uu[4 * j] = uv.x; uu[4 * j + 1] = uv.y; uu[4 * j + 2] = uv.z; uu[4 * j + 3] = uv.w;
+      }
+      tmem_wait_ld();
+      __syncwarp();
+      if (c + 1 < 4 && lane == 0) {  // inputs consumed: prefetch the next chunk's g/u
+        fence_proxy_async_smem();
+        mbar_expect_tx(ibar, 2 * BOX_BYTES);
+        tma_load_2d(stg + 2 * BOX_BYTES, tmIn, ibar, gcol_of(c + 1), row0);
+        tma_load_2d(stg + 3 * BOX_BYTES, tmIn, ibar, gcol_of(c + 1) + 128, row0);
+      }
+      // d[i] <- dg (bf16-pair packed later), reuse gu/uu for du
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float gg[2] = {bf16lo(gu[i]), bf16hi(gu[i])};
+        float uv2[2] = {bf16lo(uu[i]), bf16hi(uu[i])};
+        float rg[2], ru[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float da = __uint_as_float(d[2 * i + h]);
+          const float sg = 1.0f / (1.0f + __expf(-gg[h]));
+          ru[h] = da * gg[h] * sg;
+          rg[h] = da * uv2[h] * sg * (1.0f + gg[h] * (1.0f - sg));
+        }
+        gu[i] = pack_bf16(rg[0], rg[1]);
+        uu[i] = pack_bf16(ru[0], ru[1]);
+      }
+      if (c > 0) {
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        st_shared_v4(s0 + sw128(lane, j), gu[4 * j], gu[4 * j + 1], gu[4 * j + 2], gu[4 * j + 3]);
+        st_shared_v4(s0 + BOX_BYTES + sw128(lane, j), uu[4 * j], uu[4 * j + 1], uu[4 * j + 2], uu[4 * j + 3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tmAux, stg, gcol, row0);
+        tma_store_2d(tmAux, stg + BOX_BYTES, gcol + 128, row0);
+        bulk_commit();
+      }
+    }
+  } else {  // EPI_F32: dW_g rows (g*M + m) of a [G*M, N] fp32 matrix; beta in {0, 1}
+    const int grow0 = ti.g * a.M + ti.m0 + q * 32;
+    const bool empty = ti.kb_count == 0;
+    if (empty && a.beta != 0.0f) return;  // adding zeros
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      uint32_t v[32];
+      if (!empty) {
+        tmem_ld16(tacc + c * 32, *reinterpret_cast<uint32_t(*)[16]>(v));
+        tmem_ld16(tacc + c * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0u;
+      }
+      if (c >= 2) {
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+      }
+      const uint32_t box = s0 + (c & 1) * BOX_BYTES;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) st_shared_v4(box + sw128(lane, j), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (a.beta != 0.0f) tma_reduce_add_2d(tmC, stg + (c & 1) * BOX_BYTES, ti.n0 + c * 32, grow0);
+        else tma_store_2d(tmC, stg + (c & 1) * BOX_BYTES, ti.n0 + c * 32, grow0);
+        bulk_commit();
+      }
+    }
+  }
+}
+
 template <int A_MN, int B_MN, int RAGGED_K, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
-grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const GemmArgs args) {
+grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmAux,
+                        const __grid_constant__ CUtensorMap tmIn, const GemmArgs args) {
+  constexpr int STAGES = g2_stages<EPI>();
+  constexpr uint32_t STG = g2_stg_bytes<EPI>();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + G2_STAGES * G2_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + G2_STAGES * G2_B_BYTES);
-  uint64_t* empty = full + G2_STAGES;
-  uint64_t* tfull = empty + G2_STAGES;
+  uint8_t* sB = smem + STAGES * G2_A_BYTES;
+  uint8_t* sStg = sB + STAGES * G2_B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + 4 * STG);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* s_tile = reinterpret_cast<int*>(smem + G2_STAGES * (G2_A_BYTES + G2_B_BYTES) + 256);
+  uint64_t* ibar = tempty + 2;   // [4] per-epilogue-warp input barriers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ibar + 4);
+  int* s_tile = reinterpret_cast<int*>(sStg + 4 * STG + 256);
   int* s_off = s_tile + (GEMM_MAX_GROUPS + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -445,12 +640,15 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
     for (int i = threadIdx.x; i <= G; i += GEMM_THREADS) s_off[i] = args.group_off[i];
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int s = 0; s < G2_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
 #pragma unroll
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * 128); }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) mbar_init(&ibar[s], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+  if (warp == 3 && lane == 0) { tma_prefetch_desc(&tmC); tma_prefetch_desc(&tmAux); }
   if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
   __syncthreads();
   if (threadIdx.x == 32 * 3) {
@@ -510,7 +708,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
             tma_load_2d_2sm(b_dst, &tmB, &full[stage], nb0, b_gofs + kcoord);
             tma_load_2d_2sm(b_dst + 8192, &tmB, &full[stage], nb0 + 64, b_gofs + kcoord);
           }
-          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -544,7 +742,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
             umma_bf16_ss_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
           }
           umma_commit_2sm_mc(&empty[stage]);
-          if (++stage == G2_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         umma_commit_2sm_mc(&tfull[as]);
       }
@@ -553,6 +751,8 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
   } else if (warp >= 4) {
     // ------------------------------------------- epilogue warps (both CTAs)
     const int q = warp & 3;
+    uint8_t* stg = sStg + q * STG;
+    uint32_t iphase = 0;
     int it = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
       bool active;
@@ -562,13 +762,15 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       if (active) {
-        const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * GBN;
-        epilogue_row<EPI>(ti, trow, q * 32 + lane, args);
+        const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * GBN;
+        epilogue_tma<EPI>(ti, tacc, q, lane, args, &tmC, &tmAux, &tmIn, stg, &ibar[q], iphase);
       }
       tc_fence_before();
       if (leader) mbar_arrive(&tempty[as]);
       else mbar_arrive_cluster(&tempty[as], 0);
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   }
 
   tc_fence_before();
@@ -588,21 +790,28 @@ static bool use_2sm() {
   return v == 1;
 }
 
-static int make_tmap_bf16_2d(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer,
-                             uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
+static int make_tmap_2d(CUtensorMap* tm, const void* base, bool fp32, uint64_t inner, uint64_t outer,
+                       uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   if (!enc) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled entry point unavailable");
-  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((row_stride_elems * 2) & 15))
+  const uint64_t esz = fp32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((row_stride_elems * esz) & 15))
     return set_error(DM_ERR_ALIGN, "TMA operand base/stride not 16-byte aligned");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint64_t strides[1] = {row_stride_elems * esz};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(tm, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return DM_OK;
+}
+
+static int make_tmap_bf16_2d(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer,
+                             uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
+  return make_tmap_2d(tm, base, false, inner, outer, row_stride_elems, box_inner, box_outer);
 }
 
 // Builds both operand maps for the chosen path: the 2-SM kernel stages a
@@ -614,15 +823,35 @@ struct GemmOperand {
   bool is_b;
 };
 
+// A row-major epilogue tensor written (or, for `in`, read) by TMA in 32-row x
+// 128-byte boxes: 64 bf16 or 32 fp32 columns.
+struct EpiTensor {
+  const void* base = nullptr;
+  bool fp32 = false;
+  uint64_t cols = 0, rows = 0, ld = 0;
+};
+
+struct EpiTensors {
+  EpiTensor c, aux, in;
+};
+
 static int make_operand_map(CUtensorMap* tm, const GemmOperand& o, bool two_sm) {
   if (o.mn_major) return make_tmap_bf16_2d(tm, o.base, o.inner, o.outer, o.ld, 64, 64);
   const uint32_t rows = (o.is_b && !two_sm) ? 256 : 128;
   return make_tmap_bf16_2d(tm, o.base, o.inner, o.outer, o.ld, 64, rows);
 }
 
+static int make_epi_map(CUtensorMap* tm, const EpiTensor& t, const CUtensorMap& dummy) {
+  if (!t.base) {
+    *tm = dummy;
+    return DM_OK;
+  }
+  return make_tmap_2d(tm, t.base, t.fp32, t.cols, t.rows, t.ld, t.fp32 ? 32 : 64, 32);
+}
+
 template <int A_MN, int B_MN, int RAGGED_K, int EPI>
-static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const GemmArgs& args,
-                       cudaStream_t stream) {
+static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const EpiTensors& et,
+                       const GemmArgs& args, cudaStream_t stream) {
   const bool two = use_2sm();
   CUtensorMap ta, tb;
   int rc;
@@ -630,16 +859,22 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const GemmA
   if ((rc = make_operand_map(&tb, ob, two))) return rc;
   int grid = num_sms_current();
   if (two) {
+    if (EPI == EPI_F32 && args.beta != 0.0f && args.beta != 1.0f)
+      return set_error(DM_ERR_ARG, "wgrad beta must be 0 (overwrite) or 1 (TMA reduce-add)");
+    CUtensorMap tc, tx, ti;
+    if ((rc = make_epi_map(&tc, et.c, ta))) return rc;
+    if ((rc = make_epi_map(&tx, et.aux, ta))) return rc;
+    if ((rc = make_epi_map(&ti, et.in, ta))) return rc;
     auto kern = grouped_gemm_2sm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
+    constexpr size_t smem = g2_smem_bytes<EPI>();
     static bool configured = false;  // per instantiation
     if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)GEMM2_SMEM_BYTES);
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm2 smem)");
       configured = true;
     }
     grid &= ~1;
-    kern<<<grid, GEMM_THREADS, GEMM2_SMEM_BYTES, stream>>>(ta, tb, args);
+    kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, tc, tx, ti, args);
   } else {
     auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
     static bool configured = false;  // per instantiation
@@ -681,7 +916,10 @@ int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t
   GemmArgs a{};
   a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = 2 * De; a.K = H; a.b_group_rows = 2 * De;
   a.C = act; a.ldc = De; a.aux = reinterpret_cast<__nv_bfloat16*>(h13); a.ld_aux = 2 * De;
-  return launch_gemm<0, 0, 0, EPI_SWIGLU_FWD>(A, B, a, (cudaStream_t)stream);
+  EpiTensors et;
+  et.c = {act, false, (uint64_t)De, (uint64_t)cap_rows, (uint64_t)De};
+  et.aux = {h13, false, (uint64_t)2 * De, (uint64_t)cap_rows, (uint64_t)2 * De};
+  return launch_gemm<0, 0, 0, EPI_SWIGLU_FWD>(A, B, et, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* group_off, int G, int E,
@@ -695,7 +933,9 @@ int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* group_off,
   GemmArgs a{};
   a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = H; a.K = De; a.b_group_rows = H;
   a.C = y_perm; a.ldc = H;
-  return launch_gemm<0, 0, 0, EPI_BF16>(A, B, a, (cudaStream_t)stream);
+  EpiTensors et;
+  et.c = {y_perm, false, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H};
+  return launch_gemm<0, 0, 0, EPI_BF16>(A, B, et, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const void* h13,
@@ -711,7 +951,10 @@ int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const vo
   a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = De; a.K = H; a.b_group_rows = H;
   a.aux = reinterpret_cast<__nv_bfloat16*>(dh13); a.ld_aux = 2 * De;
   a.aux_in = reinterpret_cast<const __nv_bfloat16*>(h13); a.ld_aux_in = 2 * De;
-  return launch_gemm<0, 1, 0, EPI_SWIGLU_BWD>(A, B, a, (cudaStream_t)stream);
+  EpiTensors et;
+  et.aux = {dh13, false, (uint64_t)2 * De, (uint64_t)cap_rows, (uint64_t)2 * De};
+  et.in = {h13, false, (uint64_t)2 * De, (uint64_t)cap_rows, (uint64_t)2 * De};
+  return launch_gemm<0, 1, 0, EPI_SWIGLU_BWD>(A, B, et, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* group_off, int G, int E,
@@ -725,7 +968,9 @@ int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* group
   GemmArgs a{};
   a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = H; a.K = 2 * De; a.b_group_rows = 2 * De;
   a.C = dx_perm; a.ldc = H;
-  return launch_gemm<0, 1, 0, EPI_BF16>(A, B, a, (cudaStream_t)stream);
+  EpiTensors et;
+  et.c = {dx_perm, false, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H};
+  return launch_gemm<0, 1, 0, EPI_BF16>(A, B, et, a, (cudaStream_t)stream);
 }
 
 int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* seg_off,
@@ -745,7 +990,9 @@ int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const i
   a.num_groups = E; a.group_off = seg_off; a.M = M; a.N = N;
   a.C = dW; a.ldc = N; a.c_group_stride = (long long)M * N; a.beta = beta;
   a.seg_off = seg_off; a.nseg = nseg; a.seg_stride_rows = seg_stride_rows;
-  return launch_gemm<1, 1, 1, EPI_F32>(A, B, a, (cudaStream_t)stream);
+  EpiTensors et;
+  et.c = {dW, true, (uint64_t)N, (uint64_t)E * M, (uint64_t)N};
+  return launch_gemm<1, 1, 1, EPI_F32>(A, B, et, a, (cudaStream_t)stream);
 }
 
 }  // extern "C"
