@@ -168,7 +168,7 @@ router_wgrad_reg_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __re
   for (int e = 0; e < EM; ++e)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[e][i] = 0.0f;
-#pragma unroll 4
+#pragma unroll 8
   for (int t = t_beg; t < t_end; ++t) {
     float xf[8];
     unpack8(ld_nc_v4(x + (size_t)t * H + col), xf);

@@ -86,6 +86,110 @@ router_logits_kernel(const __nv_bfloat16* __restrict__ x, const float* __restric
   }
 }
 
+// Fused router for E <= EM (Mixtral-class gates): one pass over x computes the
+// canonical-order logits, top-k, softmax weights and the chunk histogram.
+// CTA = one 32-token chunk per pass (8 warps x 4 tokens), persistent over
+// chunks so W_g is staged into smem once per CTA; x chunks are prefetched
+// FUSED_UNROLL deep to keep enough bytes in flight for HBM.
+constexpr int FUSED_UNROLL = 4;
+
+template <int EM>
+__global__ void __launch_bounds__(256)
+router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg, int T, int H, int E,
+                    int k, float* __restrict__ logits, int32_t* __restrict__ idx, float* __restrict__ w,
+                    int32_t* __restrict__ chunk_hist) {
+  extern __shared__ float4 sw4[];
+  const float* sw = reinterpret_cast<const float*>(sw4);
+  __shared__ int shist[EM];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = H >> 3;
+  for (int i = threadIdx.x; i < E * H / 4; i += blockDim.x) sw4[i] = reinterpret_cast<const float4*>(wg)[i];
+  const int nchunk = (T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS;
+  for (int chunk = blockIdx.x; chunk < nchunk; chunk += gridDim.x) {
+    if (threadIdx.x < EM) shist[threadIdx.x] = 0;
+    __syncthreads();   // also orders the W_g fill before first use
+    const int tg = chunk * DM_CHUNK_TOKENS + warp * ROUTER_NT;
+    float acc[ROUTER_NT][EM];
+#pragma unroll
+    for (int t = 0; t < ROUTER_NT; ++t)
+#pragma unroll
+      for (int e = 0; e < EM; ++e) acc[t][e] = 0.0f;
+    for (int c0 = lane; c0 < nch; c0 += 32 * FUSED_UNROLL) {
+      int4 xv[FUSED_UNROLL][ROUTER_NT];
+#pragma unroll
+      for (int u = 0; u < FUSED_UNROLL; ++u)
+#pragma unroll
+        for (int t = 0; t < ROUTER_NT; ++t) {
+          const int c = c0 + 32 * u;
+          xv[u][t] = (c < nch && tg + t < T) ? ld_nc_v4(x + (size_t)(tg + t) * H + c * 8) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+      for (int u = 0; u < FUSED_UNROLL; ++u) {
+        const int c = c0 + 32 * u;
+        if (c >= nch) break;
+#pragma unroll
+        for (int e = 0; e < EM; ++e) {
+          if (e < E) {
+            const float4* wp = reinterpret_cast<const float4*>(sw + (size_t)e * H + c * 8);
+            const float4 w0 = wp[0], w1 = wp[1];
+#pragma unroll
+            for (int t = 0; t < ROUTER_NT; ++t) {
+              const uint32_t* xp = reinterpret_cast<const uint32_t*>(&xv[u][t]);
+              float a = acc[t][e];
+              a = __fmaf_rn(bf16lo(xp[0]), w0.x, a);
+              a = __fmaf_rn(bf16hi(xp[0]), w0.y, a);
+              a = __fmaf_rn(bf16lo(xp[1]), w0.z, a);
+              a = __fmaf_rn(bf16hi(xp[1]), w0.w, a);
+              a = __fmaf_rn(bf16lo(xp[2]), w1.x, a);
+              a = __fmaf_rn(bf16hi(xp[2]), w1.y, a);
+              a = __fmaf_rn(bf16lo(xp[3]), w1.z, a);
+              a = __fmaf_rn(bf16hi(xp[3]), w1.w, a);
+              acc[t][e] = a;
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < ROUTER_NT; ++t) {
+#pragma unroll
+      for (int e = 0; e < EM; ++e) acc[t][e] = warp_sum_butterfly(acc[t][e]);  // identical in every lane
+      const int tok = tg + t;
+      if (tok >= T) continue;
+      if (lane < E) {
+        float v = acc[t][0];
+#pragma unroll
+        for (int e = 1; e < EM; ++e) v = (lane == e) ? acc[t][e] : v;
+        logits[(size_t)tok * E + lane] = v;
+      }
+      // top-k over registers (uniform across lanes): ties -> lower expert id
+      unsigned taken = 0;
+      float sel_v[DM_MAX_TOPK];
+      int sel_e[DM_MAX_TOPK];
+      for (int j = 0; j < k; ++j) {
+        float bv = -INFINITY;
+        int be = -1;
+#pragma unroll
+        for (int e = 0; e < EM; ++e) {
+          if (e < E && !((taken >> e) & 1u) && (be < 0 || acc[t][e] > bv)) { bv = acc[t][e]; be = e; }
+        }
+        taken |= 1u << be;
+        sel_v[j] = bv;
+        sel_e[j] = be;
+      }
+      float s = 0.0f;
+      for (int j = 0; j < k; ++j) s += expf(sel_v[j] - sel_v[0]);
+      for (int j = lane; j < k; j += 32) {
+        idx[(size_t)tok * k + j] = sel_e[j];
+        w[(size_t)tok * k + j] = expf(sel_v[j] - sel_v[0]) / s;
+        atomicAdd(&shist[sel_e[j]], 1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < E) chunk_hist[(size_t)chunk * E + threadIdx.x] = shist[threadIdx.x];
+  }
+}
+
 // Warp per token: top-k by logit (ties -> lower expert id), weights = softmax
 // over the selected logits (== softmax then renormalise over the top-k).
 __global__ void __launch_bounds__(256)
@@ -198,7 +302,7 @@ __device__ __forceinline__ void zero_padding_rows(__nv_bfloat16* buf, const int3
 // (token-major (t, j) order within each expert, chunk bases from the scan);
 // then every warp copies whole token rows to their k destinations with
 // 128-bit loads/stores (x is read once, x_perm written once).
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
                const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ counts,
                const int32_t* __restrict__ pad_off, int T, int H, int E, int k,
@@ -240,14 +344,14 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
     int p[DM_MAX_TOPK];
     for (int j = 0; j < k; ++j) p[j] = spos[tt * k + j];
     int ch = lane;
-    for (; ch + 96 < nvec; ch += 128) {
-      int4 v[4];
+    for (; ch + 32 * 7 < nvec; ch += 256) {
+      int4 v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = ld_nc_v4(src + (ch + 32 * u) * 8);
+      for (int u = 0; u < 8; ++u) v[u] = ld_nc_v4(src + (ch + 32 * u) * 8);
       for (int j = 0; j < k; ++j) {
         __nv_bfloat16* dst = x_perm + (size_t)p[j] * H;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) st_v4(dst + (ch + 32 * u) * 8, v[u]);
+        for (int u = 0; u < 8; ++u) st_v4(dst + (ch + 32 * u) * 8, v[u]);
       }
     }
     for (; ch < nvec; ch += 32) {
@@ -287,6 +391,35 @@ int router_logits_launch(const void* x, const float* wg, float* logits, int T, i
       reinterpret_cast<const __nv_bfloat16*>(x), wg, logits, T, H, E, ec);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_logits launch");
+  note_launch();
+  return DM_OK;
+}
+
+// Returns -1 when the fused router does not apply (E > 16 or W_g over the smem budget).
+int router_fused_launch(const void* x, const float* wg, int T, int H, int E, int k, float* logits,
+                        int32_t* idx, float* w, int32_t* chunk_hist, cudaStream_t stream) {
+  const size_t smem = (size_t)E * H * sizeof(float);
+  if (E > 16 || smem > (size_t)ROUTER_SMEM_BUDGET) return -1;
+  if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(wg) & 15) return -1;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e1 = cudaFuncSetAttribute(router_fused_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          ROUTER_SMEM_BUDGET);
+    cudaError_t e2 = cudaFuncSetAttribute(router_fused_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          ROUTER_SMEM_BUDGET);
+    if (e1 != cudaSuccess) return set_cuda_error(e1, "cudaFuncSetAttribute(router_fused)");
+    if (e2 != cudaSuccess) return set_cuda_error(e2, "cudaFuncSetAttribute(router_fused)");
+    configured = true;
+  }
+  const int nchunk = dm_num_chunks(T);
+  int grid = nchunk < num_sms_current() ? nchunk : num_sms_current();
+  const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  if (E <= 8)
+    router_fused_kernel<8><<<grid, 256, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, chunk_hist);
+  else
+    router_fused_kernel<16><<<grid, 256, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, chunk_hist);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "router_fused launch");
   note_launch();
   return DM_OK;
 }
@@ -346,7 +479,7 @@ int dm_permute(const void* x, const int32_t* idx, const int32_t* chunk_base, con
     return set_error(DM_ERR_ALIGN, "permute rows must be 16-byte aligned");
   const int nchunk = dm_num_chunks(T);
   const size_t smem = (E + DM_CHUNK_TOKENS * k) * sizeof(int);
-  permute_kernel<<<nchunk, 128, smem, (cudaStream_t)stream>>>(
+  permute_kernel<<<nchunk, 256, smem, (cudaStream_t)stream>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), idx, chunk_base, counts, pad_off, T, H, E, k,
       row_map, src_token, reinterpret_cast<__nv_bfloat16*>(x_perm));
   cudaError_t e = cudaGetLastError();
@@ -362,8 +495,12 @@ int dm_route_and_dispatch(const void* x, const float* wg, int T, int H, int E, i
   if (rc) return rc;
   dm_route_ws ws;
   dm_route_workspace_layout(T, H, E, k, workspace, &ws);
-  if ((rc = dm_router_logits(x, wg, ws.logits, T, H, E, stream))) return rc;
-  if ((rc = dm_router_topk(ws.logits, T, E, k, idx, w, ws.chunk_hist, stream))) return rc;
+  if ((rc = router_fused_launch(x, wg, T, H, E, k, ws.logits, idx, w, ws.chunk_hist, (cudaStream_t)stream)) > 0)
+    return rc;
+  if (rc < 0) {  // gate too large for the fused kernel: logits pass + top-k pass
+    if ((rc = dm_router_logits(x, wg, ws.logits, T, H, E, stream))) return rc;
+    if ((rc = dm_router_topk(ws.logits, T, E, k, idx, w, ws.chunk_hist, stream))) return rc;
+  }
   if ((rc = dm_expert_scan(ws.chunk_hist, T, E, counts, pad_off, ws.chunk_base, stream))) return rc;
   return dm_permute(x, idx, ws.chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, x_perm, stream);
 }
