@@ -177,6 +177,7 @@ def run_ours(args, shape, exp):
     import torch.distributed as dist
 
     from paper_2605_11005_b200 import _lib
+    from paper_2605_11005_b200 import kernels as K
     from paper_2605_11005_b200.moe import MoELayer, a_combine, a_combine_bwd, a_dispatch, a_dispatch_bwd, \
         f_backward, f_forward
 
@@ -200,7 +201,8 @@ def run_ours(args, shape, exp):
     # per-stage CUDA events: GEMM (F) time and HBM-kernel (A) time inside the timed region
     class Ev:
         def __init__(self):
-            self.pairs = {"gemm": [], "dispatch": [], "combine_fwd": [], "combine_bwd": [], "permute_bwd": []}
+            self.pairs = {"gemm": [], "dispatch": [], "combine_fwd": [], "combine_bwd": [], "permute_bwd": [],
+                          "router_wgrad": []}
 
         def mark(self, name, fn):
             s = torch.cuda.Event(enable_timing=True)
@@ -225,7 +227,10 @@ def run_ours(args, shape, exp):
             ev.mark("combine_fwd", lambda: a_combine(buf))
             ev.mark("combine_bwd", lambda: a_combine_bwd(buf))
             ev.mark("gemm", lambda: f_backward(buf, layer.experts, acc, defer_wgrad=True))
-            ev.mark("permute_bwd", lambda: a_dispatch_bwd(buf, layer.router, acc))
+            ev.mark("permute_bwd", lambda: K.permute_bwd(buf.dx_perm, buf.row_map, buf.idx, buf.dlogit,
+                                                         layer.router.wg, buf.dx))
+            ev.mark("router_wgrad", lambda: K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws,
+                                                           layer.router.dwg, 1.0 if acc else 0.0))
         ev.mark("gemm", lambda: layer.wgrad(mb))
 
     for _ in range(args.warmup):
@@ -271,7 +276,8 @@ def run_ours(args, shape, exp):
     peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     hb = shape.hbm_bytes()
     hbm = {}
-    for name in ("dispatch", "combine_fwd", "combine_bwd", "permute_bwd"):
+    hb["router_wgrad"] = shape.T * shape.H * 2 + shape.T * shape.k * 8
+    for name in ("dispatch", "combine_fwd", "combine_bwd", "permute_bwd", "router_wgrad"):
         t = ev.total_ms(name) / (args.steps * mb)
         gbs = hb[name] / (t / 1e3) / 1e9
         hbm[name] = {"ms": round(t, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 3)}

@@ -26,22 +26,31 @@ __device__ __forceinline__ int4 pack8(const float (&f)[8]) {
   return v;
 }
 
+// KT = compile-time top-k (1, 2, 4, 8) so the per-token index/weight arrays stay in
+// registers and the j loops unroll; KT = 0 is the generic runtime-k version.
+#define DM_KT_ARRAY (KT ? KT : DM_MAX_TOPK)
+
 // y[t] = sum_j w[t,j] * y_perm[row_map[t,j]]
+template <int KT>
 __global__ void __launch_bounds__(256)
 combine_fwd_kernel(const __nv_bfloat16* __restrict__ y_perm, const int32_t* __restrict__ row_map,
-                   const float* __restrict__ w, int T, int H, int k, __nv_bfloat16* __restrict__ y) {
+                   const float* __restrict__ w, int T, int H, int k_rt, __nv_bfloat16* __restrict__ y) {
+  const int k = KT ? KT : k_rt;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int nvec = H >> 3;
   for (int t = warp; t < T; t += nwarps) {
-    int pos[DM_MAX_TOPK];
-    float wt[DM_MAX_TOPK];
+    int pos[DM_KT_ARRAY];
+    float wt[DM_KT_ARRAY];
+#pragma unroll
     for (int j = 0; j < k; ++j) { pos[j] = row_map[(size_t)t * k + j]; wt[j] = w[(size_t)t * k + j]; }
+#pragma unroll 4
     for (int ch = lane; ch < nvec; ch += 32) {
       float acc[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll
       for (int j = 0; j < k; ++j) {
         float f[8];
         unpack8(ld_nc_v4(y_perm + (size_t)pos[j] * H + ch * 8), f);
@@ -55,27 +64,32 @@ combine_fwd_kernel(const __nv_bfloat16* __restrict__ y_perm, const int32_t* __re
 
 // dy_perm[row_map[t,j]] = w[t,j] * dy[t];  dw[t,j] = <dy[t], y_perm[row_map[t,j]]>;
 // dlogit[t,j] = w_j * (dw_j - sum_i w_i dw_i)   (softmax over the selected logits).
+template <int KT>
 __global__ void __launch_bounds__(256)
 combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ y_perm,
                    const int32_t* __restrict__ row_map, const float* __restrict__ w,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ pad_off,
-                   int T, int H, int E, int k, __nv_bfloat16* __restrict__ dy_perm,
+                   int T, int H, int E, int k_rt, __nv_bfloat16* __restrict__ dy_perm,
                    float* __restrict__ dw, float* __restrict__ dlogit) {
+  const int k = KT ? KT : k_rt;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int nvec = H >> 3;
   for (int t = gwarp; t < T; t += nwarps) {
-    int pos[DM_MAX_TOPK];
-    float wt[DM_MAX_TOPK], part[DM_MAX_TOPK];
+    int pos[DM_KT_ARRAY];
+    float wt[DM_KT_ARRAY], part[DM_KT_ARRAY];
+#pragma unroll
     for (int j = 0; j < k; ++j) {
       pos[j] = row_map[(size_t)t * k + j];
       wt[j] = w[(size_t)t * k + j];
       part[j] = 0.0f;
     }
+#pragma unroll 4
     for (int ch = lane; ch < nvec; ch += 32) {
       float g[8];
       unpack8(ld_nc_v4(dy + (size_t)t * H + ch * 8), g);
+#pragma unroll
       for (int j = 0; j < k; ++j) {
         float f[8], o[8];
         unpack8(ld_nc_v4(y_perm + (size_t)pos[j] * H + ch * 8), f);
@@ -87,11 +101,13 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __
       }
     }
     float s = 0.0f;
+#pragma unroll
     for (int j = 0; j < k; ++j) {
       part[j] = warp_sum_butterfly(part[j]);
       s = __fmaf_rn(wt[j], part[j], s);
     }
     if (lane == 0) {
+#pragma unroll
       for (int j = 0; j < k; ++j) {
         dw[(size_t)t * k + j] = part[j];
         dlogit[(size_t)t * k + j] = wt[j] * (part[j] - s);
@@ -108,26 +124,31 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __
 }
 
 // dx[t] = sum_j dx_perm[row_map[t,j]] + sum_j dlogit[t,j] * W_g[idx[t,j], :]
+template <int KT>
 __global__ void __launch_bounds__(256)
 permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_map,
                    const int32_t* __restrict__ idx, const float* __restrict__ dlogit,
-                   const float* __restrict__ wg, int T, int H, int k, __nv_bfloat16* __restrict__ dx) {
+                   const float* __restrict__ wg, int T, int H, int k_rt, __nv_bfloat16* __restrict__ dx) {
+  const int k = KT ? KT : k_rt;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int nvec = H >> 3;
   for (int t = gwarp; t < T; t += nwarps) {
-    int pos[DM_MAX_TOPK], ex[DM_MAX_TOPK];
-    float dl[DM_MAX_TOPK];
+    int pos[DM_KT_ARRAY], ex[DM_KT_ARRAY];
+    float dl[DM_KT_ARRAY];
+#pragma unroll
     for (int j = 0; j < k; ++j) {
       pos[j] = row_map[(size_t)t * k + j];
       ex[j] = idx[(size_t)t * k + j];
       dl[j] = dlogit ? dlogit[(size_t)t * k + j] : 0.0f;
     }
+#pragma unroll 4
     for (int ch = lane; ch < nvec; ch += 32) {
       float acc[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll
       for (int j = 0; j < k; ++j) {
         float f[8];
         unpack8(ld_nc_v4(dx_perm + (size_t)pos[j] * H + ch * 8), f);
@@ -135,6 +156,7 @@ permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __r
         for (int i = 0; i < 8; ++i) acc[i] += f[i];
       }
       if (dlogit) {
+#pragma unroll
         for (int j = 0; j < k; ++j) {
           const float4* wr = reinterpret_cast<const float4*>(wg + (size_t)ex[j] * H + ch * 8);
           const float4 a = wr[0], b = wr[1];
@@ -250,9 +272,13 @@ extern "C" {
 int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,
                    void* y, void* stream) {
   if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK) return set_error(DM_ERR_SHAPE, "combine_fwd bad shape");
-  combine_fwd_kernel<<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k,
-      reinterpret_cast<__nv_bfloat16*>(y));
+  switch (k) {
+    case 1: combine_fwd_kernel<1><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
+    case 2: combine_fwd_kernel<2><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
+    case 4: combine_fwd_kernel<4><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
+    case 8: combine_fwd_kernel<8><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
+    default: combine_fwd_kernel<0><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "combine_fwd launch");
   note_launch();
@@ -263,9 +289,13 @@ int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_map, c
                    const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
                    void* dy_perm, float* dw, float* dlogit, void* stream) {
   if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK || E < 1) return set_error(DM_ERR_SHAPE, "combine_bwd bad shape");
-  combine_bwd_kernel<<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm),
-      row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit);
+  switch (k) {
+    case 1: combine_bwd_kernel<1><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
+    case 2: combine_bwd_kernel<2><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
+    case 4: combine_bwd_kernel<4><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
+    case 8: combine_bwd_kernel<8><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
+    default: combine_bwd_kernel<0><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "combine_bwd launch");
   note_launch();
@@ -275,9 +305,13 @@ int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_map, c
 int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* idx,
                    const float* dlogit, const float* wg, int T, int H, int k, void* dx, void* stream) {
   if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK) return set_error(DM_ERR_SHAPE, "permute_bwd bad shape");
-  permute_bwd_kernel<<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k,
-      reinterpret_cast<__nv_bfloat16*>(dx));
+  switch (k) {
+    case 1: permute_bwd_kernel<1><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
+    case 2: permute_bwd_kernel<2><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
+    case 4: permute_bwd_kernel<4><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
+    case 8: permute_bwd_kernel<8><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
+    default: permute_bwd_kernel<0><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "permute_bwd launch");
   note_launch();

@@ -88,38 +88,41 @@ router_logits_kernel(const __nv_bfloat16* __restrict__ x, const float* __restric
 
 // Fused router for E <= EM (Mixtral-class gates): one pass over x computes the
 // canonical-order logits, top-k, softmax weights and the chunk histogram.
-// CTA = one 32-token chunk per pass (8 warps x 4 tokens), persistent over
-// chunks so W_g is staged into smem once per CTA; x chunks are prefetched
-// FUSED_UNROLL deep to keep enough bytes in flight for HBM.
-constexpr int FUSED_UNROLL = 4;
+// A pass = 8 warps x NT tokens (NT * 8 / 32 chunks); CTAs are persistent over
+// passes so W_g is staged into smem once per CTA. Each W_g 32-byte read from
+// smem feeds NT tokens (smem bandwidth is the bound at small NT), and x chunks
+// are prefetched FUSED_UNROLL deep to keep enough bytes in flight for HBM.
+constexpr int FUSED_UNROLL = 2;
 
-template <int EM>
+template <int EM, int NT>
 __global__ void __launch_bounds__(256)
 router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg, int T, int H, int E,
                     int k, float* __restrict__ logits, int32_t* __restrict__ idx, float* __restrict__ w,
                     int32_t* __restrict__ chunk_hist) {
+  constexpr int PASS = 8 * NT;                          // tokens per CTA pass
+  constexpr int CPP = PASS / DM_CHUNK_TOKENS;           // chunks per pass
   extern __shared__ float4 sw4[];
   const float* sw = reinterpret_cast<const float*>(sw4);
-  __shared__ int shist[EM];
+  __shared__ int shist[CPP][EM];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = H >> 3;
   for (int i = threadIdx.x; i < E * H / 4; i += blockDim.x) sw4[i] = reinterpret_cast<const float4*>(wg)[i];
-  const int nchunk = (T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS;
-  for (int chunk = blockIdx.x; chunk < nchunk; chunk += gridDim.x) {
-    if (threadIdx.x < EM) shist[threadIdx.x] = 0;
+  const int npass = (T + PASS - 1) / PASS;
+  for (int pass = blockIdx.x; pass < npass; pass += gridDim.x) {
+    if (threadIdx.x < CPP * EM) (&shist[0][0])[threadIdx.x] = 0;
     __syncthreads();   // also orders the W_g fill before first use
-    const int tg = chunk * DM_CHUNK_TOKENS + warp * ROUTER_NT;
-    float acc[ROUTER_NT][EM];
+    const int tg = pass * PASS + warp * NT;
+    float acc[NT][EM];
 #pragma unroll
-    for (int t = 0; t < ROUTER_NT; ++t)
+    for (int t = 0; t < NT; ++t)
 #pragma unroll
       for (int e = 0; e < EM; ++e) acc[t][e] = 0.0f;
     for (int c0 = lane; c0 < nch; c0 += 32 * FUSED_UNROLL) {
-      int4 xv[FUSED_UNROLL][ROUTER_NT];
+      int4 xv[FUSED_UNROLL][NT];
 #pragma unroll
       for (int u = 0; u < FUSED_UNROLL; ++u)
 #pragma unroll
-        for (int t = 0; t < ROUTER_NT; ++t) {
+        for (int t = 0; t < NT; ++t) {
           const int c = c0 + 32 * u;
           xv[u][t] = (c < nch && tg + t < T) ? ld_nc_v4(x + (size_t)(tg + t) * H + c * 8) : make_int4(0, 0, 0, 0);
         }
@@ -133,7 +136,7 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
             const float4* wp = reinterpret_cast<const float4*>(sw + (size_t)e * H + c * 8);
             const float4 w0 = wp[0], w1 = wp[1];
 #pragma unroll
-            for (int t = 0; t < ROUTER_NT; ++t) {
+            for (int t = 0; t < NT; ++t) {
               const uint32_t* xp = reinterpret_cast<const uint32_t*>(&xv[u][t]);
               float a = acc[t][e];
               a = __fmaf_rn(bf16lo(xp[0]), w0.x, a);
@@ -151,7 +154,7 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
       }
     }
 #pragma unroll
-    for (int t = 0; t < ROUTER_NT; ++t) {
+    for (int t = 0; t < NT; ++t) {
 #pragma unroll
       for (int e = 0; e < EM; ++e) acc[t][e] = warp_sum_butterfly(acc[t][e]);  // identical in every lane
       const int tok = tg + t;
@@ -179,14 +182,20 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
       }
       float s = 0.0f;
       for (int j = 0; j < k; ++j) s += expf(sel_v[j] - sel_v[0]);
+      const int lc = (tok - pass * PASS) / DM_CHUNK_TOKENS;
       for (int j = lane; j < k; j += 32) {
         idx[(size_t)tok * k + j] = sel_e[j];
         w[(size_t)tok * k + j] = expf(sel_v[j] - sel_v[0]) / s;
-        atomicAdd(&shist[sel_e[j]], 1);
+        atomicAdd(&shist[lc][sel_e[j]], 1);
       }
     }
     __syncthreads();
-    if (threadIdx.x < E) chunk_hist[(size_t)chunk * E + threadIdx.x] = shist[threadIdx.x];
+    const int nchunk = (T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS;
+    if (threadIdx.x < CPP * E) {
+      const int lc = threadIdx.x / E, e = threadIdx.x % E;
+      const int chunk = pass * CPP + lc;
+      if (chunk < nchunk) chunk_hist[(size_t)chunk * E + e] = shist[lc][e];
+    }
   }
 }
 
@@ -312,7 +321,8 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
   int* run = s_perm;               // [E]
   int* spos = s_perm + E;          // [DM_CHUNK_TOKENS * k]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const int c = blockIdx.x;
+  const int split = gridDim.x / ((T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS);  // CTAs per chunk
+  const int c = blockIdx.x / split, part = blockIdx.x % split;
   const int t0 = c * DM_CHUNK_TOKENS;
   const int nt = min(DM_CHUNK_TOKENS, T - t0);
   const int nslots = nt * k;
@@ -330,8 +340,10 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
       if (valid) {
         const int pos = chunk_base[(size_t)c * E + e] + prior + rank;
         spos[s] = pos;
-        row_map[(size_t)t0 * k + s] = pos;
-        src_token[pos] = t0 + s / k;
+        if (part == 0) {
+          row_map[(size_t)t0 * k + s] = pos;
+          src_token[pos] = t0 + s / k;
+        }
         if (rank == 0) run[e] = prior + __popc(peers);
       }
       __syncwarp();
@@ -339,7 +351,7 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
   }
   __syncthreads();
   const int nvec = H >> 3;
-  for (int tt = warp; tt < nt; tt += nwarps) {
+  for (int tt = warp + part * nwarps; tt < nt; tt += nwarps * split) {
     const __nv_bfloat16* src = x + (size_t)(t0 + tt) * H;
     int p[DM_MAX_TOPK];
     for (int j = 0; j < k; ++j) p[j] = spos[tt * k + j];
@@ -359,10 +371,10 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
       for (int j = 0; j < k; ++j) st_v4(x_perm + (size_t)p[j] * H + ch * 8, v);
     }
   }
-  zero_padding_rows(x_perm, counts, pad_off, E, H, c * nwarps + warp, gridDim.x * nwarps, lane);
+  zero_padding_rows(x_perm, counts, pad_off, E, H, blockIdx.x * nwarps + warp, gridDim.x * nwarps, lane);
   // padding rows carry no token
   for (int e = 0; e < E; ++e) {
-    for (int r = pad_off[e] + counts[e] + c * blockDim.x + threadIdx.x; r < pad_off[e + 1];
+    for (int r = pad_off[e] + counts[e] + blockIdx.x * blockDim.x + threadIdx.x; r < pad_off[e + 1];
          r += gridDim.x * blockDim.x)
       src_token[r] = -1;
   }
@@ -403,21 +415,22 @@ int router_fused_launch(const void* x, const float* wg, int T, int H, int E, int
   if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(wg) & 15) return -1;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e1 = cudaFuncSetAttribute(router_fused_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e1 = cudaFuncSetAttribute(router_fused_kernel<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           ROUTER_SMEM_BUDGET);
-    cudaError_t e2 = cudaFuncSetAttribute(router_fused_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e2 = cudaFuncSetAttribute(router_fused_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           ROUTER_SMEM_BUDGET);
     if (e1 != cudaSuccess) return set_cuda_error(e1, "cudaFuncSetAttribute(router_fused)");
     if (e2 != cudaSuccess) return set_cuda_error(e2, "cudaFuncSetAttribute(router_fused)");
     configured = true;
   }
-  const int nchunk = dm_num_chunks(T);
-  int grid = nchunk < num_sms_current() ? nchunk : num_sms_current();
+  const int pass = E <= 8 ? 64 : 32;
+  const int npass = (T + pass - 1) / pass;
+  int grid = npass < num_sms_current() ? npass : num_sms_current();
   const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
   if (E <= 8)
-    router_fused_kernel<8><<<grid, 256, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, chunk_hist);
+    router_fused_kernel<8, 8><<<grid, 256, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, chunk_hist);
   else
-    router_fused_kernel<16><<<grid, 256, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, chunk_hist);
+    router_fused_kernel<16, 4><<<grid, 256, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, chunk_hist);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_fused launch");
   note_launch();
@@ -479,7 +492,11 @@ int dm_permute(const void* x, const int32_t* idx, const int32_t* chunk_base, con
     return set_error(DM_ERR_ALIGN, "permute rows must be 16-byte aligned");
   const int nchunk = dm_num_chunks(T);
   const size_t smem = (E + DM_CHUNK_TOKENS * k) * sizeof(int);
-  permute_kernel<<<nchunk, 256, smem, (cudaStream_t)stream>>>(
+  // several CTAs per 32-token chunk (each recomputes the chunk's positions) so the
+  // row copies use every SM: split = ceil(2 * SMs / chunks), at most 4
+  int split = (2 * num_sms_current() + nchunk - 1) / nchunk;
+  split = split < 1 ? 1 : (split > 4 ? 4 : split);
+  permute_kernel<<<nchunk * split, 256, smem, (cudaStream_t)stream>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), idx, chunk_base, counts, pad_off, T, H, E, k,
       row_map, src_token, reinterpret_cast<__nv_bfloat16*>(x_perm));
   cudaError_t e = cudaGetLastError();

@@ -296,10 +296,16 @@ class MoELayer:
         self.experts.dw13.zero_()
         self.experts.dw2.zero_()
 
-    # dispatch 4 + expert fwd 2 + combine 1 + combine_bwd 1 + dgrad 2 + permute_bwd 1 + router wgrad 2
-    launches_per_microbatch_deferred = 13
-    launches_per_microbatch = 15          # + 2 inline wgrad launches
     launches_per_wgrad_pass = 2
+
+    def launches_per_microbatch(self, deferred_wgrad: bool = False) -> int:
+        """dm kernel launches of one micro-batch: dispatch (fused router + scan + permute
+        = 3 when E <= 16 and W_g fits in smem, else logits + top-k + scan + permute = 4),
+        expert fwd 2, combine 1, combine bwd 1, dgrad 2, permute bwd 1, router wgrad 2,
+        plus 2 wgrad GEMMs unless deferred to the iteration's W pass."""
+        s = self.shape
+        fused = s.E <= 16 and s.E * s.H * 4 <= 160 * 1024
+        return (3 if fused else 4) + 9 + (0 if deferred_wgrad else 2)
 
 
 class MoEFunction(torch.autograd.Function):

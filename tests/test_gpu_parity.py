@@ -227,11 +227,11 @@ def test_launch_counter_moves(cuda):
     before = _lib.launch_count()
     layer.forward_backward(layer.buffers[0])
     torch.cuda.synchronize()
-    assert _lib.launch_count() - before == MoELayer.launches_per_microbatch
+    assert _lib.launch_count() - before == layer.launches_per_microbatch()
     before = _lib.launch_count()
     layer.iteration()
     torch.cuda.synchronize()
-    assert _lib.launch_count() - before == MoELayer.launches_per_microbatch_deferred + MoELayer.launches_per_wgrad_pass
+    assert _lib.launch_count() - before == layer.launches_per_microbatch(True) + MoELayer.launches_per_wgrad_pass
 
 
 def test_deferred_wgrad_equals_inline_accumulation(cuda):
