@@ -77,14 +77,15 @@ typedef struct dm_route_ws {
   float* logits;        /* [T, E] fp32 */
   int32_t* chunk_hist;  /* [nchunk, E] */
   int32_t* chunk_base;  /* [nchunk, E] */
+  int32_t* rank;        /* [T, k] stable rank of (t, j) among its chunk's slots of the same expert */
 } dm_route_ws;
 
 static inline size_t dm_align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 static inline size_t dm_route_workspace_size(int T, int H, int E, int k) {
-  (void)H; (void)k;
+  (void)H;
   size_t nchunk = (size_t)dm_num_chunks(T);
-  return dm_align256((size_t)T * E * 4) + 2 * dm_align256(nchunk * E * 4);
+  return dm_align256((size_t)T * E * 4) + 2 * dm_align256(nchunk * E * 4) + dm_align256((size_t)T * k * 4);
 }
 
 static inline void dm_route_workspace_layout(int T, int H, int E, int k, void* ws, dm_route_ws* out) {
@@ -96,6 +97,8 @@ static inline void dm_route_workspace_layout(int T, int H, int E, int k, void* w
   out->chunk_hist = (int32_t*)p;
   p += dm_align256(nchunk * E * 4);
   out->chunk_base = (int32_t*)p;
+  p += dm_align256(nchunk * E * 4);
+  out->rank = (int32_t*)p;
 }
 
 /* Tokens per router-wgrad partial block: small blocks (more parallelism) when the
@@ -123,17 +126,18 @@ DM_API size_t dm_router_wgrad_workspace_size_fn(int T, int H, int E);
 /* logits[T,E] = x[T,H] (bf16) . W_g[E,H]^T (fp32) in the canonical fixed order. */
 DM_API int dm_router_logits(const void* x, const float* wg, float* logits, int T, int H, int E, void* stream);
 /* top-k by logit (ties -> lower expert id); w = softmax over the selected logits;
- * chunk_hist[nchunk, E] per-chunk expert counts. */
-DM_API int dm_router_topk(const float* logits, int T, int E, int k, int32_t* idx, float* w,
-                   int32_t* chunk_hist, void* stream);
+ * rank[T, k] = stable rank of slot (t, j) among the slots of its DM_CHUNK_TOKENS-token
+ * chunk that chose the same expert; chunk_hist[nchunk, E] per-chunk expert counts. */
+DM_API int dm_router_topk(const float* logits, int T, int E, int k, int32_t* idx, float* w, int32_t* rank,
+                          int32_t* chunk_hist, void* stream);
 /* counts[E], pad_off[E+1] (DM_ROW_ALIGN-padded block offsets), chunk_base[nchunk, E]. */
 DM_API int dm_expert_scan(const int32_t* chunk_hist, int T, int E, int32_t* counts, int32_t* pad_off,
                    int32_t* chunk_base, void* stream);
-/* Stable counting sort: row_map[t*k+j] = position of (t,j); src_token[pos] = t
- * (-1 for padding); x_perm[pos] = x[t]; padding rows zeroed. */
-DM_API int dm_permute(const void* x, const int32_t* idx, const int32_t* chunk_base, const int32_t* counts,
-               const int32_t* pad_off, int T, int H, int E, int k, int32_t* row_map,
-               int32_t* src_token, void* x_perm, void* stream);
+/* Stable counting sort: row_map[t*k+j] = chunk_base[chunk(t), e] + rank[t*k+j];
+ * src_token[pos] = t (-1 for padding); x_perm[pos] = x[t]; padding rows zeroed. */
+DM_API int dm_permute(const void* x, const int32_t* idx, const int32_t* rank, const int32_t* chunk_base,
+                      const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
+                      int32_t* row_map, int32_t* src_token, void* x_perm, void* stream);
 /* logits -> topk -> scan -> permute; workspace of dm_route_workspace_size bytes. */
 DM_API int dm_route_and_dispatch(const void* x, const float* wg, int T, int H, int E, int k, void* workspace,
                           int32_t* idx, float* w, int32_t* counts, int32_t* pad_off,
@@ -179,7 +183,8 @@ DM_API int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row
                    void* dy_perm, float* dw, float* dlogit, void* stream);
 /* dx = sum_j dx_perm[row_map] + sum_j dlogit * W_g[idx]  (dlogit may be NULL). */
 DM_API int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* idx,
-                   const float* dlogit, const float* wg, int T, int H, int k, void* dx, void* stream);
+                          const float* dlogit, const float* wg, int T, int H, int E, int k, void* dx,
+                          void* stream);
 /* dW_g[E,H] = sum_{t,j} dlogit[t,j] x[t] at row idx[t,j] (+ beta * dW_g);
  * partial_ws of dm_router_wgrad_workspace_size bytes. */
 DM_API int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int T, int H, int E,

@@ -49,9 +49,9 @@ SIGNATURES: dict[str, tuple] = {
     "dm_route_workspace_size_fn": (_sz, [_i, _i, _i, _i]),
     "dm_router_wgrad_workspace_size_fn": (_sz, [_i, _i, _i]),
     "dm_router_logits": (_i, [_vp, _f32p, _f32p, _i, _i, _i, _vp]),
-    "dm_router_topk": (_i, [_f32p, _i, _i, _i, _i32p, _f32p, _i32p, _vp]),
+    "dm_router_topk": (_i, [_f32p, _i, _i, _i, _i32p, _f32p, _i32p, _i32p, _vp]),
     "dm_expert_scan": (_i, [_i32p, _i, _i, _i32p, _i32p, _i32p, _vp]),
-    "dm_permute": (_i, [_vp, _i32p, _i32p, _i32p, _i32p, _i, _i, _i, _i, _i32p, _i32p, _vp, _vp]),
+    "dm_permute": (_i, [_vp, _i32p, _i32p, _i32p, _i32p, _i32p, _i, _i, _i, _i, _i32p, _i32p, _vp, _vp]),
     "dm_route_and_dispatch": (_i, [_vp, _f32p, _i, _i, _i, _i, _vp, _i32p, _f32p, _i32p, _i32p,
                                    _i32p, _i32p, _vp, _vp]),
     "dm_grouped_w13_swiglu_fwd": (_i, [_vp, _vp, _i32p, _i, _i, _i, _i, _i, _vp, _vp, _vp]),
@@ -62,7 +62,7 @@ SIGNATURES: dict[str, tuple] = {
     "dm_combine_fwd": (_i, [_vp, _i32p, _f32p, _i, _i, _i, _vp, _vp]),
     "dm_combine_bwd": (_i, [_vp, _vp, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _i, _vp, _f32p,
                             _f32p, _vp]),
-    "dm_permute_bwd": (_i, [_vp, _i32p, _i32p, _f32p, _f32p, _i, _i, _i, _vp, _vp]),
+    "dm_permute_bwd": (_i, [_vp, _i32p, _i32p, _f32p, _f32p, _i, _i, _i, _i, _vp, _vp]),
     "dm_router_wgrad": (_i, [_vp, _i32p, _f32p, _i, _i, _i, _i, _f32p, _f32p, _f, _vp]),
 }
 
@@ -120,7 +120,7 @@ def num_chunks(T: int) -> int:
 def route_workspace_size(T: int, H: int, E: int, k: int) -> int:
     a = lambda v: (v + 255) & ~255  # noqa: E731
     nch = num_chunks(T)
-    return a(T * E * 4) + 2 * a(nch * E * 4)
+    return a(T * E * 4) + 2 * a(nch * E * 4) + a(T * k * 4)
 
 
 def router_wgrad_token_block(E: int) -> int:

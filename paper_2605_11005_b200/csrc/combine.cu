@@ -171,6 +171,70 @@ permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __r
   }
 }
 
+// Permute backward for E <= EM: warp per (256-column chunk, token block); each
+// lane holds its 8 columns of every W_g row in registers, so the router dx term
+// sum_j dlogit[t,j] * W_g[idx[t,j], :] costs no memory traffic (the per-token W_g
+// row reads of permute_bwd_kernel were L1-bound).
+constexpr int PBWD_TOKENS = 16;
+
+template <int EM, int KT>
+__global__ void __launch_bounds__(256)
+permute_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_map,
+                       const int32_t* __restrict__ idx, const float* __restrict__ dlogit,
+                       const float* __restrict__ wg, int T, int H, int E, int k_rt,
+                       __nv_bfloat16* __restrict__ dx) {
+  const int k = KT ? KT : k_rt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = ((blockIdx.x * (blockDim.x >> 5) + warp) * 32 + lane) * 8;
+  if (col >= H) return;
+  float wr[EM][8];
+#pragma unroll
+  for (int e = 0; e < EM; ++e) {
+    if (e < E && dlogit) {
+      const float4 a = *reinterpret_cast<const float4*>(wg + (size_t)e * H + col);
+      const float4 b = *reinterpret_cast<const float4*>(wg + (size_t)e * H + col + 4);
+      wr[e][0] = a.x; wr[e][1] = a.y; wr[e][2] = a.z; wr[e][3] = a.w;
+      wr[e][4] = b.x; wr[e][5] = b.y; wr[e][6] = b.z; wr[e][7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wr[e][i] = 0.0f;
+    }
+  }
+  const int t_beg = blockIdx.y * PBWD_TOKENS, t_end = min(T, t_beg + PBWD_TOKENS);
+#pragma unroll 2
+  for (int t = t_beg; t < t_end; ++t) {
+    int pos[KT ? KT : DM_MAX_TOPK];
+    float gw[EM];
+#pragma unroll
+    for (int e = 0; e < EM; ++e) gw[e] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < k; ++j) {
+      pos[j] = row_map[(size_t)t * k + j];
+      if (dlogit) {
+        const int ej = idx[(size_t)t * k + j];
+        const float dl = dlogit[(size_t)t * k + j];
+#pragma unroll
+        for (int e = 0; e < EM; ++e) gw[e] = (ej == e) ? dl : gw[e];
+      }
+    }
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < k; ++j) {
+      float f[8];
+      unpack8(ld_nc_v4(dx_perm + (size_t)pos[j] * H + col), f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += f[i];
+    }
+#pragma unroll
+    for (int e = 0; e < EM; ++e)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(gw[e], wr[e][i], acc[i]);
+    st_v4(dx + (size_t)t * H + col, pack8(acc));
+  }
+}
+
 // Router weight gradient, stage 1 (E <= 16): warp per (256-column chunk, token
 // block); each lane owns 8 columns and keeps acc[E][8] in registers, reading x
 // with 128-bit loads. gw[e] = dlogit[t,j] when idx[t,j] == e (each expert appears
@@ -303,14 +367,30 @@ int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_map, c
 }
 
 int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* idx,
-                   const float* dlogit, const float* wg, int T, int H, int k, void* dx, void* stream) {
-  if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK) return set_error(DM_ERR_SHAPE, "permute_bwd bad shape");
-  switch (k) {
-    case 1: permute_bwd_kernel<1><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
-    case 2: permute_bwd_kernel<2><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
-    case 4: permute_bwd_kernel<4><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
-    case 8: permute_bwd_kernel<8><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
-    default: permute_bwd_kernel<0><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dx_perm), row_map, idx, dlogit, wg, T, H, k, reinterpret_cast<__nv_bfloat16*>(dx)); break;
+                   const float* dlogit, const float* wg, int T, int H, int E, int k, void* dx, void* stream) {
+  if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK || E < 1) return set_error(DM_ERR_SHAPE, "permute_bwd bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  const __nv_bfloat16* dxp = reinterpret_cast<const __nv_bfloat16*>(dx_perm);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(dx);
+  if (E <= 16) {
+    dim3 grid((H / 8 + 255) / 256, (T + PBWD_TOKENS - 1) / PBWD_TOKENS);
+#define DM_PBWD(EMV, KTV) permute_bwd_reg_kernel<EMV, KTV><<<grid, 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, E, k, out)
+    if (E <= 8) {
+      switch (k) { case 1: DM_PBWD(8, 1); break; case 2: DM_PBWD(8, 2); break; case 4: DM_PBWD(8, 4); break;
+                   case 8: DM_PBWD(8, 8); break; default: DM_PBWD(8, 0); break; }
+    } else {
+      switch (k) { case 1: DM_PBWD(16, 1); break; case 2: DM_PBWD(16, 2); break; case 4: DM_PBWD(16, 4); break;
+                   case 8: DM_PBWD(16, 8); break; default: DM_PBWD(16, 0); break; }
+    }
+#undef DM_PBWD
+  } else {
+    switch (k) {
+      case 1: permute_bwd_kernel<1><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
+      case 2: permute_bwd_kernel<2><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
+      case 4: permute_bwd_kernel<4><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
+      case 8: permute_bwd_kernel<8><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
+      default: permute_bwd_kernel<0><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
+    }
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "permute_bwd launch");
@@ -328,12 +408,12 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
   const int ntb = (T + tbt - 1) / tbt;
   cudaStream_t st = (cudaStream_t)stream;
   if (E <= 16) {
-    dim3 grid((H / 8 + 255) / 256, ntb);
+    dim3 grid((H / 8 + 127) / 128, ntb);
     if (E <= 8)
-      router_wgrad_reg_kernel<8><<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
+      router_wgrad_reg_kernel<8><<<grid, 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
                                                        T, H, E, k, tbt, partial_ws);
     else
-      router_wgrad_reg_kernel<16><<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
+      router_wgrad_reg_kernel<16><<<grid, 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
                                                         T, H, E, k, tbt, partial_ws);
   } else {
     int cw = 128;

@@ -86,57 +86,86 @@ router_logits_kernel(const __nv_bfloat16* __restrict__ x, const float* __restric
   }
 }
 
-// Fused router for E <= EM (Mixtral-class gates): one pass over x computes the
-// canonical-order logits, top-k, softmax weights and the chunk histogram.
-// A pass = 8 warps x NT tokens (NT * 8 / 32 chunks); CTAs are persistent over
-// passes so W_g is staged into smem once per CTA. Each W_g 32-byte read from
-// smem feeds NT tokens (smem bandwidth is the bound at small NT), and x chunks
-// are prefetched FUSED_UNROLL deep to keep enough bytes in flight for HBM.
-constexpr int FUSED_UNROLL = 2;
+// Stable within-chunk ranks (warp 0): sel[] holds the chunk's expert ids in
+// token-major (t, j) order; rank[s] = number of earlier slots of the chunk that
+// chose the same expert. run[] (E ints, zeroed) ends as the chunk histogram.
+__device__ __forceinline__ void chunk_ranks(const int* sel, int nslots, int* run, int32_t* rank_out, int lane) {
+  for (int base = 0; base < nslots; base += 32) {
+    const int s = base + lane;
+    const bool valid = s < nslots;
+    const int e = valid ? sel[s] : -1 - lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int r = __popc(peers & ((1u << lane) - 1u));
+    const int prior = valid ? run[e] : 0;
+    __syncwarp();
+    if (valid) {
+      rank_out[s] = prior + r;
+      if (r == 0) run[e] = prior + __popc(peers);
+    }
+    __syncwarp();
+  }
+}
 
-template <int EM, int NT>
-__global__ void __launch_bounds__(256)
+// Fused router for E <= EM (Mixtral-class gates): one pass over x computes the
+// canonical-order logits, top-k, softmax weights, the within-chunk ranks and
+// the chunk histogram. CTA = one 32-token chunk per pass (16 warps x 2 tokens),
+// persistent over chunks so W_g is staged into smem once per CTA. W_g is stored
+// lane-interleaved ([e][iteration][half][lane] float4) so every 128-bit smem
+// read of a warp is 512 contiguous bytes (no wasted wavefronts); x is prefetched
+// FUSED_UNROLL chunks deep.
+constexpr int FUSED_UNROLL = 4;
+constexpr int FUSED_NT = 2;
+constexpr int FUSED_WARPS = DM_CHUNK_TOKENS / FUSED_NT;   // 16
+
+template <int EM>
+__global__ void __launch_bounds__(FUSED_WARPS * 32)
 router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg, int T, int H, int E,
                     int k, float* __restrict__ logits, int32_t* __restrict__ idx, float* __restrict__ w,
-                    int32_t* __restrict__ chunk_hist) {
-  constexpr int PASS = 8 * NT;                          // tokens per CTA pass
-  constexpr int CPP = PASS / DM_CHUNK_TOKENS;           // chunks per pass
+                    int32_t* __restrict__ rank, int32_t* __restrict__ chunk_hist) {
   extern __shared__ float4 sw4[];
-  const float* sw = reinterpret_cast<const float*>(sw4);
-  __shared__ int shist[CPP][EM];
+  __shared__ int sel[DM_CHUNK_TOKENS * DM_MAX_TOPK];
+  __shared__ int run[EM];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = H >> 3;
-  for (int i = threadIdx.x; i < E * H / 4; i += blockDim.x) sw4[i] = reinterpret_cast<const float4*>(wg)[i];
-  const int npass = (T + PASS - 1) / PASS;
-  for (int pass = blockIdx.x; pass < npass; pass += gridDim.x) {
-    if (threadIdx.x < CPP * EM) (&shist[0][0])[threadIdx.x] = 0;
+  const int NI = (nch + 31) >> 5;
+  for (int i = threadIdx.x; i < E * NI * 64; i += blockDim.x) {
+    const int l = i & 31, half = (i >> 5) & 1, rest = i >> 6;
+    const int it = rest % NI, e = rest / NI;
+    const int c = it * 32 + l;
+    sw4[i] = c < nch ? reinterpret_cast<const float4*>(wg + (size_t)e * H + c * 8)[half]
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int nchunk = (T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS;
+  for (int chunk = blockIdx.x; chunk < nchunk; chunk += gridDim.x) {
+    if (threadIdx.x < EM) run[threadIdx.x] = 0;
     __syncthreads();   // also orders the W_g fill before first use
-    const int tg = pass * PASS + warp * NT;
-    float acc[NT][EM];
+    const int t0 = chunk * DM_CHUNK_TOKENS;
+    const int tg = t0 + warp * FUSED_NT;
+    float acc[FUSED_NT][EM];
 #pragma unroll
-    for (int t = 0; t < NT; ++t)
+    for (int t = 0; t < FUSED_NT; ++t)
 #pragma unroll
       for (int e = 0; e < EM; ++e) acc[t][e] = 0.0f;
-    for (int c0 = lane; c0 < nch; c0 += 32 * FUSED_UNROLL) {
-      int4 xv[FUSED_UNROLL][NT];
+    for (int it0 = 0; it0 < NI; it0 += FUSED_UNROLL) {
+      int4 xv[FUSED_UNROLL][FUSED_NT];
 #pragma unroll
       for (int u = 0; u < FUSED_UNROLL; ++u)
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int c = c0 + 32 * u;
-          xv[u][t] = (c < nch && tg + t < T) ? ld_nc_v4(x + (size_t)(tg + t) * H + c * 8) : make_int4(0, 0, 0, 0);
+        for (int t = 0; t < FUSED_NT; ++t) {
+          const int c = (it0 + u) * 32 + lane;
+          xv[u][t] = (it0 + u < NI && c < nch && tg + t < T) ? ld_nc_v4(x + (size_t)(tg + t) * H + c * 8)
+                                                            : make_int4(0, 0, 0, 0);
         }
 #pragma unroll
       for (int u = 0; u < FUSED_UNROLL; ++u) {
-        const int c = c0 + 32 * u;
-        if (c >= nch) break;
+        if (it0 + u >= NI) break;
 #pragma unroll
         for (int e = 0; e < EM; ++e) {
           if (e < E) {
-            const float4* wp = reinterpret_cast<const float4*>(sw + (size_t)e * H + c * 8);
-            const float4 w0 = wp[0], w1 = wp[1];
+            const float4* wp = sw4 + ((size_t)(e * NI + it0 + u) * 2) * 32 + lane;
+            const float4 w0 = wp[0], w1 = wp[32];
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
+            for (int t = 0; t < FUSED_NT; ++t) {
               const uint32_t* xp = reinterpret_cast<const uint32_t*>(&xv[u][t]);
               float a = acc[t][e];
               a = __fmaf_rn(bf16lo(xp[0]), w0.x, a);
@@ -154,7 +183,7 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
       }
     }
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
+    for (int t = 0; t < FUSED_NT; ++t) {
 #pragma unroll
       for (int e = 0; e < EM; ++e) acc[t][e] = warp_sum_butterfly(acc[t][e]);  // identical in every lane
       const int tok = tg + t;
@@ -182,32 +211,29 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
       }
       float s = 0.0f;
       for (int j = 0; j < k; ++j) s += expf(sel_v[j] - sel_v[0]);
-      const int lc = (tok - pass * PASS) / DM_CHUNK_TOKENS;
       for (int j = lane; j < k; j += 32) {
         idx[(size_t)tok * k + j] = sel_e[j];
         w[(size_t)tok * k + j] = expf(sel_v[j] - sel_v[0]) / s;
-        atomicAdd(&shist[lc][sel_e[j]], 1);
+        sel[(tok - t0) * k + j] = sel_e[j];
       }
     }
     __syncthreads();
-    const int nchunk = (T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS;
-    if (threadIdx.x < CPP * E) {
-      const int lc = threadIdx.x / E, e = threadIdx.x % E;
-      const int chunk = pass * CPP + lc;
-      if (chunk < nchunk) chunk_hist[(size_t)chunk * E + e] = shist[lc][e];
-    }
+    if (warp == 0) chunk_ranks(sel, min(DM_CHUNK_TOKENS, T - t0) * k, run, rank + (size_t)t0 * k, lane);
+    __syncthreads();
+    if (threadIdx.x < E) chunk_hist[(size_t)chunk * E + threadIdx.x] = run[threadIdx.x];
   }
 }
 
-// Warp per token: top-k by logit (ties -> lower expert id), weights = softmax
-// over the selected logits (== softmax then renormalise over the top-k).
+// Generic top-k (any E): warp per token over the logits row; ties -> lower expert
+// id; weights = softmax over the selected logits. CTA per chunk also produces the
+// within-chunk ranks and the chunk histogram.
 __global__ void __launch_bounds__(256)
 router_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int32_t* __restrict__ idx,
-                   float* __restrict__ w, int32_t* __restrict__ chunk_hist) {
-  extern __shared__ int shist[];
+                   float* __restrict__ w, int32_t* __restrict__ rank, int32_t* __restrict__ chunk_hist) {
+  extern __shared__ int run[];   // [E]
+  __shared__ int sel[DM_CHUNK_TOKENS * DM_MAX_TOPK];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < E; i += blockDim.x) shist[i] = 0;
-  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) run[i] = 0;
   const int t0 = blockIdx.x * DM_CHUNK_TOKENS;
   for (int tt = warp; tt < DM_CHUNK_TOKENS; tt += nwarps) {
     const int t = t0 + tt;
@@ -239,12 +265,14 @@ router_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int32_
       for (int j = 0; j < k; ++j) {
         idx[(size_t)t * k + j] = sel_e[j];
         w[(size_t)t * k + j] = expf(sel_v[j] - sel_v[0]) / s;
-        atomicAdd(&shist[sel_e[j]], 1);
+        sel[tt * k + j] = sel_e[j];
       }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < E; i += blockDim.x) chunk_hist[(size_t)blockIdx.x * E + i] = shist[i];
+  if (warp == 0) chunk_ranks(sel, min(DM_CHUNK_TOKENS, T - t0) * k, run, rank + (size_t)t0 * k, lane);
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) chunk_hist[(size_t)blockIdx.x * E + i] = run[i];
 }
 
 // One CTA, warp per expert: pass 1 sums the expert's chunk counts, thread 0
@@ -275,7 +303,7 @@ expert_scan_kernel(const int32_t* __restrict__ hist, int nchunk, int E, int32_t*
   __syncthreads();
   for (int e = threadIdx.x; e <= E; e += blockDim.x) pad_off[e] = s_off[e];
   for (int e = warp; e < E; e += nwarps) {
-    int run = s_off[e];
+    int runv = s_off[e];
     for (int c0 = 0; c0 < nchunk; c0 += 32) {
       const int c = c0 + lane;
       const int v = c < nchunk ? hist[(size_t)c * E + e] : 0;
@@ -285,81 +313,50 @@ expert_scan_kernel(const int32_t* __restrict__ hist, int nchunk, int E, int32_t*
         const int o = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += o;
       }
-      if (c < nchunk) chunk_base[(size_t)c * E + e] = run + incl - v;
-      run += __shfl_sync(0xffffffffu, incl, 31);
+      if (c < nchunk) chunk_base[(size_t)c * E + e] = runv + incl - v;
+      runv += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
 }
 
-// Zero rows [pad_off[e] + counts[e], pad_off[e+1]) of a permuted buffer; the
-// caller's grid strides over them so padding never feeds NaN into wgrad.
-__device__ __forceinline__ void zero_padding_rows(__nv_bfloat16* buf, const int32_t* counts,
-                                                  const int32_t* pad_off, int E, int H,
-                                                  int worker, int nworkers, int lane) {
-  const int4 z = make_int4(0, 0, 0, 0);
-  for (int e = 0; e < E; ++e) {
-    const int beg = pad_off[e] + counts[e];
-    const int end = pad_off[e + 1];
-    for (int r = beg + worker; r < end; r += nworkers) {
-      __nv_bfloat16* row = buf + (size_t)r * H;
-      for (int c = lane; c < (H >> 3); c += 32) st_v4(row + c * 8, z);
-    }
-  }
-}
-
-// CTA per chunk of DM_CHUNK_TOKENS tokens. Warp 0 assigns stable positions
-// (token-major (t, j) order within each expert, chunk bases from the scan);
-// then every warp copies whole token rows to their k destinations with
-// 128-bit loads/stores (x is read once, x_perm written once).
+// Permute (scatter-copy), warp per token: pos(t, j) = chunk_base[chunk(t), e] +
+// rank[t, j]; x[t] is read once with 8-deep 128-bit loads and written to its k
+// expert rows. Every warp then helps zero the padding rows (they feed the
+// ragged-K wgrad, so they must be finite) and mark them src_token = -1.
+template <int KT>
 __global__ void __launch_bounds__(256)
 permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
-               const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ counts,
-               const int32_t* __restrict__ pad_off, int T, int H, int E, int k,
-               int32_t* __restrict__ row_map, int32_t* __restrict__ src_token,
+               const int32_t* __restrict__ rank, const int32_t* __restrict__ chunk_base,
+               const int32_t* __restrict__ counts, const int32_t* __restrict__ pad_off, int T, int H,
+               int E, int k_rt, int32_t* __restrict__ row_map, int32_t* __restrict__ src_token,
                __nv_bfloat16* __restrict__ x_perm) {
-  extern __shared__ int s_perm[];
-  int* run = s_perm;               // [E]
-  int* spos = s_perm + E;          // [DM_CHUNK_TOKENS * k]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const int split = gridDim.x / ((T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS);  // CTAs per chunk
-  const int c = blockIdx.x / split, part = blockIdx.x % split;
-  const int t0 = c * DM_CHUNK_TOKENS;
-  const int nt = min(DM_CHUNK_TOKENS, T - t0);
-  const int nslots = nt * k;
-  for (int i = threadIdx.x; i < E; i += blockDim.x) run[i] = 0;
-  __syncthreads();
-  if (warp == 0) {
-    for (int base = 0; base < nslots; base += 32) {
-      const int s = base + lane;
-      const bool valid = s < nslots;
-      const int e = valid ? idx[(size_t)t0 * k + s] : -1 - lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, e);
-      const int rank = __popc(peers & ((1u << lane) - 1u));
-      const int prior = valid ? run[e] : 0;
-      __syncwarp();
-      if (valid) {
-        const int pos = chunk_base[(size_t)c * E + e] + prior + rank;
-        spos[s] = pos;
-        if (part == 0) {
-          row_map[(size_t)t0 * k + s] = pos;
-          src_token[pos] = t0 + s / k;
-        }
-        if (rank == 0) run[e] = prior + __popc(peers);
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
+  const int k = KT ? KT : k_rt;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int nvec = H >> 3;
-  for (int tt = warp + part * nwarps; tt < nt; tt += nwarps * split) {
-    const __nv_bfloat16* src = x + (size_t)(t0 + tt) * H;
-    int p[DM_MAX_TOPK];
-    for (int j = 0; j < k; ++j) p[j] = spos[tt * k + j];
+  for (int t = gwarp; t < T; t += nwarps) {
+    const int c = t / DM_CHUNK_TOKENS;
+    int p[KT ? KT : DM_MAX_TOPK];
+#pragma unroll
+    for (int j = 0; j < k; ++j) {
+      const int e = idx[(size_t)t * k + j];
+      p[j] = chunk_base[(size_t)c * E + e] + rank[(size_t)t * k + j];
+    }
+    if (lane < k) {
+      int pj = p[0];
+#pragma unroll
+      for (int j = 1; j < k; ++j) pj = (lane == j) ? p[j] : pj;
+      row_map[(size_t)t * k + lane] = pj;
+      src_token[pj] = t;
+    }
+    const __nv_bfloat16* src = x + (size_t)t * H;
     int ch = lane;
     for (; ch + 32 * 7 < nvec; ch += 256) {
       int4 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) v[u] = ld_nc_v4(src + (ch + 32 * u) * 8);
+#pragma unroll
       for (int j = 0; j < k; ++j) {
         __nv_bfloat16* dst = x_perm + (size_t)p[j] * H;
 #pragma unroll
@@ -368,15 +365,18 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
     }
     for (; ch < nvec; ch += 32) {
       const int4 v = ld_nc_v4(src + ch * 8);
+#pragma unroll
       for (int j = 0; j < k; ++j) st_v4(x_perm + (size_t)p[j] * H + ch * 8, v);
     }
   }
-  zero_padding_rows(x_perm, counts, pad_off, E, H, blockIdx.x * nwarps + warp, gridDim.x * nwarps, lane);
-  // padding rows carry no token
+  const int4 z = make_int4(0, 0, 0, 0);
   for (int e = 0; e < E; ++e) {
-    for (int r = pad_off[e] + counts[e] + blockIdx.x * blockDim.x + threadIdx.x; r < pad_off[e + 1];
-         r += gridDim.x * blockDim.x)
-      src_token[r] = -1;
+    const int beg = pad_off[e] + counts[e], end = pad_off[e + 1];
+    for (int r = beg + gwarp; r < end; r += nwarps) {
+      __nv_bfloat16* row = x_perm + (size_t)r * H;
+      for (int cc = lane; cc < nvec; cc += 32) st_v4(row + cc * 8, z);
+      if (lane == 0) src_token[r] = -1;
+    }
   }
 }
 
@@ -409,32 +409,40 @@ int router_logits_launch(const void* x, const float* wg, float* logits, int T, i
 
 // Returns -1 when the fused router does not apply (E > 16 or W_g over the smem budget).
 int router_fused_launch(const void* x, const float* wg, int T, int H, int E, int k, float* logits,
-                        int32_t* idx, float* w, int32_t* chunk_hist, cudaStream_t stream) {
-  const size_t smem = (size_t)E * H * sizeof(float);
+                        int32_t* idx, float* w, int32_t* rank, int32_t* chunk_hist, cudaStream_t stream) {
+  const int NI = ((H >> 3) + 31) >> 5;
+  const size_t smem = (size_t)E * NI * 64 * sizeof(float4);
   if (E > 16 || smem > (size_t)ROUTER_SMEM_BUDGET) return -1;
   if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(wg) & 15) return -1;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e1 = cudaFuncSetAttribute(router_fused_kernel<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e1 = cudaFuncSetAttribute(router_fused_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           ROUTER_SMEM_BUDGET);
-    cudaError_t e2 = cudaFuncSetAttribute(router_fused_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e2 = cudaFuncSetAttribute(router_fused_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           ROUTER_SMEM_BUDGET);
     if (e1 != cudaSuccess) return set_cuda_error(e1, "cudaFuncSetAttribute(router_fused)");
     if (e2 != cudaSuccess) return set_cuda_error(e2, "cudaFuncSetAttribute(router_fused)");
     configured = true;
   }
-  const int pass = E <= 8 ? 64 : 32;
-  const int npass = (T + pass - 1) / pass;
-  int grid = npass < num_sms_current() ? npass : num_sms_current();
+  const int nchunk = dm_num_chunks(T);
+  const int grid = nchunk < num_sms_current() ? nchunk : num_sms_current();
   const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
   if (E <= 8)
-    router_fused_kernel<8, 8><<<grid, 256, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, chunk_hist);
+    router_fused_kernel<8><<<grid, FUSED_WARPS * 32, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, rank,
+                                                                      chunk_hist);
   else
-    router_fused_kernel<16, 4><<<grid, 256, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, chunk_hist);
+    router_fused_kernel<16><<<grid, FUSED_WARPS * 32, smem, stream>>>(xb, wg, T, H, E, k, logits, idx, w, rank,
+                                                                       chunk_hist);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_fused launch");
   note_launch();
   return DM_OK;
+}
+
+static int token_grid_dispatch(int T) {
+  int blocks = (T + 7) / 8;  // 8 warps (tokens) per 256-thread block
+  const int cap = num_sms_current() * 8;
+  return blocks < cap ? blocks : cap;
 }
 
 }  // namespace dm
@@ -459,12 +467,13 @@ int dm_router_logits(const void* x, const float* wg, float* logits, int T, int H
   return router_logits_launch(x, wg, logits, T, H, E, (cudaStream_t)stream);
 }
 
-int dm_router_topk(const float* logits, int T, int E, int k, int32_t* idx, float* w,
+int dm_router_topk(const float* logits, int T, int E, int k, int32_t* idx, float* w, int32_t* rank,
                    int32_t* chunk_hist, void* stream) {
   int rc = check_route_shape(T, 8, E, k);
   if (rc) return rc;
   const int nchunk = dm_num_chunks(T);
-  router_topk_kernel<<<nchunk, 256, E * sizeof(int), (cudaStream_t)stream>>>(logits, T, E, k, idx, w, chunk_hist);
+  router_topk_kernel<<<nchunk, 256, E * sizeof(int), (cudaStream_t)stream>>>(logits, T, E, k, idx, w, rank,
+                                                                             chunk_hist);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_topk launch");
   note_launch();
@@ -483,22 +492,24 @@ int dm_expert_scan(const int32_t* chunk_hist, int T, int E, int32_t* counts, int
   return DM_OK;
 }
 
-int dm_permute(const void* x, const int32_t* idx, const int32_t* chunk_base, const int32_t* counts,
-               const int32_t* pad_off, int T, int H, int E, int k, int32_t* row_map,
+int dm_permute(const void* x, const int32_t* idx, const int32_t* rank, const int32_t* chunk_base,
+               const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k, int32_t* row_map,
                int32_t* src_token, void* x_perm, void* stream) {
   int rc = check_route_shape(T, H, E, k);
   if (rc) return rc;
   if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(x_perm) & 15)
     return set_error(DM_ERR_ALIGN, "permute rows must be 16-byte aligned");
-  const int nchunk = dm_num_chunks(T);
-  const size_t smem = (E + DM_CHUNK_TOKENS * k) * sizeof(int);
-  // several CTAs per 32-token chunk (each recomputes the chunk's positions) so the
-  // row copies use every SM: split = ceil(2 * SMs / chunks), at most 4
-  int split = (2 * num_sms_current() + nchunk - 1) / nchunk;
-  split = split < 1 ? 1 : (split > 4 ? 4 : split);
-  permute_kernel<<<nchunk * split, 256, smem, (cudaStream_t)stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(x), idx, chunk_base, counts, pad_off, T, H, E, k,
-      row_map, src_token, reinterpret_cast<__nv_bfloat16*>(x_perm));
+  const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  __nv_bfloat16* xp = reinterpret_cast<__nv_bfloat16*>(x_perm);
+  const int grid = token_grid_dispatch(T);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (k) {
+    case 1: permute_kernel<1><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
+    case 2: permute_kernel<2><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
+    case 4: permute_kernel<4><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
+    case 8: permute_kernel<8><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
+    default: permute_kernel<0><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "permute launch");
   note_launch();
@@ -512,14 +523,15 @@ int dm_route_and_dispatch(const void* x, const float* wg, int T, int H, int E, i
   if (rc) return rc;
   dm_route_ws ws;
   dm_route_workspace_layout(T, H, E, k, workspace, &ws);
-  if ((rc = router_fused_launch(x, wg, T, H, E, k, ws.logits, idx, w, ws.chunk_hist, (cudaStream_t)stream)) > 0)
+  if ((rc = router_fused_launch(x, wg, T, H, E, k, ws.logits, idx, w, ws.rank, ws.chunk_hist,
+                                (cudaStream_t)stream)) > 0)
     return rc;
   if (rc < 0) {  // gate too large for the fused kernel: logits pass + top-k pass
     if ((rc = dm_router_logits(x, wg, ws.logits, T, H, E, stream))) return rc;
-    if ((rc = dm_router_topk(ws.logits, T, E, k, idx, w, ws.chunk_hist, stream))) return rc;
+    if ((rc = dm_router_topk(ws.logits, T, E, k, idx, w, ws.rank, ws.chunk_hist, stream))) return rc;
   }
   if ((rc = dm_expert_scan(ws.chunk_hist, T, E, counts, pad_off, ws.chunk_base, stream))) return rc;
-  return dm_permute(x, idx, ws.chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, x_perm, stream);
+  return dm_permute(x, idx, ws.rank, ws.chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, x_perm, stream);
 }
 
 }  // extern "C"

@@ -45,11 +45,13 @@ def router_logits(x, wg, logits, stream=None):
     _lib.call("dm_router_logits", _ptr(x), _ptr(wg), _ptr(logits), T, H, E, _stream(stream))
 
 
-def router_topk(logits, k, idx, w, chunk_hist, stream=None):
+def router_topk(logits, k, idx, w, rank, chunk_hist, stream=None):
     T, E = logits.shape
     _check(idx, torch.int32, (T, k), "idx"); _check(w, torch.float32, (T, k), "w")
+    _check(rank, torch.int32, (T, k), "rank")
     _check(chunk_hist, torch.int32, (_lib.num_chunks(T), E), "chunk_hist")
-    _lib.call("dm_router_topk", _ptr(logits), T, E, k, _ptr(idx), _ptr(w), _ptr(chunk_hist), _stream(stream))
+    _lib.call("dm_router_topk", _ptr(logits), T, E, k, _ptr(idx), _ptr(w), _ptr(rank), _ptr(chunk_hist),
+              _stream(stream))
 
 
 def expert_scan(chunk_hist, T, counts, pad_off, chunk_base, stream=None):
@@ -60,15 +62,15 @@ def expert_scan(chunk_hist, T, counts, pad_off, chunk_base, stream=None):
               _stream(stream))
 
 
-def permute(x, idx, chunk_base, counts, pad_off, row_map, src_token, x_perm, stream=None):
+def permute(x, idx, rank, chunk_base, counts, pad_off, row_map, src_token, x_perm, stream=None):
     T, H = x.shape
     k = idx.shape[1]
     E = counts.shape[0]
     _check(row_map, torch.int32, (T, k), "row_map")
     if x_perm.dtype != BF16 or x_perm.shape[1] != H:
         raise ValueError("x_perm must be bf16 [cap, H]")
-    _lib.call("dm_permute", _ptr(x), _ptr(idx), _ptr(chunk_base), _ptr(counts), _ptr(pad_off), T, H, E, k,
-              _ptr(row_map), _ptr(src_token), _ptr(x_perm), _stream(stream))
+    _lib.call("dm_permute", _ptr(x), _ptr(idx), _ptr(rank), _ptr(chunk_base), _ptr(counts), _ptr(pad_off), T,
+              H, E, k, _ptr(row_map), _ptr(src_token), _ptr(x_perm), _stream(stream))
 
 
 def route_and_dispatch(x, wg, k, workspace, idx, w, counts, pad_off, row_map, src_token, x_perm, stream=None):
@@ -163,7 +165,8 @@ def combine_bwd(dy, y_perm, row_map, w, counts, pad_off, dy_perm, dw, dlogit, st
 def permute_bwd(dx_perm, row_map, idx, dlogit, wg, dx, stream=None):
     T, k = row_map.shape
     H = dx.shape[1]
-    _lib.call("dm_permute_bwd", _ptr(dx_perm), _ptr(row_map), _ptr(idx), _ptr(dlogit), _ptr(wg), T, H, k,
+    E = wg.shape[0]
+    _lib.call("dm_permute_bwd", _ptr(dx_perm), _ptr(row_map), _ptr(idx), _ptr(dlogit), _ptr(wg), T, H, E, k,
               _ptr(dx), _stream(stream))
 
 

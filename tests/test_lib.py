@@ -55,7 +55,7 @@ def test_shape_errors_are_negative_codes_without_gpu(lib):
     # H not a multiple of 8 -> DM_ERR_ALIGN, topk too large -> DM_ERR_SHAPE; both checked on the host
     rc = lib.dm_router_logits(None, None, None, 16, 12, 4, None)
     assert rc == -3 and "multiple of 8" in _lib.last_error()
-    rc = lib.dm_router_topk(None, 16, 8, 17, None, None, None, None)
+    rc = lib.dm_router_topk(None, 16, 8, 17, None, None, None, None, None)
     assert rc == -1
     rc = lib.dm_grouped_w13_swiglu_fwd(None, None, None, 8, 8, 100, 4096, 14336, None, None, None)
     assert rc == -1 and "cap_rows" in _lib.last_error()
