@@ -103,7 +103,7 @@ static inline void dm_route_workspace_layout(int T, int H, int E, int k, void* w
 
 /* Tokens per router-wgrad partial block: small blocks (more parallelism) when the
  * per-block partials are small, i.e. for few experts. */
-static inline int dm_router_wgrad_token_block(int E) { return E <= 16 ? 64 : 512; }
+static inline int dm_router_wgrad_token_block(int E) { return E <= 16 ? 128 : 512; }
 
 static inline size_t dm_router_wgrad_workspace_size(int T, int H, int E) {
   int tb = dm_router_wgrad_token_block(E);

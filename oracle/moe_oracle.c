@@ -10,9 +10,12 @@
  * the top-k experts ... outputs ... reduced by a weighted sum"
  * — under the conventions written in DESIGN.md §3:
  *   1. logits = x . W_g^T in fp32, canonical order:
- *        partial[p] (p in [0,32)) = fmaf chain over 8-element chunks c with
- *        c % 32 == p, c ascending, elements ascending, starting at +0.0f;
- *        then xor butterfly with offsets 16,8,4,2,1 of round-to-nearest adds.
+ *        partial[p][s] (lane p in [0,32), parity s in {0,1}) = fmaf chain over
+ *        the 8-element chunks c with c % 32 == p (c ascending) and, inside each
+ *        chunk, the elements j with j % 2 == s (j ascending), starting at +0.0f;
+ *        v[p] = partial[p][0] + partial[p][1]; then an xor butterfly with
+ *        offsets 16,8,4,2,1 of round-to-nearest adds over v.
+ *        (Two chains per lane let the GPU use packed fp32x2 FMAs, FFMA2.)
  *   2. top-k by descending logit, ties -> lower expert id.
  *   3. weights = softmax over the k selected logits (== softmax, then
  *      renormalise over the top-k).
@@ -41,14 +44,14 @@ static inline float bf16_to_f32(uint16_t v) {
 __attribute__((target_clones("fma", "default")))
 void dm_oracle_router_logits(const uint16_t* x, const float* wg, int T, int H, int E, float* logits) {
   const int nch = H / 8;
-  float* part = (float*)malloc(sizeof(float) * 32 * (size_t)E);
+  float* part = (float*)malloc(sizeof(float) * 64 * (size_t)E);   /* [p][s][e] */
   float* xr = (float*)malloc(sizeof(float) * (size_t)H);
   for (int t = 0; t < T; ++t) {
     for (int h = 0; h < H; ++h) xr[h] = bf16_to_f32(x[(size_t)t * H + h]);
-    for (int i = 0; i < 32 * E; ++i) part[i] = 0.0f;
+    for (int i = 0; i < 64 * E; ++i) part[i] = 0.0f;
     for (int c = 0; c < nch; ++c) {
-      float* pp = part + (size_t)(c % 32) * E;
       for (int j = 0; j < 8; ++j) {
+        float* pp = part + ((size_t)(c % 32) * 2 + (j & 1)) * E;
         const int h = c * 8 + j;
         const float xv = xr[h];
         for (int e = 0; e < E; ++e) pp[e] = fmaf(xv, wg[(size_t)e * H + h], pp[e]);
@@ -56,7 +59,7 @@ void dm_oracle_router_logits(const uint16_t* x, const float* wg, int T, int H, i
     }
     for (int e = 0; e < E; ++e) {
       float v[32];
-      for (int p = 0; p < 32; ++p) v[p] = part[(size_t)p * E + e];
+      for (int p = 0; p < 32; ++p) v[p] = part[((size_t)p * 2) * E + e] + part[((size_t)p * 2 + 1) * E + e];
       for (int off = 16; off > 0; off >>= 1) {
         float nxt[32];
         for (int l = 0; l < 32; ++l) nxt[l] = v[l] + v[l ^ off];

@@ -124,7 +124,7 @@ def route_workspace_size(T: int, H: int, E: int, k: int) -> int:
 
 
 def router_wgrad_token_block(E: int) -> int:
-    return 64 if E <= 16 else 512
+    return 128 if E <= 16 else 512
 
 
 def router_wgrad_workspace_size(T: int, H: int, E: int) -> int:

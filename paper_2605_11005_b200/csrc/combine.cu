@@ -178,7 +178,7 @@ permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __r
 constexpr int PBWD_TOKENS = 16;
 
 template <int EM, int KT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 permute_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_map,
                        const int32_t* __restrict__ idx, const float* __restrict__ dlogit,
                        const float* __restrict__ wg, int T, int H, int E, int k_rt,
@@ -235,18 +235,21 @@ permute_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t*
   }
 }
 
-// Router weight gradient, stage 1 (E <= 16): warp per (256-column chunk, token
-// block); each lane owns 8 columns and keeps acc[E][8] in registers, reading x
-// with 128-bit loads. gw[e] = dlogit[t,j] when idx[t,j] == e (each expert appears
-// at most once per token), accumulated over the block's tokens in ascending order.
+// Router weight gradient, stage 1 (E <= 16): CTA per (256-column chunk, token
+// block); lane owns 8 columns and keeps acc[E][8] in registers, reading x with
+// 128-bit loads; the NW warps take interleaved tokens of the block and are then
+// reduced through smem in fixed warp order (deterministic). gw[e] = dlogit[t,j]
+// when idx[t,j] == e (each expert appears at most once per token).
 template <int EM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(EM == 8 ? 256 : 128)
 router_wgrad_reg_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
                         const float* __restrict__ dlogit, int T, int H, int E, int k, int tb_tokens,
                         float* __restrict__ partial) {
+  constexpr int NW = EM == 8 ? 8 : 4;
+  extern __shared__ float red[];   // [NW][EM][8][32]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int col = ((blockIdx.x * (blockDim.x >> 5) + warp) * 32 + lane) * 8;
-  if (col >= H) return;
+  const int col = (blockIdx.x * 32 + lane) * 8;
+  const bool live = col < H;
   const int tb = blockIdx.y;
   const int t_beg = tb * tb_tokens, t_end = min(T, t_beg + tb_tokens);
   float acc[EM][8];
@@ -254,28 +257,46 @@ router_wgrad_reg_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __re
   for (int e = 0; e < EM; ++e)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[e][i] = 0.0f;
-#pragma unroll 8
-  for (int t = t_beg; t < t_end; ++t) {
-    float xf[8];
-    unpack8(ld_nc_v4(x + (size_t)t * H + col), xf);
-    float gw[EM];
+  if (live) {
+#pragma unroll 4
+    for (int t = t_beg + warp; t < t_end; t += NW) {
+      float xf[8];
+      unpack8(ld_nc_v4(x + (size_t)t * H + col), xf);
+      float gw[EM];
 #pragma unroll
-    for (int e = 0; e < EM; ++e) gw[e] = 0.0f;
-    for (int j = 0; j < k; ++j) {
-      const int ej = idx[(size_t)t * k + j];
-      const float dl = dlogit[(size_t)t * k + j];
+      for (int e = 0; e < EM; ++e) gw[e] = 0.0f;
+      for (int j = 0; j < k; ++j) {
+        const int ej = idx[(size_t)t * k + j];
+        const float dl = dlogit[(size_t)t * k + j];
 #pragma unroll
-      for (int e = 0; e < EM; ++e) gw[e] = (ej == e) ? dl : gw[e];
+        for (int e = 0; e < EM; ++e) gw[e] = (ej == e) ? dl : gw[e];
+      }
+#pragma unroll
+      for (int e = 0; e < EM; ++e)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[e][i] = __fmaf_rn(gw[e], xf[i], acc[e][i]);
     }
-#pragma unroll
-    for (int e = 0; e < EM; ++e)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[e][i] = __fmaf_rn(gw[e], xf[i], acc[e][i]);
   }
-  for (int e = 0; e < E && e < EM; ++e) {
-    float4* o = reinterpret_cast<float4*>(partial + ((size_t)tb * E + e) * H + col);
-    o[0] = make_float4(acc[e][0], acc[e][1], acc[e][2], acc[e][3]);
-    o[1] = make_float4(acc[e][4], acc[e][5], acc[e][6], acc[e][7]);
+#pragma unroll
+  for (int e = 0; e < EM; ++e)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[((warp * EM + e) * 8 + i) * 32 + lane] = acc[e][i];
+  __syncthreads();
+  // warp w finalises experts w, w+NW, ...: sum over warps 0..NW-1 in order
+  for (int e = warp; e < E; e += NW) {
+    float o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float v = 0.0f;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) v += red[((q * EM + e) * 8 + i) * 32 + lane];
+      o[i] = v;
+    }
+    if (live) {
+      float4* dst = reinterpret_cast<float4*>(partial + ((size_t)tb * E + e) * H + col);
+      dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+      dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+    }
   }
 }
 
@@ -408,12 +429,22 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
   const int ntb = (T + tbt - 1) / tbt;
   cudaStream_t st = (cudaStream_t)stream;
   if (E <= 16) {
-    dim3 grid((H / 8 + 127) / 128, ntb);
+    dim3 grid((H / 8 + 31) / 32, ntb);
+    static bool cfg = false;
+    if (!cfg) {
+      cudaError_t e1 = cudaFuncSetAttribute(router_wgrad_reg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            8 * 8 * 8 * 32 * 4);
+      cudaError_t e2 = cudaFuncSetAttribute(router_wgrad_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            4 * 16 * 8 * 32 * 4);
+      if (e1 != cudaSuccess) return set_cuda_error(e1, "cudaFuncSetAttribute(router_wgrad_reg)");
+      if (e2 != cudaSuccess) return set_cuda_error(e2, "cudaFuncSetAttribute(router_wgrad_reg)");
+      cfg = true;
+    }
     if (E <= 8)
-      router_wgrad_reg_kernel<8><<<grid, 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
+      router_wgrad_reg_kernel<8><<<grid, 256, 8 * 8 * 8 * 32 * 4, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
                                                        T, H, E, k, tbt, partial_ws);
     else
-      router_wgrad_reg_kernel<16><<<grid, 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
+      router_wgrad_reg_kernel<16><<<grid, 128, 4 * 16 * 8 * 32 * 4, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
                                                         T, H, E, k, tbt, partial_ws);
   } else {
     int cw = 128;

@@ -10,10 +10,12 @@
 // (oracle/moe_oracle.c) restates the exact same order, so expert ids,
 // permutation indices and counts are bit-exact.
 //
-// Canonical logit order (shared with oracle/moe_oracle.c:dm_oracle_router):
-//   partial[p], p in [0,32): fmaf chain over 8-element chunks c with c % 32 == p,
-//   c ascending, elements ascending; then an xor butterfly 16,8,4,2,1 with
-//   round-to-nearest fp32 adds.
+// Canonical logit order (shared with oracle/moe_oracle.c:dm_oracle_router_logits):
+//   partial[p][s], lane p in [0,32), parity s in {0,1}: fmaf chain over the
+//   8-element chunks c with c % 32 == p (c ascending) and the elements j of each
+//   chunk with j % 2 == s (ascending); v[p] = partial[p][0] + partial[p][1]; then
+//   an xor butterfly 16,8,4,2,1 of round-to-nearest fp32 adds. Two chains per
+//   lane map onto packed fp32x2 FMAs (FFMA2), bit-identical to scalar fmaf.
 #include "dm_common.cuh"
 #include "dm_internal.h"
 
@@ -40,11 +42,11 @@ router_logits_kernel(const __nv_bfloat16* __restrict__ x, const float* __restric
     for (int tg = (blockIdx.x * ROUTER_WARPS + warp) * ROUTER_NT; tg < T;
          tg += gridDim.x * ROUTER_WARPS * ROUTER_NT) {
       for (int er = 0; er < ecur; er += ROUTER_ER) {
-        float acc[ROUTER_NT][ROUTER_ER];
+        float2 acc[ROUTER_NT][ROUTER_ER];   // {even-element chain, odd-element chain}
 #pragma unroll
         for (int t = 0; t < ROUTER_NT; ++t)
 #pragma unroll
-          for (int e = 0; e < ROUTER_ER; ++e) acc[t][e] = 0.0f;
+          for (int e = 0; e < ROUTER_ER; ++e) acc[t][e] = make_float2(0.f, 0.f);
         for (int c = lane; c < nch; c += 32) {
           int4 xv[ROUTER_NT];
 #pragma unroll
@@ -58,15 +60,11 @@ router_logits_kernel(const __nv_bfloat16* __restrict__ x, const float* __restric
 #pragma unroll
               for (int t = 0; t < ROUTER_NT; ++t) {
                 const uint32_t* xp = reinterpret_cast<const uint32_t*>(&xv[t]);
-                float a = acc[t][e];
-                a = __fmaf_rn(bf16lo(xp[0]), w0.x, a);
-                a = __fmaf_rn(bf16hi(xp[0]), w0.y, a);
-                a = __fmaf_rn(bf16lo(xp[1]), w0.z, a);
-                a = __fmaf_rn(bf16hi(xp[1]), w0.w, a);
-                a = __fmaf_rn(bf16lo(xp[2]), w1.x, a);
-                a = __fmaf_rn(bf16hi(xp[2]), w1.y, a);
-                a = __fmaf_rn(bf16lo(xp[3]), w1.z, a);
-                a = __fmaf_rn(bf16hi(xp[3]), w1.w, a);
+                float2 a = acc[t][e];
+                a = ffma2(make_float2(bf16lo(xp[0]), bf16hi(xp[0])), make_float2(w0.x, w0.y), a);
+                a = ffma2(make_float2(bf16lo(xp[1]), bf16hi(xp[1])), make_float2(w0.z, w0.w), a);
+                a = ffma2(make_float2(bf16lo(xp[2]), bf16hi(xp[2])), make_float2(w1.x, w1.y), a);
+                a = ffma2(make_float2(bf16lo(xp[3]), bf16hi(xp[3])), make_float2(w1.z, w1.w), a);
                 acc[t][e] = a;
               }
             }
@@ -76,7 +74,7 @@ router_logits_kernel(const __nv_bfloat16* __restrict__ x, const float* __restric
         for (int t = 0; t < ROUTER_NT; ++t) {
 #pragma unroll
           for (int e = 0; e < ROUTER_ER; ++e) {
-            const float v = warp_sum_butterfly(acc[t][e]);
+            const float v = warp_sum_butterfly(__fadd_rn(acc[t][e].x, acc[t][e].y));
             if (lane == e && er + e < ecur && tg + t < T)
               logits[(size_t)(tg + t) * E + e0 + er + e] = v;
           }
@@ -109,10 +107,11 @@ __device__ __forceinline__ void chunk_ranks(const int* sel, int nslots, int* run
 // Fused router for E <= EM (Mixtral-class gates): one pass over x computes the
 // canonical-order logits, top-k, softmax weights, the within-chunk ranks and
 // the chunk histogram. CTA = one 32-token chunk per pass (16 warps x 2 tokens),
-// persistent over chunks so W_g is staged into smem once per CTA. W_g is stored
-// lane-interleaved ([e][iteration][half][lane] float4) so every 128-bit smem
-// read of a warp is 512 contiguous bytes (no wasted wavefronts); x is prefetched
-// FUSED_UNROLL chunks deep.
+// persistent over chunks so W_g is staged into smem once per CTA, stored
+// lane-interleaved ([e][iteration][half][lane] float4) so each 128-bit smem read
+// of a warp is 512 contiguous bytes. The even/odd element chains of the
+// canonical order run as packed fp32x2 FMAs (FFMA2) on naturally paired
+// registers. W_g rows e >= E are zero-filled, so the hot loop has no E checks.
 constexpr int FUSED_UNROLL = 4;
 constexpr int FUSED_NT = 2;
 constexpr int FUSED_WARPS = DM_CHUNK_TOKENS / FUSED_NT;   // 16
@@ -128,12 +127,12 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = H >> 3;
   const int NI = (nch + 31) >> 5;
-  for (int i = threadIdx.x; i < E * NI * 64; i += blockDim.x) {
+  for (int i = threadIdx.x; i < EM * NI * 64; i += blockDim.x) {
     const int l = i & 31, half = (i >> 5) & 1, rest = i >> 6;
     const int it = rest % NI, e = rest / NI;
     const int c = it * 32 + l;
-    sw4[i] = c < nch ? reinterpret_cast<const float4*>(wg + (size_t)e * H + c * 8)[half]
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    sw4[i] = (c < nch && e < E) ? reinterpret_cast<const float4*>(wg + (size_t)e * H + c * 8)[half]
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int nchunk = (T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS;
   for (int chunk = blockIdx.x; chunk < nchunk; chunk += gridDim.x) {
@@ -141,11 +140,11 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
     __syncthreads();   // also orders the W_g fill before first use
     const int t0 = chunk * DM_CHUNK_TOKENS;
     const int tg = t0 + warp * FUSED_NT;
-    float acc[FUSED_NT][EM];
+    float2 acc[FUSED_NT][EM];   // {even-element chain, odd-element chain}
 #pragma unroll
     for (int t = 0; t < FUSED_NT; ++t)
 #pragma unroll
-      for (int e = 0; e < EM; ++e) acc[t][e] = 0.0f;
+      for (int e = 0; e < EM; ++e) acc[t][e] = make_float2(0.f, 0.f);
     for (int it0 = 0; it0 < NI; it0 += FUSED_UNROLL) {
       int4 xv[FUSED_UNROLL][FUSED_NT];
 #pragma unroll
@@ -159,39 +158,40 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
 #pragma unroll
       for (int u = 0; u < FUSED_UNROLL; ++u) {
         if (it0 + u >= NI) break;
+        float2 xp[FUSED_NT][4];
+#pragma unroll
+        for (int t = 0; t < FUSED_NT; ++t) {
+          const uint32_t* q = reinterpret_cast<const uint32_t*>(&xv[u][t]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) xp[t][i] = make_float2(bf16lo(q[i]), bf16hi(q[i]));
+        }
 #pragma unroll
         for (int e = 0; e < EM; ++e) {
-          if (e < E) {
-            const float4* wp = sw4 + ((size_t)(e * NI + it0 + u) * 2) * 32 + lane;
-            const float4 w0 = wp[0], w1 = wp[32];
+          const float4* wp = sw4 + ((size_t)(e * NI + it0 + u) * 2) * 32 + lane;
+          const float4 w0 = wp[0], w1 = wp[32];
 #pragma unroll
-            for (int t = 0; t < FUSED_NT; ++t) {
-              const uint32_t* xp = reinterpret_cast<const uint32_t*>(&xv[u][t]);
-              float a = acc[t][e];
-              a = __fmaf_rn(bf16lo(xp[0]), w0.x, a);
-              a = __fmaf_rn(bf16hi(xp[0]), w0.y, a);
-              a = __fmaf_rn(bf16lo(xp[1]), w0.z, a);
-              a = __fmaf_rn(bf16hi(xp[1]), w0.w, a);
-              a = __fmaf_rn(bf16lo(xp[2]), w1.x, a);
-              a = __fmaf_rn(bf16hi(xp[2]), w1.y, a);
-              a = __fmaf_rn(bf16lo(xp[3]), w1.z, a);
-              a = __fmaf_rn(bf16hi(xp[3]), w1.w, a);
-              acc[t][e] = a;
-            }
+          for (int t = 0; t < FUSED_NT; ++t) {
+            float2 a = acc[t][e];
+            a = ffma2(xp[t][0], make_float2(w0.x, w0.y), a);
+            a = ffma2(xp[t][1], make_float2(w0.z, w0.w), a);
+            a = ffma2(xp[t][2], make_float2(w1.x, w1.y), a);
+            a = ffma2(xp[t][3], make_float2(w1.z, w1.w), a);
+            acc[t][e] = a;
           }
         }
       }
     }
 #pragma unroll
     for (int t = 0; t < FUSED_NT; ++t) {
+      float lg[EM];
 #pragma unroll
-      for (int e = 0; e < EM; ++e) acc[t][e] = warp_sum_butterfly(acc[t][e]);  // identical in every lane
+      for (int e = 0; e < EM; ++e) lg[e] = warp_sum_butterfly(__fadd_rn(acc[t][e].x, acc[t][e].y));
       const int tok = tg + t;
       if (tok >= T) continue;
       if (lane < E) {
-        float v = acc[t][0];
+        float v = lg[0];
 #pragma unroll
-        for (int e = 1; e < EM; ++e) v = (lane == e) ? acc[t][e] : v;
+        for (int e = 1; e < EM; ++e) v = (lane == e) ? lg[e] : v;
         logits[(size_t)tok * E + lane] = v;
       }
       // top-k over registers (uniform across lanes): ties -> lower expert id
@@ -203,7 +203,7 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
         int be = -1;
 #pragma unroll
         for (int e = 0; e < EM; ++e) {
-          if (e < E && !((taken >> e) & 1u) && (be < 0 || acc[t][e] > bv)) { bv = acc[t][e]; be = e; }
+          if (e < E && !((taken >> e) & 1u) && (be < 0 || lg[e] > bv)) { bv = lg[e]; be = e; }
         }
         taken |= 1u << be;
         sel_v[j] = bv;
@@ -411,7 +411,7 @@ int router_logits_launch(const void* x, const float* wg, float* logits, int T, i
 int router_fused_launch(const void* x, const float* wg, int T, int H, int E, int k, float* logits,
                         int32_t* idx, float* w, int32_t* rank, int32_t* chunk_hist, cudaStream_t stream) {
   const int NI = ((H >> 3) + 31) >> 5;
-  const size_t smem = (size_t)E * NI * 64 * sizeof(float4);
+  const size_t smem = (size_t)(E <= 8 ? 8 : 16) * NI * 64 * sizeof(float4);
   if (E > 16 || smem > (size_t)ROUTER_SMEM_BUDGET) return -1;
   if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(wg) & 15) return -1;
   static bool configured = false;

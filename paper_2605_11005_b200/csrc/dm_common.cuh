@@ -248,6 +248,19 @@ __device__ __forceinline__ void umma_commit_2sm_mc(uint64_t* bar) {
       :: "r"(smem_u32(bar)) : "memory");
 }
 
+// Packed fp32x2 fused multiply-add (sm_100 FFMA2): two independent, correctly
+// rounded FMAs — bit-identical to two fmaf() calls.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long ra, rb, rc, rd;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rc) : "f"(c.x), "f"(c.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  float2 d;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+  return d;
+}
+
 // -------------------------------------------------------------- warp utils
 __device__ __forceinline__ float warp_sum_butterfly(float v) {
   // Fixed xor tree 16,8,4,2,1: every lane ends with the identical value.
