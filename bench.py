@@ -54,7 +54,7 @@ def _peaks():
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -77,7 +77,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, which: str) -> None:
+        setattr(self, "t_" + which, time.time())
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -91,20 +94,25 @@ class ClockSampler:
             self._t.join(timeout=2)
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = getattr(self, "t_start", 0.0) - 0.05
+        t1 = getattr(self, "t_end", float("inf")) + 0.15   # nvidia-smi output lags its sample
+        window = [ln for t, ln in self.lines if t0 <= t <= t1]
+        if not window:  # very short timed region: fall back to the samples nearest to it
+            window = [ln for _, ln in self.lines[-3:]]
+        for ln in window:
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                smax.append(float(f[2]))
+                sm.append(float(f[2]))
+                smax.append(float(f[3]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
+            for n, v in zip(names, f[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window_s": round(t1 - t0 - 0.2, 3)}
 
 
 def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: int | None = None):
@@ -233,14 +241,16 @@ def run_ours(args, shape, exp):
                                                            layer.router.dwg, 1.0 if acc else 0.0))
         ev.mark("gemm", lambda: layer.wgrad(mb))
 
+    sampler = ClockSampler(dev.index) if rank == 0 else None
+    if sampler:
+        sampler.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(dev.index) if rank == 0 else None
     if sampler:
-        sampler.start()
+        sampler.mark("start")
     ev = Ev()
     launches0 = _lib.launch_count()
     t_s = torch.cuda.Event(enable_timing=True)
@@ -251,6 +261,8 @@ def run_ours(args, shape, exp):
         step(ev)
     t_e.record(stream)
     torch.cuda.synchronize()
+    if sampler:
+        sampler.mark("end")
     launches = _lib.launch_count() - launches0
     ms = t_s.elapsed_time(t_e)
     if world > 1:
@@ -364,13 +376,15 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
         for b in r.bufs:
             b.x.normal_()
             b.dy.normal_()
+    sampler = ClockSampler(dev.index) if rank == 0 else None
+    if sampler:
+        sampler.start()
     for _ in range(args.warmup):
         r.run_iteration()
     torch.cuda.synchronize()
     dist.barrier()
-    sampler = ClockSampler(dev.index) if rank == 0 else None
     if sampler:
-        sampler.start()
+        sampler.mark("start")
     n0 = _lib.launch_count()
     t_s, t_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -380,6 +394,8 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
         r.run_iteration()
     t_e.record()
     torch.cuda.synchronize()
+    if sampler:
+        sampler.mark("end")
     launches = _lib.launch_count() - n0
     ms = t_s.elapsed_time(t_e)
     tt = torch.tensor([ms, float(launches)], device=dev)
@@ -546,13 +562,15 @@ def run_e2e(args, layer, shape, mb, dev, world):
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=str(ROOT / "configs" / "mixtral_layer.yaml"))
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--n-attn", type=int, default=None, help="A ranks for N>1 (default N/2)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent fused replicas instead of AF-Pipe")
+    ap.add_argument("--seq-len", type=int, default=None, help="override workload.seq_len (sweeps)")
+    ap.add_argument("--microbatches", type=int, default=None, help="override workload.num_microbatches")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
@@ -560,6 +578,12 @@ def main(argv=None):
     from paper_2605_11005_b200.moe import MoEShape
 
     exp = load_experiment(args.config)
+    if args.seq_len or args.microbatches:
+        import dataclasses
+
+        wl = dataclasses.replace(exp.workload, seq_len=args.seq_len or exp.workload.seq_len,
+                                 num_microbatches=args.microbatches or exp.workload.num_microbatches)
+        exp = dataclasses.replace(exp, workload=wl)
     shape = MoEShape.from_experiment(exp)
     if args.impl == "reference":
         return run_reference(args, shape, exp)
