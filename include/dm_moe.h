@@ -173,6 +173,9 @@ DM_API int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, 
                             int nseg, int E, int total_rows, int seg_stride_rows, float* dW, float beta,
                             void* stream);
 
+/* Debug: route 2-SM GEMM wait-cycle counters into a device u64[5] buffer (NULL = off). */
+DM_API int dm_debug_gemm_profile(void* buf);
+
 /* ---- combine (A side) ------------------------------------------------- */
 DM_API int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,
                    void* y, void* stream);

@@ -52,7 +52,22 @@ struct GemmArgs {
   const int* seg_off;
   int nseg;
   int seg_stride_rows;
+  // optional instrumentation (dm_debug_gemm_profile): u64 cycle counters
+  // [0] producer waits on empty, [1] MMA waits on tempty, [2] MMA waits on full,
+  // [3] epilogue waits on tfull (lane 0 of each epilogue warp), [4] CTA lifetime
+  unsigned long long* prof;
 };
+
+#define DM_PROF_WAIT(slot, call)                                                  \
+  do {                                                                            \
+    if (args.prof) {                                                              \
+      const long long _t = clock64();                                             \
+      call;                                                                       \
+      if ((threadIdx.x & 31) == 0) atomicAdd(args.prof + (slot), (unsigned long long)(clock64() - _t)); \
+    } else {                                                                      \
+      call;                                                                       \
+    }                                                                             \
+  } while (0)
 
 struct TileInfo {
   int g, m0, n0, kb_count, row_base;
@@ -613,6 +628,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
                         const __grid_constant__ CUtensorMap tmIn, const GemmArgs args) {
   constexpr int STAGES = g2_stages<EPI>();
   constexpr uint32_t STG = g2_stg_bytes<EPI>();
+  const long long prof_t0 = clock64();
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
@@ -692,7 +708,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
           } else {
             kcoord = kb * GBK;
           }
-          mbar_wait(&empty[stage], phase ^ 1);
+          DM_PROF_WAIT(0, mbar_wait(&empty[stage], phase ^ 1));
           if (leader) mbar_expect_tx(&full[stage], 2 * (G2_A_BYTES + G2_B_BYTES));
           uint8_t* a_dst = sA + stage * G2_A_BYTES;
           uint8_t* b_dst = sB + stage * G2_B_BYTES;
@@ -725,11 +741,11 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
         const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, G, args, rank, active);
         const int as = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
-        mbar_wait(&tempty[as], aphase ^ 1);
+        DM_PROF_WAIT(1, mbar_wait(&tempty[as], aphase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * GBN;
         for (int kb = 0; kb < ti.kb_count; ++kb) {
-          mbar_wait(&full[stage], phase);
+          DM_PROF_WAIT(2, mbar_wait(&full[stage], phase));
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * G2_A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * G2_B_BYTES);
@@ -759,7 +775,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, G, args, rank, active);
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      mbar_wait(&tfull[as], aphase);
+      DM_PROF_WAIT(3, mbar_wait(&tfull[as], aphase));
       tc_fence_after();
       if (active) {
         const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * GBN;
@@ -777,9 +793,12 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   cluster_sync_all();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_2sm(tmem_base, 512);
+  if (args.prof && threadIdx.x == 0) atomicAdd(args.prof + 4, (unsigned long long)(clock64() - prof_t0));
 }
 
 // ------------------------------------------------------------------- host side
+
+static unsigned long long* g_gemm_prof = nullptr;
 
 static bool use_2sm() {
   static int v = -1;
@@ -874,7 +893,9 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const EpiTe
       configured = true;
     }
     grid &= ~1;
-    kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, tc, tx, ti, args);
+    GemmArgs a2 = args;
+    a2.prof = g_gemm_prof;
+    kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, tc, tx, ti, a2);
   } else {
     auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
     static bool configured = false;  // per instantiation
@@ -993,6 +1014,13 @@ int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const i
   EpiTensors et;
   et.c = {dW, true, (uint64_t)N, (uint64_t)E * M, (uint64_t)N};
   return launch_gemm<1, 1, 1, EPI_F32>(A, B, et, a, (cudaStream_t)stream);
+}
+
+/* Debug/profiling hook: when `buf` (device, >= 5 u64, zeroed by the caller) is
+ * non-NULL every subsequent 2-SM GEMM launch accumulates per-role wait cycles. */
+int dm_debug_gemm_profile(void* buf) {
+  g_gemm_prof = reinterpret_cast<unsigned long long*>(buf);
+  return DM_OK;
 }
 
 }  // extern "C"
