@@ -211,15 +211,20 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
       "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}"
       :: "r"(smem_u32(bar)), "r"(cta) : "memory");
 }
+// L2 cache-policy operands for .L2::cache_hint (CUTLASS TMA::CacheHintSm90 values).
+constexpr uint64_t L2_EVICT_NORMAL = 0x1000000000000000ull;
+constexpr uint64_t L2_EVICT_FIRST = 0x12F0000000000000ull;
+constexpr uint64_t L2_EVICT_LAST = 0x14F0000000000000ull;
+
 // 2-SM TMA load: data lands in this CTA's smem, the transaction bytes are
 // credited to the leader (rank 0) CTA's barrier at the same offset.
 __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* tm, uint64_t* bar,
-                                                int c0, int c1) {
+                                                int c0, int c1, uint64_t policy = L2_EVICT_NORMAL) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];"
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;"
       :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar) & 0xFEFFFFFFu),
-         "r"(c0), "r"(c1)
+         "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* dst_smem, uint32_t ncols) {

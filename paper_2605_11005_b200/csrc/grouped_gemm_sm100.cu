@@ -389,15 +389,18 @@ constexpr uint32_t G2_A_BYTES = 128 * GBK * 2;   // 16 KiB (this CTA's M half)
 constexpr uint32_t G2_B_BYTES = 128 * GBK * 2;   // 16 KiB (this CTA's N half)
 constexpr uint32_t BOX_BYTES = 4096;             // one 32-row x 128-byte staging box
 
+// Ring depth. The MMA issuer waits on TMA data 12-20% of the time
+// (scripts/gemm_waits.py); a 6-stage ring did not reduce that (supply-rate, not
+// latency, bound) and was slower, so 5 stages (4 next to the SwiGLU-bwd staging).
 template <int EPI> constexpr int g2_stages() { return EPI == EPI_SWIGLU_BWD ? 4 : 5; }
 // per-epilogue-warp staging: BF16/F32 2 boxes (double buffer); SwiGLU fwd gate/up/act;
 // SwiGLU bwd dg/du out + g/u in
 template <int EPI> constexpr uint32_t g2_stg_bytes() {
   return EPI == EPI_SWIGLU_FWD ? 3 * BOX_BYTES : EPI == EPI_SWIGLU_BWD ? 4 * BOX_BYTES : 2 * BOX_BYTES;
 }
+// fixed part; the two [G+1]-int tile tables are appended at launch (G-dependent)
 template <int EPI> constexpr size_t g2_smem_bytes() {
-  return 1024 + g2_stages<EPI>() * (G2_A_BYTES + G2_B_BYTES) + 4 * g2_stg_bytes<EPI>() + 256 +
-         2 * (GEMM_MAX_GROUPS + 1) * sizeof(int);
+  return 1024 + g2_stages<EPI>() * (G2_A_BYTES + G2_B_BYTES) + 4 * g2_stg_bytes<EPI>() + 256;
 }
 
 template <int RAGGED_K>
@@ -642,7 +645,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   uint64_t* ibar = tempty + 2;   // [4] per-epilogue-warp input barriers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ibar + 4);
   int* s_tile = reinterpret_cast<int*>(sStg + 4 * STG + 256);
-  int* s_off = s_tile + (GEMM_MAX_GROUPS + 1);
+  int* s_off = s_tile + (args.num_groups + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -685,6 +688,10 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   if (warp == 0) {
     // ------------------------------------------- TMA producer (both CTAs)
     if (lane == 0) {
+      // L2 policy: evict-last/evict-first hints on the re-read/streamed operand
+      // were measured slower than the default policy on every variant.
+      const uint64_t pol_a = L2_EVICT_NORMAL;
+      const uint64_t pol_b = L2_EVICT_NORMAL;
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
@@ -713,16 +720,16 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
           uint8_t* a_dst = sA + stage * G2_A_BYTES;
           uint8_t* b_dst = sB + stage * G2_B_BYTES;
           if (!A_MN) {
-            tma_load_2d_2sm(a_dst, &tmA, &full[stage], kcoord, ti.m0);
+            tma_load_2d_2sm(a_dst, &tmA, &full[stage], kcoord, ti.m0, pol_a);
           } else {
-            tma_load_2d_2sm(a_dst, &tmA, &full[stage], ti.m0, kcoord);
-            tma_load_2d_2sm(a_dst + 8192, &tmA, &full[stage], ti.m0 + 64, kcoord);
+            tma_load_2d_2sm(a_dst, &tmA, &full[stage], ti.m0, kcoord, pol_a);
+            tma_load_2d_2sm(a_dst + 8192, &tmA, &full[stage], ti.m0 + 64, kcoord, pol_a);
           }
           if (!B_MN) {
-            tma_load_2d_2sm(b_dst, &tmB, &full[stage], kcoord, b_gofs + nb0);
+            tma_load_2d_2sm(b_dst, &tmB, &full[stage], kcoord, b_gofs + nb0, pol_b);
           } else {
-            tma_load_2d_2sm(b_dst, &tmB, &full[stage], nb0, b_gofs + kcoord);
-            tma_load_2d_2sm(b_dst + 8192, &tmB, &full[stage], nb0 + 64, b_gofs + kcoord);
+            tma_load_2d_2sm(b_dst, &tmB, &full[stage], nb0, b_gofs + kcoord, pol_b);
+            tma_load_2d_2sm(b_dst + 8192, &tmB, &full[stage], nb0 + 64, b_gofs + kcoord, pol_b);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -885,10 +892,11 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const EpiTe
     if ((rc = make_epi_map(&tx, et.aux, ta))) return rc;
     if ((rc = make_epi_map(&ti, et.in, ta))) return rc;
     auto kern = grouped_gemm_2sm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
-    constexpr size_t smem = g2_smem_bytes<EPI>();
+    const size_t smem = g2_smem_bytes<EPI>() + 2 * ((size_t)args.num_groups + 1) * sizeof(int);
+    if (smem > 232448) return set_error(DM_ERR_SHAPE, "too many groups (%d) for the GEMM smem budget", args.num_groups);
     static bool configured = false;  // per instantiation
     if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
       if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm2 smem)");
       configured = true;
     }
