@@ -415,6 +415,10 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
     r.record_events = False
     gathered = [None] * world if rank == 0 else None
     dist.gather_object({"rank": rank, "role": r.role, "ivs": ivs}, gathered, dst=0)
+    if rank == 0 and args.trace:
+        from paper_2605_11005_b200.profile import export_trace
+
+        Path(args.trace).write_text(json.dumps(export_trace(gathered), indent=1))
 
     # e2e: A ranks feed x/dy from pinned host memory and read y/dx back every micro-batch
     T, H = shape.T, shape.H
@@ -570,6 +574,7 @@ def main(argv=None):
     ap.add_argument("--n-attn", type=int, default=None, help="A ranks for N>1 (default N/2)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent fused replicas instead of AF-Pipe")
     ap.add_argument("--seq-len", type=int, default=None, help="override workload.seq_len (sweeps)")
+    ap.add_argument("--trace", default=None, help="N>1: write the instrumented iteration as reference-schema trace JSON")
     ap.add_argument("--microbatches", type=int, default=None, help="override workload.num_microbatches")
     args = ap.parse_args(argv)
     if args.warmup < 3:
