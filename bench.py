@@ -187,6 +187,7 @@ def run_ours(args, shape, exp):
     from paper_2605_11005_b200 import _lib
     from paper_2605_11005_b200 import kernels as K
     from paper_2605_11005_b200.moe import MoELayer, a_combine, a_combine_bwd, a_dispatch, a_dispatch_bwd, \
+        a_permute_bwd, a_router_wgrad, \
         f_backward, f_forward
 
     world = _env_int("WORLD_SIZE", 1)
@@ -235,10 +236,8 @@ def run_ours(args, shape, exp):
             ev.mark("combine_fwd", lambda: a_combine(buf))
             ev.mark("combine_bwd", lambda: a_combine_bwd(buf))
             ev.mark("gemm", lambda: f_backward(buf, layer.experts, acc, defer_wgrad=True))
-            ev.mark("permute_bwd", lambda: K.permute_bwd(buf.dx_perm, buf.row_map, buf.idx, buf.dlogit,
-                                                         layer.router.wg, buf.dx))
-            ev.mark("router_wgrad", lambda: K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws,
-                                                           layer.router.dwg, 1.0 if acc else 0.0))
+            ev.mark("permute_bwd", lambda: a_permute_bwd(buf, layer.router))
+            ev.mark("router_wgrad", lambda: a_router_wgrad(buf, layer.router, acc))
         ev.mark("gemm", lambda: layer.wgrad(mb))
 
     sampler = ClockSampler(dev.index) if rank == 0 else None

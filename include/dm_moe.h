@@ -180,10 +180,10 @@ DM_API int dm_debug_gemm_profile(void* buf);
 DM_API int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,
                    void* y, void* stream);
 /* dy_perm = w * dy scattered (padding zeroed); dw = <dy, y_perm>;
- * dlogit[t,j] = w_j (dw_j - sum_i w_i dw_i). */
+ * dlogit[t,j] = w_j (dw_j - sum_i w_i dw_i); optional dl_perm[row_map[t,j]] = dlogit[t,j]. */
 DM_API int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_map, const float* w,
-                   const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
-                   void* dy_perm, float* dw, float* dlogit, void* stream);
+                          const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
+                          void* dy_perm, float* dw, float* dlogit, float* dl_perm, void* stream);
 /* dx = sum_j dx_perm[row_map] + sum_j dlogit * W_g[idx]  (dlogit may be NULL). */
 DM_API int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* idx,
                           const float* dlogit, const float* wg, int T, int H, int E, int k, void* dx,
@@ -192,6 +192,12 @@ DM_API int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int
  * partial_ws of dm_router_wgrad_workspace_size bytes. */
 DM_API int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int T, int H, int E,
                     int k, float* partial_ws, float* dwg, float beta, void* stream);
+
+/* dW_g[e,:] = sum over expert e's permuted rows r of dl_perm[r] * x[src_token[r], :]
+ * (+ beta * dW_g): deterministic single-pass router gradient for large E. */
+DM_API int dm_router_wgrad_sorted(const void* x, const int32_t* src_token, const float* dl_perm,
+                                  const int32_t* counts, const int32_t* pad_off, int T, int H, int E,
+                                  float* dwg, float beta, void* stream);
 
 #ifdef __cplusplus
 }

@@ -70,7 +70,7 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __
                    const int32_t* __restrict__ row_map, const float* __restrict__ w,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ pad_off,
                    int T, int H, int E, int k_rt, __nv_bfloat16* __restrict__ dy_perm,
-                   float* __restrict__ dw, float* __restrict__ dlogit) {
+                   float* __restrict__ dw, float* __restrict__ dlogit, float* __restrict__ dl_perm) {
   const int k = KT ? KT : k_rt;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -111,16 +111,12 @@ combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __
       for (int j = 0; j < k; ++j) {
         dw[(size_t)t * k + j] = part[j];
         dlogit[(size_t)t * k + j] = wt[j] * (part[j] - s);
+        if (dl_perm) dl_perm[pos[j]] = wt[j] * (part[j] - s);
       }
     }
   }
   // zero padding rows of dy_perm so the ragged-K wgrad sees exact zeros
-  const int4 z = make_int4(0, 0, 0, 0);
-  for (int e = 0; e < E; ++e) {
-    const int beg = pad_off[e] + counts[e], end = pad_off[e + 1];
-    for (int r = beg + gwarp; r < end; r += nwarps)
-      for (int ch = lane; ch < nvec; ch += 32) st_v4(dy_perm + (size_t)r * H + ch * 8, z);
-  }
+  zero_padding_rows(dy_perm, H, counts, pad_off, E, gwarp, nwarps, lane, nullptr);
 }
 
 // dx[t] = sum_j dx_perm[row_map[t,j]] + sum_j dlogit[t,j] * W_g[idx[t,j], :]
@@ -342,6 +338,42 @@ __global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, in
   }
 }
 
+// Router weight gradient for large E, deterministic and single pass: the rows of
+// expert e in the permuted layout are exactly the (t, j) slots with idx == e in
+// ascending t, so dW_g[e, :] = sum over the block of dl_perm[r] * x[src_token[r], :]
+// (dl_perm = dlogit scattered to permuted positions by combine_bwd). CTA per
+// (1024-column chunk, expert); x rows are gathered with 128-bit loads (L2-resident).
+__global__ void __launch_bounds__(128)
+router_wgrad_sorted_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ src_token,
+                           const float* __restrict__ dl_perm, const int32_t* __restrict__ counts,
+                           const int32_t* __restrict__ pad_off, int H, float* __restrict__ dwg, float beta) {
+  const int e = blockIdx.y;
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (col >= H) return;
+  const int beg = pad_off[e], n = counts[e];
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll 4
+  for (int r = beg; r < beg + n; ++r) {
+    const int t = src_token[r];
+    const float d = dl_perm[r];
+    float f[8];
+    unpack8(ld_nc_v4(x + (size_t)t * H + col), f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(d, f[i], acc[i]);
+  }
+  float4* o = reinterpret_cast<float4*>(dwg + (size_t)e * H + col);
+  float4 a = make_float4(acc[0], acc[1], acc[2], acc[3]), b = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  if (beta != 0.0f) {
+    const float4 oa = o[0], ob = o[1];
+    a.x += beta * oa.x; a.y += beta * oa.y; a.z += beta * oa.z; a.w += beta * oa.w;
+    b.x += beta * ob.x; b.y += beta * ob.y; b.z += beta * ob.z; b.w += beta * ob.w;
+  }
+  o[0] = a;
+  o[1] = b;
+}
+
 static int token_grid(int T) {
   int blocks = (T + 7) / 8;  // 8 warps (tokens) per 256-thread block
   const int cap = num_sms_current() * 8;
@@ -372,14 +404,14 @@ int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, i
 
 int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_map, const float* w,
                    const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
-                   void* dy_perm, float* dw, float* dlogit, void* stream) {
+                   void* dy_perm, float* dw, float* dlogit, float* dl_perm, void* stream) {
   if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK || E < 1) return set_error(DM_ERR_SHAPE, "combine_bwd bad shape");
   switch (k) {
-    case 1: combine_bwd_kernel<1><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
-    case 2: combine_bwd_kernel<2><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
-    case 4: combine_bwd_kernel<4><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
-    case 8: combine_bwd_kernel<8><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
-    default: combine_bwd_kernel<0><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit); break;
+    case 1: combine_bwd_kernel<1><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit, dl_perm); break;
+    case 2: combine_bwd_kernel<2><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit, dl_perm); break;
+    case 4: combine_bwd_kernel<4><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit, dl_perm); break;
+    case 8: combine_bwd_kernel<8><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit, dl_perm); break;
+    default: combine_bwd_kernel<0><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(dy), reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, counts, pad_off, T, H, E, k, reinterpret_cast<__nv_bfloat16*>(dy_perm), dw, dlogit, dl_perm); break;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "combine_bwd launch");
@@ -470,6 +502,19 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
   router_wgrad_reduce_kernel<<<rblocks, 256, 0, st>>>(partial_ws, ntb, EH, dwg, beta);
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_reduce launch");
+  note_launch();
+  return DM_OK;
+}
+
+int dm_router_wgrad_sorted(const void* x, const int32_t* src_token, const float* dl_perm, const int32_t* counts,
+                           const int32_t* pad_off, int T, int H, int E, float* dwg, float beta, void* stream) {
+  if (T < 1 || H % 8 || E < 1 || E > DM_MAX_EXPERTS) return set_error(DM_ERR_SHAPE, "router_wgrad_sorted bad shape");
+  if (reinterpret_cast<uintptr_t>(dwg) & 15) return set_error(DM_ERR_ALIGN, "dW_g must be 16-byte aligned");
+  dim3 grid((H / 8 + 127) / 128, E);
+  router_wgrad_sorted_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), src_token, dl_perm, counts, pad_off, H, dwg, beta);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_sorted launch");
   note_launch();
   return DM_OK;
 }

@@ -369,19 +369,138 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
       for (int j = 0; j < k; ++j) st_v4(x_perm + (size_t)p[j] * H + ch * 8, v);
     }
   }
-  const int4 z = make_int4(0, 0, 0, 0);
-  for (int e = 0; e < E; ++e) {
-    const int beg = pad_off[e] + counts[e], end = pad_off[e + 1];
-    for (int r = beg + gwarp; r < end; r += nwarps) {
-      __nv_bfloat16* row = x_perm + (size_t)r * H;
-      for (int cc = lane; cc < nvec; cc += 32) st_v4(row + cc * 8, z);
-      if (lane == 0) src_token[r] = -1;
+  zero_padding_rows(x_perm, H, counts, pad_off, E, gwarp, nwarps, lane, src_token);
+}
+
+// Tiled router logits for large E (DeepSeek-class gates). Same canonical order:
+// lane p of a warp owns chunk p of every 256-element k-tile (even/odd element
+// chains as one FFMA2 pair) for each of the warp's 8-token x 8-expert outputs,
+// and the 32 lane partials are reduced by the xor butterfly at the end. A CTA of
+// 8 warps (4 token groups x 2 expert groups) covers 32 tokens x 16 experts; the
+// x (bf16) and W_g (fp32) k-tiles are staged L2 -> smem by cp.async (no register
+// round trip) through a 3-deep ring. Per k-tile a warp reads 8 x 16 B of x and
+// 8 x 32 B of W_g per lane for 256 FFMA2 (8 tokens x 8 experts x 4 pairs), which
+// keeps shared-memory reads below the FMA-pipe time.
+constexpr int RT_TOK = 32, RT_EXP = 16, RT_THREADS = 256, RT_STAGES = 3;
+constexpr int RT_STAGE_INT4 = RT_TOK * 32 + RT_EXP * 2 * 32;  // 16 KB x + 16 KB W_g
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(RT_THREADS, 1)
+router_logits_tiled_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg,
+                           float* __restrict__ logits, int T, int H, int E) {
+  extern __shared__ int4 rt_smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t0 = blockIdx.x * RT_TOK, e0 = blockIdx.y * RT_EXP;
+  const int wt = (warp & 3) * 8, we = (warp >> 2) * 8;   // this warp's 8 tokens x 8 experts
+  const int nch = H >> 3, nkt = (nch + 31) >> 5;
+  // stage layout: xs[tok][lane] int4, then ws[exp][half][lane] float4
+  auto xs = [&](int st, int t, int l) -> int4* { return rt_smem + st * RT_STAGE_INT4 + t * 32 + l; };
+  auto ws = [&](int st, int e, int h, int l) -> int4* {
+    return rt_smem + st * RT_STAGE_INT4 + RT_TOK * 32 + (e * 2 + h) * 32 + l;
+  };
+  auto issue = [&](int kt) {
+    const int st = kt % RT_STAGES;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int f = tid + q * RT_THREADS;            // 32 tokens x 32 chunks
+      const int t = f >> 5, l = f & 31, c = kt * 32 + l;
+      const bool ok = t0 + t < T && c < nch;
+      cp_async16(xs(st, t, l), ok ? (const void*)(x + (size_t)(t0 + t) * H + c * 8) : (const void*)x, ok);
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int f = tid + q * RT_THREADS;            // 16 experts x 32 chunks x 2 halves
+      const int e = f >> 6, l = (f >> 1) & 31, h = f & 1, c = kt * 32 + l;
+      const bool ok = e0 + e < E && c < nch;
+      cp_async16(ws(st, e, h, l), ok ? (const void*)(wg + (size_t)(e0 + e) * H + c * 8 + h * 4) : (const void*)wg,
+                 ok);
+    }
+  };
+  float2 acc[8][8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[t][e] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int kt = 0; kt < RT_STAGES - 1; ++kt) {
+    if (kt < nkt) issue(kt);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  for (int kt = 0; kt < nkt; ++kt) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(RT_STAGES - 2) : "memory");
+    __syncthreads();   // stage kt landed for all threads; stage kt-1 is no longer read
+    if (kt + RT_STAGES - 1 < nkt) issue(kt + RT_STAGES - 1);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    const int st = kt % RT_STAGES;
+    float2 w[8][4];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float4 a = *reinterpret_cast<const float4*>(ws(st, we + e, 0, lane));
+      const float4 b = *reinterpret_cast<const float4*>(ws(st, we + e, 1, lane));
+      w[e][0] = make_float2(a.x, a.y);
+      w[e][1] = make_float2(a.z, a.w);
+      w[e][2] = make_float2(b.x, b.y);
+      w[e][3] = make_float2(b.z, b.w);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int4 v = *xs(st, wt + t, lane);
+      const uint32_t* q = reinterpret_cast<const uint32_t*>(&v);
+      float2 xp[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) xp[i] = make_float2(bf16lo(q[i]), bf16hi(q[i]));
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float2 a = acc[t][e];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a = ffma2(xp[i], w[e][i], a);
+        acc[t][e] = a;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  float out0 = 0.0f, out1 = 0.0f;
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float v = warp_sum_butterfly(__fadd_rn(acc[t][e].x, acc[t][e].y));
+      if (lane == (t & 3) * 8 + e) {
+        if (t < 4) out0 = v; else out1 = v;
+      }
+    }
+  const int ex = e0 + we + (lane & 7);
+  const int tok0 = t0 + wt + (lane >> 3), tok1 = tok0 + 4;
+  if (ex < E) {
+    if (tok0 < T) logits[(size_t)tok0 * E + ex] = out0;
+    if (tok1 < T) logits[(size_t)tok1 * E + ex] = out1;
   }
 }
 
 int router_logits_launch(const void* x, const float* wg, float* logits, int T, int H, int E,
                          cudaStream_t stream) {
+  if (E > 16) {
+    constexpr size_t rt_smem = (size_t)RT_STAGES * RT_STAGE_INT4 * sizeof(int4);
+    static bool rt_cfg = false;
+    if (!rt_cfg) {
+      cudaError_t e = cudaFuncSetAttribute(router_logits_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)rt_smem);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router_tiled)");
+      rt_cfg = true;
+    }
+    dim3 grid((T + RT_TOK - 1) / RT_TOK, (E + RT_EXP - 1) / RT_EXP);
+    router_logits_tiled_kernel<<<grid, RT_THREADS, rt_smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(x), wg,
+                                                                logits, T, H, E);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "router_logits_tiled launch");
+    note_launch();
+    return DM_OK;
+  }
   const size_t row_bytes = (size_t)H * sizeof(float);
   int ec = (int)(ROUTER_SMEM_BUDGET / row_bytes);
   if (ec < 1) return set_error(DM_ERR_SHAPE, "router: hidden %d too large for one smem row", H);

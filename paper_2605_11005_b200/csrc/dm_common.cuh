@@ -277,4 +277,30 @@ __device__ __forceinline__ float warp_sum_butterfly(float v) {
   return v;
 }
 
+// Zero the padding rows [pad_off[e] + counts[e], pad_off[e+1]) of every expert
+// block of a [*, H] bf16 buffer, spread evenly over all warps of the grid: each
+// warp strides over rows of the whole padded range and finds its expert by a
+// binary search of pad_off (L1-resident), so E = 256 experts with a few dozen
+// padding rows each keep every warp busy instead of the first few. Optionally
+// marks the rows' src_token as -1.
+__device__ __forceinline__ void zero_padding_rows(__nv_bfloat16* __restrict__ buf, int H,
+                                                  const int32_t* __restrict__ counts,
+                                                  const int32_t* __restrict__ pad_off, int E, int gwarp,
+                                                  int nwarps, int lane, int32_t* __restrict__ src_token) {
+  const int end = pad_off[E];
+  const int nvec = H >> 3;
+  const int4 z = make_int4(0, 0, 0, 0);
+  for (int r = gwarp; r < end; r += nwarps) {
+    int lo = 0, hi = E;  // largest e with pad_off[e] <= r
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pad_off[mid] <= r) lo = mid; else hi = mid;
+    }
+    if (r < pad_off[lo] + counts[lo]) continue;
+    __nv_bfloat16* row = buf + (size_t)r * H;
+    for (int ch = lane; ch < nvec; ch += 32) st_v4(row + ch * 8, z);
+    if (src_token && lane == 0) src_token[r] = -1;
+  }
+}
+
 }  // namespace dm

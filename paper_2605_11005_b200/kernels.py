@@ -154,12 +154,19 @@ def combine_fwd(y_perm, row_map, w, y, stream=None):
     _lib.call("dm_combine_fwd", _ptr(y_perm), _ptr(row_map), _ptr(w), T, H, k, _ptr(y), _stream(stream))
 
 
-def combine_bwd(dy, y_perm, row_map, w, counts, pad_off, dy_perm, dw, dlogit, stream=None):
+def combine_bwd(dy, y_perm, row_map, w, counts, pad_off, dy_perm, dw, dlogit, stream=None, dl_perm=None):
     T, H = dy.shape
     k = row_map.shape[1]
     E = counts.shape[0]
     _lib.call("dm_combine_bwd", _ptr(dy), _ptr(y_perm), _ptr(row_map), _ptr(w), _ptr(counts), _ptr(pad_off),
-              T, H, E, k, _ptr(dy_perm), _ptr(dw), _ptr(dlogit), _stream(stream))
+              T, H, E, k, _ptr(dy_perm), _ptr(dw), _ptr(dlogit), _ptr(dl_perm), _stream(stream))
+
+
+def router_wgrad_sorted(x, src_token, dl_perm, counts, pad_off, dwg, beta=0.0, stream=None):
+    T, H = x.shape
+    E = dwg.shape[0]
+    _lib.call("dm_router_wgrad_sorted", _ptr(x), _ptr(src_token), _ptr(dl_perm), _ptr(counts), _ptr(pad_off),
+              T, H, E, _ptr(dwg), float(beta), _stream(stream))
 
 
 def permute_bwd(dx_perm, row_map, idx, dlogit, wg, dx, stream=None):

@@ -27,6 +27,8 @@ from . import kernels as K
 BF16 = torch.bfloat16
 F32 = torch.float32
 I32 = torch.int32
+# above this many experts the router weight gradient runs over the expert-sorted rows
+SORTED_WGRAD_MIN_E = 16
 
 
 @dataclass(frozen=True)
@@ -175,6 +177,7 @@ class MicroBatchBuffers:
             self.dy = z(s.T, s.H)
             self.dw = z(s.T, s.k, dt=F32)
             self.dlogit = z(s.T, s.k, dt=F32)
+            self.dl_perm = z(slab.cap, dt=F32) if s.E > SORTED_WGRAD_MIN_E else None
             self.dx = z(s.T, s.H)
         self.x_perm = slab.x_perm[rows]
         self.y_perm = slab.y_perm[rows]
@@ -205,7 +208,7 @@ def a_combine(buf: MicroBatchBuffers, stream=None) -> None:
 
 def a_combine_bwd(buf: MicroBatchBuffers, stream=None) -> None:
     K.combine_bwd(buf.dy, buf.y_perm, buf.row_map, buf.w, buf.counts, buf.pad_off, buf.dy_perm, buf.dw,
-                  buf.dlogit, stream)
+                  buf.dlogit, stream, dl_perm=buf.dl_perm)
 
 
 def f_backward(buf: MicroBatchBuffers, experts: ExpertParams, accumulate: bool, pad_off=None,
@@ -230,8 +233,22 @@ def f_wgrad(slab: ActivationSlab, n: int, experts: ExpertParams, accumulate: boo
 
 
 def a_dispatch_bwd(buf: MicroBatchBuffers, router: RouterParams, accumulate: bool, stream=None) -> None:
+    a_permute_bwd(buf, router, stream)
+    a_router_wgrad(buf, router, accumulate, stream)
+
+
+def a_permute_bwd(buf: MicroBatchBuffers, router: RouterParams, stream=None) -> None:
     K.permute_bwd(buf.dx_perm, buf.row_map, buf.idx, buf.dlogit, router.wg, buf.dx, stream)
-    K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws, router.dwg, 1.0 if accumulate else 0.0, stream)
+
+
+def a_router_wgrad(buf: MicroBatchBuffers, router: RouterParams, accumulate: bool, stream=None) -> None:
+    """dW_g (+)= dlogit^T x: over the expert-sorted rows for large E (one pass, no
+    workspace), else token-blocked partials + a fixed-order reduce."""
+    beta = 1.0 if accumulate else 0.0
+    if buf.dl_perm is not None:
+        K.router_wgrad_sorted(buf.x, buf.src, buf.dl_perm, buf.counts, buf.pad_off, router.dwg, beta, stream)
+    else:
+        K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws, router.dwg, beta, stream)
 
 
 class MoELayer:
@@ -305,7 +322,8 @@ class MoELayer:
         plus 2 wgrad GEMMs unless deferred to the iteration's W pass."""
         s = self.shape
         fused = s.E <= 16 and s.E * s.H * 4 <= 160 * 1024
-        return (3 if fused else 4) + 9 + (0 if deferred_wgrad else 2)
+        router_wgrad = 1 if s.E > SORTED_WGRAD_MIN_E else 2
+        return (3 if fused else 4) + 7 + router_wgrad + (0 if deferred_wgrad else 2)
 
 
 class MoEFunction(torch.autograd.Function):

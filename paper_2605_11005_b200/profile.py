@@ -100,8 +100,7 @@ def measure_stages(shape, device="cuda", iters: int = 5, link_gbs: float = 700.0
     """Time each stage of the fused layer with CUDA events (GPU only)."""
     import torch
 
-    from . import kernels as K
-    from .moe import MoELayer, a_combine, a_combine_bwd, a_dispatch, f_backward, f_forward
+    from .moe import MoELayer, a_combine, a_combine_bwd, a_dispatch, a_dispatch_bwd, f_backward, f_forward
 
     layer = MoELayer.random(shape, device=device, seed=3, num_buffers=2)
     for b in layer.buffers:
@@ -124,8 +123,7 @@ def measure_stages(shape, device="cuda", iters: int = 5, link_gbs: float = 700.0
     f_fwd = timed(lambda: f_forward(buf, layer.experts))
     a_turn = timed(lambda: (a_combine(buf), a_combine_bwd(buf)))
     f_bwd = timed(lambda: f_backward(buf, layer.experts, False, defer_wgrad=True))
-    a_bwd = timed(lambda: (K.permute_bwd(buf.dx_perm, buf.row_map, buf.idx, buf.dlogit, layer.router.wg, buf.dx),
-                           K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws, layer.router.dwg)))
+    a_bwd = timed(lambda: a_dispatch_bwd(buf, layer.router, False))
     layer.forward_backward(layer.buffers[1], defer_wgrad=True)
     f_w = timed(lambda: layer.wgrad(2)) / 2
     s = shape

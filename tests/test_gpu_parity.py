@@ -274,3 +274,33 @@ def test_iteration_matches_oracle_sum_over_microbatches(cuda):
     g1, _ = split_w13(layer.experts.dw13)
     assert O.normwise_rel_err(f32(g1), dw1) < TOL_BF16
     assert O.normwise_rel_err(f32(layer.experts.dw2), dw2) < TOL_BF16
+
+
+def test_router_wgrad_sorted_matches_token_blocked(cuda):
+    """Large-E router gradient over expert-sorted rows == the token-blocked path,
+    is bit-deterministic across runs, and accumulates with beta=1."""
+    from paper_2605_11005_b200 import kernels as K
+    from paper_2605_11005_b200.moe import MoELayer, MoEShape, a_router_wgrad
+
+    shape = MoEShape(T=1000, H=1024, E=64, k=6, De=256)
+    layer = MoELayer.random(shape, device=cuda, seed=9)
+    buf = layer.buffers[0]
+    buf.x.normal_()
+    buf.dy.normal_()
+    layer.forward_backward(buf, accumulate=False)
+    torch.cuda.synchronize()
+    assert buf.dl_perm is not None
+    # dl_perm is dlogit scattered to the permuted rows
+    rm = buf.row_map.long().flatten()
+    assert torch.equal(buf.dl_perm[rm], buf.dlogit.flatten())
+    sorted_dwg = layer.router.dwg.clone()
+    ref = torch.empty_like(sorted_dwg)
+    K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws, ref, 0.0)
+    torch.cuda.synchronize()
+    assert O.normwise_rel_err(f32(sorted_dwg), f32(ref)) < 1e-5
+    a_router_wgrad(buf, layer.router, False)
+    torch.cuda.synchronize()
+    assert torch.equal(layer.router.dwg, sorted_dwg)
+    a_router_wgrad(buf, layer.router, True)
+    torch.cuda.synchronize()
+    assert torch.equal(layer.router.dwg, 2 * sorted_dwg)
