@@ -115,8 +115,10 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "window_s": round(t1 - t0 - 0.2, 3)}
 
 
-def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: int | None = None):
-    """Time the oracle port (numpy fp32 BLAS, all host threads) on a bounded token sample."""
+def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: int | None = None,
+                 layers: int = 1):
+    """Time the oracle port (numpy fp32 BLAS, all host threads) on a bounded token sample
+    of one layer; a stack of `layers` identical-shape layers costs `layers` times that."""
     import numpy as np
 
     from oracle import oracle as O
@@ -151,9 +153,10 @@ def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: i
             break
         T *= 2
     T, dt = best
-    return {"value": T / dt, "unit": UNIT, "cores": threads, "kind": "port",
+    return {"value": T / dt / layers, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{T} tokens of the {shape.T}-token micro-batch, full layer fwd+bwd "
-                      f"(H={H}, E={E}, k={k}, D_e={De}), numpy fp32 BLAS oracle, {dt:.2f} s"}
+                      f"(H={H}, E={E}, k={k}, D_e={De}), numpy fp32 BLAS oracle, {dt:.2f} s"
+                      + (f"; x{layers} layers" if layers > 1 else "")}
 
 
 def run_reference(args, shape, exp):
@@ -163,7 +166,7 @@ def run_reference(args, shape, exp):
     steps, warm = args.steps, args.warmup
     samples = []
     for i in range(warm + steps):
-        r = cpu_baseline(shape, tokens_budget_s=8.0, max_tokens=256)
+        r = cpu_baseline(shape, tokens_budget_s=8.0, max_tokens=256, layers=exp.model.layers)
         if i >= warm:
             samples.append(r)
     value = statistics.median(s["value"] for s in samples)
@@ -172,7 +175,8 @@ def run_reference(args, shape, exp):
         "steps": steps, "warmup": warm, "ms_per_step": None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E,
-                   "k": shape.k, "D_e": shape.De, "microbatches": exp.workload.num_microbatches},
+                   "k": shape.k, "D_e": shape.De, "layers": exp.model.layers,
+                   "microbatches": exp.workload.num_microbatches},
         "cpu_baseline": {**samples[-1], "value": value},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -186,9 +190,8 @@ def run_ours(args, shape, exp):
 
     from paper_2605_11005_b200 import _lib
     from paper_2605_11005_b200 import kernels as K
-    from paper_2605_11005_b200.moe import MoELayer, a_combine, a_combine_bwd, a_dispatch, a_dispatch_bwd, \
-        a_permute_bwd, a_router_wgrad, \
-        f_backward, f_forward
+    from paper_2605_11005_b200.moe import MoELayer, MoEStack, a_combine, a_combine_bwd, a_dispatch, \
+        a_permute_bwd, a_router_wgrad, f_backward, f_forward
 
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
@@ -201,11 +204,15 @@ def run_ours(args, shape, exp):
     if world > 1 and not args.replicas:
         return run_afpipe(args, shape, exp, world, rank, local, dev)
     mb = exp.workload.num_microbatches
-    layer = MoELayer.random(shape, device=dev, seed=1234 + rank, num_buffers=mb)
+    L = exp.model.layers
+    # L > 1: the stack of residual MoE blocks (configs[0]: 2 layers); L = 1: the plain layer
+    stack = MoEStack([MoELayer.random(shape, device=dev, seed=1234 + rank + 1000 * l, num_buffers=mb,
+                                      residual=L > 1) for l in range(L)])
+    layer = stack.layers[0]
     stream = torch.cuda.current_stream(dev)
-    for b in layer.buffers:
+    for b, ob in zip(stack.buffers, stack.out_buffers):
         b.x.normal_()
-        b.dy.normal_()
+        ob.dy.normal_()
 
     # per-stage CUDA events: GEMM (F) time and HBM-kernel (A) time inside the timed region
     class Ev:
@@ -226,43 +233,57 @@ def run_ours(args, shape, exp):
 
     def step(ev=None):
         if ev is None:
-            layer.iteration(mb)
+            stack.iteration(mb)
             return
         for i in range(mb):
-            buf = layer.buffers[i]
             acc = i > 0
-            ev.mark("dispatch", lambda: a_dispatch(buf, layer.router))
-            ev.mark("gemm", lambda: f_forward(buf, layer.experts))
-            ev.mark("combine_fwd", lambda: a_combine(buf))
-            ev.mark("combine_bwd", lambda: a_combine_bwd(buf))
-            ev.mark("gemm", lambda: f_backward(buf, layer.experts, acc, defer_wgrad=True))
-            ev.mark("permute_bwd", lambda: a_permute_bwd(buf, layer.router))
-            ev.mark("router_wgrad", lambda: a_router_wgrad(buf, layer.router, acc))
-        ev.mark("gemm", lambda: layer.wgrad(mb))
+            for ly in stack.layers:
+                buf = ly.buffers[i]
+                ev.mark("dispatch", lambda: a_dispatch(buf, ly.router))
+                ev.mark("gemm", lambda: f_forward(buf, ly.experts))
+                ev.mark("combine_fwd", lambda: a_combine(buf))
+            for ly in reversed(stack.layers):
+                buf = ly.buffers[i]
+                ev.mark("combine_bwd", lambda: a_combine_bwd(buf))
+                ev.mark("gemm", lambda: f_backward(buf, ly.experts, acc, defer_wgrad=True))
+                ev.mark("permute_bwd", lambda: a_permute_bwd(buf, ly.router))
+                ev.mark("router_wgrad", lambda: a_router_wgrad(buf, ly.router, acc))
+        for ly in stack.layers:
+            ev.mark("gemm", lambda: ly.wgrad(mb))
+
+    # the iteration as CUDA graphs (one per micro-batch + the W pass): same kernels,
+    # n+1 host launches per step instead of ~13 per layer and micro-batch
+    graphs = stack.capture(mb) if not args.eager else None
+
+    def run():
+        if graphs is not None:
+            graphs.replay()
+        else:
+            step()
 
     sampler = ClockSampler(dev.index) if rank == 0 else None
     if sampler:
         sampler.start()
     for _ in range(args.warmup):
-        step()
+        run()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     if sampler:
         sampler.mark("start")
-    ev = Ev()
     launches0 = _lib.launch_count()
     t_s = torch.cuda.Event(enable_timing=True)
     t_e = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     t_s.record(stream)
     for _ in range(args.steps):
-        step(ev)
+        run()
     t_e.record(stream)
     torch.cuda.synchronize()
     if sampler:
         sampler.mark("end")
-    launches = _lib.launch_count() - launches0
+    launches = (graphs.launches_per_iteration * args.steps if graphs is not None
+                else _lib.launch_count() - launches0)
     ms = t_s.elapsed_time(t_e)
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -271,8 +292,14 @@ def run_ours(args, shape, exp):
         dist.barrier()
     clocks = sampler.stop() if sampler else None
 
+    # per-stage breakdown: a separate eager pass with CUDA events around every stage
+    ev = Ev()
+    for _ in range(args.steps):
+        step(ev)
+    torch.cuda.synchronize()
+
     # ---- e2e: public API with pinned host buffers, copies inside the timed region
-    e2e = run_e2e(args, layer, shape, mb, dev, world)
+    e2e = run_e2e(args, stack, shape, mb, dev, world, graphs)
 
     if rank != 0:
         if world > 1:
@@ -282,14 +309,14 @@ def run_ours(args, shape, exp):
     tokens = args.steps * mb * shape.T * world
     value = tokens / (ms / 1e3)
     gemm_ms = ev.total_ms("gemm")
-    gemm_flops = args.steps * mb * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd())
+    gemm_flops = args.steps * mb * L * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd())
     achieved_tf = gemm_flops / (gemm_ms / 1e3) / 1e12
     peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     hb = shape.hbm_bytes()
     hbm = {}
     hb["router_wgrad"] = shape.T * shape.H * 2 + shape.T * shape.k * 8
     for name in ("dispatch", "combine_fwd", "combine_bwd", "permute_bwd", "router_wgrad"):
-        t = ev.total_ms(name) / (args.steps * mb)
+        t = ev.total_ms(name) / (args.steps * mb * L)
         gbs = hb[name] / (t / 1e3) / 1e9
         hbm[name] = {"ms": round(t, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 3)}
     traffic = None
@@ -305,17 +332,19 @@ def run_ours(args, shape, exp):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {
             "workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E, "k": shape.k,
-            "D_e": shape.De, "microbatches": mb, "tokens_per_step": mb * shape.T * world,
+            "D_e": shape.De, "layers": L, "microbatches": mb, "tokens_per_step": mb * shape.T * world,
             "parallelism": "fused single-device (A+F on one GPU)" if world == 1 else f"replicas x{world}",
             "weights": "random-init", "l2": "inputs+weights (2.8 GB) larger than L2 (126 MB)",
             "wgrad": "fp32, deferred: one grouped GEMM per iteration over all micro-batches (K = mb*T*k rows)",
+            "launch": "eager" if graphs is None else "CUDA graphs (per micro-batch + W pass)",
+            "stage_breakdown": "separate eager pass with CUDA events per stage (not the timed region)",
         },
         "roofline": {
             "bound": "tensor", "kernel": "grouped expert GEMMs (K4/K5/K8, 6 launches per micro-batch)",
             "achieved": round(achieved_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
             "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
             "peak_kind": f"{peak_kind} sustained bf16 (MEASURED_PEAKS.json)",
-            "gemm_ms_per_microbatch": round(gemm_ms / (args.steps * mb), 4),
+            "gemm_ms_per_microbatch_layer": round(gemm_ms / (args.steps * mb * L), 4),
             "frac_of_burst": round(achieved_tf / peaks["bf16_tflops"], 4),
         },
         "roofline_hbm": {"peak_GB/s": peaks["hbm_gbs"], **hbm},
@@ -324,7 +353,7 @@ def run_ours(args, shape, exp):
         "e2e": e2e,
     }
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(shape, layer=layer)
+        line["cpu_baseline"] = cpu_baseline(shape, layer=layer, layers=L)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -369,12 +398,13 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
 
     mb = exp.workload.num_microbatches
     topo = Topology.default(world, shape.E, args.n_attn)
-    r = AFPipeRank(shape, topo, rank, mb, dev, seed=1234)
+    L = exp.model.layers
+    r = AFPipeRank(shape, topo, rank, mb, dev, seed=1234, layers=L)
     r.init_groups()
     if r.role == "A":
-        for b in r.bufs:
+        for b, ob in zip(r.bufs, r.out_bufs):
             b.x.normal_()
-            b.dy.normal_()
+            ob.dy.normal_()
     sampler = ClockSampler(dev.index) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -457,7 +487,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
             link += [b / ((e - s) / 1e3) / 1e9 for n, i, lane, s, e, b in g["ivs"]
                      if lane != "compute" and e > s and b > 0]
         exposed = _uncovered(comm_all, comp_all)
-        f_flops = mb * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd()) * topo.n_attn
+        f_flops = mb * L * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd()) * topo.n_attn
         achieved = f_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
         peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         line = {
@@ -466,7 +496,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {
                 "workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E, "k": shape.k,
-                "D_e": shape.De, "microbatches": mb, "tokens_per_step": mb * shape.T * topo.n_attn,
+                "D_e": shape.De, "layers": L, "microbatches": mb, "tokens_per_step": mb * shape.T * topo.n_attn,
                 "parallelism": f"AF-Pipe {topo.n_attn}A:{topo.n_ffn}F (A: DP routing/combine, F: EP experts)",
                 "transport": "NCCL send/recv (torch.distributed P2P) over NVLink",
                 "weights": "random-init", "l2": "inputs+weights larger than L2",
@@ -502,7 +532,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
     return 0
 
 
-def run_e2e(args, layer, shape, mb, dev, world):
+def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
     """Same metric through the public API with host buffers: per micro-batch H2D of
     x and dy from pinned memory and D2H of y and dx, overlapped on a copy stream."""
     import torch
@@ -515,7 +545,7 @@ def run_e2e(args, layer, shape, mb, dev, world):
     hdy = [torch.randn(T, H).to(torch.bfloat16).pin_memory() for _ in range(mb)]
     hy = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(mb)]
     hdx = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(mb)]
-    bufs = layer.buffers
+    bufs, obufs = stack.buffers, stack.out_buffers
 
     def step():
         loaded = [torch.cuda.Event() for _ in range(mb)]
@@ -524,18 +554,24 @@ def run_e2e(args, layer, shape, mb, dev, world):
         with torch.cuda.stream(copy):
             for i in range(mb):
                 bufs[i].x.copy_(hx[i], non_blocking=True)
-                bufs[i].dy.copy_(hdy[i], non_blocking=True)
+                obufs[i].dy.copy_(hdy[i], non_blocking=True)
                 loaded[i].record(copy)
         for i in range(mb):
-            b = bufs[i]
             comp.wait_event(loaded[i])
-            layer.forward_backward(b, accumulate=i > 0, defer_wgrad=True)
+            if graphs is not None:
+                graphs.microbatch[i].replay()
+            else:
+                stack.forward_backward(i, accumulate=i > 0, defer_wgrad=True)
             done[i].record(comp)
             with torch.cuda.stream(copy):
                 copy.wait_event(done[i])
-                hy[i].copy_(b.y, non_blocking=True)
-                hdx[i].copy_(b.dx, non_blocking=True)
-        layer.wgrad(mb)
+                hy[i].copy_(obufs[i].y, non_blocking=True)
+                hdx[i].copy_(bufs[i].dx, non_blocking=True)
+        if graphs is not None:
+            graphs.wgrad.replay()
+        else:
+            for ly in stack.layers:
+                ly.wgrad(mb)
         comp.wait_stream(copy)
 
     for _ in range(max(1, args.warmup)):
@@ -559,7 +595,8 @@ def run_e2e(args, layer, shape, mb, dev, world):
     return {"value": round(args.steps * mb * T * world / (ms / 1e3), 1), "unit": UNIT,
             "h2d_bytes_per_step": 2 * per * mb, "d2h_bytes_per_step": 2 * per * mb,
             "ms_per_step": round(ms / args.steps, 3),
-            "path": "MoELayer.forward_backward with pinned host x/dy in, y/dx out (copy stream overlapped)"}
+            "path": ("MoEStack.capture graphs (one per micro-batch + W pass)" if graphs is not None else
+                     "MoEStack.forward_backward") + " with pinned host x/dy in, y/dx out (copy stream overlapped)"}
 
 
 def main(argv=None):
@@ -575,6 +612,7 @@ def main(argv=None):
     ap.add_argument("--seq-len", type=int, default=None, help="override workload.seq_len (sweeps)")
     ap.add_argument("--trace", default=None, help="N>1: write the instrumented iteration as reference-schema trace JSON")
     ap.add_argument("--microbatches", type=int, default=None, help="override workload.num_microbatches")
+    ap.add_argument("--eager", action="store_true", help="N=1: launch kernels eagerly instead of CUDA graphs")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

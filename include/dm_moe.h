@@ -177,17 +177,20 @@ DM_API int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, 
 DM_API int dm_debug_gemm_profile(void* buf);
 
 /* ---- combine (A side) ------------------------------------------------- */
+/* y[t] = resid[t] + sum_j w[t,j] * y_perm[row_map[t,j]]  (fp32 accumulation; resid may be
+ * NULL, else the residual stream of a layer stack; it must not alias y). */
 DM_API int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,
-                   void* y, void* stream);
+                          const void* resid, void* y, void* stream);
 /* dy_perm = w * dy scattered (padding zeroed); dw = <dy, y_perm>;
  * dlogit[t,j] = w_j (dw_j - sum_i w_i dw_i); optional dl_perm[row_map[t,j]] = dlogit[t,j]. */
 DM_API int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_map, const float* w,
                           const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
                           void* dy_perm, float* dw, float* dlogit, float* dl_perm, void* stream);
-/* dx = sum_j dx_perm[row_map] + sum_j dlogit * W_g[idx]  (dlogit may be NULL). */
+/* dx = resid + sum_j dx_perm[row_map] + sum_j dlogit * W_g[idx]  (dlogit and resid may be
+ * NULL; resid is the residual-path gradient of a layer stack and must not alias dx). */
 DM_API int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* idx,
-                          const float* dlogit, const float* wg, int T, int H, int E, int k, void* dx,
-                          void* stream);
+                          const float* dlogit, const float* wg, int T, int H, int E, int k,
+                          const void* resid, void* dx, void* stream);
 /* dW_g[E,H] = sum_{t,j} dlogit[t,j] x[t] at row idx[t,j] (+ beta * dW_g);
  * partial_ws of dm_router_wgrad_workspace_size bytes. */
 DM_API int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int T, int H, int E,

@@ -260,6 +260,33 @@ def moe_backward(fwd: Forward, x_bits, wg, w1, w3, w2, dy, dtype=np.float64) -> 
     return Backward(dx, dwg, dw1, dw3, dw2, dw, dlogit, dy_perm, dx_perm)
 
 
+def moe_stack(x_bits, layers, k, dy, inputs=None):
+    """Stack of residual MoE blocks x_{l+1} = bf16(x_l + MoE_l(x_l)) (the runtime's
+    layers > 1 model; the reference's tiny config has 2 layers, BASELINE configs[0]).
+    layers: [(wg, w1, w3, w2)] per layer. Returns (y [T,H] float, dx, forwards,
+    backwards, xs); the gradient entering layer l is bf16-rounded like the GPU's dx.
+
+    inputs: optional bf16 bits of the layer inputs x_1..x_{L-1} as produced by the
+    device under test. Routing is discontinuous, so a one-ulp difference in x_l can
+    legitimately flip a near-tied expert; feeding the device's own x_l checks every
+    layer bit-exactly on identical inputs (the chain itself is checked by comparing
+    xs[l] with inputs[l-1] within tolerance)."""
+    xs, fs = [x_bits], []
+    for l, (wg, w1, w3, w2) in enumerate(layers):
+        f = moe_forward(xs[-1] if l == 0 or inputs is None else inputs[l - 1], wg, w1, w3, w2, k)
+        fs.append(f)
+        base = xs[-1] if l == 0 or inputs is None else inputs[l - 1]
+        xs.append(f32_to_bf16_bits((bf16_bits_to_f32(base) + f.y).astype(np.float32)))
+    g = round_bf16(np.asarray(dy, np.float32))
+    bs = [None] * len(layers)
+    for l in reversed(range(len(layers))):
+        xl = xs[l] if l == 0 or inputs is None else inputs[l - 1]
+        b = moe_backward(fs[l], xl, *layers[l], g)
+        bs[l] = b
+        g = round_bf16((g + b.dx).astype(np.float32))
+    return bf16_bits_to_f32(xs[-1]), g, fs, bs, xs
+
+
 def normwise_rel_err(got, ref) -> float:
     """max|got - ref| / max|ref| (DESIGN.md §3 error metric)."""
     got = np.asarray(got, np.float64)

@@ -215,38 +215,58 @@ class LayerDurations:
     m2n: int         # one exchange in either direction
 
 
-def build_layer_dag(microbatches: int, d: LayerDurations, a_credit: int = 2, f_credit: int = 2) -> Plan:
+def build_layer_dag(microbatches: int, d: LayerDurations, a_credit: int = 2, f_credit: int = 2,
+                    layers: int = 1) -> Plan:
+    """Runtime chain of a stack of `layers` residual MoE blocks on one A group and one
+    F group (pipeline_depth 1, virtual_stages = layers; reference taskgraph.py:307-356
+    with the loss turnaround on the A side). Per micro-batch:
+
+        A_f[0] M2N[0] F_f[0] N2M[0] A_f[1] ... F_f[L-1] N2M[L-1] A_t
+        M2N_b[L-1] F_b[L-1] N2M_b[L-1] A_b[L-1] M2N_b[L-2] ... A_b[0]
+
+    where A_f[l>0] is layer l-1's combine fused with layer l's dispatch and A_b[l>0]
+    includes layer l-1's combine backward. layers=1 is the single-layer chain."""
     tasks: list[PlanTask] = []
 
-    def new(kind, owner, lane, dur, deps, mb, comp, direction, name):
-        t = PlanTask(len(tasks), kind, owner, lane, dur, tuple(deps), mb, 0, 0, comp, direction)
+    def new(kind, owner, lane, dur, deps, mb, layer, comp, direction, name):
+        t = PlanTask(len(tasks), kind, owner, lane, dur, tuple(deps), mb, layer, layer, comp, direction)
         t.name = name  # type: ignore[attr-defined]
         tasks.append(t)
         return t.id
 
-    def exchange(src, dst, dep, mb, direction, name):
-        s = new("M2NSend", src, SEND, d.m2n, (dep,), mb, None, direction, name)
-        r = new("M2NRecv", dst, RECV, d.m2n, (dep,), mb, None, direction, name)
+    def exchange(src, dst, dep, mb, layer, direction, name):
+        s = new("M2NSend", src, SEND, d.m2n, (dep,), mb, layer, None, direction, name)
+        r = new("M2NRecv", dst, RECV, d.m2n, (dep,), mb, layer, None, direction, name)
         tasks[s].twin, tasks[r].twin = r, s
         return r
 
     for mb in range(microbatches):
-        af = new("FwdCompute", "A0", COMPUTE, d.a_fwd, (), mb, "A", FWD, "A_f")
-        r = exchange("A0", "F0", af, mb, FWD, "M2N")
-        ff = new("FwdCompute", "F0", COMPUTE, d.f_fwd, (r,), mb, "F", FWD, "F_f")
-        r = exchange("F0", "A0", ff, mb, FWD, "N2M")
-        at = new("BwdCompute", "A0", COMPUTE, d.a_turn, (r,), mb, "A", BWD, "A_t")
-        r = exchange("A0", "F0", at, mb, BWD, "M2N_b")
-        fb = new("BwdCompute", "F0", COMPUTE, d.f_bwd, (r,), mb, "F", BWD, "F_b")
-        r = exchange("F0", "A0", fb, mb, BWD, "N2M_b")
-        new("BwdCompute", "A0", COMPUTE, d.a_bwd, (r,), mb, "A", BWD, "A_b")
+        r = None
+        for layer in range(layers):
+            dur = d.a_fwd if layer == 0 else d.a_fwd + d.a_turn // 2
+            af = new("FwdCompute", "A0", COMPUTE, dur, () if r is None else (r,), mb, layer, "A", FWD, "A_f")
+            r = exchange("A0", "F0", af, mb, layer, FWD, "M2N")
+            ff = new("FwdCompute", "F0", COMPUTE, d.f_fwd, (r,), mb, layer, "F", FWD, "F_f")
+            r = exchange("F0", "A0", ff, mb, layer, FWD, "N2M")
+        top = layers - 1
+        at = new("BwdCompute", "A0", COMPUTE, d.a_turn, (r,), mb, top, "A", BWD, "A_t")
+        r = exchange("A0", "F0", at, mb, top, BWD, "M2N_b")
+        for layer in reversed(range(layers)):
+            fb = new("BwdCompute", "F0", COMPUTE, d.f_bwd, (r,), mb, layer, "F", BWD, "F_b")
+            r = exchange("F0", "A0", fb, mb, layer, BWD, "N2M_b")
+            dur = d.a_bwd if layer == 0 else d.a_bwd + d.a_turn // 2
+            ab = new("BwdCompute", "A0", COMPUTE, dur, (r,), mb, layer, "A", BWD, "A_b")
+            if layer > 0:
+                r = exchange("A0", "F0", ab, mb, layer - 1, BWD, "M2N_b")
     return Plan(tasks, {"A0": a_credit, "F0": f_credit})
 
 
-def plan_layer(microbatches: int, d: LayerDurations, a_credit: int = 2, f_credit: int = 2) -> Plan:
-    """Scheduled single-layer chain; every rank issues its tasks in planned-start order,
-    which keeps the per-pair send/recv order identical on both ends (twins share a start)."""
-    return schedule(build_layer_dag(microbatches, d, a_credit, f_credit))
+def plan_layer(microbatches: int, d: LayerDurations, a_credit: int = 2, f_credit: int = 2,
+               layers: int = 1) -> Plan:
+    """Scheduled runtime chain; every rank issues its tasks in planned-start order,
+    which keeps the per-pair send/recv order identical on both ends (twins share a start).
+    Credits scale with the stack depth (reference taskgraph.py:316-321: 2L visits)."""
+    return schedule(build_layer_dag(microbatches, d, a_credit * layers, f_credit * layers, layers))
 
 
 def issue_order(plan: Plan, owner: str) -> list[PlanTask]:

@@ -34,7 +34,8 @@ __device__ __forceinline__ int4 pack8(const float (&f)[8]) {
 template <int KT>
 __global__ void __launch_bounds__(256)
 combine_fwd_kernel(const __nv_bfloat16* __restrict__ y_perm, const int32_t* __restrict__ row_map,
-                   const float* __restrict__ w, int T, int H, int k_rt, __nv_bfloat16* __restrict__ y) {
+                   const float* __restrict__ w, int T, int H, int k_rt, const __nv_bfloat16* __restrict__ resid,
+                   __nv_bfloat16* __restrict__ y) {
   const int k = KT ? KT : k_rt;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -48,8 +49,12 @@ combine_fwd_kernel(const __nv_bfloat16* __restrict__ y_perm, const int32_t* __re
 #pragma unroll 4
     for (int ch = lane; ch < nvec; ch += 32) {
       float acc[8];
+      if (resid) {
+        unpack8(ld_nc_v4(resid + (size_t)t * H + ch * 8), acc);
+      } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+      }
 #pragma unroll
       for (int j = 0; j < k; ++j) {
         float f[8];
@@ -124,7 +129,8 @@ template <int KT>
 __global__ void __launch_bounds__(256)
 permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_map,
                    const int32_t* __restrict__ idx, const float* __restrict__ dlogit,
-                   const float* __restrict__ wg, int T, int H, int k_rt, __nv_bfloat16* __restrict__ dx) {
+                   const float* __restrict__ wg, int T, int H, int k_rt, const __nv_bfloat16* __restrict__ resid,
+                   __nv_bfloat16* __restrict__ dx) {
   const int k = KT ? KT : k_rt;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -142,8 +148,12 @@ permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __r
 #pragma unroll 4
     for (int ch = lane; ch < nvec; ch += 32) {
       float acc[8];
+      if (resid) {
+        unpack8(ld_nc_v4(resid + (size_t)t * H + ch * 8), acc);
+      } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+      }
 #pragma unroll
       for (int j = 0; j < k; ++j) {
         float f[8];
@@ -178,7 +188,7 @@ __global__ void __launch_bounds__(256, 2)
 permute_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_map,
                        const int32_t* __restrict__ idx, const float* __restrict__ dlogit,
                        const float* __restrict__ wg, int T, int H, int E, int k_rt,
-                       __nv_bfloat16* __restrict__ dx) {
+                       const __nv_bfloat16* __restrict__ resid, __nv_bfloat16* __restrict__ dx) {
   const int k = KT ? KT : k_rt;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = ((blockIdx.x * (blockDim.x >> 5) + warp) * 32 + lane) * 8;
@@ -214,8 +224,12 @@ permute_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t*
       }
     }
     float acc[8];
+    if (resid) {
+      unpack8(ld_nc_v4(resid + (size_t)t * H + col), acc);
+    } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+      for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+    }
 #pragma unroll
     for (int j = 0; j < k; ++j) {
       float f[8];
@@ -387,14 +401,19 @@ using namespace dm;
 extern "C" {
 
 int dm_combine_fwd(const void* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,
-                   void* y, void* stream) {
+                   const void* resid, void* y, void* stream) {
   if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK) return set_error(DM_ERR_SHAPE, "combine_fwd bad shape");
+  if (resid && resid == y) return set_error(DM_ERR_SHAPE, "combine_fwd: resid must not alias y");
+  const __nv_bfloat16* yp = reinterpret_cast<const __nv_bfloat16*>(y_perm);
+  const __nv_bfloat16* rs = reinterpret_cast<const __nv_bfloat16*>(resid);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(y);
+  cudaStream_t st = (cudaStream_t)stream;
   switch (k) {
-    case 1: combine_fwd_kernel<1><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
-    case 2: combine_fwd_kernel<2><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
-    case 4: combine_fwd_kernel<4><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
-    case 8: combine_fwd_kernel<8><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
-    default: combine_fwd_kernel<0><<<token_grid(T), 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const __nv_bfloat16*>(y_perm), row_map, w, T, H, k, reinterpret_cast<__nv_bfloat16*>(y)); break;
+    case 1: combine_fwd_kernel<1><<<token_grid(T), 256, 0, st>>>(yp, row_map, w, T, H, k, rs, out); break;
+    case 2: combine_fwd_kernel<2><<<token_grid(T), 256, 0, st>>>(yp, row_map, w, T, H, k, rs, out); break;
+    case 4: combine_fwd_kernel<4><<<token_grid(T), 256, 0, st>>>(yp, row_map, w, T, H, k, rs, out); break;
+    case 8: combine_fwd_kernel<8><<<token_grid(T), 256, 0, st>>>(yp, row_map, w, T, H, k, rs, out); break;
+    default: combine_fwd_kernel<0><<<token_grid(T), 256, 0, st>>>(yp, row_map, w, T, H, k, rs, out); break;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "combine_fwd launch");
@@ -419,15 +438,17 @@ int dm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_map, c
   return DM_OK;
 }
 
-int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* idx,
-                   const float* dlogit, const float* wg, int T, int H, int E, int k, void* dx, void* stream) {
+int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* idx, const float* dlogit,
+                   const float* wg, int T, int H, int E, int k, const void* resid, void* dx, void* stream) {
   if (T < 1 || H % 8 || k < 1 || k > DM_MAX_TOPK || E < 1) return set_error(DM_ERR_SHAPE, "permute_bwd bad shape");
+  if (resid && resid == dx) return set_error(DM_ERR_SHAPE, "permute_bwd: resid must not alias dx");
+  const __nv_bfloat16* rs = reinterpret_cast<const __nv_bfloat16*>(resid);
   cudaStream_t st = (cudaStream_t)stream;
   const __nv_bfloat16* dxp = reinterpret_cast<const __nv_bfloat16*>(dx_perm);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(dx);
   if (E <= 16) {
     dim3 grid((H / 8 + 255) / 256, (T + PBWD_TOKENS - 1) / PBWD_TOKENS);
-#define DM_PBWD(EMV, KTV) permute_bwd_reg_kernel<EMV, KTV><<<grid, 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, E, k, out)
+#define DM_PBWD(EMV, KTV) permute_bwd_reg_kernel<EMV, KTV><<<grid, 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, E, k, rs, out)
     if (E <= 8) {
       switch (k) { case 1: DM_PBWD(8, 1); break; case 2: DM_PBWD(8, 2); break; case 4: DM_PBWD(8, 4); break;
                    case 8: DM_PBWD(8, 8); break; default: DM_PBWD(8, 0); break; }
@@ -438,11 +459,11 @@ int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* i
 #undef DM_PBWD
   } else {
     switch (k) {
-      case 1: permute_bwd_kernel<1><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
-      case 2: permute_bwd_kernel<2><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
-      case 4: permute_bwd_kernel<4><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
-      case 8: permute_bwd_kernel<8><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
-      default: permute_bwd_kernel<0><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, out); break;
+      case 1: permute_bwd_kernel<1><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, rs, out); break;
+      case 2: permute_bwd_kernel<2><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, rs, out); break;
+      case 4: permute_bwd_kernel<4><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, rs, out); break;
+      case 8: permute_bwd_kernel<8><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, rs, out); break;
+      default: permute_bwd_kernel<0><<<token_grid(T), 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, k, rs, out); break;
     }
   }
   cudaError_t e = cudaGetLastError();

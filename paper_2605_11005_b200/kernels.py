@@ -147,11 +147,15 @@ def wgrad(a_tok, b_tok, seg_off, dW, beta=0.0, stream=None, seg_stride_rows=None
 
 
 # ------------------------------------------------------------------ combine
-def combine_fwd(y_perm, row_map, w, y, stream=None):
+def combine_fwd(y_perm, row_map, w, y, stream=None, resid=None):
+    """y = resid + sum_j w_j * y_perm[row_map[:, j]] (resid: optional residual input)."""
     T, k = row_map.shape
     H = y_perm.shape[1]
     _check(y, BF16, (T, H), "y")
-    _lib.call("dm_combine_fwd", _ptr(y_perm), _ptr(row_map), _ptr(w), T, H, k, _ptr(y), _stream(stream))
+    if resid is not None:
+        _check(resid, BF16, (T, H), "resid")
+    _lib.call("dm_combine_fwd", _ptr(y_perm), _ptr(row_map), _ptr(w), T, H, k, _ptr(resid), _ptr(y),
+              _stream(stream))
 
 
 def combine_bwd(dy, y_perm, row_map, w, counts, pad_off, dy_perm, dw, dlogit, stream=None, dl_perm=None):
@@ -169,12 +173,15 @@ def router_wgrad_sorted(x, src_token, dl_perm, counts, pad_off, dwg, beta=0.0, s
               T, H, E, _ptr(dwg), float(beta), _stream(stream))
 
 
-def permute_bwd(dx_perm, row_map, idx, dlogit, wg, dx, stream=None):
+def permute_bwd(dx_perm, row_map, idx, dlogit, wg, dx, stream=None, resid=None):
+    """dx = resid + sum_j dx_perm[row_map[:, j]] + sum_j dlogit_j * W_g[idx_j] (resid optional)."""
     T, k = row_map.shape
     H = dx.shape[1]
     E = wg.shape[0]
+    if resid is not None:
+        _check(resid, BF16, (T, H), "resid")
     _lib.call("dm_permute_bwd", _ptr(dx_perm), _ptr(row_map), _ptr(idx), _ptr(dlogit), _ptr(wg), T, H, E, k,
-              _ptr(dx), _stream(stream))
+              _ptr(resid), _ptr(dx), _stream(stream))
 
 
 def router_wgrad(x, idx, dlogit, partial_ws, dwg, beta=0.0, stream=None):

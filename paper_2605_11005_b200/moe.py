@@ -152,10 +152,15 @@ class ActivationSlab:
 
 class MicroBatchBuffers:
     """Device buffers of one in-flight micro-batch; permuted/F-side tensors are
-    views into an ActivationSlab (both sides live on one device on the fused path)."""
+    views into an ActivationSlab (both sides live on one device on the fused path).
 
-    def __init__(self, shape: MoEShape, device, slab: ActivationSlab, index: int, a_side: bool = True):
+    residual=True makes the layer a residual block, y = x + MoE(x) and
+    dx = dy + J^T dy, fused into combine_fwd / permute_bwd (layer stacks)."""
+
+    def __init__(self, shape: MoEShape, device, slab: ActivationSlab, index: int, a_side: bool = True,
+                 residual: bool = False):
         s = shape
+        self.residual = residual
         dev = torch.device(device)
         z = lambda *sh, dt=BF16: torch.empty(*sh, dtype=dt, device=dev)  # noqa: E731
         self.shape = s
@@ -203,7 +208,7 @@ def f_forward(buf: MicroBatchBuffers, experts: ExpertParams, pad_off=None, strea
 
 
 def a_combine(buf: MicroBatchBuffers, stream=None) -> None:
-    K.combine_fwd(buf.y_perm, buf.row_map, buf.w, buf.y, stream)
+    K.combine_fwd(buf.y_perm, buf.row_map, buf.w, buf.y, stream, resid=buf.x if buf.residual else None)
 
 
 def a_combine_bwd(buf: MicroBatchBuffers, stream=None) -> None:
@@ -238,7 +243,8 @@ def a_dispatch_bwd(buf: MicroBatchBuffers, router: RouterParams, accumulate: boo
 
 
 def a_permute_bwd(buf: MicroBatchBuffers, router: RouterParams, stream=None) -> None:
-    K.permute_bwd(buf.dx_perm, buf.row_map, buf.idx, buf.dlogit, router.wg, buf.dx, stream)
+    K.permute_bwd(buf.dx_perm, buf.row_map, buf.idx, buf.dlogit, router.wg, buf.dx, stream,
+                  resid=buf.dy if buf.residual else None)
 
 
 def a_router_wgrad(buf: MicroBatchBuffers, router: RouterParams, accumulate: bool, stream=None) -> None:
@@ -260,7 +266,7 @@ class MoELayer:
     """
 
     def __init__(self, shape: MoEShape, wg: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor,
-                 device="cuda", num_buffers: int = 1):
+                 device="cuda", num_buffers: int = 1, residual: bool = False):
         shape.validate()
         _lib.load()  # fail loudly if the sm_100a library is absent
         self.shape = shape
@@ -268,10 +274,12 @@ class MoELayer:
         self.router = RouterParams(wg.to(self.device, F32))
         self.experts = ExpertParams(w13.to(self.device, BF16), w2.to(self.device, BF16))
         self.slab = ActivationSlab(shape, num_buffers, self.device)
-        self.buffers = [MicroBatchBuffers(shape, self.device, self.slab, i) for i in range(num_buffers)]
+        self.buffers = [MicroBatchBuffers(shape, self.device, self.slab, i, residual=residual)
+                        for i in range(num_buffers)]
 
     @classmethod
-    def random(cls, shape: MoEShape, device="cuda", seed: int = 0, num_buffers: int = 1) -> "MoELayer":
+    def random(cls, shape: MoEShape, device="cuda", seed: int = 0, num_buffers: int = 1,
+               residual: bool = False) -> "MoELayer":
         g = torch.Generator(device="cpu").manual_seed(seed)
         wg = torch.randn(shape.E, shape.H, generator=g) * 0.02
         dev = torch.device(device)
@@ -280,7 +288,7 @@ class MoELayer:
         gd = torch.Generator(device=dev).manual_seed(seed + 1)
         w13.normal_(0.0, 0.02, generator=gd)
         w2.normal_(0.0, 0.02, generator=gd)
-        return cls(shape, wg, w13, w2, device, num_buffers)
+        return cls(shape, wg, w13, w2, device, num_buffers, residual)
 
     def forward(self, buf: MicroBatchBuffers, stream=None) -> None:
         a_dispatch(buf, self.router, stream)
@@ -324,6 +332,99 @@ class MoELayer:
         fused = s.E <= 16 and s.E * s.H * 4 <= 160 * 1024
         router_wgrad = 1 if s.E > SORTED_WGRAD_MIN_E else 2
         return (3 if fused else 4) + 7 + router_wgrad + (0 if deferred_wgrad else 2)
+
+
+def link_residual_stack(stack_bufs: list[list[MicroBatchBuffers]]) -> None:
+    """Chain per-layer buffers of a residual layer stack in place: layer l+1 reads its
+    input from layer l's output (x_{l+1} is y_l) and layer l's upstream gradient is
+    layer l+1's input gradient (dy_l is dx_{l+1}), so no copies sit between layers."""
+    for lo, hi in zip(stack_bufs[:-1], stack_bufs[1:]):
+        for a, b in zip(lo, hi):
+            b.x = a.y
+            a.dy = b.dx
+
+
+class MoEStack:
+    """Fused single-device stack of residual MoE blocks, x_{l+1} = x_l + MoE_l(x_l)
+    (the tiny config's 2-layer model with the A-side attention omitted).
+
+    Inputs go to `buffers[i].x` (layer 0), upstream gradients to `out_buffers[i].dy`
+    (last layer); outputs are `out_buffers[i].y` and `buffers[i].dx`.
+    """
+
+    def __init__(self, layers: list[MoELayer]):
+        if not layers:
+            raise ValueError("empty stack")
+        self.layers = layers
+        link_residual_stack([l.buffers for l in layers])
+        self.buffers = layers[0].buffers
+        self.out_buffers = layers[-1].buffers
+
+    @classmethod
+    def random(cls, shape: MoEShape, num_layers: int, device="cuda", seed: int = 0,
+               num_buffers: int = 1) -> "MoEStack":
+        return cls([MoELayer.random(shape, device, seed + 1000 * l, num_buffers, residual=True)
+                    for l in range(num_layers)])
+
+    def forward_backward(self, i: int, accumulate: bool = False, stream=None, defer_wgrad: bool = False) -> None:
+        for layer in self.layers:
+            layer.forward(layer.buffers[i], stream)
+        for layer in reversed(self.layers):
+            layer.backward(layer.buffers[i], accumulate, stream, defer_wgrad)
+
+    def iteration(self, n: int | None = None, accumulate: bool = False, stream=None) -> None:
+        n = len(self.buffers) if n is None else n
+        for i in range(n):
+            self.forward_backward(i, accumulate or i > 0, stream, defer_wgrad=True)
+        for layer in self.layers:
+            layer.wgrad(n, accumulate, stream)
+
+    def zero_grad(self) -> None:
+        for layer in self.layers:
+            layer.zero_grad()
+
+    def capture(self, n: int | None = None, accumulate: bool = False) -> "StackGraphs":
+        """Record the iteration as CUDA graphs: one per micro-batch (fwd + bwd of every
+        layer, wgrad deferred) and one for the W pass. Every launch is stream-ordered
+        with device-side sizes and fixed buffers, so the graphs replay with new data
+        written in place; the host then issues n + 1 graph launches per iteration
+        instead of ~13 kernel launches per layer and micro-batch."""
+        n = len(self.buffers) if n is None else n
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):          # warm-up: lazy kernel attributes, TMA paths
+            self.iteration(n, accumulate)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graphs, launches = [], 0
+        for i in range(n):
+            g = torch.cuda.CUDAGraph()
+            c0 = _lib.launch_count()
+            with torch.cuda.graph(g):
+                self.forward_backward(i, accumulate or i > 0, defer_wgrad=True)
+            launches += _lib.launch_count() - c0
+            graphs.append(g)
+        gw = torch.cuda.CUDAGraph()
+        c0 = _lib.launch_count()
+        with torch.cuda.graph(gw):
+            for layer in self.layers:
+                layer.wgrad(n, accumulate)
+        launches += _lib.launch_count() - c0
+        return StackGraphs(graphs, gw, launches)
+
+
+@dataclass
+class StackGraphs:
+    """Captured iteration of a MoEStack: `microbatch[i]` then `wgrad` (MoEStack.capture)."""
+
+    microbatch: list
+    wgrad: object
+    launches_per_iteration: int
+
+    def replay(self) -> None:
+        for g in self.microbatch:
+            g.replay()
+        self.wgrad.replay()
 
 
 class MoEFunction(torch.autograd.Function):

@@ -1,5 +1,5 @@
 """AF-Pipe runtime: attention (A) ranks and FFN (F) ranks of one node exchanging
-micro-batches of one MoE layer over NCCL (NVLink 5 / NVSwitch).
+micro-batches of a stack of MoE layers over NCCL (NVLink 5 / NVSwitch).
 
 One process per GPU (torchrun). Ranks [0, n_attn) are A ranks — data parallel,
 each routes its own micro-batches with a replicated router W_g; ranks
@@ -16,8 +16,14 @@ Per micro-batch i (afpipe.build_layer_dag):
     A_t   combine (weighted sum), loss turnaround, combine bwd -> dy_perm
     M2N_b A -> F: dy_perm slices;   F_b: dgrad GEMMs (wgrad deferred)
     N2M_b F -> A: dx_perm slices;   A_b: permute bwd + router grads
-    end:  F: one wgrad pass over all (micro-batch, A rank) segments;
+    end:  F: one wgrad pass per layer over all (micro-batch, A rank) segments;
           A: all-reduce of dW_g over the A group (the only DP collective).
+
+With `layers` = L > 1 (pipeline_depth 1, virtual_stages L: BASELINE configs[0]) the
+layers are residual blocks x_{l+1} = x_l + MoE_l(x_l): A_f of layer l > 0 is layer
+l-1's combine (residual fused) followed by layer l's dispatch, A_t turns around the
+last layer, and A_b of layer l > 0 also runs layer l-1's combine backward
+(afpipe.build_layer_dag). Layer l+1's input buffer IS layer l's output buffer.
 
 Message sizes are data dependent; the only host synchronisation is reading the
 128-aligned offsets once per micro-batch (A: its own pad_off after dispatch;
@@ -40,7 +46,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .afpipe import COMPUTE, RECV, SEND, LayerDurations, issue_order, plan_layer
-from .moe import ActivationSlab, ExpertParams, MicroBatchBuffers, MoEShape, RouterParams
+from .moe import ActivationSlab, ExpertParams, MicroBatchBuffers, MoEShape, RouterParams, link_residual_stack
 
 BF16, F32, I32 = torch.bfloat16, torch.float32, torch.int32
 
@@ -148,10 +154,14 @@ class GpuStages:
 
         a_dispatch(buf, router)
 
-    def a_turnaround(self, buf: MicroBatchBuffers):
-        from .moe import a_combine, a_combine_bwd
+    def a_combine(self, buf: MicroBatchBuffers):
+        from .moe import a_combine
 
         a_combine(buf)
+
+    def a_combine_bwd(self, buf: MicroBatchBuffers):
+        from .moe import a_combine_bwd
+
         a_combine_bwd(buf)
 
     def a_backward(self, buf: MicroBatchBuffers, router: RouterParams, accumulate: bool):
@@ -204,55 +214,79 @@ class IterationStats:
 
 
 class AFPipeRank:
-    """One rank of the AF-Pipe runtime for a single MoE layer."""
+    """One rank of the AF-Pipe runtime for a stack of `layers` MoE layers (p = 1).
+
+    A ranks: `lbufs[l][i]` (layer l, micro-batch i), `routers[l]`; inputs in
+    `bufs[i].x` (layer 0), upstream gradients in `out_bufs[i].dy` (last layer).
+    F ranks: `expert_layers[l]`, one activation slab per layer. `router` / `experts`
+    alias layer 0 (the single-layer API)."""
 
     def __init__(self, shape: MoEShape, topo: Topology, rank: int, microbatches: int, device,
                  stages=None, seed: int = 0, weights=None, durations: LayerDurations | None = None,
-                 record_events: bool = False):
+                 record_events: bool = False, layers: int = 1, residual: bool | None = None):
         shape.validate() if device.type == "cuda" else None
-        self.shape, self.topo, self.rank, self.mb = shape, topo, rank, microbatches
+        if layers < 1:
+            raise ValueError(f"layers must be >= 1, got {layers}")
+        self.shape, self.topo, self.rank, self.mb, self.L = shape, topo, rank, microbatches, layers
+        self.residual = layers > 1 if residual is None else residual
         self.device = torch.device(device)
         self.role, self.idx = topo.role(rank)
         self.stages = stages if stages is not None else GpuStages()
         self.st = _Streams(self.device)
         self.record_events = record_events and self.st.cuda
         d = durations or self._default_durations()
-        self.plan = plan_layer(microbatches, d)
+        self.plan = plan_layer(microbatches, d, layers=layers)
         self.order = issue_order(self.plan, "A0" if self.role == "A" else "F0")
+        if isinstance(weights, dict):
+            weights = [weights]
+        if weights is not None and len(weights) != layers:
+            raise ValueError(f"{len(weights)} weight sets for {layers} layers")
         s = shape
         if self.role == "A":
-            if weights:
-                wg = weights["wg"]
-            else:
-                wg = torch.randn(s.E, s.H, generator=torch.Generator().manual_seed(seed)) * 0.02
-            self.router = RouterParams(wg.to(self.device, F32))
-            self.slab = ActivationSlab(s, microbatches, self.device, f_side=False)
-            self.bufs = [MicroBatchBuffers(s, self.device, self.slab, i) for i in range(microbatches)]
-            self.pad_host = [torch.empty(s.E + 1, dtype=I32, pin_memory=self.st.cuda) for _ in range(microbatches)]
-            self.pad_ready = [None] * microbatches
+            self.routers, self.lbufs = [], []
+            for l in range(layers):
+                if weights:
+                    wg = weights[l]["wg"]
+                else:
+                    wg = torch.randn(s.E, s.H, generator=torch.Generator().manual_seed(seed + 1000 * l)) * 0.02
+                self.routers.append(RouterParams(wg.to(self.device, F32)))
+                slab = ActivationSlab(s, microbatches, self.device, f_side=False)
+                self.lbufs.append([MicroBatchBuffers(s, self.device, slab, i, residual=self.residual)
+                                   for i in range(microbatches)])
+            link_residual_stack(self.lbufs)
+            self.router, self.bufs, self.out_bufs = self.routers[0], self.lbufs[0], self.lbufs[-1]
+            self.pad_host = [[torch.empty(s.E + 1, dtype=I32, pin_memory=self.st.cuda) for _ in range(microbatches)]
+                             for _ in range(layers)]
+            self.pad_ready = [[None] * microbatches for _ in range(layers)]
             self.a_group = None
         else:
             lo, hi = topo.expert_block(self.idx)
             self.lo, self.hi, self.E_loc = lo, hi, hi - lo
-            if weights:
-                w13, w2 = weights["w13"][lo:hi], weights["w2"][lo:hi]
-            else:
-                g = torch.Generator(device=self.device).manual_seed(seed + 1 + self.idx)
-                w13 = torch.empty(self.E_loc, 2 * s.De, s.H, dtype=BF16, device=self.device).normal_(0, 0.02, generator=g)
-                w2 = torch.empty(self.E_loc, s.H, s.De, dtype=BF16, device=self.device).normal_(0, 0.02, generator=g)
-            self.experts = ExpertParams(w13.to(self.device), w2.to(self.device))
             # worst case: every routed row of every A rank lands on this F rank
             self.cap_f = topo.n_attn * s.cap
-            self.slab = ActivationSlab(s, microbatches, self.device, rows=self.cap_f)
-            self.fmb = []
-            for i in range(microbatches):
-                r = self.slab.rows(i)
-                sl = self.slab
-                self.fmb.append(_FMicroBatch(sl.x_perm[r], sl.y_perm[r], sl.dy_perm[r], sl.dx_perm[r],
-                                             sl.h13[r], sl.act[r], sl.dh13[r]))
-                self.fmb[-1].headers = [torch.zeros(self.E_loc + 1, dtype=I32, device=self.device)
-                                        for _ in range(topo.n_attn)]
-            self.seg_off = torch.zeros(microbatches * topo.n_attn, self.E_loc + 1, dtype=I32, device=self.device)
+            self.expert_layers, self.slabs, self.lfmb, self.seg_offs = [], [], [], []
+            for l in range(layers):
+                if weights:
+                    w13, w2 = weights[l]["w13"][lo:hi], weights[l]["w2"][lo:hi]
+                else:
+                    g = torch.Generator(device=self.device).manual_seed(seed + 1 + self.idx + 1000 * l)
+                    w13 = torch.empty(self.E_loc, 2 * s.De, s.H, dtype=BF16, device=self.device).normal_(0, 0.02, generator=g)
+                    w2 = torch.empty(self.E_loc, s.H, s.De, dtype=BF16, device=self.device).normal_(0, 0.02, generator=g)
+                self.expert_layers.append(ExpertParams(w13.to(self.device), w2.to(self.device)))
+                sl = ActivationSlab(s, microbatches, self.device, rows=self.cap_f)
+                fmb = []
+                for i in range(microbatches):
+                    r = sl.rows(i)
+                    fmb.append(_FMicroBatch(sl.x_perm[r], sl.y_perm[r], sl.dy_perm[r], sl.dx_perm[r],
+                                            sl.h13[r], sl.act[r], sl.dh13[r]))
+                    fmb[-1].headers = [torch.zeros(self.E_loc + 1, dtype=I32, device=self.device)
+                                       for _ in range(topo.n_attn)]
+                self.slabs.append(sl)
+                self.lfmb.append(fmb)
+                self.seg_offs.append(torch.zeros(microbatches * topo.n_attn, self.E_loc + 1, dtype=I32,
+                                                 device=self.device))
+            self.experts, self.slab, self.fmb, self.seg_off = (self.expert_layers[0], self.slabs[0],
+                                                               self.lfmb[0], self.seg_offs[0])
         self.trace: list = []
         self.t0 = None
         self.host_io = None
@@ -289,13 +323,13 @@ class AFPipeRank:
             self.trace.append((name, i, COMPUTE, ev0, self.st.event("compute", True), 0))
 
     # ------------------------------------------------------------- A side
-    def _a_pad(self, i: int) -> list[int]:
-        ev = self.pad_ready[i]
+    def _a_pad(self, layer: int, i: int) -> list[int]:
+        ev = self.pad_ready[layer][i]
         if ev is not None:
             ev.synchronize()
-        return self.pad_host[i].tolist()
+        return self.pad_host[layer][i].tolist()
 
-    def _a_slices(self, i: int, pad: list[int]):
+    def _a_slices(self, pad: list[int]):
         out = []
         for f in range(self.topo.n_ffn):
             lo, hi = self.topo.expert_block(f)
@@ -311,46 +345,56 @@ class AFPipeRank:
         xs, dys, _, _ = self.host_io
         self.h2d_ready = []
         with self.st.ctx("copy"):
-            for b, x, dy in zip(self.bufs, xs, dys):
+            for b, ob, x, dy in zip(self.bufs, self.out_bufs, xs, dys):
                 b.x.copy_(x, non_blocking=True)
-                b.dy.copy_(dy, non_blocking=True)
+                ob.dy.copy_(dy, non_blocking=True)
                 self.h2d_ready.append(self.st.event("copy"))
 
-    def a_task(self, name: str, i: int, accumulate: bool):
-        b = self.bufs[i]
+    def a_task(self, name: str, i: int, layer: int, accumulate: bool):
+        b = self.lbufs[layer][i]
         if name == "A_f":
-            if self.host_io is not None:
-                self.st.wait("compute", self.h2d_ready[i])
-            self.stages.a_dispatch(b, self.router)
+            if layer == 0:
+                if self.host_io is not None:
+                    self.st.wait("compute", self.h2d_ready[i])
+            else:   # previous layer's combine writes this layer's input (residual fused)
+                prev = self.lbufs[layer - 1][i]
+                self._wait_works(prev, "N2M")
+                self.stages.a_combine(prev)
+            self.stages.a_dispatch(b, self.routers[layer])
             done = self.st.event("compute")
             with self.st.ctx("copy"):
                 self.st.wait("copy", done)
-                self.pad_host[i].copy_(b.pad_off, non_blocking=self.st.cuda)
-                self.pad_ready[i] = self.st.event("copy")
+                self.pad_host[layer][i].copy_(b.pad_off, non_blocking=self.st.cuda)
+                self.pad_ready[layer][i] = self.st.event("copy")
             b.fwd_done = done
         elif name == "A_t":
             self._wait_works(b, "N2M")
-            self.stages.a_turnaround(b)
+            self.stages.a_combine(b)
+            self.stages.a_combine_bwd(b)
             b.turn_done = self.st.event("compute")
         elif name == "A_b":
             self._wait_works(b, "N2M_b")
-            self.stages.a_backward(b, self.router, accumulate)
-            if self.host_io is not None:
+            self.stages.a_backward(b, self.routers[layer], accumulate)
+            if layer > 0:   # this layer's dx is the previous layer's upstream gradient
+                prev = self.lbufs[layer - 1][i]
+                self.stages.a_combine_bwd(prev)
+                prev.turn_done = self.st.event("compute")
+            elif self.host_io is not None:
                 _, _, ys, dxs = self.host_io
                 done = self.st.event("compute")
                 with self.st.ctx("copy"):
                     self.st.wait("copy", done)
-                    ys[i].copy_(b.y, non_blocking=True)
+                    ys[i].copy_(self.out_bufs[i].y, non_blocking=True)
                     dxs[i].copy_(b.dx, non_blocking=True)
 
-    def a_comm(self, name: str, i: int, lane: str):
-        b = self.bufs[i]
-        pad = self._a_pad(i)
+    def a_comm(self, name: str, i: int, layer: int):
+        b = self.lbufs[layer][i]
+        pad = self._a_pad(layer, i)
         ops = []
         if name == "M2N":
             with self.st.ctx("send"):
                 self.st.wait("send", b.fwd_done)
-                for f, r0, r1, lo, hi in self._a_slices(i, pad):
+                for f, r0, r1, lo, hi in self._a_slices(pad):
                     peer = self.topo.f_rank(f)
                     hdr = b.pad_off[lo:hi + 1]
                     ops += [("send", hdr, peer), ("send", b.x_perm[r0:r1], peer)]
@@ -358,13 +402,13 @@ class AFPipeRank:
         elif name == "M2N_b":
             with self.st.ctx("send"):
                 self.st.wait("send", b.turn_done)
-                for f, r0, r1, lo, hi in self._a_slices(i, pad):
+                for f, r0, r1, lo, hi in self._a_slices(pad):
                     ops.append(("send", b.dy_perm[r0:r1], self.topo.f_rank(f)))
                 b.works_M2N_b = self._xchg(ops, name, i)
         elif name in ("N2M", "N2M_b"):
             dst = b.y_perm if name == "N2M" else b.dx_perm
             with self.st.ctx("recv"):
-                for f, r0, r1, lo, hi in self._a_slices(i, pad):
+                for f, r0, r1, lo, hi in self._a_slices(pad):
                     ops.append(("recv", dst[r0:r1], self.topo.f_rank(f)))
                 setattr(b, "works_" + name, _exchange(ops))
 
@@ -373,8 +417,8 @@ class AFPipeRank:
             w.wait()  # CUDA: the current (compute) stream waits on the NCCL stream
 
     # ------------------------------------------------------------- F side
-    def f_comm(self, name: str, i: int):
-        fm = self.fmb[i]
+    def f_comm(self, name: str, i: int, layer: int):
+        fm = self.lfmb[layer][i]
         n_a = self.topo.n_attn
         if name == "M2N":
             with self.st.ctx("recv"):
@@ -408,7 +452,7 @@ class AFPipeRank:
                 go, seg = go.pin_memory(), seg.pin_memory()
             fm.group_off = torch.empty(len(offs), dtype=I32, device=self.device)
             fm.group_off.copy_(go, non_blocking=self.st.cuda)
-            self.seg_off[i * n_a:(i + 1) * n_a].copy_(seg, non_blocking=self.st.cuda)
+            self.seg_offs[layer][i * n_a:(i + 1) * n_a].copy_(seg, non_blocking=self.st.cuda)
             with self.st.ctx("recv"):
                 ops = [("recv", fm.x_perm[b0:b0 + r], self.topo.a_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
                 fm.works["M2N"] = _exchange(ops)
@@ -424,17 +468,18 @@ class AFPipeRank:
                 ops = [("send", src[b0:b0 + r], self.topo.a_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
                 fm.works[name] = self._xchg(ops, name, i)
 
-    def f_task(self, name: str, i: int):
-        fm = self.fmb[i]
+    def f_task(self, name: str, i: int, layer: int):
+        fm = self.lfmb[layer][i]
+        experts = self.expert_layers[layer]
         if name == "F_f":
             for w in fm.works.get("M2N", []):
                 w.wait()
-            self.stages.f_forward(fm, self.experts, fm.group_off)
+            self.stages.f_forward(fm, experts, fm.group_off)
             fm.works["N2M_ready"] = self.st.event("compute")
         elif name == "F_b":
             for w in fm.works.get("M2N_b", []):
                 w.wait()
-            self.stages.f_backward(fm, self.experts, fm.group_off)
+            self.stages.f_backward(fm, experts, fm.group_off)
             fm.works["N2M_b_ready"] = self.st.event("compute")
 
     # ------------------------------------------------------------ iteration
@@ -449,32 +494,37 @@ class AFPipeRank:
         if self.host_io is not None and self.role == "A":
             self._h2d_inputs()
         for t in self.order:
-            name, i = t.name, t.microbatch
+            name, i, layer = t.name, t.microbatch, t.layer
             if self.role == "A":
                 if t.lane == COMPUTE:
-                    self._compute(name, i, lambda: self.a_task(name, i, accumulate or i > 0))
+                    self._compute(name, i, lambda: self.a_task(name, i, layer, accumulate or i > 0))
                 else:
-                    self.a_comm(name, i, t.lane)
+                    self.a_comm(name, i, layer)
             else:
                 if t.lane == COMPUTE:
-                    self._compute(name, i, lambda: self.f_task(name, i))
+                    self._compute(name, i, lambda: self.f_task(name, i, layer))
                 else:
-                    self.f_comm(name, i)
+                    self.f_comm(name, i, layer)
         if self.role == "F":
-            self._compute("W", -1, lambda: self.stages.f_wgrad(self.slab, self.experts, self.seg_off, accumulate))
+            def w_pass():
+                for sl, ex, so in zip(self.slabs, self.expert_layers, self.seg_offs):
+                    self.stages.f_wgrad(sl, ex, so, accumulate)
+            self._compute("W", -1, w_pass)
+            for fmb in self.lfmb:
+                for fm in fmb:
+                    for k in ("N2M", "N2M_b"):
+                        for w in fm.works.get(k, []):
+                            w.wait()
         else:
-            for b in self.bufs:
-                self._wait_works(b, "M2N")
-                self._wait_works(b, "M2N_b")
+            for bufs in self.lbufs:
+                for b in bufs:
+                    self._wait_works(b, "M2N")
+                    self._wait_works(b, "M2N_b")
             if self.host_io is not None:
                 self.st.compute.wait_stream(self.st.copy) if self.st.cuda else None
             if self.a_group is not None and self.topo.n_attn > 1:
-                dist.all_reduce(self.router.dwg, group=self.a_group)
-        if self.role == "F":
-            for fm in self.fmb:
-                for k in ("N2M", "N2M_b"):
-                    for w in fm.works.get(k, []):
-                        w.wait()
+                for r in self.routers:
+                    dist.all_reduce(r.dwg, group=self.a_group)
 
     def init_groups(self):
         """Create the A-group communicator (collective: every rank must call it)."""

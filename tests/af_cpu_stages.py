@@ -51,11 +51,18 @@ class CpuStages:
         occ = torch.from_numpy(src >= 0)
         buf.x_perm[occ] = buf.x[torch.from_numpy(src[src >= 0]).long()]
 
-    def a_turnaround(self, buf):
+    def a_combine(self, buf):
         rm = buf.row_map.long()
         yp = buf.y_perm.float()[rm]                       # [T, k, H]
+        y = (yp * buf.w.unsqueeze(-1)).sum(1)
+        if buf.residual:
+            y = y + buf.x.float()
+        buf.y.copy_(y.to(BF16))
+
+    def a_combine_bwd(self, buf):
+        rm = buf.row_map.long()
+        yp = buf.y_perm.float()[rm]
         w = buf.w
-        buf.y.copy_((yp * w.unsqueeze(-1)).sum(1).to(BF16))
         dy = buf.dy.float()
         dw = (yp * dy.unsqueeze(1)).sum(-1)
         buf.dw.copy_(dw)
@@ -67,6 +74,8 @@ class CpuStages:
         rm = buf.row_map.long()
         idx = buf.idx.long()
         dx = buf.dx_perm.float()[rm].sum(1) + torch.einsum("tk,tkh->th", buf.dlogit, router.wg[idx])
+        if buf.residual:
+            dx = dx + buf.dy.float()
         buf.dx.copy_(dx.to(BF16))
         g = torch.zeros_like(router.dwg)
         g.index_add_(0, idx.reshape(-1), (buf.dlogit.unsqueeze(-1) * buf.x.float().unsqueeze(1)).reshape(-1, g.shape[1]))

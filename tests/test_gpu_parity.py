@@ -304,3 +304,72 @@ def test_router_wgrad_sorted_matches_token_blocked(cuda):
     a_router_wgrad(buf, layer.router, True)
     torch.cuda.synchronize()
     assert torch.equal(layer.router.dwg, 2 * sorted_dwg)
+
+
+@pytest.mark.parametrize("E,k", [(8, 2), (32, 4)])
+def test_residual_stack_matches_oracle(cuda, E, k):
+    """Fused single-device 2-layer residual stack (x_{l+1} = x_l + MoE_l(x_l)): the
+    residual adds fused into combine_fwd / permute_bwd and the in-place layer chaining
+    reproduce the oracle stack; all four micro-batch gradients accumulate."""
+    from paper_2605_11005_b200.moe import MoELayer, MoEShape, MoEStack, interleave_w13, split_w13
+
+    T, H, De, L = 200, 256, 256, 2
+    ws = []
+    for l in range(L):
+        _, wg, w1, w3, w2, _ = O.make_inputs(T, H, E, k, De, seed=300 + l)
+        ws.append((wg, w1, w3, w2))
+    shape = MoEShape(T=T, H=H, E=E, k=k, De=De)
+    layers = [MoELayer(shape, torch.from_numpy(wg), interleave_w13(to_dev_bf16(w1, cuda), to_dev_bf16(w3, cuda)),
+                       to_dev_bf16(w2, cuda), cuda, num_buffers=2, residual=True) for wg, w1, w3, w2 in ws]
+    stack = MoEStack(layers)
+    ins = [O.make_inputs(T, H, E, k, De, seed=400 + i) for i in range(2)]
+    for i, (x, *_, dy) in enumerate(ins):
+        stack.buffers[i].x.copy_(to_dev_bf16_bits(x, cuda))
+        stack.out_buffers[i].dy.copy_(to_dev_bf16(dy, cuda))
+    stack.iteration()
+    torch.cuda.synchronize()
+    acc = [{n: 0 for n in ("dwg", "dw1", "dw2")} for _ in range(L)]
+    for i, (x, *_, dy) in enumerate(ins):
+        x1 = layers[1].buffers[i].x.view(torch.int16).cpu().numpy().view(np.uint16)
+        y, dx, fs, bs, xs = O.moe_stack(x, ws, k, dy, inputs=[x1])
+        assert O.normwise_rel_err(O.bf16_bits_to_f32(x1), O.bf16_bits_to_f32(xs[1])) < TOL_BF16
+        assert np.array_equal(layers[1].buffers[i].idx.cpu().numpy(), fs[1].idx), "layer-1 routing differs"
+        assert O.normwise_rel_err(f32(stack.out_buffers[i].y), y) < TOL_BF16
+        assert O.normwise_rel_err(f32(stack.buffers[i].dx), dx) < TOL_BF16
+        for l in range(L):
+            for n in acc[l]:
+                acc[l][n] = acc[l][n] + getattr(bs[l], n)
+    for l in range(L):
+        assert O.normwise_rel_err(f32(layers[l].router.dwg), acc[l]["dwg"]) < TOL_BF16
+        g1, _ = split_w13(layers[l].experts.dw13)
+        assert O.normwise_rel_err(f32(g1), acc[l]["dw1"]) < TOL_BF16
+        assert O.normwise_rel_err(f32(layers[l].experts.dw2), acc[l]["dw2"]) < TOL_BF16
+
+
+def test_stack_graph_replay_matches_eager(cuda):
+    """MoEStack.capture(): CUDA-graph replays give bit-identical outputs and gradients
+    to eager launches, including after new inputs are written in place."""
+    from paper_2605_11005_b200.moe import MoEShape, MoEStack
+
+    shape = MoEShape(T=300, H=256, E=8, k=2, De=256)
+    stack = MoEStack.random(shape, 2, device=cuda, seed=5, num_buffers=2)
+    graphs = stack.capture()
+    assert graphs.launches_per_iteration > 0
+
+    def snap():
+        torch.cuda.synchronize()
+        out = [b.y.clone() for b in stack.out_buffers] + [b.dx.clone() for b in stack.buffers]
+        for ly in stack.layers:
+            out += [ly.router.dwg.clone(), ly.experts.dw13.clone(), ly.experts.dw2.clone()]
+        return out
+
+    for trial in range(2):
+        for b, ob in zip(stack.buffers, stack.out_buffers):
+            b.x.normal_()
+            ob.dy.normal_()
+        stack.iteration()
+        eager = snap()
+        graphs.replay()
+        replay = snap()
+        for a, b_ in zip(eager, replay):
+            assert torch.equal(a, b_)

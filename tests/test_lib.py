@@ -62,7 +62,7 @@ def test_shape_errors_are_negative_codes_without_gpu(lib):
     rc = lib.dm_grouped_wgrad(None, 100, None, 256, None, 1, 8, 1024, 1024, None, ctypes.c_float(0.0), None)
     assert rc == -1
     with pytest.raises(_lib.DMShapeError):
-        _lib.call("dm_combine_fwd", None, None, None, 4, 10, 2, None, None)
+        _lib.call("dm_combine_fwd", None, None, None, 4, 10, 2, None, None, None)
 
 
 def test_missing_library_fails_loudly(tmp_path):

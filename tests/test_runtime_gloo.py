@@ -26,10 +26,10 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _weights():
+def _weights(layer: int = 0):
     from oracle import oracle as O
 
-    _, wg, w1, w3, w2, _ = O.make_inputs(T, H, E, K, DE, seed=7)
+    _, wg, w1, w3, w2, _ = O.make_inputs(T, H, E, K, DE, seed=7 + 31 * layer)
     return wg, w1, w3, w2
 
 
@@ -40,7 +40,7 @@ def _inputs(a: int, i: int):
     return x, dy
 
 
-def _worker(rank, world, n_attn, port, outdir):
+def _worker(rank, world, n_attn, port, outdir, layers=1):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -50,68 +50,81 @@ def _worker(rank, world, n_attn, port, outdir):
     from paper_2605_11005_b200.moe import MoEShape, interleave_w13
     from paper_2605_11005_b200.runtime import AFPipeRank, Topology
 
-    wg, w1, w3, w2 = _weights()
     bf = lambda a: torch.from_numpy(O.f32_to_bf16_bits(a).view(np.int16).copy()).view(torch.bfloat16)  # noqa: E731
-    weights = {"wg": torch.from_numpy(wg), "w13": interleave_w13(bf(w1), bf(w3)), "w2": bf(w2)}
+    weights = []
+    for l in range(layers):
+        wg, w1, w3, w2 = _weights(l)
+        weights.append({"wg": torch.from_numpy(wg), "w13": interleave_w13(bf(w1), bf(w3)), "w2": bf(w2)})
     topo = Topology(world, n_attn, E)
     r = AFPipeRank(MoEShape(T, H, E, K, DE), topo, rank, MB, torch.device("cpu"), stages=CpuStages(),
-                   weights=weights)
+                   weights=weights, layers=layers)
     r.init_groups()
     if r.role == "A":
-        for i, b in enumerate(r.bufs):
+        for i, (b, ob) in enumerate(zip(r.bufs, r.out_bufs)):
             x, dy = _inputs(r.idx, i)
             b.x.copy_(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16))
-            b.dy.copy_(bf(dy))
+            ob.dy.copy_(bf(dy))
     r.run_iteration()
     out = {"role": r.role, "idx": r.idx}
     if r.role == "A":
         out["dx"] = [b.dx.float().numpy() for b in r.bufs]
-        out["y"] = [b.y.float().numpy() for b in r.bufs]
-        out["dwg"] = r.router.dwg.numpy()
+        out["xs"] = [[r.lbufs[l][i].x.view(torch.int16).numpy().view(np.uint16) for l in range(1, layers)]
+                     for i in range(MB)]
+        out["y"] = [b.y.float().numpy() for b in r.out_bufs]
+        out["dwg"] = [rt.dwg.numpy() for rt in r.routers]
     else:
         out["lo"], out["hi"] = r.lo, r.hi
-        out["dw13"] = r.experts.dw13.numpy()
-        out["dw2"] = r.experts.dw2.numpy()
+        out["dw13"] = [ex.dw13.numpy() for ex in r.expert_layers]
+        out["dw2"] = [ex.dw2.numpy() for ex in r.expert_layers]
     torch.save(out, os.path.join(outdir, f"rank{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n_attn", [(2, 1), (3, 1), (3, 2), (4, 2)])
-def test_afpipe_runtime_matches_oracle(world, n_attn):
+def check_against_oracle(outs, n_attn, layers, tol=1e-2):
+    """Compare gathered rank outputs with the oracle residual stack (layers == 1: the
+    plain MoE layer), summing parameter gradients over A ranks and micro-batches."""
     from oracle import oracle as O
 
-    with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, n_attn, _free_port(), d), nprocs=world, join=True)
-        outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
-    wg, w1, w3, w2 = _weights()
-    dwg = np.zeros_like(wg, dtype=np.float64)
-    dw1 = np.zeros_like(w1, dtype=np.float64)
-    dw3 = np.zeros_like(w3, dtype=np.float64)
-    dw2 = np.zeros_like(w2, dtype=np.float64)
+    ws = [_weights(l) for l in range(layers)]
+    acc = [{k: 0 for k in ("dwg", "dw1", "dw3", "dw2")} for _ in range(layers)]
     for a in range(n_attn):
         got = next(o for o in outs if o["role"] == "A" and o["idx"] == a)
         for i in range(MB):
             x, dy = _inputs(a, i)
-            f = O.moe_forward(x, wg, w1, w3, w2, K)
-            b = O.moe_backward(f, x, wg, w1, w3, w2, dy)
-            assert O.normwise_rel_err(got["y"][i], f.y) < 1e-2
-            assert O.normwise_rel_err(got["dx"][i], b.dx) < 1e-2
-            dwg += b.dwg
-            dw1 += b.dw1
-            dw3 += b.dw3
-            dw2 += b.dw2
+            if layers == 1:
+                f = O.moe_forward(x, *ws[0], K)
+                b = O.moe_backward(f, x, *ws[0], dy)
+                y, dx, bs = f.y, b.dx, [b]
+            else:
+                y, dx, _, bs, xs = O.moe_stack(x, ws, K, dy, inputs=got["xs"][i])
+                for a_got, a_ref in zip(got["xs"][i], xs[1:]):
+                    assert O.normwise_rel_err(O.bf16_bits_to_f32(a_got), O.bf16_bits_to_f32(a_ref)) < tol
+            assert O.normwise_rel_err(got["y"][i], y) < tol
+            assert O.normwise_rel_err(got["dx"][i], dx) < tol
+            for l in range(layers):
+                for k in acc[l]:
+                    acc[l][k] = acc[l][k] + getattr(bs[l], k)
     for o in outs:
-        if o["role"] == "A":
-            assert O.normwise_rel_err(o["dwg"], dwg) < 1e-2  # all-reduced over the A group
-        else:
-            lo, hi = o["lo"], o["hi"]
-            v = o["dw13"].reshape(hi - lo, DE // 128, 2, 128, H)
-            g1 = v[:, :, 0].reshape(hi - lo, DE, H)
-            g3 = v[:, :, 1].reshape(hi - lo, DE, H)
-            assert O.normwise_rel_err(g1, dw1[lo:hi]) < 1e-2
-            assert O.normwise_rel_err(g3, dw3[lo:hi]) < 1e-2
-            assert O.normwise_rel_err(o["dw2"], dw2[lo:hi]) < 1e-2
+        for l in range(layers):
+            if o["role"] == "A":
+                assert O.normwise_rel_err(o["dwg"][l], acc[l]["dwg"]) < tol  # all-reduced over the A group
+            else:
+                lo, hi = o["lo"], o["hi"]
+                v = o["dw13"][l].reshape(hi - lo, DE // 128, 2, 128, H)
+                g1 = v[:, :, 0].reshape(hi - lo, DE, H)
+                g3 = v[:, :, 1].reshape(hi - lo, DE, H)
+                assert O.normwise_rel_err(g1, acc[l]["dw1"][lo:hi]) < tol
+                assert O.normwise_rel_err(g3, acc[l]["dw3"][lo:hi]) < tol
+                assert O.normwise_rel_err(o["dw2"][l], acc[l]["dw2"][lo:hi]) < tol
+
+
+@pytest.mark.parametrize("world,n_attn,layers", [(2, 1, 1), (3, 1, 1), (3, 2, 1), (4, 2, 1), (2, 1, 2), (3, 1, 3)])
+def test_afpipe_runtime_matches_oracle(world, n_attn, layers):
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers), nprocs=world, join=True)
+        outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
+    check_against_oracle(outs, n_attn, layers)
 
 
 def test_topology_blocks_match_reference_balanced_blocks():
