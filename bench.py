@@ -133,7 +133,7 @@ def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: i
         w1 = w1t.float().cpu().numpy()
         w3 = w3t.float().cpu().numpy()
         w2 = layer.experts.w2.float().cpu().numpy()
-        wg = layer.router.wg.float().cpu().numpy()
+        wg = (layer.router.wg if hasattr(layer, "router") else layer.wg).float().cpu().numpy()
     else:
         w1 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02)
         w3 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02)
@@ -190,8 +190,7 @@ def run_ours(args, shape, exp):
 
     from paper_2605_11005_b200 import _lib
     from paper_2605_11005_b200 import kernels as K
-    from paper_2605_11005_b200.moe import MoELayer, MoEStack, a_combine, a_combine_bwd, a_dispatch, \
-        a_permute_bwd, a_router_wgrad, f_backward, f_forward
+    from paper_2605_11005_b200.moe import MoELayer, MoEStack
 
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
@@ -205,8 +204,15 @@ def run_ours(args, shape, exp):
         return run_afpipe(args, shape, exp, world, rank, local, dev)
     mb = exp.workload.num_microbatches
     L = exp.model.layers
+    fp32 = exp.model.bytes_per_element == 4
+    if exp.model.bytes_per_element not in (2, 4):
+        raise SystemExit(f"bytes_per_element {exp.model.bytes_per_element}: only bf16 (2) and fp32 (4) modes exist")
+    if fp32:
+        from paper_2605_11005_b200.moe_f32 import MoELayerF32 as LayerCls
+    else:
+        LayerCls = MoELayer
     # L > 1: the stack of residual MoE blocks (configs[0]: 2 layers); L = 1: the plain layer
-    stack = MoEStack([MoELayer.random(shape, device=dev, seed=1234 + rank + 1000 * l, num_buffers=mb,
+    stack = MoEStack([LayerCls.random(shape, device=dev, seed=1234 + rank + 1000 * l, num_buffers=mb,
                                       residual=L > 1) for l in range(L)])
     layer = stack.layers[0]
     stream = torch.cuda.current_stream(dev)
@@ -239,15 +245,15 @@ def run_ours(args, shape, exp):
             acc = i > 0
             for ly in stack.layers:
                 buf = ly.buffers[i]
-                ev.mark("dispatch", lambda: a_dispatch(buf, ly.router))
-                ev.mark("gemm", lambda: f_forward(buf, ly.experts))
-                ev.mark("combine_fwd", lambda: a_combine(buf))
+                ev.mark("dispatch", lambda: ly.stage_dispatch(buf))
+                ev.mark("gemm", lambda: ly.stage_f_forward(buf))
+                ev.mark("combine_fwd", lambda: ly.stage_combine(buf))
             for ly in reversed(stack.layers):
                 buf = ly.buffers[i]
-                ev.mark("combine_bwd", lambda: a_combine_bwd(buf))
-                ev.mark("gemm", lambda: f_backward(buf, ly.experts, acc, defer_wgrad=True))
-                ev.mark("permute_bwd", lambda: a_permute_bwd(buf, ly.router))
-                ev.mark("router_wgrad", lambda: a_router_wgrad(buf, ly.router, acc))
+                ev.mark("combine_bwd", lambda: ly.stage_combine_bwd(buf))
+                ev.mark("gemm", lambda: ly.stage_f_backward(buf, acc))
+                ev.mark("permute_bwd", lambda: ly.stage_permute_bwd(buf))
+                ev.mark("router_wgrad", lambda: ly.stage_router_wgrad(buf, acc))
         for ly in stack.layers:
             ev.mark("gemm", lambda: ly.wgrad(mb))
 
@@ -312,9 +318,10 @@ def run_ours(args, shape, exp):
     gemm_flops = args.steps * mb * L * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd())
     achieved_tf = gemm_flops / (gemm_ms / 1e3) / 1e12
     peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    hb = shape.hbm_bytes()
+    esz = 4 if fp32 else 2
+    hb = shape.hbm_bytes(esz)
     hbm = {}
-    hb["router_wgrad"] = shape.T * shape.H * 2 + shape.T * shape.k * 8
+    hb["router_wgrad"] = shape.T * shape.H * esz + shape.T * shape.k * 8
     for name in ("dispatch", "combine_fwd", "combine_bwd", "permute_bwd", "router_wgrad"):
         t = ev.total_ms(name) / (args.steps * mb * L)
         gbs = hb[name] / (t / 1e3) / 1e9
@@ -329,10 +336,13 @@ def run_ours(args, shape, exp):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if fp32 else "bf16", "data": "synthetic",
         "config": {
             "workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E, "k": shape.k,
-            "D_e": shape.De, "layers": L, "microbatches": mb, "tokens_per_step": mb * shape.T * world,
+            "D_e": shape.De, "layers": L,
+            "precision": ("fp32 mode: fp32 activations/weights, split-3 bf16 tensor-core GEMMs (3x MMA work)"
+                          if fp32 else "bf16 operands, fp32 accumulation and weight gradients"),
+            "microbatches": mb, "tokens_per_step": mb * shape.T * world,
             "parallelism": "fused single-device (A+F on one GPU)" if world == 1 else f"replicas x{world}",
             "weights": "random-init", "l2": "inputs+weights (2.8 GB) larger than L2 (126 MB)",
             "wgrad": "fp32, deferred: one grouped GEMM per iteration over all micro-batches (K = mb*T*k rows)",
@@ -396,6 +406,9 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
     from paper_2605_11005_b200 import _lib
     from paper_2605_11005_b200.runtime import AFPipeRank, Topology, trace_intervals
 
+    if exp.model.bytes_per_element != 2:
+        raise SystemExit("AF-Pipe runtime exchanges bf16 micro-batches; fp32 mode (bytes_per_element 4) runs on "
+                         "the fused single-device path (N=1, or --replicas)")
     mb = exp.workload.num_microbatches
     topo = Topology.default(world, shape.E, args.n_attn)
     L = exp.model.layers
@@ -539,12 +552,13 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
     import torch.distributed as dist
 
     T, H = shape.T, shape.H
+    dt = stack.layers[0].dtype
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
-    hx = [torch.randn(T, H).to(torch.bfloat16).pin_memory() for _ in range(mb)]
-    hdy = [torch.randn(T, H).to(torch.bfloat16).pin_memory() for _ in range(mb)]
-    hy = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(mb)]
-    hdx = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(mb)]
+    hx = [torch.randn(T, H).to(dt).pin_memory() for _ in range(mb)]
+    hdy = [torch.randn(T, H).to(dt).pin_memory() for _ in range(mb)]
+    hy = [torch.empty(T, H, dtype=dt).pin_memory() for _ in range(mb)]
+    hdx = [torch.empty(T, H, dtype=dt).pin_memory() for _ in range(mb)]
     bufs, obufs = stack.buffers, stack.out_buffers
 
     def step():
@@ -591,7 +605,7 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = tt.item()
-    per = T * H * 2
+    per = T * H * hx[0].element_size()
     return {"value": round(args.steps * mb * T * world / (ms / 1e3), 1), "unit": UNIT,
             "h2d_bytes_per_step": 2 * per * mb, "d2h_bytes_per_step": 2 * per * mb,
             "ms_per_step": round(ms / args.steps, 3),

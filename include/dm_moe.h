@@ -202,6 +202,48 @@ DM_API int dm_router_wgrad_sorted(const void* x, const int32_t* src_token, const
                                   const int32_t* counts, const int32_t* pad_off, int T, int H, int E,
                                   float* dwg, float beta, void* stream);
 
+/* ---- fp32 mode (experiment bytes_per_element = 4; 1e-4 parity) ---------------
+ * fp32 activations / gradients / master weights. GEMM operands are bf16 "split-3":
+ * v = hi + lo with hi = bf16(v), lo = bf16(v - hi); activations are stored as rows
+ * [hi | hi | lo] along K (3K columns), weights as [hi | lo | hi] (K-major) or with
+ * per-matrix stacked rows [hi; lo; hi] (MN-major), so one tcgen05 bf16 GEMM over
+ * K3 = 3K sums a_hi.b_hi + a_hi.b_lo + a_lo.b_hi into fp32 (error ~2^-16).
+ *   replaces (reference): the fp32 path selected by ModelConfig.bytes_per_element
+ *                          pkg/src/afpipe/config.py:45-60 (costs only, costs.py:95-103) */
+/* Router (fp32 x, canonical order) + top-k + scan + permute into x3 [cap, 3H]. */
+DM_API int dm_route_and_dispatch_f32(const float* x, const float* wg, int T, int H, int E, int k, void* workspace,
+                                     int32_t* idx, float* w, int32_t* counts, int32_t* pad_off, int32_t* row_map,
+                                     int32_t* src_token, void* x3, void* stream);
+/* C[cap, N] fp32 = A3[cap, K3] . B3_g (group g uses matrix g % E): B3 K-major [E*N, K3]
+ * (b_mn_major 0) or MN-major [E*K3, N] (1). Groups as in the bf16 GEMMs. */
+DM_API int dm_grouped_gemm_f32(const void* a3, const void* b3, int b_mn_major, const int32_t* group_off, int G,
+                               int E, int cap_rows, int N, int K3, float* c, void* stream);
+DM_API int dm_combine_fwd_f32(const float* y_perm, const int32_t* row_map, const float* w, int T, int H, int k,
+                              const float* resid, float* y, void* stream);
+/* dy3 [cap, 3H] = split-3 of w * dy at the permuted rows (padding zeroed). */
+DM_API int dm_combine_bwd_f32(const float* dy, const float* y_perm, const int32_t* row_map, const float* w,
+                              const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
+                              void* dy3, float* dw, float* dlogit, float* dl_perm, void* stream);
+DM_API int dm_permute_bwd_f32(const float* dx_perm, const int32_t* row_map, const int32_t* idx,
+                              const float* dlogit, const float* wg, int T, int H, int E, int k, const float* resid,
+                              float* dx, void* stream);
+DM_API int dm_router_wgrad_sorted_f32(const float* x, const int32_t* src_token, const float* dl_perm,
+                                      const int32_t* counts, const int32_t* pad_off, int T, int H, int E,
+                                      float* dwg, float beta, void* stream);
+/* act3 [rows, 3De] = split-3(silu(gate) * up) of fp32 h13 [rows, 2De] (128-col blocks). */
+DM_API int dm_swiglu_fwd_split(const float* h13, int rows, int De, void* act3, void* stream);
+/* dh13_3 [rows, 6De] = split-3 of the SwiGLU backward of fp32 d_act [rows, De]. */
+DM_API int dm_swiglu_bwd_split(const float* d_act, const float* h13, int rows, int De, void* dh13_3,
+                               void* stream);
+/* dm_grouped_wgrad with explicit row strides (elements) of the token-major operands,
+ * e.g. the hi / lo column blocks of split-3 activations. */
+DM_API int dm_grouped_wgrad_strided(const void* a_tok, int M, int lda, const void* b_tok, int N, int ldb,
+                                    const int32_t* seg_off, int nseg, int E, int total_rows, int seg_stride_rows,
+                                    float* dW, float beta, void* stream);
+/* fp32 [groups*rows, cols] -> bf16 split-3; layout 0: [hi|hi|lo] rows, 1: [hi|lo|hi]
+ * rows, 2: per group of `rows` rows, stacked [hi; lo; hi] (dst [groups*3*rows, cols]). */
+DM_API int dm_split3(const float* src, int groups, int rows, int cols, int layout, void* dst, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

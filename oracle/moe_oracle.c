@@ -42,12 +42,13 @@ static inline float bf16_to_f32(uint16_t v) {
  * visits its elements in ascending order, which is all the convention fixes.
  * target_clones picks a hardware-FMA build at load time when the CPU has one. */
 __attribute__((target_clones("fma", "default")))
-void dm_oracle_router_logits(const uint16_t* x, const float* wg, int T, int H, int E, float* logits) {
+static void router_logits_core(const uint16_t* xb, const float* xf, const float* wg, int T, int H, int E,
+                               float* logits) {
   const int nch = H / 8;
   float* part = (float*)malloc(sizeof(float) * 64 * (size_t)E);   /* [p][s][e] */
   float* xr = (float*)malloc(sizeof(float) * (size_t)H);
   for (int t = 0; t < T; ++t) {
-    for (int h = 0; h < H; ++h) xr[h] = bf16_to_f32(x[(size_t)t * H + h]);
+    for (int h = 0; h < H; ++h) xr[h] = xb ? bf16_to_f32(xb[(size_t)t * H + h]) : xf[(size_t)t * H + h];
     for (int i = 0; i < 64 * E; ++i) part[i] = 0.0f;
     for (int c = 0; c < nch; ++c) {
       for (int j = 0; j < 8; ++j) {
@@ -70,6 +71,15 @@ void dm_oracle_router_logits(const uint16_t* x, const float* wg, int T, int H, i
   }
   free(xr);
   free(part);
+}
+
+void dm_oracle_router_logits(const uint16_t* x, const float* wg, int T, int H, int E, float* logits) {
+  router_logits_core(x, NULL, wg, T, H, E, logits);
+}
+
+/* fp32 mode (bytes_per_element 4): the same canonical order on fp32 activations. */
+void dm_oracle_router_logits_f32(const float* x, const float* wg, int T, int H, int E, float* logits) {
+  router_logits_core(NULL, x, wg, T, H, E, logits);
 }
 
 /* idx[T*k], w[T*k] from logits (conventions 2-3). */

@@ -69,6 +69,7 @@ def clib() -> C.CDLL:
         p = C.c_void_p
         _clib.dm_oracle_router.argtypes = [p, p, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p]
         _clib.dm_oracle_router_logits.argtypes = [p, p, C.c_int, C.c_int, C.c_int, p]
+        _clib.dm_oracle_router_logits_f32.argtypes = [p, p, C.c_int, C.c_int, C.c_int, p]
         _clib.dm_oracle_topk.argtypes = [p, C.c_int, C.c_int, C.c_int, p, p]
         _clib.dm_oracle_dispatch.argtypes = [p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, p, p, p, p]
         _clib.dm_oracle_dispatch.restype = C.c_int
@@ -89,6 +90,18 @@ def router(x_bits: np.ndarray, wg: np.ndarray, k: int):
     idx = np.empty((T, k), np.int32)
     w = np.empty((T, k), np.float32)
     clib().dm_oracle_router(_ptr(x_bits), _ptr(wg), T, H, E, k, _ptr(logits), _ptr(idx), _ptr(w))
+    return logits, idx, w
+
+
+def router_f32(x: np.ndarray, wg: np.ndarray, k: int):
+    """fp32 mode: canonical-order logits of fp32 activations, top-k, softmax weights."""
+    T, H = x.shape
+    E = wg.shape[0]
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    wg = np.ascontiguousarray(wg, dtype=np.float32)
+    logits = np.empty((T, E), np.float32)
+    clib().dm_oracle_router_logits_f32(_ptr(x), _ptr(wg), T, H, E, _ptr(logits))
+    idx, w = topk(logits, k)
     return logits, idx, w
 
 
@@ -179,15 +192,21 @@ class Forward:
     y: np.ndarray = field(repr=False)        # [T, H]
 
 
+def _values(x) -> np.ndarray:
+    """uint16 arrays are bf16 bit patterns (bf16 mode); float arrays are values (fp32 mode)."""
+    return bf16_bits_to_f32(x) if x.dtype == np.uint16 else np.asarray(x, np.float32)
+
+
 def moe_forward(x_bits, wg, w1, w3, w2, k, dtype=np.float64) -> Forward:
-    """Full layer forward. x_bits: uint16 bf16 [T,H]; w1/w3 [E,D_e,H], w2 [E,H,D_e]
-    as float arrays holding bf16 values; wg fp32 [E,H]."""
+    """Full layer forward. x_bits: uint16 bf16 [T,H] (bf16 mode) or float32 [T,H]
+    (fp32 mode, bytes_per_element 4); w1/w3 [E,D_e,H], w2 [E,H,D_e] as float arrays
+    (bf16 values in bf16 mode); wg fp32 [E,H]."""
     T, H = x_bits.shape
     E = wg.shape[0]
     De = w1.shape[1]
-    logits, idx, w = router(x_bits, wg, k)
+    logits, idx, w = router(x_bits, wg, k) if x_bits.dtype == np.uint16 else router_f32(x_bits, wg, k)
     counts, pad_off, row_map, src = dispatch(idx, E)
-    x = bf16_bits_to_f32(x_bits).astype(dtype)
+    x = _values(x_bits).astype(dtype)
     cap = src.shape[0]
     g = np.zeros((cap, De), dtype)
     u = np.zeros((cap, De), dtype)
@@ -225,7 +244,7 @@ def moe_backward(fwd: Forward, x_bits, wg, w1, w3, w2, dy, dtype=np.float64) -> 
     """Gradients of <y, dy> w.r.t. x, W_g, W1, W3, W2 (dy given as float values)."""
     T, H = x_bits.shape
     E, De, _ = w1.shape
-    x = bf16_bits_to_f32(x_bits).astype(dtype)
+    x = _values(x_bits).astype(dtype)
     dy = np.asarray(dy, dtype)
     w = fwd.w.astype(dtype)
     rm = fwd.row_map

@@ -66,6 +66,19 @@ SIGNATURES: dict[str, tuple] = {
     "dm_router_wgrad_sorted": (_i, [_vp, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _f32p, _f, _vp]),
     "dm_permute_bwd": (_i, [_vp, _i32p, _i32p, _f32p, _f32p, _i, _i, _i, _i, _vp, _vp, _vp]),
     "dm_router_wgrad": (_i, [_vp, _i32p, _f32p, _i, _i, _i, _i, _f32p, _f32p, _f, _vp]),
+    # fp32 mode (bytes_per_element 4)
+    "dm_route_and_dispatch_f32": (_i, [_f32p, _f32p, _i, _i, _i, _i, _vp, _i32p, _f32p, _i32p, _i32p,
+                                       _i32p, _i32p, _vp, _vp]),
+    "dm_grouped_gemm_f32": (_i, [_vp, _vp, _i, _i32p, _i, _i, _i, _i, _i, _f32p, _vp]),
+    "dm_combine_fwd_f32": (_i, [_f32p, _i32p, _f32p, _i, _i, _i, _f32p, _f32p, _vp]),
+    "dm_combine_bwd_f32": (_i, [_f32p, _f32p, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _i, _vp, _f32p,
+                                _f32p, _f32p, _vp]),
+    "dm_permute_bwd_f32": (_i, [_f32p, _i32p, _i32p, _f32p, _f32p, _i, _i, _i, _i, _f32p, _f32p, _vp]),
+    "dm_router_wgrad_sorted_f32": (_i, [_f32p, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _f32p, _f, _vp]),
+    "dm_swiglu_fwd_split": (_i, [_f32p, _i, _i, _vp, _vp]),
+    "dm_swiglu_bwd_split": (_i, [_f32p, _f32p, _i, _i, _vp, _vp]),
+    "dm_split3": (_i, [_f32p, _i, _i, _i, _i, _vp, _vp]),
+    "dm_grouped_wgrad_strided": (_i, [_vp, _i, _i, _vp, _i, _i, _i32p, _i, _i, _i, _i, _f32p, _f, _vp]),
 }
 
 _lib = None

@@ -1002,19 +1002,21 @@ int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* group
   return launch_gemm<0, 1, 0, EPI_BF16>(A, B, et, a, (cudaStream_t)stream);
 }
 
-int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* seg_off,
-                     int nseg, int E, int total_rows, int seg_stride_rows, float* dW, float beta,
-                     void* stream) {
+int dm_grouped_wgrad_strided(const void* a_tok, int M, int lda, const void* b_tok, int N, int ldb,
+                             const int32_t* seg_off, int nseg, int E, int total_rows, int seg_stride_rows,
+                             float* dW, float beta, void* stream) {
   int rc = check_groups(E, E, total_rows);
   if (rc) return rc;
   if (M % 256 || N % GBN || M <= 0 || N <= 0)
     return set_error(DM_ERR_SHAPE, "wgrad needs M %% 256 == 0 and N %% 256 == 0 (M=%d, N=%d)", M, N);
+  if (lda < M || ldb < N || lda % 8 || ldb % 8)
+    return set_error(DM_ERR_SHAPE, "wgrad row strides (lda=%d, ldb=%d) must be >= M/N and multiples of 8", lda, ldb);
   if (nseg < 1 || nseg > 64) return set_error(DM_ERR_SHAPE, "wgrad segments %d outside [1, 64]", nseg);
   if (seg_stride_rows < 0 || (long long)(nseg - 1) * seg_stride_rows > total_rows)
     return set_error(DM_ERR_SHAPE, "wgrad segment stride %d inconsistent with %d rows", seg_stride_rows, total_rows);
   if (reinterpret_cast<uintptr_t>(dW) & 15) return set_error(DM_ERR_ALIGN, "dW not 16-byte aligned");
-  const GemmOperand A{a_tok, (uint64_t)M, (uint64_t)total_rows, (uint64_t)M, true, false};
-  const GemmOperand B{b_tok, (uint64_t)N, (uint64_t)total_rows, (uint64_t)N, true, true};
+  const GemmOperand A{a_tok, (uint64_t)M, (uint64_t)total_rows, (uint64_t)lda, true, false};
+  const GemmOperand B{b_tok, (uint64_t)N, (uint64_t)total_rows, (uint64_t)ldb, true, true};
   GemmArgs a{};
   a.num_groups = E; a.group_off = seg_off; a.M = M; a.N = N;
   a.C = dW; a.ldc = N; a.c_group_stride = (long long)M * N; a.beta = beta;
@@ -1022,6 +1024,36 @@ int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const i
   EpiTensors et;
   et.c = {dW, true, (uint64_t)N, (uint64_t)E * M, (uint64_t)N};
   return launch_gemm<1, 1, 1, EPI_F32>(A, B, et, a, (cudaStream_t)stream);
+}
+
+int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, const int32_t* seg_off,
+                     int nseg, int E, int total_rows, int seg_stride_rows, float* dW, float beta,
+                     void* stream) {
+  return dm_grouped_wgrad_strided(a_tok, M, M, b_tok, N, N, seg_off, nseg, E, total_rows, seg_stride_rows, dW,
+                                  beta, stream);
+}
+
+int dm_grouped_gemm_f32(const void* a3, const void* b3, int b_mn_major, const int32_t* group_off, int G, int E,
+                        int cap_rows, int N, int K3, float* c, void* stream) {
+  int rc = check_groups(G, E, cap_rows);
+  if (rc) return rc;
+  if (K3 % GBK || K3 < GBK || N % GBN || N < GBN)
+    return set_error(DM_ERR_SHAPE, "gemm_f32 needs K3 %% 64 == 0 and N %% 256 == 0 (K3=%d, N=%d)", K3, N);
+  if (reinterpret_cast<uintptr_t>(c) & 15) return set_error(DM_ERR_ALIGN, "C not 16-byte aligned");
+  const GemmOperand A{a3, (uint64_t)K3, (uint64_t)cap_rows, (uint64_t)K3, false, false};
+  GemmArgs a{};
+  a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = N; a.K = K3; a.M = 0;
+  a.C = c; a.ldc = N; a.beta = 0.0f;
+  EpiTensors et;
+  et.c = {c, true, (uint64_t)N, (uint64_t)cap_rows, (uint64_t)N};
+  if (b_mn_major) {
+    const GemmOperand B{b3, (uint64_t)N, (uint64_t)E * K3, (uint64_t)N, true, true};
+    a.b_group_rows = K3;
+    return launch_gemm<0, 1, 0, EPI_F32>(A, B, et, a, (cudaStream_t)stream);
+  }
+  const GemmOperand B{b3, (uint64_t)K3, (uint64_t)E * N, (uint64_t)K3, false, true};
+  a.b_group_rows = N;
+  return launch_gemm<0, 0, 0, EPI_F32>(A, B, et, a, (cudaStream_t)stream);
 }
 
 /* Debug/profiling hook: when `buf` (device, >= 5 u64, zeroed by the caller) is

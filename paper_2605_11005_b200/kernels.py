@@ -12,6 +12,7 @@ import torch
 from . import _lib
 
 BF16 = torch.bfloat16
+F32 = torch.float32
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -193,3 +194,90 @@ def router_wgrad(x, idx, dlogit, partial_ws, dwg, beta=0.0, stream=None):
         raise ValueError(f"router wgrad workspace too small ({need} bytes needed)")
     _lib.call("dm_router_wgrad", _ptr(x), _ptr(idx), _ptr(dlogit), T, H, E, k, _ptr(partial_ws), _ptr(dwg),
               float(beta), _stream(stream))
+
+
+# ------------------------------------------------------------------ fp32 mode
+# (bytes_per_element 4): fp32 activations, split-3 bf16 GEMM operands (dm_moe.h).
+SPLIT_ACT, SPLIT_WK, SPLIT_WMN = 0, 1, 2
+
+
+def split3(src, dst, layout, groups=1, stream=None):
+    """fp32 [groups*rows, cols] -> split-3 bf16 (layout SPLIT_ACT / SPLIT_WK / SPLIT_WMN)."""
+    rows_total, cols = src.reshape(-1, src.shape[-1]).shape
+    _lib.call("dm_split3", _ptr(src), groups, rows_total // groups, cols, layout, _ptr(dst), _stream(stream))
+
+
+def route_and_dispatch_f32(x, wg, k, workspace, idx, w, counts, pad_off, row_map, src_token, x3, stream=None):
+    T, H = x.shape
+    E = wg.shape[0]
+    _check(x, F32, (T, H), "x")
+    _lib.call("dm_route_and_dispatch_f32", _ptr(x), _ptr(wg), T, H, E, k, _ptr(workspace), _ptr(idx), _ptr(w),
+              _ptr(counts), _ptr(pad_off), _ptr(row_map), _ptr(src_token), _ptr(x3), _stream(stream))
+
+
+def gemm_f32(a3, b3, b_mn_major, group_off, c, num_weights, stream=None):
+    """c[cap, N] fp32 = a3[cap, K3] . B3_(g % E); B3 K-major [E*N, K3] or MN-major [E*K3, N]."""
+    cap, K3 = a3.shape
+    N = c.shape[1]
+    G = group_off.shape[-1] - 1
+    _check(c, F32, (cap, N), "c")
+    _lib.call("dm_grouped_gemm_f32", _ptr(a3), _ptr(b3), int(b_mn_major), _ptr(group_off), G, num_weights, cap,
+              N, K3, _ptr(c), _stream(stream))
+
+
+def combine_fwd_f32(y_perm, row_map, w, y, stream=None, resid=None):
+    T, k = row_map.shape
+    H = y_perm.shape[1]
+    _check(y, F32, (T, H), "y")
+    _lib.call("dm_combine_fwd_f32", _ptr(y_perm), _ptr(row_map), _ptr(w), T, H, k, _ptr(resid), _ptr(y),
+              _stream(stream))
+
+
+def combine_bwd_f32(dy, y_perm, row_map, w, counts, pad_off, dy3, dw, dlogit, dl_perm, stream=None):
+    T, H = dy.shape
+    k = row_map.shape[1]
+    E = counts.shape[0]
+    _lib.call("dm_combine_bwd_f32", _ptr(dy), _ptr(y_perm), _ptr(row_map), _ptr(w), _ptr(counts), _ptr(pad_off),
+              T, H, E, k, _ptr(dy3), _ptr(dw), _ptr(dlogit), _ptr(dl_perm), _stream(stream))
+
+
+def permute_bwd_f32(dx_perm, row_map, idx, dlogit, wg, dx, stream=None, resid=None):
+    T, k = row_map.shape
+    H = dx.shape[1]
+    E = wg.shape[0]
+    _lib.call("dm_permute_bwd_f32", _ptr(dx_perm), _ptr(row_map), _ptr(idx), _ptr(dlogit), _ptr(wg), T, H, E, k,
+              _ptr(resid), _ptr(dx), _stream(stream))
+
+
+def router_wgrad_sorted_f32(x, src_token, dl_perm, counts, pad_off, dwg, beta=0.0, stream=None):
+    T, H = x.shape
+    E = dwg.shape[0]
+    _lib.call("dm_router_wgrad_sorted_f32", _ptr(x), _ptr(src_token), _ptr(dl_perm), _ptr(counts), _ptr(pad_off),
+              T, H, E, _ptr(dwg), float(beta), _stream(stream))
+
+
+def swiglu_fwd_split(h13, act3, stream=None):
+    rows, two_de = h13.shape
+    _lib.call("dm_swiglu_fwd_split", _ptr(h13), rows, two_de // 2, _ptr(act3), _stream(stream))
+
+
+def swiglu_bwd_split(d_act, h13, dh13_3, stream=None):
+    rows, De = d_act.shape
+    _lib.call("dm_swiglu_bwd_split", _ptr(d_act), _ptr(h13), rows, De, _ptr(dh13_3), _stream(stream))
+
+
+def wgrad_split3(a3, M, b3, N, seg_off, dW, beta=0.0, stream=None, seg_stride_rows=None):
+    """dW[g] (+)= A^T B over each group's rows from split-3 operands a3 [R, 3M], b3 [R, 3N]:
+    three strided ragged-K GEMMs a_hi.b_hi + a_hi.b_lo + a_lo.b_hi (fp32 reduce-add)."""
+    total_rows = a3.shape[0]
+    so = seg_off.reshape(-1, seg_off.shape[-1])
+    nseg, E = so.shape[0], so.shape[1] - 1
+    stride = total_rows // nseg if seg_stride_rows is None else seg_stride_rows
+    if not (a3.is_contiguous() and b3.is_contiguous()):
+        raise ValueError("split-3 operands must be contiguous")
+    base_a, base_b = a3.data_ptr(), b3.data_ptr()
+    hi_a, lo_a = base_a, base_a + 2 * M * a3.element_size()
+    hi_b, lo_b = base_b, base_b + 2 * N * b3.element_size()
+    for i, (pa, pb) in enumerate(((hi_a, hi_b), (hi_a, lo_b), (lo_a, hi_b))):
+        _lib.call("dm_grouped_wgrad_strided", pa, M, 3 * M, pb, N, 3 * N, _ptr(so), nseg, E, total_rows, stride,
+                  _ptr(dW), float(beta) if i == 0 else 1.0, _stream(stream))

@@ -64,8 +64,8 @@ class MoEShape:
     def gemm_flops_bwd(self) -> int:
         return 12 * self.R * self.H * self.De
 
-    def hbm_bytes(self) -> dict[str, int]:
-        T, H, R, e = self.T, self.H, self.R, 2
+    def hbm_bytes(self, e: int = 2) -> dict[str, int]:
+        T, H, R = self.T, self.H, self.R
         return {
             "dispatch": T * H * e + R * H * e + 8 * R,
             "combine_fwd": R * H * e + 4 * R + T * H * e,
@@ -290,6 +290,30 @@ class MoELayer:
         w2.normal_(0.0, 0.02, generator=gd)
         return cls(shape, wg, w13, w2, device, num_buffers, residual)
 
+    # stage entry points shared with moe_f32.MoELayerF32 (bench / profiling use these)
+    def stage_dispatch(self, buf, stream=None):
+        a_dispatch(buf, self.router, stream)
+
+    def stage_f_forward(self, buf, stream=None):
+        f_forward(buf, self.experts, stream=stream)
+
+    def stage_combine(self, buf, stream=None):
+        a_combine(buf, stream)
+
+    def stage_combine_bwd(self, buf, stream=None):
+        a_combine_bwd(buf, stream)
+
+    def stage_f_backward(self, buf, accumulate: bool, stream=None):
+        f_backward(buf, self.experts, accumulate, stream=stream, defer_wgrad=True)
+
+    def stage_permute_bwd(self, buf, stream=None):
+        a_permute_bwd(buf, self.router, stream)
+
+    def stage_router_wgrad(self, buf, accumulate: bool, stream=None):
+        a_router_wgrad(buf, self.router, accumulate, stream)
+
+    dtype = BF16
+
     def forward(self, buf: MicroBatchBuffers, stream=None) -> None:
         a_dispatch(buf, self.router, stream)
         f_forward(buf, self.experts, stream=stream)
@@ -463,4 +487,9 @@ class MoEFunction(torch.autograd.Function):
 
 
 def moe(x: torch.Tensor, wg: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor, k: int) -> torch.Tensor:
+    """y = MoE(x); bf16 x -> the bf16 path, fp32 x -> fp32 mode (moe_f32)."""
+    if x.dtype == F32:
+        from .moe_f32 import MoEFunctionF32
+
+        return MoEFunctionF32.apply(x, wg, w13, w2, k)
     return MoEFunction.apply(x, wg, w13, w2, k)

@@ -373,3 +373,96 @@ def test_stack_graph_replay_matches_eager(cuda):
         replay = snap()
         for a, b_ in zip(eager, replay):
             assert torch.equal(a, b_)
+
+
+TOL_FP32 = 1e-4
+
+
+@pytest.mark.parametrize("T,H,E,k,De", [
+    pytest.param(256, 256, 8, 2, 256, id="f32_tiny"),
+    pytest.param(200, 512, 16, 4, 256, id="f32_E16_k4"),
+    pytest.param(100, 256, 64, 8, 512, id="f32_E64_k8"),
+])
+def test_fp32_mode_matches_oracle(cuda, T, H, E, k, De):
+    """fp32 mode (bytes_per_element 4): routing bit-exact on fp32 activations; outputs and
+    all gradients within 1e-4 normwise of the fp64 oracle (split-3 tensor-core GEMMs)."""
+    from paper_2605_11005_b200.moe import MoEShape, interleave_w13, split_w13
+    from paper_2605_11005_b200.moe_f32 import MoELayerF32
+
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((T, H), dtype=np.float32)
+    wg = (rng.standard_normal((E, H), dtype=np.float32) * 0.02).astype(np.float32)
+    w1 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02).astype(np.float32)
+    w3 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02).astype(np.float32)
+    w2 = (rng.standard_normal((E, H, De), dtype=np.float32) * 0.02).astype(np.float32)
+    dy = rng.standard_normal((T, H), dtype=np.float32)
+    f = O.moe_forward(x, wg, w1, w3, w2, k)
+    b = O.moe_backward(f, x, wg, w1, w3, w2, dy)
+    t = lambda a: torch.from_numpy(a).to(cuda)  # noqa: E731
+    layer = MoELayerF32(MoEShape(T=T, H=H, E=E, k=k, De=De), torch.from_numpy(wg),
+                        interleave_w13(t(w1), t(w3)), t(w2), cuda)
+    buf = layer.buffers[0]
+    buf.x.copy_(t(x))
+    buf.dy.copy_(t(dy))
+    layer.forward_backward(buf)
+    torch.cuda.synchronize()
+    assert np.array_equal(buf.idx.cpu().numpy(), f.idx), "expert ids differ"
+    assert np.array_equal(buf.row_map.cpu().numpy(), f.row_map), "permutation differs"
+    assert np.array_equal(buf.pad_off.cpu().numpy(), f.pad_off)
+    errs = {
+        "y": O.normwise_rel_err(f32(buf.y), f.y),
+        "dx": O.normwise_rel_err(f32(buf.dx), b.dx),
+        "dwg": O.normwise_rel_err(f32(layer.dwg), b.dwg),
+        "dw2": O.normwise_rel_err(f32(layer.experts.dw2), b.dw2),
+    }
+    g1, g3 = split_w13(layer.experts.dw13)
+    errs["dw1"] = O.normwise_rel_err(f32(g1), b.dw1)
+    errs["dw3"] = O.normwise_rel_err(f32(g3), b.dw3)
+    assert max(errs.values()) < TOL_FP32, errs
+
+
+def test_fp32_autograd_and_iteration(cuda):
+    """moe() on fp32 tensors runs fp32 mode; the deferred W pass over a 2-micro-batch
+    slab equals the per-micro-batch inline wgrad (split-3 strided wgrad path)."""
+    from paper_2605_11005_b200.moe import MoEShape, moe, split_w13
+    from paper_2605_11005_b200.moe_f32 import MoELayerF32
+
+    T, H, E, k, De = 128, 256, 8, 2, 256
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((T, H), dtype=np.float32)
+    wg = (rng.standard_normal((E, H), dtype=np.float32) * 0.02).astype(np.float32)
+    w1 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02).astype(np.float32)
+    w3 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02).astype(np.float32)
+    w2 = (rng.standard_normal((E, H, De), dtype=np.float32) * 0.02).astype(np.float32)
+    dy = rng.standard_normal((T, H), dtype=np.float32)
+    f = O.moe_forward(x, wg, w1, w3, w2, k)
+    b = O.moe_backward(f, x, wg, w1, w3, w2, dy)
+    from paper_2605_11005_b200.moe import interleave_w13
+
+    t = lambda a: torch.from_numpy(a).to(cuda)  # noqa: E731
+    xt = t(x).requires_grad_(True)
+    wgt = t(wg).requires_grad_(True)
+    w13 = interleave_w13(t(w1), t(w3)).requires_grad_(True)
+    w2t = t(w2).requires_grad_(True)
+    y = moe(xt, wgt, w13, w2t, k)
+    y.backward(t(dy))
+    assert y.dtype == torch.float32
+    assert O.normwise_rel_err(f32(y), f.y) < TOL_FP32
+    assert O.normwise_rel_err(f32(xt.grad), b.dx) < TOL_FP32
+    assert O.normwise_rel_err(f32(wgt.grad), b.dwg) < TOL_FP32
+    g1, _ = split_w13(w13.grad)
+    assert O.normwise_rel_err(f32(g1), b.dw1) < TOL_FP32
+    assert O.normwise_rel_err(f32(w2t.grad), b.dw2) < TOL_FP32
+
+    layer = MoELayerF32.random(MoEShape(T=300, H=256, E=8, k=2, De=256), cuda, seed=2, num_buffers=2)
+    for bb in layer.buffers:
+        bb.x.normal_()
+        bb.dy.normal_()
+    for i, bb in enumerate(layer.buffers):
+        layer.forward_backward(bb, accumulate=i > 0)
+    inline = (layer.experts.dw13.clone(), layer.experts.dw2.clone(), layer.dwg.clone())
+    layer.zero_grad()
+    layer.iteration()
+    torch.cuda.synchronize()
+    for a, b_ in zip(inline, (layer.experts.dw13, layer.experts.dw2, layer.dwg)):
+        assert O.normwise_rel_err(f32(b_), f32(a)) < 1e-5
