@@ -211,20 +211,27 @@ def run_ours(args, shape, exp):
         from paper_2605_11005_b200.moe_f32 import MoELayerF32 as LayerCls
     else:
         LayerCls = MoELayer
-    # L > 1: the stack of residual MoE blocks (configs[0]: 2 layers); L = 1: the plain layer
+    # L > 1: the stack of residual MoE blocks (configs[0]: 2 layers); L = 1: the plain layer;
+    # --attention: each layer = A-side attention block + residual MoE block
+    attn = None
+    if args.attention:
+        from paper_2605_11005_b200.attention import AttentionBlock
+
+        attn = [AttentionBlock(shape.H, exp.model.gqa_group, dev, seed=77 + l) for l in range(L)]
     stack = MoEStack([LayerCls.random(shape, device=dev, seed=1234 + rank + 1000 * l, num_buffers=mb,
-                                      residual=L > 1) for l in range(L)])
+                                      residual=L > 1 or attn is not None) for l in range(L)],
+                     attention=attn, seq_len=exp.workload.seq_len)
     layer = stack.layers[0]
     stream = torch.cuda.current_stream(dev)
-    for b, ob in zip(stack.buffers, stack.out_buffers):
-        b.x.normal_()
-        ob.dy.normal_()
+    for i in range(mb):
+        stack.input(i).normal_()
+        stack.output_grad(i).normal_()
 
     # per-stage CUDA events: GEMM (F) time and HBM-kernel (A) time inside the timed region
     class Ev:
         def __init__(self):
             self.pairs = {"gemm": [], "dispatch": [], "combine_fwd": [], "combine_bwd": [], "permute_bwd": [],
-                          "router_wgrad": []}
+                          "router_wgrad": [], "attention": []}
 
         def mark(self, name, fn):
             s = torch.cuda.Event(enable_timing=True)
@@ -243,23 +250,36 @@ def run_ours(args, shape, exp):
             return
         for i in range(mb):
             acc = i > 0
-            for ly in stack.layers:
+            for l, ly in enumerate(stack.layers):
                 buf = ly.buffers[i]
+                if attn is not None:
+                    x_in = stack.inp[i] if l == 0 else stack.layers[l - 1].buffers[i].y
+                    ev.mark("attention", lambda: attn[l].forward(i, x_in, buf.x, stack.seq_len))
                 ev.mark("dispatch", lambda: ly.stage_dispatch(buf))
                 ev.mark("gemm", lambda: ly.stage_f_forward(buf))
                 ev.mark("combine_fwd", lambda: ly.stage_combine(buf))
-            for ly in reversed(stack.layers):
+            for l in reversed(range(L)):
+                ly = stack.layers[l]
                 buf = ly.buffers[i]
                 ev.mark("combine_bwd", lambda: ly.stage_combine_bwd(buf))
                 ev.mark("gemm", lambda: ly.stage_f_backward(buf, acc))
                 ev.mark("permute_bwd", lambda: ly.stage_permute_bwd(buf))
                 ev.mark("router_wgrad", lambda: ly.stage_router_wgrad(buf, acc))
+                if attn is not None:
+                    dst = stack.dinp[i] if l == 0 else stack.layers[l - 1].buffers[i].dy
+                    ev.mark("attention", lambda: attn[l].backward(i, buf.dx, dst, acc))
         for ly in stack.layers:
             ev.mark("gemm", lambda: ly.wgrad(mb))
 
     # the iteration as CUDA graphs (one per micro-batch + the W pass): same kernels,
     # n+1 host launches per step instead of ~13 per layer and micro-batch
-    graphs = stack.capture(mb) if not args.eager else None
+    graphs = None
+    if not args.eager:
+        try:
+            graphs = stack.capture(mb)
+        except RuntimeError as ex:   # e.g. a library attention backend that cannot be captured
+            print(f"[bench] CUDA-graph capture failed ({str(ex)[:160]}); timing eager launches", file=sys.stderr)
+            graphs = None
 
     def run():
         if graphs is not None:
@@ -362,6 +382,15 @@ def run_ours(args, shape, exp):
         "clocks": clocks,
         "e2e": e2e,
     }
+    if attn is not None:
+        a_ms = ev.total_ms("attention") / (args.steps * mb * L)
+        fa, fb = attn[0].flops(exp.workload.seq_len, exp.workload.micro_batch)
+        line["attention"] = {
+            "ms_per_microbatch_layer": round(a_ms, 4), "TFLOP/s": round((fa + fb) / (a_ms / 1e3) / 1e12, 1),
+            "impl": "library stopgap (SURVEY §8f-3): cuBLAS projections + torch SDPA (cuDNN/flash), autograd",
+            "gqa_group": exp.model.gqa_group, "seq_len": exp.workload.seq_len}
+        line["config"]["layer"] = "attention + residual MoE block"
+        line["config"]["launch"] = "CUDA graphs" if graphs is not None else "eager"
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(shape, layer=layer, layers=L)
     print(json.dumps(line), flush=True)
@@ -412,12 +441,13 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
     mb = exp.workload.num_microbatches
     topo = Topology.default(world, shape.E, args.n_attn)
     L = exp.model.layers
-    r = AFPipeRank(shape, topo, rank, mb, dev, seed=1234, layers=L)
+    r = AFPipeRank(shape, topo, rank, mb, dev, seed=1234, layers=L, attention=args.attention,
+                   seq_len=exp.workload.seq_len, gqa_group=exp.model.gqa_group)
     r.init_groups()
     if r.role == "A":
-        for b, ob in zip(r.bufs, r.out_bufs):
-            b.x.normal_()
-            ob.dy.normal_()
+        for i in range(mb):
+            r.input(i).normal_()
+            r.out_bufs[i].dy.normal_()
     sampler = ClockSampler(dev.index) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -510,7 +540,10 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
             "config": {
                 "workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E, "k": shape.k,
                 "D_e": shape.De, "layers": L, "microbatches": mb, "tokens_per_step": mb * shape.T * topo.n_attn,
-                "parallelism": f"AF-Pipe {topo.n_attn}A:{topo.n_ffn}F (A: DP routing/combine, F: EP experts)",
+                "parallelism": f"AF-Pipe {topo.n_attn}A:{topo.n_ffn}F (A: DP "
+                               + ("attention + " if args.attention else "") + "routing/combine, F: EP experts)",
+                "layer": "attention + residual MoE block (attention: library stopgap)" if args.attention
+                         else "MoE block",
                 "transport": "NCCL send/recv (torch.distributed P2P) over NVLink",
                 "weights": "random-init", "l2": "inputs+weights larger than L2",
                 "wgrad": "fp32, deferred per iteration on F ranks",
@@ -559,7 +592,6 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
     hdy = [torch.randn(T, H).to(dt).pin_memory() for _ in range(mb)]
     hy = [torch.empty(T, H, dtype=dt).pin_memory() for _ in range(mb)]
     hdx = [torch.empty(T, H, dtype=dt).pin_memory() for _ in range(mb)]
-    bufs, obufs = stack.buffers, stack.out_buffers
 
     def step():
         loaded = [torch.cuda.Event() for _ in range(mb)]
@@ -567,8 +599,8 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
         copy.wait_stream(comp)  # previous step finished with the input buffers
         with torch.cuda.stream(copy):
             for i in range(mb):
-                bufs[i].x.copy_(hx[i], non_blocking=True)
-                obufs[i].dy.copy_(hdy[i], non_blocking=True)
+                stack.input(i).copy_(hx[i], non_blocking=True)
+                stack.output_grad(i).copy_(hdy[i], non_blocking=True)
                 loaded[i].record(copy)
         for i in range(mb):
             comp.wait_event(loaded[i])
@@ -579,8 +611,8 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
             done[i].record(comp)
             with torch.cuda.stream(copy):
                 copy.wait_event(done[i])
-                hy[i].copy_(obufs[i].y, non_blocking=True)
-                hdx[i].copy_(bufs[i].dx, non_blocking=True)
+                hy[i].copy_(stack.output(i), non_blocking=True)
+                hdx[i].copy_(stack.input_grad(i), non_blocking=True)
         if graphs is not None:
             graphs.wgrad.replay()
         else:
@@ -627,6 +659,8 @@ def main(argv=None):
     ap.add_argument("--trace", default=None, help="N>1: write the instrumented iteration as reference-schema trace JSON")
     ap.add_argument("--microbatches", type=int, default=None, help="override workload.num_microbatches")
     ap.add_argument("--eager", action="store_true", help="N=1: launch kernels eagerly instead of CUDA graphs")
+    ap.add_argument("--attention", action="store_true",
+                    help="add the A-side causal attention block to every layer (library stopgap; sweeps)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -370,19 +370,43 @@ def link_residual_stack(stack_bufs: list[list[MicroBatchBuffers]]) -> None:
 
 class MoEStack:
     """Fused single-device stack of residual MoE blocks, x_{l+1} = x_l + MoE_l(x_l)
-    (the tiny config's 2-layer model with the A-side attention omitted).
+    (the tiny config's 2-layer model), optionally preceded per layer by the A-side
+    attention block (attention.AttentionBlock: h_l = x_l + attn(x_l), then
+    x_{l+1} = h_l + MoE_l(h_l)). A 1-layer stack without attention is the plain layer.
 
-    Inputs go to `buffers[i].x` (layer 0), upstream gradients to `out_buffers[i].dy`
-    (last layer); outputs are `out_buffers[i].y` and `buffers[i].dx`.
+    I/O per micro-batch i: `input(i)`, `output_grad(i)` in; `output(i)`, `input_grad(i)` out.
     """
 
-    def __init__(self, layers: list[MoELayer]):
+    def __init__(self, layers: list, attention: list | None = None, seq_len: int | None = None):
         if not layers:
             raise ValueError("empty stack")
+        if attention is not None and len(attention) != len(layers):
+            raise ValueError("one attention block per layer")
         self.layers = layers
-        link_residual_stack([l.buffers for l in layers])
+        self.attn = attention
         self.buffers = layers[0].buffers
         self.out_buffers = layers[-1].buffers
+        if attention is None:
+            link_residual_stack([l.buffers for l in layers])
+        else:
+            s = layers[0].shape
+            self.seq_len = seq_len or s.T
+            dt, dev = layers[0].dtype, layers[0].device
+            n = len(self.buffers)
+            self.inp = [torch.empty(s.T, s.H, dtype=dt, device=dev) for _ in range(n)]
+            self.dinp = [torch.empty(s.T, s.H, dtype=dt, device=dev) for _ in range(n)]
+
+    def input(self, i: int) -> torch.Tensor:
+        return self.buffers[i].x if self.attn is None else self.inp[i]
+
+    def input_grad(self, i: int) -> torch.Tensor:
+        return self.buffers[i].dx if self.attn is None else self.dinp[i]
+
+    def output(self, i: int) -> torch.Tensor:
+        return self.out_buffers[i].y
+
+    def output_grad(self, i: int) -> torch.Tensor:
+        return self.out_buffers[i].dy
 
     @classmethod
     def random(cls, shape: MoEShape, num_layers: int, device="cuda", seed: int = 0,
@@ -390,11 +414,24 @@ class MoEStack:
         return cls([MoELayer.random(shape, device, seed + 1000 * l, num_buffers, residual=True)
                     for l in range(num_layers)])
 
-    def forward_backward(self, i: int, accumulate: bool = False, stream=None, defer_wgrad: bool = False) -> None:
-        for layer in self.layers:
+    def forward(self, i: int, stream=None) -> None:
+        for l, layer in enumerate(self.layers):
+            if self.attn is not None:
+                x_in = self.inp[i] if l == 0 else self.layers[l - 1].buffers[i].y
+                self.attn[l].forward(i, x_in, layer.buffers[i].x, self.seq_len)
             layer.forward(layer.buffers[i], stream)
-        for layer in reversed(self.layers):
+
+    def backward(self, i: int, accumulate: bool = False, stream=None, defer_wgrad: bool = False) -> None:
+        for l in reversed(range(len(self.layers))):
+            layer = self.layers[l]
             layer.backward(layer.buffers[i], accumulate, stream, defer_wgrad)
+            if self.attn is not None:
+                dst = self.dinp[i] if l == 0 else self.layers[l - 1].buffers[i].dy
+                self.attn[l].backward(i, layer.buffers[i].dx, dst, accumulate)
+
+    def forward_backward(self, i: int, accumulate: bool = False, stream=None, defer_wgrad: bool = False) -> None:
+        self.forward(i, stream)
+        self.backward(i, accumulate, stream, defer_wgrad)
 
     def iteration(self, n: int | None = None, accumulate: bool = False, stream=None) -> None:
         n = len(self.buffers) if n is None else n

@@ -223,17 +223,25 @@ class AFPipeRank:
 
     def __init__(self, shape: MoEShape, topo: Topology, rank: int, microbatches: int, device,
                  stages=None, seed: int = 0, weights=None, durations: LayerDurations | None = None,
-                 record_events: bool = False, layers: int = 1, residual: bool | None = None):
+                 record_events: bool = False, layers: int = 1, residual: bool | None = None,
+                 attention: bool = False, seq_len: int | None = None, gqa_group: int = 1):
         shape.validate() if device.type == "cuda" else None
         if layers < 1:
             raise ValueError(f"layers must be >= 1, got {layers}")
         self.shape, self.topo, self.rank, self.mb, self.L = shape, topo, rank, microbatches, layers
-        self.residual = layers > 1 if residual is None else residual
+        self.attention = attention
+        self.seq_len = seq_len or shape.T
+        self.residual = (layers > 1 or attention) if residual is None else residual
         self.device = torch.device(device)
         self.role, self.idx = topo.role(rank)
         self.stages = stages if stages is not None else GpuStages()
         self.st = _Streams(self.device)
         self.record_events = record_events and self.st.cuda
+        self._attn_flops = None
+        if attention:
+            from .attention import attention_flops
+
+            self._attn_flops = attention_flops(shape.H, gqa_group, self.seq_len, shape.T // self.seq_len)
         d = durations or self._default_durations()
         self.plan = plan_layer(microbatches, d, layers=layers)
         self.order = issue_order(self.plan, "A0" if self.role == "A" else "F0")
@@ -253,7 +261,15 @@ class AFPipeRank:
                 slab = ActivationSlab(s, microbatches, self.device, f_side=False)
                 self.lbufs.append([MicroBatchBuffers(s, self.device, slab, i, residual=self.residual)
                                    for i in range(microbatches)])
-            link_residual_stack(self.lbufs)
+            self.attn = None
+            if attention:   # A-side attention per layer (library stopgap, attention.py)
+                from .attention import AttentionBlock
+
+                self.attn = [AttentionBlock(s.H, gqa_group, self.device, seed=seed + 77 + l) for l in range(layers)]
+                self.inp = [torch.empty(s.T, s.H, dtype=BF16, device=self.device) for _ in range(microbatches)]
+                self.dinp = [torch.empty(s.T, s.H, dtype=BF16, device=self.device) for _ in range(microbatches)]
+            else:
+                link_residual_stack(self.lbufs)
             self.router, self.bufs, self.out_bufs = self.routers[0], self.lbufs[0], self.lbufs[-1]
             self.pad_host = [[torch.empty(s.E + 1, dtype=I32, pin_memory=self.st.cuda) for _ in range(microbatches)]
                              for _ in range(layers)]
@@ -300,7 +316,11 @@ class AFPipeRank:
         f_fwd = int(6 * s.R * s.H * s.De * self.topo.n_attn / per_f / tflops * 1e9)
         m2n = int(2 * s.R * s.H / max(1, min(self.topo.n_attn, per_f)) / 7.0e11 * 1e9)
         a = int(sum(s.hbm_bytes().values()) / 4 / 5.0e12 * 1e9)
-        return LayerDurations(a_fwd=a, a_turn=2 * a, a_bwd=2 * a, f_fwd=f_fwd, f_bwd=2 * f_fwd, m2n=max(1, m2n))
+        af = ab = 0
+        if self._attn_flops is not None:
+            af, ab = (int(f / tflops * 1e9) for f in self._attn_flops)
+        return LayerDurations(a_fwd=a + af, a_turn=2 * a, a_bwd=2 * a + ab, f_fwd=f_fwd, f_bwd=2 * f_fwd,
+                              m2n=max(1, m2n))
 
     # ------------------------------------------------------------ tracing
     def _xchg(self, ops, name: str, i: int):
@@ -345,10 +365,17 @@ class AFPipeRank:
         xs, dys, _, _ = self.host_io
         self.h2d_ready = []
         with self.st.ctx("copy"):
-            for b, ob, x, dy in zip(self.bufs, self.out_bufs, xs, dys):
-                b.x.copy_(x, non_blocking=True)
-                ob.dy.copy_(dy, non_blocking=True)
+            for i, (x, dy) in enumerate(zip(xs, dys)):
+                self.input(i).copy_(x, non_blocking=True)
+                self.out_bufs[i].dy.copy_(dy, non_blocking=True)
                 self.h2d_ready.append(self.st.event("copy"))
+
+    def input(self, i: int) -> torch.Tensor:
+        """A rank: micro-batch i's input activations (layer 0, before attention if any)."""
+        return self.inp[i] if self.attn is not None else self.bufs[i].x
+
+    def input_grad(self, i: int) -> torch.Tensor:
+        return self.dinp[i] if self.attn is not None else self.bufs[i].dx
 
     def a_task(self, name: str, i: int, layer: int, accumulate: bool):
         b = self.lbufs[layer][i]
@@ -356,10 +383,14 @@ class AFPipeRank:
             if layer == 0:
                 if self.host_io is not None:
                     self.st.wait("compute", self.h2d_ready[i])
+                x_in = self.inp[i] if self.attn is not None else None
             else:   # previous layer's combine writes this layer's input (residual fused)
                 prev = self.lbufs[layer - 1][i]
                 self._wait_works(prev, "N2M")
                 self.stages.a_combine(prev)
+                x_in = prev.y
+            if self.attn is not None:
+                self.attn[layer].forward(i, x_in, b.x, self.seq_len)
             self.stages.a_dispatch(b, self.routers[layer])
             done = self.st.event("compute")
             with self.st.ctx("copy"):
@@ -375,6 +406,9 @@ class AFPipeRank:
         elif name == "A_b":
             self._wait_works(b, "N2M_b")
             self.stages.a_backward(b, self.routers[layer], accumulate)
+            if self.attn is not None:
+                dst = self.dinp[i] if layer == 0 else self.lbufs[layer - 1][i].dy
+                self.attn[layer].backward(i, b.dx, dst, accumulate)
             if layer > 0:   # this layer's dx is the previous layer's upstream gradient
                 prev = self.lbufs[layer - 1][i]
                 self.stages.a_combine_bwd(prev)
@@ -385,7 +419,7 @@ class AFPipeRank:
                 with self.st.ctx("copy"):
                     self.st.wait("copy", done)
                     ys[i].copy_(self.out_bufs[i].y, non_blocking=True)
-                    dxs[i].copy_(b.dx, non_blocking=True)
+                    dxs[i].copy_(self.input_grad(i), non_blocking=True)
 
     def a_comm(self, name: str, i: int, layer: int):
         b = self.lbufs[layer][i]
@@ -525,6 +559,9 @@ class AFPipeRank:
             if self.a_group is not None and self.topo.n_attn > 1:
                 for r in self.routers:
                     dist.all_reduce(r.dwg, group=self.a_group)
+                for blk in self.attn or []:
+                    for g in blk.grads():
+                        dist.all_reduce(g, group=self.a_group)
 
     def init_groups(self):
         """Create the A-group communicator (collective: every rank must call it)."""

@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--attention", action="store_true", help="A-side attention in every layer (bench --attention)")
+    ap.add_argument("--with-fused", action="store_true", help="also run each point on 1 GPU (fused path)")
     a = ap.parse_args()
     points = []
     if a.what == "alloc":
@@ -48,12 +50,21 @@ def main():
             points.append((["--seq-len", str(s), "--microbatches", str(mb)], {"seq_len": s, "mb": mb}))
     with open(a.out, "w") as fh:
         for i, (extra, meta) in enumerate(points):
+            if a.attention:
+                extra = extra + ["--attention"]
             line = run(a.gpus, extra, 29600 + i, a.steps, a.warmup)
             if line is None:
                 continue
-            row = {**meta, "tokens_per_s": line["value"], "ms_per_step": line["ms_per_step"],
+            row = {**meta, "attention": a.attention, "tokens_per_s": line["value"], "ms_per_step": line["ms_per_step"],
                    "exposed_comm": line.get("exposed_comm"), "gemm_frac": line["roofline"]["frac"],
                    "clocks": line.get("clocks"), "e2e": line["e2e"]["value"]}
+            if a.with_fused:
+                fused = run(1, [x for x in extra if x not in ("--n-attn",)] if "--n-attn" not in extra else
+                            extra[:extra.index("--n-attn")] + extra[extra.index("--n-attn") + 2:], 0, a.steps, a.warmup)
+                if fused is not None:
+                    row["fused_1gpu_tokens_per_s"] = fused["value"]
+                    row["fused_attention_ms_per_mb"] = (fused.get("attention") or {}).get("ms_per_microbatch_layer")
+                    row["speedup_vs_fused"] = round(line["value"] / fused["value"], 3)
             fh.write(json.dumps(row) + "\n")
             fh.flush()
             print(json.dumps(row), flush=True)

@@ -139,3 +139,122 @@ def test_topology_blocks_match_reference_balanced_blocks():
         Topology(4, 0, 8)
     with pytest.raises(ValueError):
         Topology(10, 1, 8)
+
+
+def _attn_worker(rank, world, n_attn, port, outdir, layers):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from af_cpu_stages import CpuStages
+    from paper_2605_11005_b200.moe import MoEShape
+    from paper_2605_11005_b200.runtime import AFPipeRank, Topology
+
+    weights = _attn_weights(layers)
+    r = AFPipeRank(MoEShape(T, H, E, K, DE), Topology(world, n_attn, E), rank, MB, torch.device("cpu"),
+                   stages=CpuStages(), weights=weights, layers=layers, attention=True, seq_len=T)
+    r.init_groups()
+    out = {"role": r.role, "idx": r.idx}
+    if r.role == "A":
+        for i in range(MB):
+            x, dy = _attn_inputs(r.idx, i)
+            r.input(i).copy_(x)
+            r.out_bufs[i].dy.copy_(dy)
+    r.run_iteration()
+    if r.role == "A":
+        out["y"] = [b.y.float() for b in r.out_bufs]
+        out["dx"] = [r.input_grad(i).float() for i in range(MB)]
+        out["dwg"] = [rt.dwg.clone() for rt in r.routers]
+        out["dqkv"] = [a.dw_qkv.clone() for a in r.attn]
+    else:
+        out["lo"], out["hi"] = r.lo, r.hi
+        out["dw2"] = [ex.dw2.clone() for ex in r.expert_layers]
+    torch.save(out, os.path.join(outdir, f"rank{rank}.pt"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _attn_weights(layers):
+    from oracle import oracle as O
+    from paper_2605_11005_b200.moe import interleave_w13
+
+    bf = lambda a: torch.from_numpy(O.f32_to_bf16_bits(a).view(np.int16).copy()).view(torch.bfloat16)  # noqa: E731
+    out = []
+    for l in range(layers):
+        wg, w1, w3, w2 = _weights(l)
+        out.append({"wg": torch.from_numpy(wg), "w13": interleave_w13(bf(w1), bf(w3)), "w2": bf(w2)})
+    return out
+
+
+def _attn_inputs(a, i):
+    g = torch.Generator().manual_seed(500 + 10 * a + i)
+    return (torch.randn(T, H, generator=g).to(torch.bfloat16), torch.randn(T, H, generator=g).to(torch.bfloat16))
+
+
+def _sequential_reference(n_attn, layers):
+    """Single process, same CPU stage arithmetic and attention blocks, full expert set,
+    micro-batches run one after another: what the distributed schedule must reproduce."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from af_cpu_stages import CpuStages
+    from paper_2605_11005_b200.attention import AttentionBlock
+    from paper_2605_11005_b200.moe import ActivationSlab, ExpertParams, MicroBatchBuffers, MoEShape, RouterParams
+
+    st = CpuStages()
+    shape = MoEShape(T, H, E, K, DE)
+    ws = _attn_weights(layers)
+    res = {}
+    for a in range(n_attn):
+        blocks = [AttentionBlock(H, 1, "cpu", seed=77 + l) for l in range(layers)]
+        routers = [RouterParams(w["wg"].float()) for w in ws]
+        experts = [ExpertParams(w["w13"], w["w2"]) for w in ws]
+        slabs = [ActivationSlab(shape, MB, "cpu") for _ in range(layers)]
+        bufs = [[MicroBatchBuffers(shape, "cpu", slabs[l], i, residual=True) for i in range(MB)] for l in range(layers)]
+        ys, dxs = [], []
+        for i in range(MB):
+            x, dy = _attn_inputs(a, i)
+            dx = torch.empty(T, H, dtype=torch.bfloat16)
+            x_in = x
+            for l in range(layers):
+                b = bufs[l][i]
+                blocks[l].forward(i, x_in, b.x, T)
+                st.a_dispatch(b, routers[l])
+                st.f_forward(b, experts[l], b.pad_off)
+                st.a_combine(b)
+                x_in = b.y
+            ys.append(bufs[-1][i].y.float())
+            bufs[-1][i].dy.copy_(dy)
+            for l in reversed(range(layers)):
+                b = bufs[l][i]
+                st.a_combine_bwd(b)
+                st.f_backward(b, experts[l], b.pad_off)
+                st.a_backward(b, routers[l], i > 0)
+                dst = dx if l == 0 else bufs[l - 1][i].dy
+                blocks[l].backward(i, b.dx, dst, i > 0)
+            dxs.append(dx.float())
+        res[a] = {"y": ys, "dx": dxs, "dwg": [r.dwg for r in routers], "dqkv": [b.dw_qkv for b in blocks]}
+    return res
+
+
+@pytest.mark.parametrize("world,n_attn,layers", [(2, 1, 2), (3, 2, 1)])
+def test_afpipe_runtime_with_attention_matches_sequential(world, n_attn, layers):
+    """A-side attention inside the AF-Pipe schedule (attention.py): the distributed run
+    reproduces a single-process sequential execution of the same blocks; attention and
+    router gradients are all-reduced over the A group."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_attn_worker, args=(world, n_attn, _free_port(), d, layers), nprocs=world, join=True)
+        outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
+    ref = _sequential_reference(n_attn, layers)
+    from oracle import oracle as O
+
+    tot_dwg = [sum(ref[a]["dwg"][l] for a in ref) for l in range(layers)]
+    tot_qkv = [sum(ref[a]["dqkv"][l] for a in ref) for l in range(layers)]
+    for o in outs:
+        if o["role"] != "A":
+            continue
+        r = ref[o["idx"]]
+        for i in range(MB):
+            assert O.normwise_rel_err(o["y"][i].numpy(), r["y"][i].numpy()) < 1e-2
+            assert O.normwise_rel_err(o["dx"][i].numpy(), r["dx"][i].numpy()) < 1e-2
+        for l in range(layers):
+            assert O.normwise_rel_err(o["dwg"][l].numpy(), tot_dwg[l].numpy()) < 1e-2
+            assert O.normwise_rel_err(o["dqkv"][l].numpy(), tot_qkv[l].numpy()) < 1e-2

@@ -72,3 +72,69 @@ def test_afpipe_runtime_gpu_matches_oracle(world, n_attn, layers):
         mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
     check_against_oracle(outs, n_attn, layers)
+
+
+def _attn_worker(rank, world, n_attn, port, outdir, layers):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    from test_runtime_gloo import _attn_inputs, _attn_weights
+
+    from paper_2605_11005_b200.moe import MoEShape
+    from paper_2605_11005_b200.runtime import AFPipeRank, Topology
+
+    r = AFPipeRank(MoEShape(T, H, E, K, DE), Topology(world, n_attn, E), rank, MB, dev,
+                   weights=_attn_weights(layers), layers=layers, attention=True, seq_len=T)
+    r.init_groups()
+    if r.role == "A":
+        for i in range(MB):
+            x, dy = _attn_inputs(r.idx, i)
+            r.input(i).copy_(x)
+            r.out_bufs[i].dy.copy_(dy)
+    r.run_iteration()
+    torch.cuda.synchronize()
+    out = {"role": r.role, "idx": r.idx}
+    if r.role == "A":
+        out["y"] = [b.y.float().cpu() for b in r.out_bufs]
+        out["dx"] = [r.input_grad(i).float().cpu() for i in range(MB)]
+        out["dqkv"] = [a.dw_qkv.cpu() for a in r.attn]
+        out["dwg"] = [rt.dwg.cpu() for rt in r.routers]
+    torch.save(out, os.path.join(outdir, f"rank{rank}.pt"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_afpipe_attention_gpu_matches_fused_stack():
+    """1A+1F over NCCL with A-side attention (2 layers) == the fused single-GPU stack
+    (MoEStack with attention) on the same weights and inputs."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from test_runtime_gloo import _attn_inputs, _attn_weights
+
+    from oracle import oracle as O
+    from paper_2605_11005_b200.attention import AttentionBlock
+    from paper_2605_11005_b200.moe import MoELayer, MoEShape, MoEStack
+
+    layers = 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_attn_worker, args=(2, 1, _free_port(), d, layers), nprocs=2, join=True)
+        got = torch.load(os.path.join(d, "rank0.pt"), weights_only=False)
+    dev = torch.device("cuda", 0)
+    shape = MoEShape(T, H, E, K, DE)
+    ws = _attn_weights(layers)
+    stack = MoEStack([MoELayer(shape, w["wg"], w["w13"], w["w2"], dev, num_buffers=MB, residual=True) for w in ws],
+                     attention=[AttentionBlock(H, 1, dev, seed=77 + l) for l in range(layers)], seq_len=T)
+    for i in range(MB):
+        x, dy = _attn_inputs(0, i)
+        stack.input(i).copy_(x)
+        stack.output_grad(i).copy_(dy)
+    stack.iteration()
+    torch.cuda.synchronize()
+    for i in range(MB):
+        assert O.normwise_rel_err(got["y"][i].numpy(), stack.output(i).float().cpu().numpy()) < 1e-2
+        assert O.normwise_rel_err(got["dx"][i].numpy(), stack.input_grad(i).float().cpu().numpy()) < 1e-2
+    for l in range(layers):
+        assert O.normwise_rel_err(got["dqkv"][l].numpy(), stack.attn[l].dw_qkv.cpu().numpy()) < 1e-2
+        assert O.normwise_rel_err(got["dwg"][l].numpy(), stack.layers[l].router.dwg.cpu().numpy()) < 1e-2
