@@ -346,6 +346,20 @@ def run_ours(args, shape, exp):
         t = ev.total_ms(name) / (args.steps * mb * L)
         gbs = hb[name] / (t / 1e3) / 1e9
         hbm[name] = {"ms": round(t, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 3)}
+    # A-side kernels in isolation: CUDA-graph replays of [L2 flush, stage] minus [L2 flush]
+    # (flush = 512 MB memset > 126 MB L2), i.e. cold-L2 kernel time at the live clocks,
+    # without the per-stage event overhead of the in-step numbers above
+    iso = {}
+    if world == 1 and not args.no_isolated:
+        b0, ly0 = stack.layers[0].buffers[0], stack.layers[0]
+        fns = {"dispatch": lambda: ly0.stage_dispatch(b0), "combine_fwd": lambda: ly0.stage_combine(b0),
+               "combine_bwd": lambda: ly0.stage_combine_bwd(b0), "permute_bwd": lambda: ly0.stage_permute_bwd(b0),
+               "router_wgrad": lambda: ly0.stage_router_wgrad(b0, False)}
+        iso = isolated_stage_ms(fns, dev)
+        for name, t in iso.items():
+            gbs = hb[name] / (t / 1e3) / 1e9
+            hbm[name]["isolated_ms"] = round(t, 4)
+            hbm[name]["isolated_frac"] = round(gbs / peaks["hbm_gbs"], 3)
     traffic = None
     tfile = ROOT / "profiles" / "ncu_gemm_traffic.json"
     if tfile.exists():
@@ -377,7 +391,9 @@ def run_ours(args, shape, exp):
             "gemm_ms_per_microbatch_layer": round(gemm_ms / (args.steps * mb * L), 4),
             "frac_of_burst": round(achieved_tf / peaks["bf16_tflops"], 4),
         },
-        "roofline_hbm": {"peak_GB/s": peaks["hbm_gbs"], **hbm},
+        "roofline_hbm": {"peak_GB/s": peaks["hbm_gbs"], **hbm,
+                         "note": "ms/frac: in-step CUDA events around each stage; isolated_*: graph replay, "
+                                 "L2 flushed before every launch (flush time subtracted)"},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": e2e,
@@ -578,6 +594,40 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
     return 0
 
 
+def isolated_stage_ms(fns: dict, dev, reps: int = 10) -> dict:
+    """ms per launch of each stage with a cold L2: graph([flush, fn] x reps) - graph([flush] x reps)."""
+    import torch
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream(dev)
+
+    def timed(g):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g.replay()
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    g0 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g0, stream=s):
+        for _ in range(reps):
+            flush.zero_()
+    base = timed(g0)
+    out = {}
+    for name, fn in fns.items():
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                flush.zero_()
+                fn()
+        out[name] = max(timed(g) - base, 1e-6) / reps
+    return out
+
+
 def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
     """Same metric through the public API with host buffers: per micro-batch H2D of
     x and dy from pinned memory and D2H of y and dx, overlapped on a copy stream."""
@@ -659,6 +709,7 @@ def main(argv=None):
     ap.add_argument("--trace", default=None, help="N>1: write the instrumented iteration as reference-schema trace JSON")
     ap.add_argument("--microbatches", type=int, default=None, help="override workload.num_microbatches")
     ap.add_argument("--eager", action="store_true", help="N=1: launch kernels eagerly instead of CUDA graphs")
+    ap.add_argument("--no-isolated", action="store_true", help="skip the isolated A-side kernel timing")
     ap.add_argument("--attention", action="store_true",
                     help="add the A-side causal attention block to every layer (library stopgap; sweeps)")
     args = ap.parse_args(argv)

@@ -177,14 +177,18 @@ permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __r
   }
 }
 
-// Permute backward for E <= EM: warp per (256-column chunk, token block); each
-// lane holds its 8 columns of every W_g row in registers, so the router dx term
-// sum_j dlogit[t,j] * W_g[idx[t,j], :] costs no memory traffic (the per-token W_g
-// row reads of permute_bwd_kernel were L1-bound).
-constexpr int PBWD_TOKENS = 16;
+// Permute backward for E <= EM: each warp owns one 256-column chunk for the whole
+// launch and its lanes hold their 8 columns of every W_g row in registers, so the
+// router dx term sum_j dlogit[t,j] * W_g[idx[t,j], :] costs no memory traffic (the
+// per-token W_g row reads of permute_bwd_kernel were L1-bound). The grid is sized
+// to the resident CTA slots (2 per SM) and each CTA strides over groups of
+// PBWD_TG tokens, so there is no partial last wave and every warp keeps
+// PBWD_TG * k 128-bit gathers in flight.
+template <int EM> constexpr int pbwd_tg() { return EM <= 8 ? 4 : 2; }
+template <int EM> constexpr int pbwd_ctas_per_sm() { return EM <= 8 ? 2 : 1; }
 
 template <int EM, int KT>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, pbwd_ctas_per_sm<EM>())
 permute_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_map,
                        const int32_t* __restrict__ idx, const float* __restrict__ dlogit,
                        const float* __restrict__ wg, int T, int H, int E, int k_rt,
@@ -206,42 +210,46 @@ permute_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t*
       for (int i = 0; i < 8; ++i) wr[e][i] = 0.0f;
     }
   }
-  const int t_beg = blockIdx.y * PBWD_TOKENS, t_end = min(T, t_beg + PBWD_TOKENS);
-#pragma unroll 2
-  for (int t = t_beg; t < t_end; ++t) {
-    int pos[KT ? KT : DM_MAX_TOPK];
-    float gw[EM];
+  constexpr int TG = pbwd_tg<EM>();
+  for (int t0 = blockIdx.y * TG; t0 < T; t0 += gridDim.y * TG) {
 #pragma unroll
-    for (int e = 0; e < EM; ++e) gw[e] = 0.0f;
+    for (int u = 0; u < TG; ++u) {
+      const int t = t0 + u;
+      if (t >= T) break;
+      int pos[KT ? KT : DM_MAX_TOPK];
+      float gw[EM];
 #pragma unroll
-    for (int j = 0; j < k; ++j) {
-      pos[j] = row_map[(size_t)t * k + j];
-      if (dlogit) {
-        const int ej = idx[(size_t)t * k + j];
-        const float dl = dlogit[(size_t)t * k + j];
+      for (int e = 0; e < EM; ++e) gw[e] = 0.0f;
 #pragma unroll
-        for (int e = 0; e < EM; ++e) gw[e] = (ej == e) ? dl : gw[e];
+      for (int j = 0; j < k; ++j) {
+        pos[j] = row_map[(size_t)t * k + j];
+        if (dlogit) {
+          const int ej = idx[(size_t)t * k + j];
+          const float dl = dlogit[(size_t)t * k + j];
+#pragma unroll
+          for (int e = 0; e < EM; ++e) gw[e] = (ej == e) ? dl : gw[e];
+        }
       }
+      float acc[8];
+      if (resid) {
+        unpack8(ld_nc_v4(resid + (size_t)t * H + col), acc);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+      }
+#pragma unroll
+      for (int j = 0; j < k; ++j) {
+        float f[8];
+        unpack8(ld_nc_v4(dx_perm + (size_t)pos[j] * H + col), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += f[i];
+      }
+#pragma unroll
+      for (int e = 0; e < EM; ++e)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(gw[e], wr[e][i], acc[i]);
+      st_v4(dx + (size_t)t * H + col, pack8(acc));
     }
-    float acc[8];
-    if (resid) {
-      unpack8(ld_nc_v4(resid + (size_t)t * H + col), acc);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-    }
-#pragma unroll
-    for (int j = 0; j < k; ++j) {
-      float f[8];
-      unpack8(ld_nc_v4(dx_perm + (size_t)pos[j] * H + col), f);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] += f[i];
-    }
-#pragma unroll
-    for (int e = 0; e < EM; ++e)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(gw[e], wr[e][i], acc[i]);
-    st_v4(dx + (size_t)t * H + col, pack8(acc));
   }
 }
 
@@ -447,7 +455,13 @@ int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* i
   const __nv_bfloat16* dxp = reinterpret_cast<const __nv_bfloat16*>(dx_perm);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(dx);
   if (E <= 16) {
-    dim3 grid((H / 8 + 255) / 256, (T + PBWD_TOKENS - 1) / PBWD_TOKENS);
+    const int gx = (H / 8 + 255) / 256;
+    const int per_sm = E <= 8 ? pbwd_ctas_per_sm<8>() : pbwd_ctas_per_sm<16>();
+    const int tg = E <= 8 ? pbwd_tg<8>() : pbwd_tg<16>();
+    int gy = (per_sm * num_sms_current() + gx - 1) / gx;
+    const int groups = (T + tg - 1) / tg;
+    if (gy > groups) gy = groups;
+    dim3 grid(gx, gy);
 #define DM_PBWD(EMV, KTV) permute_bwd_reg_kernel<EMV, KTV><<<grid, 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, E, k, rs, out)
     if (E <= 8) {
       switch (k) { case 1: DM_PBWD(8, 1); break; case 2: DM_PBWD(8, 2); break; case 4: DM_PBWD(8, 4); break;
