@@ -106,16 +106,16 @@ __device__ __forceinline__ void chunk_ranks(const int* sel, int nslots, int* run
 
 // Fused router for E <= EM (Mixtral-class gates): one pass over x computes the
 // canonical-order logits, top-k, softmax weights, the within-chunk ranks and
-// the chunk histogram. CTA = one 32-token chunk per pass (8 warps x 4 tokens: each
-// W_g value read from smem feeds 4 tokens, halving the smem traffic of 2 tokens/warp),
+// the chunk histogram. CTA = one 32-token chunk per pass (16 warps x 2 tokens; 8 warps
+// x 4 tokens halves the smem reads but measured slower: 28.7 vs 23.5 us, fewer warps),
 // persistent over chunks so W_g is staged into smem once per CTA, stored
 // lane-interleaved ([e][iteration][half][lane] float4) so each 128-bit smem read
 // of a warp is 512 contiguous bytes. The even/odd element chains of the
 // canonical order run as packed fp32x2 FMAs (FFMA2) on naturally paired
 // registers. W_g rows e >= E are zero-filled, so the hot loop has no E checks.
-constexpr int FUSED_UNROLL = 2;
-constexpr int FUSED_NT = 4;
-constexpr int FUSED_WARPS = DM_CHUNK_TOKENS / FUSED_NT;   // 8
+constexpr int FUSED_UNROLL = 4;
+constexpr int FUSED_NT = 2;
+constexpr int FUSED_WARPS = DM_CHUNK_TOKENS / FUSED_NT;   // 16
 
 template <int EM>
 __global__ void __launch_bounds__(FUSED_WARPS * 32)
