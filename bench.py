@@ -338,6 +338,13 @@ def run_ours(args, shape, exp):
     gemm_flops = args.steps * mb * L * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd())
     achieved_tf = gemm_flops / (gemm_ms / 1e3) / 1e12
     peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    # which roofline binds the GEMMs: tensor FLOPs or the HBM bytes they must move
+    # (weights streamed per micro-batch fwd + dgrad, fp32 dW, activations)
+    gemm_bytes = args.steps * L * shape.gemm_hbm_bytes(mb, 4 if fp32 else 2)
+    ideal_tensor_ms = gemm_flops / (peak_tf * 1e12) * 1e3
+    ideal_hbm_ms = gemm_bytes / (peaks["hbm_gbs"] * 1e9) * 1e3
+    hbm_bound = ideal_hbm_ms > ideal_tensor_ms
+    achieved_gbs = gemm_bytes / (gemm_ms / 1e3) / 1e9
     esz = 4 if fp32 else 2
     hb = shape.hbm_bytes(esz)
     hbm = {}
@@ -360,11 +367,12 @@ def run_ours(args, shape, exp):
             gbs = hb[name] / (t / 1e3) / 1e9
             hbm[name]["isolated_ms"] = round(t, 4)
             hbm[name]["isolated_frac"] = round(gbs / peaks["hbm_gbs"], 3)
+    # measured DRAM bytes of one iteration's GEMM launches (ncu; scripts/gemm_traffic.py),
+    # per step like `achieved`, when a capture for this workload is committed
     traffic = None
-    tfile = ROOT / "profiles" / "ncu_gemm_traffic.json"
-    if tfile.exists():
+    for tfile in sorted((ROOT / "profiles").glob(f"*/gemm_traffic_{Path(args.config).stem}.json")):
         try:
-            traffic = json.loads(tfile.read_text()).get("bytes_per_microbatch")
+            traffic = json.loads(tfile.read_text()).get("bytes_per_iteration")
         except (ValueError, OSError):
             traffic = None
     line = {
@@ -383,14 +391,25 @@ def run_ours(args, shape, exp):
             "launch": "eager" if graphs is None else "CUDA graphs (per micro-batch + W pass)",
             "stage_breakdown": "separate eager pass with CUDA events per stage (not the timed region)",
         },
-        "roofline": {
+        "roofline": ({
+            "bound": "hbm", "kernel": "grouped expert GEMMs (K4/K5/K8, 6 launches per micro-batch)",
+            "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved_gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
+            "peak_kind": f"{peak_kind} HBM copy bandwidth (MEASURED_PEAKS.json)",
+            "algorithmic_bytes_per_step": gemm_bytes // args.steps,
+            "tensor_achieved_tflops": round(achieved_tf, 1), "tensor_frac": round(achieved_tf / peak_tf, 4),
+            "why": f"ideal HBM time {ideal_hbm_ms / args.steps:.2f} ms/step > ideal tensor time "
+                   f"{ideal_tensor_ms / args.steps:.2f} ms/step (weights streamed per micro-batch)",
+            "gemm_ms_per_microbatch_layer": round(gemm_ms / (args.steps * mb * L), 4),
+        } if hbm_bound else {
             "bound": "tensor", "kernel": "grouped expert GEMMs (K4/K5/K8, 6 launches per micro-batch)",
             "achieved": round(achieved_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
             "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
             "peak_kind": f"{peak_kind} sustained bf16 (MEASURED_PEAKS.json)",
             "gemm_ms_per_microbatch_layer": round(gemm_ms / (args.steps * mb * L), 4),
             "frac_of_burst": round(achieved_tf / peaks["bf16_tflops"], 4),
-        },
+            "hbm_achieved_gbs": round(achieved_gbs, 1),
+        }),
         "roofline_hbm": {"peak_GB/s": peaks["hbm_gbs"], **hbm,
                          "note": "ms/frac: in-step CUDA events around each stage; isolated_*: graph replay, "
                                  "L2 flushed before every launch (flush time subtracted)"},
@@ -449,6 +468,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
     import torch.distributed as dist
 
     from paper_2605_11005_b200 import _lib
+    from paper_2605_11005_b200.profile import reference_memory_estimate
     from paper_2605_11005_b200.runtime import AFPipeRank, Topology, trace_intervals
 
     if exp.model.bytes_per_element != 2:
@@ -492,6 +512,11 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
     lsum = torch.tensor([float(launches)], device=dev)
     dist.all_reduce(lsum)
     clocks = sampler.stop() if sampler else None
+
+    # measured peak device memory per rank vs the reference's memory model
+    mem_all = [None] * world
+    dist.all_gather_object(mem_all, {"rank": rank, "role": r.role,
+                                     "peak_GB": round(torch.cuda.max_memory_allocated(dev) / 1e9, 3)})
 
     # one instrumented iteration: per-task CUDA-event intervals on every rank
     r.record_events = True
@@ -582,6 +607,14 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                      "peak_GB/s": 900.0, "note": "bytes / (data ready -> send complete), per transfer group"},
             "gpu_launches": int(lsum.item()),
             "clocks": clocks,
+            "memory": {
+                "measured_peak_GB": {f"{m['role']}{m['rank']}": m["peak_GB"] for m in mem_all},
+                "reference_model_GB": {c: round(reference_memory_estimate(exp, c, topo.n_attn, topo.n_ffn) / 1e9, 3)
+                                       for c in ("A", "F")},
+                "note": "reference placement.memory_estimate: bf16 params + 8 B/param optimizer + in-flight hidden "
+                        "states; measured: weights + fp32 grads (no optimizer) + every micro-batch's activations "
+                        "resident for the deferred W pass (+ attention graphs with --attention)",
+            },
             "e2e": {"value": round(tokens / (ems / 1e3), 1), "unit": UNIT,
                     "h2d_bytes_per_step": 2 * T * H * 2 * mb * topo.n_attn,
                     "d2h_bytes_per_step": 2 * T * H * 2 * mb * topo.n_attn,

@@ -197,10 +197,11 @@ DM_API int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogi
                     int k, float* partial_ws, float* dwg, float beta, void* stream);
 
 /* dW_g[e,:] = sum over expert e's permuted rows r of dl_perm[r] * x[src_token[r], :]
- * (+ beta * dW_g): deterministic single-pass router gradient for large E. */
+ * (+ beta * dW_g), deterministic. partial_ws (dm_router_wgrad_workspace_size bytes, may be
+ * NULL) lets few-expert layers split each expert's rows into segments reduced in order. */
 DM_API int dm_router_wgrad_sorted(const void* x, const int32_t* src_token, const float* dl_perm,
                                   const int32_t* counts, const int32_t* pad_off, int T, int H, int E,
-                                  float* dwg, float beta, void* stream);
+                                  float* partial_ws, float* dwg, float beta, void* stream);
 
 /* ---- fp32 mode (experiment bytes_per_element = 4; 1e-4 parity) ---------------
  * fp32 activations / gradients / master weights. GEMM operands are bf16 "split-3":

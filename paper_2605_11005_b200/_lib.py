@@ -63,7 +63,7 @@ SIGNATURES: dict[str, tuple] = {
     "dm_combine_fwd": (_i, [_vp, _i32p, _f32p, _i, _i, _i, _vp, _vp, _vp]),
     "dm_combine_bwd": (_i, [_vp, _vp, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _i, _vp, _f32p,
                             _f32p, _f32p, _vp]),
-    "dm_router_wgrad_sorted": (_i, [_vp, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _f32p, _f, _vp]),
+    "dm_router_wgrad_sorted": (_i, [_vp, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _f32p, _f32p, _f, _vp]),
     "dm_permute_bwd": (_i, [_vp, _i32p, _i32p, _f32p, _f32p, _i, _i, _i, _i, _vp, _vp, _vp]),
     "dm_router_wgrad": (_i, [_vp, _i32p, _f32p, _i, _i, _i, _i, _f32p, _f32p, _f, _vp]),
     # fp32 mode (bytes_per_element 4)

@@ -177,77 +177,88 @@ permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __r
   }
 }
 
-// Permute backward for E <= EM: each warp owns one 256-column chunk for the whole
-// launch and its lanes hold their 8 columns of every W_g row in registers, so the
-// router dx term sum_j dlogit[t,j] * W_g[idx[t,j], :] costs no memory traffic (the
-// per-token W_g row reads of permute_bwd_kernel were L1-bound). The grid is sized
-// to the resident CTA slots (2 per SM) and each CTA strides over groups of
-// PBWD_TG tokens, so there is no partial last wave and every warp keeps
-// PBWD_TG * k 128-bit gathers in flight.
-template <int EM> constexpr int pbwd_tg() { return EM <= 8 ? 4 : 2; }
-template <int EM> constexpr int pbwd_ctas_per_sm() { return EM <= 8 ? 2 : 1; }
+// Permute backward for small E: CTA = 8 warps sharing one 256-column chunk whose
+// W_g columns ([E][256] fp32, <= 16 KB) sit in smem, so the router dx term
+// sum_j dlogit[t,j] * W_g[idx[t,j], :] reads only the k selected rows from smem (the
+// per-token W_g reads of the generic kernel were L1-bound; holding all E rows in
+// registers cost 64-128 registers and capped occupancy at 25%). Warps stride over
+// groups of PBWD_TG tokens; the grid fills the resident CTA slots in one wave.
+constexpr int PBWD_TG = 4;
+constexpr int PBWD_MAX_E = 16;
 
-template <int EM, int KT>
-__global__ void __launch_bounds__(256, pbwd_ctas_per_sm<EM>())
-permute_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_map,
-                       const int32_t* __restrict__ idx, const float* __restrict__ dlogit,
-                       const float* __restrict__ wg, int T, int H, int E, int k_rt,
-                       const __nv_bfloat16* __restrict__ resid, __nv_bfloat16* __restrict__ dx) {
+template <int KT>
+__global__ void __launch_bounds__(256)
+permute_bwd_smem_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_map,
+                        const int32_t* __restrict__ idx, const float* __restrict__ dlogit,
+                        const float* __restrict__ wg, int T, int H, int E, int k_rt,
+                        const __nv_bfloat16* __restrict__ resid, __nv_bfloat16* __restrict__ dx) {
   const int k = KT ? KT : k_rt;
+  __shared__ float4 ws[PBWD_MAX_E * 64];   // [e][256 columns] as float4
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int col = ((blockIdx.x * (blockDim.x >> 5) + warp) * 32 + lane) * 8;
-  if (col >= H) return;
-  float wr[EM][8];
-#pragma unroll
-  for (int e = 0; e < EM; ++e) {
-    if (e < E && dlogit) {
-      const float4 a = *reinterpret_cast<const float4*>(wg + (size_t)e * H + col);
-      const float4 b = *reinterpret_cast<const float4*>(wg + (size_t)e * H + col + 4);
-      wr[e][0] = a.x; wr[e][1] = a.y; wr[e][2] = a.z; wr[e][3] = a.w;
-      wr[e][4] = b.x; wr[e][5] = b.y; wr[e][6] = b.z; wr[e][7] = b.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) wr[e][i] = 0.0f;
+  const int col0 = blockIdx.x * 256;
+  if (dlogit) {
+    for (int i = threadIdx.x; i < E * 64; i += blockDim.x) {
+      const int e = i >> 6, c4 = i & 63;
+      ws[i] = (col0 + c4 * 4 < H) ? reinterpret_cast<const float4*>(wg + (size_t)e * H + col0)[c4]
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    __syncthreads();
   }
-  constexpr int TG = pbwd_tg<EM>();
-  for (int t0 = blockIdx.y * TG; t0 < T; t0 += gridDim.y * TG) {
+  const int col = col0 + lane * 8;
+  if (col >= H) return;
+  const int nw = gridDim.y * 8;
+  constexpr int KK = KT ? KT : 1;   // staged gathers per token (runtime k falls back to a loop)
+  for (int t0 = (blockIdx.y * 8 + warp) * PBWD_TG; t0 < T; t0 += nw * PBWD_TG) {
+    // stage 1: every token's indices, then all TG * k row gathers in flight at once
+    int pos[PBWD_TG][KK];
+    int4 v[PBWD_TG][KK];
+    int4 rv[PBWD_TG];
 #pragma unroll
-    for (int u = 0; u < TG; ++u) {
+    for (int u = 0; u < PBWD_TG; ++u) {
+      const int t = min(t0 + u, T - 1);
+#pragma unroll
+      for (int j = 0; j < KK; ++j) pos[u][j] = KT ? row_map[(size_t)t * k + j] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < PBWD_TG; ++u) {
+      const int t = min(t0 + u, T - 1);
+      rv[u] = resid ? ld_nc_v4(resid + (size_t)t * H + col) : make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < KK; ++j) v[u][j] = KT ? ld_nc_v4(dx_perm + (size_t)pos[u][j] * H + col) : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < PBWD_TG; ++u) {
       const int t = t0 + u;
       if (t >= T) break;
-      int pos[KT ? KT : DM_MAX_TOPK];
-      float gw[EM];
+      float acc[8];
+      unpack8(rv[u], acc);
+      if (KT) {
 #pragma unroll
-      for (int e = 0; e < EM; ++e) gw[e] = 0.0f;
+        for (int j = 0; j < KK; ++j) {
+          float f[8];
+          unpack8(v[u][j], f);
 #pragma unroll
-      for (int j = 0; j < k; ++j) {
-        pos[j] = row_map[(size_t)t * k + j];
-        if (dlogit) {
-          const int ej = idx[(size_t)t * k + j];
-          const float dl = dlogit[(size_t)t * k + j];
+          for (int i = 0; i < 8; ++i) acc[i] += f[i];
+        }
+      } else {
+        for (int j = 0; j < k; ++j) {
+          float f[8];
+          unpack8(ld_nc_v4(dx_perm + (size_t)row_map[(size_t)t * k + j] * H + col), f);
 #pragma unroll
-          for (int e = 0; e < EM; ++e) gw[e] = (ej == e) ? dl : gw[e];
+          for (int i = 0; i < 8; ++i) acc[i] += f[i];
         }
       }
-      float acc[8];
-      if (resid) {
-        unpack8(ld_nc_v4(resid + (size_t)t * H + col), acc);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+      if (dlogit) {
+        for (int j = 0; j < k; ++j) {
+          const int e = idx[(size_t)t * k + j];
+          const float dl = dlogit[(size_t)t * k + j];
+          const float4 a = ws[e * 64 + lane * 2], b = ws[e * 64 + lane * 2 + 1];
+          acc[0] = __fmaf_rn(dl, a.x, acc[0]); acc[1] = __fmaf_rn(dl, a.y, acc[1]);
+          acc[2] = __fmaf_rn(dl, a.z, acc[2]); acc[3] = __fmaf_rn(dl, a.w, acc[3]);
+          acc[4] = __fmaf_rn(dl, b.x, acc[4]); acc[5] = __fmaf_rn(dl, b.y, acc[5]);
+          acc[6] = __fmaf_rn(dl, b.z, acc[6]); acc[7] = __fmaf_rn(dl, b.w, acc[7]);
+        }
       }
-#pragma unroll
-      for (int j = 0; j < k; ++j) {
-        float f[8];
-        unpack8(ld_nc_v4(dx_perm + (size_t)pos[j] * H + col), f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += f[i];
-      }
-#pragma unroll
-      for (int e = 0; e < EM; ++e)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(gw[e], wr[e][i], acc[i]);
       st_v4(dx + (size_t)t * H + col, pack8(acc));
     }
   }
@@ -347,6 +358,7 @@ __global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, in
   for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < EH;
        i += (size_t)gridDim.x * blockDim.x * 4) {
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
     for (int tb = 0; tb < ntb; ++tb) {
       const float4 v = *reinterpret_cast<const float4*>(partial + (size_t)tb * EH + i);
       s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
@@ -360,24 +372,31 @@ __global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, in
   }
 }
 
-// Router weight gradient for large E, deterministic and single pass: the rows of
-// expert e in the permuted layout are exactly the (t, j) slots with idx == e in
-// ascending t, so dW_g[e, :] = sum over the block of dl_perm[r] * x[src_token[r], :]
-// (dl_perm = dlogit scattered to permuted positions by combine_bwd). CTA per
-// (1024-column chunk, expert); x rows are gathered with 128-bit loads (L2-resident).
+// Router weight gradient over the expert-sorted rows: the rows of expert e in the
+// permuted layout are exactly the (t, j) slots with idx == e in ascending t, so
+// dW_g[e, :] = sum over the block of dl_perm[r] * x[src_token[r], :] (dl_perm =
+// dlogit scattered to permuted positions by combine_bwd). CTA per (1024-column
+// chunk, expert, row segment); x rows are gathered with 128-bit loads (x is
+// L2-resident after the forward). With nseg > 1 (few experts, long blocks) each
+// segment writes a partial [seg][E][H] that router_wgrad_reduce_kernel sums in
+// segment order, so the result is deterministic either way. 8 accumulators per
+// thread keep occupancy high enough to cover the gather latency.
 __global__ void __launch_bounds__(128)
 router_wgrad_sorted_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ src_token,
                            const float* __restrict__ dl_perm, const int32_t* __restrict__ counts,
-                           const int32_t* __restrict__ pad_off, int H, float* __restrict__ dwg, float beta) {
-  const int e = blockIdx.y;
+                           const int32_t* __restrict__ pad_off, int H, int E, int nseg, float* __restrict__ partial,
+                           float* __restrict__ dwg, float beta) {
+  const int e = blockIdx.y, seg = blockIdx.z;
   const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (col >= H) return;
-  const int beg = pad_off[e], n = counts[e];
+  const int n = counts[e];
+  const int r0 = pad_off[e] + (int)((long long)n * seg / nseg);
+  const int r1 = pad_off[e] + (int)((long long)n * (seg + 1) / nseg);
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-#pragma unroll 4
-  for (int r = beg; r < beg + n; ++r) {
+#pragma unroll 8
+  for (int r = r0; r < r1; ++r) {
     const int t = src_token[r];
     const float d = dl_perm[r];
     float f[8];
@@ -385,8 +404,14 @@ router_wgrad_sorted_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* _
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(d, f[i], acc[i]);
   }
-  float4* o = reinterpret_cast<float4*>(dwg + (size_t)e * H + col);
   float4 a = make_float4(acc[0], acc[1], acc[2], acc[3]), b = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  if (nseg > 1) {
+    float4* o = reinterpret_cast<float4*>(partial + ((size_t)seg * E + e) * H + col);
+    o[0] = a;
+    o[1] = b;
+    return;
+  }
+  float4* o = reinterpret_cast<float4*>(dwg + (size_t)e * H + col);
   if (beta != 0.0f) {
     const float4 oa = o[0], ob = o[1];
     a.x += beta * oa.x; a.y += beta * oa.y; a.z += beta * oa.z; a.w += beta * oa.w;
@@ -454,22 +479,17 @@ int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* i
   cudaStream_t st = (cudaStream_t)stream;
   const __nv_bfloat16* dxp = reinterpret_cast<const __nv_bfloat16*>(dx_perm);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(dx);
-  if (E <= 16) {
-    const int gx = (H / 8 + 255) / 256;
-    const int per_sm = E <= 8 ? pbwd_ctas_per_sm<8>() : pbwd_ctas_per_sm<16>();
-    const int tg = E <= 8 ? pbwd_tg<8>() : pbwd_tg<16>();
-    int gy = (per_sm * num_sms_current() + gx - 1) / gx;
-    const int groups = (T + tg - 1) / tg;
+  if (E <= PBWD_MAX_E) {
+    static int occ = 0;
+    if (!occ) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, permute_bwd_smem_kernel<2>, 256, 0);
+    const int gx = (H + 255) / 256;
+    int gy = ((occ > 0 ? occ : 2) * num_sms_current() + gx - 1) / gx;
+    const int groups = (T + 8 * PBWD_TG - 1) / (8 * PBWD_TG);
     if (gy > groups) gy = groups;
     dim3 grid(gx, gy);
-#define DM_PBWD(EMV, KTV) permute_bwd_reg_kernel<EMV, KTV><<<grid, 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, E, k, rs, out)
-    if (E <= 8) {
-      switch (k) { case 1: DM_PBWD(8, 1); break; case 2: DM_PBWD(8, 2); break; case 4: DM_PBWD(8, 4); break;
-                   case 8: DM_PBWD(8, 8); break; default: DM_PBWD(8, 0); break; }
-    } else {
-      switch (k) { case 1: DM_PBWD(16, 1); break; case 2: DM_PBWD(16, 2); break; case 4: DM_PBWD(16, 4); break;
-                   case 8: DM_PBWD(16, 8); break; default: DM_PBWD(16, 0); break; }
-    }
+#define DM_PBWD(KTV) permute_bwd_smem_kernel<KTV><<<grid, 256, 0, st>>>(dxp, row_map, idx, dlogit, wg, T, H, E, k, rs, out)
+    switch (k) { case 1: DM_PBWD(1); break; case 2: DM_PBWD(2); break; case 4: DM_PBWD(4); break;
+                 case 8: DM_PBWD(8); break; default: DM_PBWD(0); break; }
 #undef DM_PBWD
   } else {
     switch (k) {
@@ -492,12 +512,12 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
     return set_error(DM_ERR_SHAPE, "router_wgrad bad shape");
   if (((size_t)E * H) % 4 || reinterpret_cast<uintptr_t>(dwg) & 15 || reinterpret_cast<uintptr_t>(partial_ws) & 15)
     return set_error(DM_ERR_ALIGN, "router_wgrad needs 16-byte aligned fp32 buffers");
-  const int tbt = dm_router_wgrad_token_block(E);
-  const int ntb = (T + tbt - 1) / tbt;
+  int tbt = dm_router_wgrad_token_block(E);
+  int ntb = (T + tbt - 1) / tbt;   // the workspace holds this many partial blocks
   cudaStream_t st = (cudaStream_t)stream;
   if (E <= 16) {
-    dim3 grid((H / 8 + 31) / 32, ntb);
     static bool cfg = false;
+    static int occ8 = 1, occ16 = 1;
     if (!cfg) {
       cudaError_t e1 = cudaFuncSetAttribute(router_wgrad_reg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             8 * 8 * 8 * 32 * 4);
@@ -505,8 +525,22 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
                                             4 * 16 * 8 * 32 * 4);
       if (e1 != cudaSuccess) return set_cuda_error(e1, "cudaFuncSetAttribute(router_wgrad_reg)");
       if (e2 != cudaSuccess) return set_cuda_error(e2, "cudaFuncSetAttribute(router_wgrad_reg)");
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ8, router_wgrad_reg_kernel<8>, 256, 8 * 8 * 8 * 32 * 4);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ16, router_wgrad_reg_kernel<16>, 128, 4 * 16 * 8 * 32 * 4);
       cfg = true;
     }
+    // One wave: as many token blocks as the resident CTA slots allow per column chunk
+    // (never more than the workspace's ntb), each a contiguous run of tbt tokens.
+    const int gx = (H / 8 + 31) / 32;
+    const int slots = (E <= 8 ? occ8 : occ16) * num_sms_current();
+    int want = slots / gx;
+    if (want < 1) want = 1;
+    if (want < ntb) {
+      tbt = (T + want - 1) / want;
+      tbt = (tbt + 7) & ~7;
+      ntb = (T + tbt - 1) / tbt;
+    }
+    dim3 grid(gx, ntb);
     if (E <= 8)
       router_wgrad_reg_kernel<8><<<grid, 256, 8 * 8 * 8 * 32 * 4, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
                                                        T, H, E, k, tbt, partial_ws);
@@ -542,15 +576,37 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
 }
 
 int dm_router_wgrad_sorted(const void* x, const int32_t* src_token, const float* dl_perm, const int32_t* counts,
-                           const int32_t* pad_off, int T, int H, int E, float* dwg, float beta, void* stream) {
+                           const int32_t* pad_off, int T, int H, int E, float* partial_ws, float* dwg, float beta,
+                           void* stream) {
   if (T < 1 || H % 8 || E < 1 || E > DM_MAX_EXPERTS) return set_error(DM_ERR_SHAPE, "router_wgrad_sorted bad shape");
-  if (reinterpret_cast<uintptr_t>(dwg) & 15) return set_error(DM_ERR_ALIGN, "dW_g must be 16-byte aligned");
-  dim3 grid((H / 8 + 127) / 128, E);
-  router_wgrad_sorted_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(x), src_token, dl_perm, counts, pad_off, H, dwg, beta);
+  if (reinterpret_cast<uintptr_t>(dwg) & 15 || reinterpret_cast<uintptr_t>(partial_ws) & 15)
+    return set_error(DM_ERR_ALIGN, "dW_g / workspace must be 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int gx = (H / 8 + 127) / 128;
+  // enough row segments for ~4 CTAs per SM, bounded by the workspace's partial blocks
+  int nseg = 1;
+  if (partial_ws) {
+    const int tbt = dm_router_wgrad_token_block(E);
+    const int cap_seg = (T + tbt - 1) / tbt;
+    nseg = (4 * num_sms_current() + gx * E - 1) / (gx * E);
+    if (nseg > cap_seg) nseg = cap_seg;
+    if (nseg < 1) nseg = 1;
+  }
+  dim3 grid(gx, E, nseg);
+  router_wgrad_sorted_kernel<<<grid, 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), src_token, dl_perm,
+                                                   counts, pad_off, H, E, nseg, partial_ws, dwg, beta);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_sorted launch");
   note_launch();
+  if (nseg > 1) {
+    const size_t EH = (size_t)E * H;
+    int rblocks = (int)((EH / 4 + 63) / 64);
+    if (rblocks > num_sms_current() * 8) rblocks = num_sms_current() * 8;
+    router_wgrad_reduce_kernel<<<rblocks, 64, 0, st>>>(partial_ws, nseg, EH, dwg, beta);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_sorted reduce launch");
+    note_launch();
+  }
   return DM_OK;
 }
 

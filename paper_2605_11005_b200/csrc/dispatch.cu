@@ -146,8 +146,10 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
     for (int t = 0; t < FUSED_NT; ++t)
 #pragma unroll
       for (int e = 0; e < EM; ++e) acc[t][e] = make_float2(0.f, 0.f);
-    for (int it0 = 0; it0 < NI; it0 += FUSED_UNROLL) {
-      int4 xv[FUSED_UNROLL][FUSED_NT];
+    // x k-tiles are double-buffered in registers: the loads of batch i+1 are in flight
+    // while batch i is multiplied (the loop is unrolled by two batches).
+    int4 xa[FUSED_UNROLL][FUSED_NT], xb[FUSED_UNROLL][FUSED_NT];
+    auto load = [&](int4 (&xv)[FUSED_UNROLL][FUSED_NT], int it0) {
 #pragma unroll
       for (int u = 0; u < FUSED_UNROLL; ++u)
 #pragma unroll
@@ -156,6 +158,8 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
           xv[u][t] = (it0 + u < NI && c < nch && tg + t < T) ? ld_nc_v4(x + (size_t)(tg + t) * H + c * 8)
                                                             : make_int4(0, 0, 0, 0);
         }
+    };
+    auto compute = [&](const int4 (&xv)[FUSED_UNROLL][FUSED_NT], int it0) {
 #pragma unroll
       for (int u = 0; u < FUSED_UNROLL; ++u) {
         if (it0 + u >= NI) break;
@@ -181,6 +185,14 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
           }
         }
       }
+    };
+    load(xa, 0);
+    for (int it0 = 0; it0 < NI; it0 += 2 * FUSED_UNROLL) {
+      if (it0 + FUSED_UNROLL < NI) load(xb, it0 + FUSED_UNROLL);
+      compute(xa, it0);
+      if (it0 + FUSED_UNROLL >= NI) break;
+      if (it0 + 2 * FUSED_UNROLL < NI) load(xa, it0 + 2 * FUSED_UNROLL);
+      compute(xb, it0 + FUSED_UNROLL);
     }
 #pragma unroll
     for (int t = 0; t < FUSED_NT; ++t) {

@@ -167,11 +167,11 @@ def combine_bwd(dy, y_perm, row_map, w, counts, pad_off, dy_perm, dw, dlogit, st
               T, H, E, k, _ptr(dy_perm), _ptr(dw), _ptr(dlogit), _ptr(dl_perm), _stream(stream))
 
 
-def router_wgrad_sorted(x, src_token, dl_perm, counts, pad_off, dwg, beta=0.0, stream=None):
+def router_wgrad_sorted(x, src_token, dl_perm, counts, pad_off, dwg, beta=0.0, stream=None, partial_ws=None):
     T, H = x.shape
     E = dwg.shape[0]
     _lib.call("dm_router_wgrad_sorted", _ptr(x), _ptr(src_token), _ptr(dl_perm), _ptr(counts), _ptr(pad_off),
-              T, H, E, _ptr(dwg), float(beta), _stream(stream))
+              T, H, E, _ptr(partial_ws), _ptr(dwg), float(beta), _stream(stream))
 
 
 def permute_bwd(dx_perm, row_map, idx, dlogit, wg, dx, stream=None, resid=None):

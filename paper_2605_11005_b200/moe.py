@@ -27,8 +27,6 @@ from . import kernels as K
 BF16 = torch.bfloat16
 F32 = torch.float32
 I32 = torch.int32
-# above this many experts the router weight gradient runs over the expert-sorted rows
-SORTED_WGRAD_MIN_E = 16
 
 
 @dataclass(frozen=True)
@@ -63,6 +61,19 @@ class MoEShape:
 
     def gemm_flops_bwd(self) -> int:
         return 12 * self.R * self.H * self.De
+
+    def gemm_hbm_bytes(self, microbatches: int, e: int = 2) -> int:
+        """Algorithmic HBM bytes of one iteration's expert GEMMs (unpadded rows): per
+        micro-batch the forward and dgrad passes each stream W13 + W2 and their
+        activation operands/outputs; the deferred W pass reads every micro-batch's
+        operands once and writes dW13 + dW2 in fp32. Fine-grained MoE (DeepSeek-V3:
+        ~128 rows per expert) is bound by this, not by tensor FLOPs."""
+        T, H, E, De, R = self.T, self.H, self.E, self.De, self.R
+        w = E * 3 * H * De * e
+        fwd = w + R * (H + 2 * De + De + De + H) * e          # x_perm, h13, act (w+r), y_perm
+        dgrad = w + R * (H + 2 * De + 2 * De + 2 * De + H) * e  # dy_perm, h13, dh13 (w+r), dx_perm
+        wgrad = microbatches * R * (H + De + 2 * De + H) * e + E * 3 * H * De * 4
+        return microbatches * (fwd + dgrad) + wgrad
 
     def hbm_bytes(self, e: int = 2) -> dict[str, int]:
         T, H, R = self.T, self.H, self.R
@@ -182,7 +193,7 @@ class MicroBatchBuffers:
             self.dy = z(s.T, s.H)
             self.dw = z(s.T, s.k, dt=F32)
             self.dlogit = z(s.T, s.k, dt=F32)
-            self.dl_perm = z(slab.cap, dt=F32) if s.E > SORTED_WGRAD_MIN_E else None
+            self.dl_perm = z(slab.cap, dt=F32)
             self.dx = z(s.T, s.H)
         self.x_perm = slab.x_perm[rows]
         self.y_perm = slab.y_perm[rows]
@@ -248,13 +259,12 @@ def a_permute_bwd(buf: MicroBatchBuffers, router: RouterParams, stream=None) -> 
 
 
 def a_router_wgrad(buf: MicroBatchBuffers, router: RouterParams, accumulate: bool, stream=None) -> None:
-    """dW_g (+)= dlogit^T x: over the expert-sorted rows for large E (one pass, no
-    workspace), else token-blocked partials + a fixed-order reduce."""
+    """dW_g (+)= dlogit^T x over the expert-sorted rows (dlogit scattered to them by
+    combine_bwd); few-expert layers split each expert's rows into segments whose
+    partials are reduced in a fixed order (deterministic)."""
     beta = 1.0 if accumulate else 0.0
-    if buf.dl_perm is not None:
-        K.router_wgrad_sorted(buf.x, buf.src, buf.dl_perm, buf.counts, buf.pad_off, router.dwg, beta, stream)
-    else:
-        K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws, router.dwg, beta, stream)
+    K.router_wgrad_sorted(buf.x, buf.src, buf.dl_perm, buf.counts, buf.pad_off, router.dwg, beta, stream,
+                          partial_ws=buf.wgrad_ws)
 
 
 class MoELayer:
@@ -354,8 +364,18 @@ class MoELayer:
         plus 2 wgrad GEMMs unless deferred to the iteration's W pass."""
         s = self.shape
         fused = s.E <= 16 and s.E * s.H * 4 <= 160 * 1024
-        router_wgrad = 1 if s.E > SORTED_WGRAD_MIN_E else 2
+        router_wgrad = 2 if _router_wgrad_segments(s) > 1 else 1
         return (3 if fused else 4) + 7 + router_wgrad + (0 if deferred_wgrad else 2)
+
+
+def _router_wgrad_segments(s: MoEShape) -> int:
+    """Row segments dm_router_wgrad_sorted uses (mirrors combine.cu's launcher)."""
+    import math
+
+    sms = _lib.load().dm_num_sms(torch.cuda.current_device())
+    gx = math.ceil(s.H / 8 / 128)
+    cap_seg = math.ceil(s.T / _lib.router_wgrad_token_block(s.E))
+    return max(1, min(math.ceil(4 * sms / (gx * s.E)), cap_seg))
 
 
 def link_residual_stack(stack_bufs: list[list[MicroBatchBuffers]]) -> None:

@@ -163,3 +163,32 @@ def export_trace(ranks: list[dict]) -> list[dict]:
             task += 1
     events.sort(key=lambda ev: (ev["ts"], ev["pid"], ev["tid"], ev["args"]["task"]))
     return events
+
+
+def reference_memory_estimate(exp, component: str, n_attn: int, n_ffn: int) -> float:
+    """Per-GPU bytes of the reference's memory model for pipeline_depth p and the
+    largest group (restated from `placement.memory_estimate`, placement.py:78-120):
+    bf16 parameters + 8 B/param optimizer state + one hidden-state tensor per
+    assigned layer per in-flight micro-batch. Attention parameters (QKV + output,
+    H²(2 + 2/g) + H² per layer) are replicated across the A group; expert
+    parameters (E·2·H·D_e per layer) are sharded over the F group's GPUs. Used to
+    compare the model with the runtime's measured peak memory."""
+    from fractions import Fraction
+
+    m, w = exp.model, exp.workload
+    p = max(1, exp.pipeline_depth)
+    layers = -(-m.layers // p)                       # virtual stages of the largest group
+    h, g = m.hidden, m.gqa_group
+    if component == "A":
+        per_layer = Fraction(2 * (g + 1), g) * h * h + h * h
+        params = float(layers * per_layer)
+        first_visit = 0
+    else:
+        per_gpu_group = n_ffn / p
+        params = layers * m.experts * 2 * h * m.moe_hidden / per_gpu_group
+        first_visit = 1
+    param_bytes = params * 2
+    optimizer_bytes = params * 8.0
+    hidden = m.bytes_per_element * w.micro_batch * w.seq_len * h
+    in_flight = min(w.num_microbatches, max(1, 2 * p * layers - first_visit))
+    return param_bytes + optimizer_bytes + float(layers * hidden * in_flight)

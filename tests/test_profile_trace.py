@@ -77,3 +77,23 @@ def test_trace_export_validates_against_reference_schema():
 
     triples = parse_trace_events(json.dumps(events))
     assert len(triples) == 6 and triples[0] == (0, 100000, "A0")
+
+
+@pytest.mark.skipif(not REF.exists(), reason="reference not mounted")
+def test_reference_memory_estimate_restatement_matches_reference():
+    sys.path.insert(0, str(REF))
+    from afpipe.allocator import canonical_allocation
+    from afpipe.config import load_experiment as ref_load
+    from afpipe.placement import assign_layers, memory_estimate
+
+    from paper_2605_11005_b200.profile import reference_memory_estimate
+
+    for cfg in ("tiny.yaml", "mixtral_layer.yaml", "dsv3_layer.yaml"):
+        path = str(ROOT / "configs" / cfg)
+        ours, ref = load_experiment(path), ref_load(path)
+        for n_attn, n_ffn in ((1, 1), (2, 6), (4, 4)):
+            alloc = canonical_allocation(n_attn, n_ffn, n_attn + n_ffn, n_attn + n_ffn, n_attn + n_ffn)
+            for comp in ("A", "F"):
+                plan = assign_layers(ref.model.layers, ref.pipeline_depth, comp)
+                want = memory_estimate(plan, ref.model, ref.workload, alloc).total
+                assert reference_memory_estimate(ours, comp, n_attn, n_ffn) == pytest.approx(want, rel=1e-12)
