@@ -475,15 +475,17 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
         raise SystemExit("AF-Pipe runtime exchanges bf16 micro-batches; fp32 mode (bytes_per_element 4) runs on "
                          "the fused single-device path (N=1, or --replicas)")
     mb = exp.workload.num_microbatches
-    topo = Topology.default(world, shape.E, args.n_attn)
+    topo = Topology.default(world, shape.E, args.n_attn, args.depth or exp.pipeline_depth)
     L = exp.model.layers
     r = AFPipeRank(shape, topo, rank, mb, dev, seed=1234, layers=L, attention=args.attention,
                    seq_len=exp.workload.seq_len, gqa_group=exp.model.gqa_group)
     r.init_groups()
     if r.role == "A":
         for i in range(mb):
-            r.input(i).normal_()
-            r.out_bufs[i].dy.normal_()
+            if r.has_input:
+                r.input(i).normal_()
+            if r.has_output:
+                r.out_bufs[i].dy.normal_()
     sampler = ClockSampler(dev.index) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -555,7 +557,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
 
     if rank == 0:
         peaks, peak_kind = _peaks()
-        tokens = args.steps * mb * shape.T * topo.n_attn
+        tokens = args.steps * mb * shape.T * topo.streams
         value = tokens / (ms / 1e3)
         comp_all, comm_all, per_rank, it_end = [], [], {}, 0.0
         gemm_ms, link = 0.0, []
@@ -571,7 +573,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
             link += [b / ((e - s) / 1e3) / 1e9 for n, i, lane, s, e, b in g["ivs"]
                      if lane != "compute" and e > s and b > 0]
         exposed = _uncovered(comm_all, comp_all)
-        f_flops = mb * L * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd()) * topo.n_attn
+        f_flops = mb * L * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd()) * topo.streams
         achieved = f_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
         peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         line = {
@@ -580,8 +582,10 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {
                 "workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E, "k": shape.k,
-                "D_e": shape.De, "layers": L, "microbatches": mb, "tokens_per_step": mb * shape.T * topo.n_attn,
-                "parallelism": f"AF-Pipe {topo.n_attn}A:{topo.n_ffn}F (A: DP "
+                "D_e": shape.De, "layers": L, "microbatches": mb, "tokens_per_step": mb * shape.T * topo.streams,
+                "pipeline_depth": topo.depth,
+                "parallelism": f"AF-Pipe {topo.n_attn}A:{topo.n_ffn}F" + (f" x {topo.depth} pipeline groups"
+                                                                           if topo.depth > 1 else "") + " (A: DP "
                                + ("attention + " if args.attention else "") + "routing/combine, F: EP experts)",
                 "layer": "attention + residual MoE block (attention: library stopgap)" if args.attention
                          else "MoE block",
@@ -616,8 +620,8 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                         "resident for the deferred W pass (+ attention graphs with --attention)",
             },
             "e2e": {"value": round(tokens / (ems / 1e3), 1), "unit": UNIT,
-                    "h2d_bytes_per_step": 2 * T * H * 2 * mb * topo.n_attn,
-                    "d2h_bytes_per_step": 2 * T * H * 2 * mb * topo.n_attn,
+                    "h2d_bytes_per_step": 2 * T * H * 2 * mb * topo.streams,
+                    "d2h_bytes_per_step": 2 * T * H * 2 * mb * topo.streams,
                     "ms_per_step": round(ems / args.steps, 3),
                     "path": "AFPipeRank.run_iteration with pinned host x/dy in, y/dx out per micro-batch"},
         }
@@ -741,6 +745,9 @@ def main(argv=None):
     ap.add_argument("--seq-len", type=int, default=None, help="override workload.seq_len (sweeps)")
     ap.add_argument("--trace", default=None, help="N>1: write the instrumented iteration as reference-schema trace JSON")
     ap.add_argument("--microbatches", type=int, default=None, help="override workload.num_microbatches")
+    ap.add_argument("--layers", type=int, default=None, help="override model.layers")
+    ap.add_argument("--depth", type=int, default=None,
+                    help="N>1: pipeline depth p (layers alternate over p A+F groups); default schedule.pipeline_depth")
     ap.add_argument("--eager", action="store_true", help="N=1: launch kernels eagerly instead of CUDA graphs")
     ap.add_argument("--no-isolated", action="store_true", help="skip the isolated A-side kernel timing")
     ap.add_argument("--attention", action="store_true",
@@ -752,12 +759,14 @@ def main(argv=None):
     from paper_2605_11005_b200.moe import MoEShape
 
     exp = load_experiment(args.config)
-    if args.seq_len or args.microbatches:
+    if args.seq_len or args.microbatches or args.layers:
         import dataclasses
 
         wl = dataclasses.replace(exp.workload, seq_len=args.seq_len or exp.workload.seq_len,
                                  num_microbatches=args.microbatches or exp.workload.num_microbatches)
-        exp = dataclasses.replace(exp, workload=wl)
+        md = dataclasses.replace(exp.model, layers=args.layers or exp.model.layers)
+        exp = dataclasses.replace(exp, workload=wl, model=md,
+                                  virtual_stages=md.layers if args.layers else exp.virtual_stages)
     shape = MoEShape.from_experiment(exp)
     if args.impl == "reference":
         return run_reference(args, shape, exp)

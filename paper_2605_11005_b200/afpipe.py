@@ -216,57 +216,81 @@ class LayerDurations:
 
 
 def build_layer_dag(microbatches: int, d: LayerDurations, a_credit: int = 2, f_credit: int = 2,
-                    layers: int = 1) -> Plan:
-    """Runtime chain of a stack of `layers` residual MoE blocks on one A group and one
-    F group (pipeline_depth 1, virtual_stages = layers; reference taskgraph.py:307-356
-    with the loss turnaround on the A side). Per micro-batch:
+                    layers: int = 1, depth: int = 1) -> Plan:
+    """Runtime chain of a stack of `layers` residual MoE blocks, layer l on A group and
+    F group l mod `depth` (reference taskgraph.py:307-356 with the loss turnaround on the
+    A side; virtual_stages = ceil(layers / depth)). Per micro-batch, depth 1:
 
         A_f[0] M2N[0] F_f[0] N2M[0] A_f[1] ... F_f[L-1] N2M[L-1] A_t
         M2N_b[L-1] F_b[L-1] N2M_b[L-1] A_b[L-1] M2N_b[L-2] ... A_b[0]
 
     where A_f[l>0] is layer l-1's combine fused with layer l's dispatch and A_b[l>0]
-    includes layer l-1's combine backward. layers=1 is the single-layer chain."""
+    includes layer l-1's combine backward (same rank). With depth > 1 consecutive layers
+    live on different A groups: layer l's combine (A_c) stays on the rank holding its
+    routing, the residual stream x_{l+1} moves A_g -> A_g' (A2A), and backward the
+    gradient of x_l returns A_g' -> A_g (A2A_b) ahead of layer l-1's combine backward
+    (A_cb). layers=1 is the single-layer chain."""
     tasks: list[PlanTask] = []
+    p = depth
 
     def new(kind, owner, lane, dur, deps, mb, layer, comp, direction, name):
-        t = PlanTask(len(tasks), kind, owner, lane, dur, tuple(deps), mb, layer, layer, comp, direction)
+        t = PlanTask(len(tasks), kind, owner, lane, dur, tuple(deps), mb, layer, layer // p, comp, direction)
         t.name = name  # type: ignore[attr-defined]
         tasks.append(t)
         return t.id
 
-    def exchange(src, dst, dep, mb, layer, direction, name):
-        s = new("M2NSend", src, SEND, d.m2n, (dep,), mb, layer, None, direction, name)
-        r = new("M2NRecv", dst, RECV, d.m2n, (dep,), mb, layer, None, direction, name)
+    def exchange(src, dst, dep, mb, layer, direction, name, dur=None):
+        s = new("M2NSend", src, SEND, d.m2n if dur is None else dur, (dep,), mb, layer, None, direction, name)
+        r = new("M2NRecv", dst, RECV, d.m2n if dur is None else dur, (dep,), mb, layer, None, direction, name)
         tasks[s].twin, tasks[r].twin = r, s
         return r
 
+    A = lambda l: f"A{l % p}"  # noqa: E731
+    F = lambda l: f"F{l % p}"  # noqa: E731
+    a2a = max(1, d.m2n // 2)   # T x H residual stream vs T x k x H routed rows
     for mb in range(microbatches):
         r = None
         for layer in range(layers):
-            dur = d.a_fwd if layer == 0 else d.a_fwd + d.a_turn // 2
-            af = new("FwdCompute", "A0", COMPUTE, dur, () if r is None else (r,), mb, layer, "A", FWD, "A_f")
-            r = exchange("A0", "F0", af, mb, layer, FWD, "M2N")
-            ff = new("FwdCompute", "F0", COMPUTE, d.f_fwd, (r,), mb, layer, "F", FWD, "F_f")
-            r = exchange("F0", "A0", ff, mb, layer, FWD, "N2M")
+            fused = layer > 0 and p == 1
+            dur = d.a_fwd + (d.a_turn // 2 if fused else 0)
+            af = new("FwdCompute", A(layer), COMPUTE, dur, () if r is None else (r,), mb, layer, "A", FWD, "A_f")
+            r = exchange(A(layer), F(layer), af, mb, layer, FWD, "M2N")
+            ff = new("FwdCompute", F(layer), COMPUTE, d.f_fwd, (r,), mb, layer, "F", FWD, "F_f")
+            r = exchange(F(layer), A(layer), ff, mb, layer, FWD, "N2M")
+            if p > 1 and layer < layers - 1:
+                ac = new("FwdCompute", A(layer), COMPUTE, d.a_turn // 2, (r,), mb, layer, "A", FWD, "A_c")
+                r = exchange(A(layer), A(layer + 1), ac, mb, layer, FWD, "A2A", a2a)
         top = layers - 1
-        at = new("BwdCompute", "A0", COMPUTE, d.a_turn, (r,), mb, top, "A", BWD, "A_t")
-        r = exchange("A0", "F0", at, mb, top, BWD, "M2N_b")
+        at = new("BwdCompute", A(top), COMPUTE, d.a_turn, (r,), mb, top, "A", BWD, "A_t")
+        r = exchange(A(top), F(top), at, mb, top, BWD, "M2N_b")
         for layer in reversed(range(layers)):
-            fb = new("BwdCompute", "F0", COMPUTE, d.f_bwd, (r,), mb, layer, "F", BWD, "F_b")
-            r = exchange("F0", "A0", fb, mb, layer, BWD, "N2M_b")
-            dur = d.a_bwd if layer == 0 else d.a_bwd + d.a_turn // 2
-            ab = new("BwdCompute", "A0", COMPUTE, dur, (r,), mb, layer, "A", BWD, "A_b")
+            fb = new("BwdCompute", F(layer), COMPUTE, d.f_bwd, (r,), mb, layer, "F", BWD, "F_b")
+            r = exchange(F(layer), A(layer), fb, mb, layer, BWD, "N2M_b")
+            fused = layer > 0 and p == 1
+            dur = d.a_bwd + (d.a_turn // 2 if fused else 0)
+            ab = new("BwdCompute", A(layer), COMPUTE, dur, (r,), mb, layer, "A", BWD, "A_b")
             if layer > 0:
-                r = exchange("A0", "F0", ab, mb, layer - 1, BWD, "M2N_b")
-    return Plan(tasks, {"A0": a_credit, "F0": f_credit})
+                if p == 1:
+                    r = exchange(A(layer), F(layer - 1), ab, mb, layer - 1, BWD, "M2N_b")
+                else:
+                    r = exchange(A(layer), A(layer - 1), ab, mb, layer - 1, BWD, "A2A_b", a2a)
+                    acb = new("BwdCompute", A(layer - 1), COMPUTE, d.a_turn // 2, (r,), mb, layer - 1, "A", BWD,
+                              "A_cb")
+                    r = exchange(A(layer - 1), F(layer - 1), acb, mb, layer - 1, BWD, "M2N_b")
+    credits = {}
+    for g in range(p):
+        credits[f"A{g}"] = a_credit
+        credits[f"F{g}"] = f_credit
+    return Plan(tasks, credits)
 
 
 def plan_layer(microbatches: int, d: LayerDurations, a_credit: int = 2, f_credit: int = 2,
-               layers: int = 1) -> Plan:
+               layers: int = 1, depth: int = 1) -> Plan:
     """Scheduled runtime chain; every rank issues its tasks in planned-start order,
     which keeps the per-pair send/recv order identical on both ends (twins share a start).
-    Credits scale with the stack depth (reference taskgraph.py:316-321: 2L visits)."""
-    return schedule(build_layer_dag(microbatches, d, a_credit * layers, f_credit * layers, layers))
+    Credits scale with the virtual stages as in the reference (taskgraph.py:316-321)."""
+    v = -(-layers // depth)
+    return schedule(build_layer_dag(microbatches, d, a_credit * v, f_credit * v, layers, depth))
 
 
 def issue_order(plan: Plan, owner: str) -> list[PlanTask]:

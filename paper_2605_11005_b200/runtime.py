@@ -60,40 +60,73 @@ def balanced_blocks(total: int, parts: int) -> list[int]:
 
 @dataclass(frozen=True)
 class Topology:
+    """A:F split of `world` ranks, optionally into `depth` = p pipeline groups
+    (reference pipeline_depth; placement.assign_layers, placement.py:42-55): ranks
+    [0, n_attn) are A ranks, A group g = ranks [g*a_p, (g+1)*a_p) with a_p = n_attn/p;
+    the rest are F ranks, F group g = the g-th block of f_p = n_ffn/p ranks. Layer l runs
+    on A group and F group l mod p; stream j (a DP replica of the micro-batch chain) uses
+    member j of every A group."""
+
     world: int
     n_attn: int
     experts: int
+    depth: int = 1
 
     def __post_init__(self):
         if not (1 <= self.n_attn < self.world):
             raise ValueError(f"need 1 <= n_attn < world (n_attn={self.n_attn}, world={self.world})")
-        if self.n_ffn > self.experts:
-            raise ValueError(f"{self.n_ffn} FFN ranks for {self.experts} experts")
+        if self.depth < 1 or self.n_attn % self.depth or self.n_ffn % self.depth:
+            raise ValueError(f"pipeline depth {self.depth} must divide n_attn={self.n_attn} and n_ffn={self.n_ffn}")
+        if self.f_per_group > self.experts:
+            raise ValueError(f"{self.f_per_group} FFN ranks per group for {self.experts} experts")
 
     @property
     def n_ffn(self) -> int:
         return self.world - self.n_attn
 
+    @property
+    def a_per_group(self) -> int:
+        return self.n_attn // self.depth
+
+    @property
+    def f_per_group(self) -> int:
+        return self.n_ffn // self.depth
+
+    @property
+    def streams(self) -> int:
+        """Independent micro-batch chains (tokens per step = streams * mb * T)."""
+        return self.a_per_group
+
     def role(self, rank: int) -> tuple[str, int]:
         return ("A", rank) if rank < self.n_attn else ("F", rank - self.n_attn)
 
-    def a_rank(self, a: int) -> int:
-        return a
+    def group_of(self, rank: int) -> tuple[int, int]:
+        """(pipeline group, member index within the group) of a rank."""
+        role, i = self.role(rank)
+        per = self.a_per_group if role == "A" else self.f_per_group
+        return i // per, i % per
 
-    def f_rank(self, f: int) -> int:
-        return self.n_attn + f
+    def a_rank(self, a: int, group: int = 0) -> int:
+        return group * self.a_per_group + a
+
+    def f_rank(self, f: int, group: int = 0) -> int:
+        return self.n_attn + group * self.f_per_group + f
 
     def expert_block(self, f: int) -> tuple[int, int]:
-        sizes = balanced_blocks(self.experts, self.n_ffn)
+        """Expert range of member f of an F group (every group holds all experts of its layers)."""
+        sizes = balanced_blocks(self.experts, self.f_per_group)
         lo = sum(sizes[:f])
         return lo, lo + sizes[f]
 
+    def layers_of(self, group: int, layers: int) -> list[int]:
+        return list(range(group, layers, self.depth))
+
     @classmethod
-    def default(cls, world: int, experts: int, n_attn: int | None = None) -> "Topology":
+    def default(cls, world: int, experts: int, n_attn: int | None = None, depth: int = 1) -> "Topology":
         """A:F = n_attn : world-n_attn; default half/half (BASELINE configs[1]: 4 + 4)."""
         if n_attn is None:
             n_attn = max(1, world // 2)
-        return cls(world, n_attn, experts)
+        return cls(world, n_attn, experts, depth)
 
 
 # ------------------------------------------------------------------ streams
@@ -214,12 +247,14 @@ class IterationStats:
 
 
 class AFPipeRank:
-    """One rank of the AF-Pipe runtime for a stack of `layers` MoE layers (p = 1).
+    """One rank of the AF-Pipe runtime for a stack of `layers` MoE layers over
+    `topo.depth` pipeline groups (layer l on A group / F group l mod depth).
 
-    A ranks: `lbufs[l][i]` (layer l, micro-batch i), `routers[l]`; inputs in
-    `bufs[i].x` (layer 0), upstream gradients in `out_bufs[i].dy` (last layer).
-    F ranks: `expert_layers[l]`, one activation slab per layer. `router` / `experts`
-    alias layer 0 (the single-layer API)."""
+    A ranks: `lbufs[l][i]` (layer l, micro-batch i) and `routers[l]` for the layers of
+    their group; `input(i)` / `input_grad(i)` on group 0, `out_bufs[i]` (y, dy) on the
+    group of the last layer. F ranks: `expert_layers[l]`, one activation slab per layer
+    of their group. Per-layer state is keyed by layer index; `router` / `experts` /
+    `bufs` alias the group's first layer (the single-layer API)."""
 
     def __init__(self, shape: MoEShape, topo: Topology, rank: int, microbatches: int, device,
                  stages=None, seed: int = 0, weights=None, durations: LayerDurations | None = None,
@@ -228,12 +263,17 @@ class AFPipeRank:
         shape.validate() if device.type == "cuda" else None
         if layers < 1:
             raise ValueError(f"layers must be >= 1, got {layers}")
+        if topo.depth > layers:
+            raise ValueError(f"pipeline depth {topo.depth} > layers {layers}")
         self.shape, self.topo, self.rank, self.mb, self.L = shape, topo, rank, microbatches, layers
+        self.p = topo.depth
         self.attention = attention
         self.seq_len = seq_len or shape.T
         self.residual = (layers > 1 or attention) if residual is None else residual
         self.device = torch.device(device)
         self.role, self.idx = topo.role(rank)
+        self.group, self.member = topo.group_of(rank)
+        self.my_layers = topo.layers_of(self.group, layers)
         self.stages = stages if stages is not None else GpuStages()
         self.st = _Streams(self.device)
         self.record_events = record_events and self.st.cuda
@@ -243,66 +283,77 @@ class AFPipeRank:
 
             self._attn_flops = attention_flops(shape.H, gqa_group, self.seq_len, shape.T // self.seq_len)
         d = durations or self._default_durations()
-        self.plan = plan_layer(microbatches, d, layers=layers)
-        self.order = issue_order(self.plan, "A0" if self.role == "A" else "F0")
+        self.plan = plan_layer(microbatches, d, layers=layers, depth=self.p)
+        self.order = issue_order(self.plan, f"{self.role}{self.group}")
         if isinstance(weights, dict):
             weights = [weights]
         if weights is not None and len(weights) != layers:
             raise ValueError(f"{len(weights)} weight sets for {layers} layers")
         s = shape
+        mbr = range(microbatches)
         if self.role == "A":
-            self.routers, self.lbufs = [], []
-            for l in range(layers):
+            self.routers, self.lbufs = {}, {}
+            for l in self.my_layers:
                 if weights:
                     wg = weights[l]["wg"]
                 else:
                     wg = torch.randn(s.E, s.H, generator=torch.Generator().manual_seed(seed + 1000 * l)) * 0.02
-                self.routers.append(RouterParams(wg.to(self.device, F32)))
+                self.routers[l] = RouterParams(wg.to(self.device, F32))
                 slab = ActivationSlab(s, microbatches, self.device, f_side=False)
-                self.lbufs.append([MicroBatchBuffers(s, self.device, slab, i, residual=self.residual)
-                                   for i in range(microbatches)])
+                self.lbufs[l] = [MicroBatchBuffers(s, self.device, slab, i, residual=self.residual) for i in mbr]
             self.attn = None
+            e = lambda: torch.empty(s.T, s.H, dtype=BF16, device=self.device)  # noqa: E731
             if attention:   # A-side attention per layer (library stopgap, attention.py)
                 from .attention import AttentionBlock
 
-                self.attn = [AttentionBlock(s.H, gqa_group, self.device, seed=seed + 77 + l) for l in range(layers)]
-                self.inp = [torch.empty(s.T, s.H, dtype=BF16, device=self.device) for _ in range(microbatches)]
-                self.dinp = [torch.empty(s.T, s.H, dtype=BF16, device=self.device) for _ in range(microbatches)]
-            else:
-                link_residual_stack(self.lbufs)
-            self.router, self.bufs, self.out_bufs = self.routers[0], self.lbufs[0], self.lbufs[-1]
-            self.pad_host = [[torch.empty(s.E + 1, dtype=I32, pin_memory=self.st.cuda) for _ in range(microbatches)]
-                             for _ in range(layers)]
-            self.pad_ready = [[None] * microbatches for _ in range(layers)]
+                self.attn = {l: AttentionBlock(s.H, gqa_group, self.device, seed=seed + 77 + l) for l in self.my_layers}
+                # attention input x_l and its gradient: the stream input/grad on layer 0,
+                # received from / sent to the previous layer's A group otherwise
+                self.xin = {l: [e() for _ in mbr] for l in self.my_layers}
+                self.gin = {l: [e() for _ in mbr] for l in self.my_layers}
+                if self.p == 1:
+                    for l in self.my_layers[1:]:
+                        self.xin[l] = [b.y for b in self.lbufs[l - 1]]
+                        self.gin[l] = [b.dy for b in self.lbufs[l - 1]]
+            elif self.p == 1:
+                link_residual_stack([self.lbufs[l] for l in self.my_layers])
+            first = self.my_layers[0]
+            self.router, self.bufs = self.routers[first], self.lbufs[first]
+            if layers - 1 in self.lbufs:
+                self.out_bufs = self.lbufs[layers - 1]
+            self.pad_host = {l: [torch.empty(s.E + 1, dtype=I32, pin_memory=self.st.cuda) for _ in mbr]
+                             for l in self.my_layers}
+            self.pad_ready = {l: [None] * microbatches for l in self.my_layers}
             self.a_group = None
         else:
-            lo, hi = topo.expert_block(self.idx)
+            lo, hi = topo.expert_block(self.member)
             self.lo, self.hi, self.E_loc = lo, hi, hi - lo
-            # worst case: every routed row of every A rank lands on this F rank
-            self.cap_f = topo.n_attn * s.cap
-            self.expert_layers, self.slabs, self.lfmb, self.seg_offs = [], [], [], []
-            for l in range(layers):
+            self.n_src = topo.a_per_group   # A ranks feeding this F group
+            # worst case: every routed row of every A rank of the group lands on this F rank
+            self.cap_f = self.n_src * s.cap
+            self.expert_layers, self.slabs, self.lfmb, self.seg_offs = {}, {}, {}, {}
+            for l in self.my_layers:
                 if weights:
                     w13, w2 = weights[l]["w13"][lo:hi], weights[l]["w2"][lo:hi]
                 else:
-                    g = torch.Generator(device=self.device).manual_seed(seed + 1 + self.idx + 1000 * l)
+                    g = torch.Generator(device=self.device).manual_seed(seed + 1 + self.member + 1000 * l)
                     w13 = torch.empty(self.E_loc, 2 * s.De, s.H, dtype=BF16, device=self.device).normal_(0, 0.02, generator=g)
                     w2 = torch.empty(self.E_loc, s.H, s.De, dtype=BF16, device=self.device).normal_(0, 0.02, generator=g)
-                self.expert_layers.append(ExpertParams(w13.to(self.device), w2.to(self.device)))
+                self.expert_layers[l] = ExpertParams(w13.to(self.device), w2.to(self.device))
                 sl = ActivationSlab(s, microbatches, self.device, rows=self.cap_f)
                 fmb = []
-                for i in range(microbatches):
+                for i in mbr:
                     r = sl.rows(i)
                     fmb.append(_FMicroBatch(sl.x_perm[r], sl.y_perm[r], sl.dy_perm[r], sl.dx_perm[r],
                                             sl.h13[r], sl.act[r], sl.dh13[r]))
                     fmb[-1].headers = [torch.zeros(self.E_loc + 1, dtype=I32, device=self.device)
-                                       for _ in range(topo.n_attn)]
-                self.slabs.append(sl)
-                self.lfmb.append(fmb)
-                self.seg_offs.append(torch.zeros(microbatches * topo.n_attn, self.E_loc + 1, dtype=I32,
-                                                 device=self.device))
-            self.experts, self.slab, self.fmb, self.seg_off = (self.expert_layers[0], self.slabs[0],
-                                                               self.lfmb[0], self.seg_offs[0])
+                                       for _ in range(self.n_src)]
+                self.slabs[l] = sl
+                self.lfmb[l] = fmb
+                self.seg_offs[l] = torch.zeros(microbatches * self.n_src, self.E_loc + 1, dtype=I32, device=self.device)
+            first = self.my_layers[0]
+            self.experts, self.slab, self.fmb, self.seg_off = (self.expert_layers[first], self.slabs[first],
+                                                               self.lfmb[first], self.seg_offs[first])
         self.trace: list = []
         self.t0 = None
         self.host_io = None
@@ -312,9 +363,10 @@ class AFPipeRank:
         """Rough per-stage estimates (ns) to derive the issue order; only the order matters."""
         s = self.shape
         tflops = 1.0e15
-        per_f = max(1, self.topo.n_ffn)
-        f_fwd = int(6 * s.R * s.H * s.De * self.topo.n_attn / per_f / tflops * 1e9)
-        m2n = int(2 * s.R * s.H / max(1, min(self.topo.n_attn, per_f)) / 7.0e11 * 1e9)
+        per_f = max(1, self.topo.f_per_group)
+        n_src = self.topo.a_per_group
+        f_fwd = int(6 * s.R * s.H * s.De * n_src / per_f / tflops * 1e9)
+        m2n = int(2 * s.R * s.H / max(1, min(n_src, per_f)) / 7.0e11 * 1e9)
         a = int(sum(s.hbm_bytes().values()) / 4 / 5.0e12 * 1e9)
         af = ab = 0
         if self._attn_flops is not None:
@@ -351,31 +403,49 @@ class AFPipeRank:
 
     def _a_slices(self, pad: list[int]):
         out = []
-        for f in range(self.topo.n_ffn):
+        for f in range(self.topo.f_per_group):
             lo, hi = self.topo.expert_block(f)
             out.append((f, pad[lo], pad[hi], lo, hi))
         return out
 
     def set_host_io(self, xs, dys, ys, dxs) -> None:
         """Pinned host tensors per micro-batch: inputs copied in on the copy stream at
-        iteration start, y / dx copied back as each micro-batch finishes (e2e mode)."""
+        iteration start, y / dx copied back as each micro-batch finishes (e2e mode).
+        Group 0 ranks use x / dx, the last layer's group y / dy."""
         self.host_io = (xs, dys, ys, dxs)
+
+    @property
+    def has_input(self) -> bool:
+        return self.role == "A" and 0 in self.my_layers
+
+    @property
+    def has_output(self) -> bool:
+        return self.role == "A" and (self.L - 1) in self.my_layers
 
     def _h2d_inputs(self):
         xs, dys, _, _ = self.host_io
         self.h2d_ready = []
         with self.st.ctx("copy"):
             for i, (x, dy) in enumerate(zip(xs, dys)):
-                self.input(i).copy_(x, non_blocking=True)
-                self.out_bufs[i].dy.copy_(dy, non_blocking=True)
+                if self.has_input:
+                    self.input(i).copy_(x, non_blocking=True)
+                if self.has_output:
+                    self.out_bufs[i].dy.copy_(dy, non_blocking=True)
                 self.h2d_ready.append(self.st.event("copy"))
 
     def input(self, i: int) -> torch.Tensor:
-        """A rank: micro-batch i's input activations (layer 0, before attention if any)."""
-        return self.inp[i] if self.attn is not None else self.bufs[i].x
+        """A rank of group 0: micro-batch i's input activations (before attention if any)."""
+        return self.xin[0][i] if self.attn is not None else self.lbufs[0][i].x
 
     def input_grad(self, i: int) -> torch.Tensor:
-        return self.dinp[i] if self.attn is not None else self.bufs[i].dx
+        return self.gin[0][i] if self.attn is not None else self.lbufs[0][i].dx
+
+    def _layer_input(self, layer: int, i: int) -> torch.Tensor:
+        """Where layer l's residual-stream input x_l lives on this rank."""
+        return self.xin[layer][i] if self.attn is not None else self.lbufs[layer][i].x
+
+    def _layer_input_grad(self, layer: int, i: int) -> torch.Tensor:
+        return self.gin[layer][i] if self.attn is not None else self.lbufs[layer][i].dx
 
     def a_task(self, name: str, i: int, layer: int, accumulate: bool):
         b = self.lbufs[layer][i]
@@ -383,14 +453,14 @@ class AFPipeRank:
             if layer == 0:
                 if self.host_io is not None:
                     self.st.wait("compute", self.h2d_ready[i])
-                x_in = self.inp[i] if self.attn is not None else None
-            else:   # previous layer's combine writes this layer's input (residual fused)
+            elif self.p == 1:   # previous layer's combine writes this layer's input (residual fused)
                 prev = self.lbufs[layer - 1][i]
                 self._wait_works(prev, "N2M")
                 self.stages.a_combine(prev)
-                x_in = prev.y
+            else:               # x_l arrived from the previous layer's A group
+                self._wait_works(b, "A2A")
             if self.attn is not None:
-                self.attn[layer].forward(i, x_in, b.x, self.seq_len)
+                self.attn[layer].forward(i, self._layer_input(layer, i), b.x, self.seq_len)
             self.stages.a_dispatch(b, self.routers[layer])
             done = self.st.event("compute")
             with self.st.ctx("copy"):
@@ -398,38 +468,54 @@ class AFPipeRank:
                 self.pad_host[layer][i].copy_(b.pad_off, non_blocking=self.st.cuda)
                 self.pad_ready[layer][i] = self.st.event("copy")
             b.fwd_done = done
+        elif name == "A_c":     # depth > 1: this layer's combine, then x_{l+1} leaves (A2A)
+            self._wait_works(b, "N2M")
+            self.stages.a_combine(b)
+            b.comb_done = self.st.event("compute")
         elif name == "A_t":
             self._wait_works(b, "N2M")
             self.stages.a_combine(b)
+            self.stages.a_combine_bwd(b)
+            b.turn_done = self.st.event("compute")
+        elif name == "A_cb":    # depth > 1: dy_l arrived (A2A_b); this layer's combine backward
+            self._wait_works(b, "A2A_b")
             self.stages.a_combine_bwd(b)
             b.turn_done = self.st.event("compute")
         elif name == "A_b":
             self._wait_works(b, "N2M_b")
             self.stages.a_backward(b, self.routers[layer], accumulate)
             if self.attn is not None:
-                dst = self.dinp[i] if layer == 0 else self.lbufs[layer - 1][i].dy
-                self.attn[layer].backward(i, b.dx, dst, accumulate)
-            if layer > 0:   # this layer's dx is the previous layer's upstream gradient
+                self.attn[layer].backward(i, b.dx, self._layer_input_grad(layer, i), accumulate)
+            if layer > 0 and self.p == 1:   # this layer's dx is the previous layer's upstream gradient
                 prev = self.lbufs[layer - 1][i]
                 self.stages.a_combine_bwd(prev)
                 prev.turn_done = self.st.event("compute")
-            elif self.host_io is not None:
+            else:
+                b.bwd_done = self.st.event("compute")
+            if layer == 0 and self.host_io is not None:
                 _, _, ys, dxs = self.host_io
                 done = self.st.event("compute")
                 with self.st.ctx("copy"):
                     self.st.wait("copy", done)
-                    ys[i].copy_(self.out_bufs[i].y, non_blocking=True)
                     dxs[i].copy_(self.input_grad(i), non_blocking=True)
+            if layer == self.L - 1 and self.host_io is not None:
+                _, _, ys, _ = self.host_io
+                with self.st.ctx("copy"):
+                    self.st.wait("copy", b.turn_done)
+                    ys[i].copy_(self.out_bufs[i].y, non_blocking=True)
 
-    def a_comm(self, name: str, i: int, layer: int):
+    def a_comm(self, name: str, i: int, layer: int, lane: str):
+        if name in ("A2A", "A2A_b"):
+            return self._a2a(name, i, layer, lane)
         b = self.lbufs[layer][i]
         pad = self._a_pad(layer, i)
+        g = self.group
         ops = []
         if name == "M2N":
             with self.st.ctx("send"):
                 self.st.wait("send", b.fwd_done)
                 for f, r0, r1, lo, hi in self._a_slices(pad):
-                    peer = self.topo.f_rank(f)
+                    peer = self.topo.f_rank(f, g)
                     hdr = b.pad_off[lo:hi + 1]
                     ops += [("send", hdr, peer), ("send", b.x_perm[r0:r1], peer)]
                 b.works_M2N = self._xchg(ops, name, i)
@@ -437,14 +523,44 @@ class AFPipeRank:
             with self.st.ctx("send"):
                 self.st.wait("send", b.turn_done)
                 for f, r0, r1, lo, hi in self._a_slices(pad):
-                    ops.append(("send", b.dy_perm[r0:r1], self.topo.f_rank(f)))
+                    ops.append(("send", b.dy_perm[r0:r1], self.topo.f_rank(f, g)))
                 b.works_M2N_b = self._xchg(ops, name, i)
         elif name in ("N2M", "N2M_b"):
             dst = b.y_perm if name == "N2M" else b.dx_perm
             with self.st.ctx("recv"):
                 for f, r0, r1, lo, hi in self._a_slices(pad):
-                    ops.append(("recv", dst[r0:r1], self.topo.f_rank(f)))
+                    ops.append(("recv", dst[r0:r1], self.topo.f_rank(f, g)))
                 setattr(b, "works_" + name, _exchange(ops))
+
+    def _a2a(self, name: str, i: int, layer: int, lane: str):
+        """depth > 1: the residual stream between consecutive layers' A groups (same
+        stream member). Forward x_{l+1} = layer l's combine output; backward its gradient."""
+        p, j = self.p, self.member
+        if name == "A2A":       # task layer = l (the producer); consumer layer l + 1
+            if lane == SEND:
+                b = self.lbufs[layer][i]
+                peer = self.topo.a_rank(j, (layer + 1) % p)
+                with self.st.ctx("send"):
+                    self.st.wait("send", b.comb_done)
+                    b.works_A2A_send = self._xchg([("send", b.y, peer)], name, i)
+            else:
+                nb = self.lbufs[layer + 1][i]
+                peer = self.topo.a_rank(j, layer % p)
+                with self.st.ctx("recv"):
+                    nb.works_A2A = _exchange([("recv", self._layer_input(layer + 1, i), peer)])
+        else:                   # "A2A_b": task layer = l - 1 (the consumer); producer layer l
+            if lane == SEND:
+                src = self.lbufs[layer + 1][i]
+                peer = self.topo.a_rank(j, layer % p)
+                with self.st.ctx("send"):
+                    self.st.wait("send", src.bwd_done)
+                    src.works_A2A_b_send = self._xchg([("send", self._layer_input_grad(layer + 1, i), peer)],
+                                                      name, i)
+            else:
+                b = self.lbufs[layer][i]
+                peer = self.topo.a_rank(j, (layer + 1) % p)
+                with self.st.ctx("recv"):
+                    b.works_A2A_b = _exchange([("recv", b.dy, peer)])
 
     def _wait_works(self, obj, name):
         for w in getattr(obj, "works_" + name, []) or []:
@@ -453,10 +569,11 @@ class AFPipeRank:
     # ------------------------------------------------------------- F side
     def f_comm(self, name: str, i: int, layer: int):
         fm = self.lfmb[layer][i]
-        n_a = self.topo.n_attn
+        n_a = self.n_src
+        src_rank = lambda a: self.topo.a_rank(a, self.group)  # noqa: E731
         if name == "M2N":
             with self.st.ctx("recv"):
-                hw = _exchange([("recv", fm.headers[a], self.topo.a_rank(a)) for a in range(n_a)])
+                hw = _exchange([("recv", fm.headers[a], src_rank(a)) for a in range(n_a)])
                 for w in hw:
                     w.wait()
             with self.st.ctx("copy"):
@@ -488,18 +605,18 @@ class AFPipeRank:
             fm.group_off.copy_(go, non_blocking=self.st.cuda)
             self.seg_offs[layer][i * n_a:(i + 1) * n_a].copy_(seg, non_blocking=self.st.cuda)
             with self.st.ctx("recv"):
-                ops = [("recv", fm.x_perm[b0:b0 + r], self.topo.a_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
+                ops = [("recv", fm.x_perm[b0:b0 + r], src_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
                 fm.works["M2N"] = _exchange(ops)
         elif name == "M2N_b":
             with self.st.ctx("recv"):
-                ops = [("recv", fm.dy_perm[b0:b0 + r], self.topo.a_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
+                ops = [("recv", fm.dy_perm[b0:b0 + r], src_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
                 fm.works["M2N_b"] = _exchange(ops)
         elif name in ("N2M", "N2M_b"):
             src = fm.y_perm if name == "N2M" else fm.dx_perm
             ready = fm.works.get(name + "_ready")
             with self.st.ctx("send"):
                 self.st.wait("send", ready)
-                ops = [("send", src[b0:b0 + r], self.topo.a_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
+                ops = [("send", src[b0:b0 + r], src_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
                 fm.works[name] = self._xchg(ops, name, i)
 
     def f_task(self, name: str, i: int, layer: int):
@@ -533,7 +650,7 @@ class AFPipeRank:
                 if t.lane == COMPUTE:
                     self._compute(name, i, lambda: self.a_task(name, i, layer, accumulate or i > 0))
                 else:
-                    self.a_comm(name, i, layer)
+                    self.a_comm(name, i, layer, t.lane)
             else:
                 if t.lane == COMPUTE:
                     self._compute(name, i, lambda: self.f_task(name, i, layer))
@@ -541,34 +658,36 @@ class AFPipeRank:
                     self.f_comm(name, i, layer)
         if self.role == "F":
             def w_pass():
-                for sl, ex, so in zip(self.slabs, self.expert_layers, self.seg_offs):
-                    self.stages.f_wgrad(sl, ex, so, accumulate)
+                for l in self.my_layers:
+                    self.stages.f_wgrad(self.slabs[l], self.expert_layers[l], self.seg_offs[l], accumulate)
             self._compute("W", -1, w_pass)
-            for fmb in self.lfmb:
-                for fm in fmb:
+            for l in self.my_layers:
+                for fm in self.lfmb[l]:
                     for k in ("N2M", "N2M_b"):
                         for w in fm.works.get(k, []):
                             w.wait()
         else:
-            for bufs in self.lbufs:
-                for b in bufs:
-                    self._wait_works(b, "M2N")
-                    self._wait_works(b, "M2N_b")
+            for l in self.my_layers:
+                for b in self.lbufs[l]:
+                    for k in ("M2N", "M2N_b", "A2A_send", "A2A_b_send"):
+                        self._wait_works(b, k)
             if self.host_io is not None:
                 self.st.compute.wait_stream(self.st.copy) if self.st.cuda else None
-            if self.a_group is not None and self.topo.n_attn > 1:
-                for r in self.routers:
-                    dist.all_reduce(r.dwg, group=self.a_group)
-                for blk in self.attn or []:
+            if self.a_group is not None and self.topo.a_per_group > 1:
+                for l in self.my_layers:
+                    dist.all_reduce(self.routers[l].dwg, group=self.a_group)
+                for blk in (self.attn or {}).values():
                     for g in blk.grads():
                         dist.all_reduce(g, group=self.a_group)
 
     def init_groups(self):
-        """Create the A-group communicator (collective: every rank must call it)."""
-        ranks = list(range(self.topo.n_attn))
-        g = dist.new_group(ranks)
-        if self.role == "A":
-            self.a_group = g
+        """Create the per-pipeline-group A communicators (collective: every rank calls
+        new_group for every group, in the same order)."""
+        for g in range(self.topo.depth):
+            ranks = [self.topo.a_rank(j, g) for j in range(self.topo.a_per_group)]
+            pg = dist.new_group(ranks)
+            if self.role == "A" and self.group == g:
+                self.a_group = pg
 
 
 def trace_intervals(rank: "AFPipeRank") -> list[tuple[str, int, str, float, float, int]]:

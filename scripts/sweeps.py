@@ -31,7 +31,7 @@ def run(gpus: int, extra: list[str], port: int, steps: int, warmup: int) -> dict
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["alloc", "seqlen"])
+    ap.add_argument("what", choices=["alloc", "seqlen", "layers"])
     ap.add_argument("--gpus", type=int, default=4)
     ap.add_argument("--out", required=True)
     ap.add_argument("--steps", type=int, default=8)
@@ -44,6 +44,9 @@ def main():
         for n_attn in range(1, a.gpus):
             for mb in (2, 4, 8):
                 points.append((["--n-attn", str(n_attn), "--microbatches", str(mb)], {"A": n_attn, "F": a.gpus - n_attn, "mb": mb}))
+    elif a.what == "layers":   # virtual stages (p = 1): measured memory vs the reference model
+        for L in (1, 2, 4):
+            points.append((["--layers", str(L)], {"layers": L}))
     else:
         for s in (2048, 4096, 8192, 16384, 32768):
             mb = 4 if s <= 8192 else 2
@@ -57,7 +60,7 @@ def main():
                 continue
             row = {**meta, "attention": a.attention, "tokens_per_s": line["value"], "ms_per_step": line["ms_per_step"],
                    "exposed_comm": line.get("exposed_comm"), "gemm_frac": line["roofline"]["frac"],
-                   "clocks": line.get("clocks"), "e2e": line["e2e"]["value"]}
+                   "clocks": line.get("clocks"), "e2e": line["e2e"]["value"], "memory": line.get("memory")}
             if a.with_fused:
                 fused = run(1, [x for x in extra if x not in ("--n-attn",)] if "--n-attn" not in extra else
                             extra[:extra.index("--n-attn")] + extra[extra.index("--n-attn") + 2:], 0, a.steps, a.warmup)

@@ -40,7 +40,25 @@ def _inputs(a: int, i: int):
     return x, dy
 
 
-def _worker(rank, world, n_attn, port, outdir, layers=1):
+def collect(r, to_np=lambda t: t.numpy()):
+    """Per-rank results keyed by layer (a rank holds only its pipeline group's layers)."""
+    out = {"role": r.role, "group": r.group, "member": r.member, "layers": r.my_layers}
+    bits = lambda t: to_np(t.contiguous().view(torch.int16)).view(np.uint16)  # noqa: E731
+    if r.role == "A":
+        if r.has_input:
+            out["dx"] = [to_np(r.input_grad(i).float()) for i in range(MB)]
+        if r.has_output:
+            out["y"] = [to_np(b.y.float()) for b in r.out_bufs]
+        out["xin"] = {l: [bits(r.lbufs[l][i].x) for i in range(MB)] for l in r.my_layers if l > 0}
+        out["dwg"] = {l: to_np(rt.dwg) for l, rt in r.routers.items()}
+    else:
+        out["lo"], out["hi"] = r.lo, r.hi
+        out["dw13"] = {l: to_np(ex.dw13) for l, ex in r.expert_layers.items()}
+        out["dw2"] = {l: to_np(ex.dw2) for l, ex in r.expert_layers.items()}
+    return out
+
+
+def _worker(rank, world, n_attn, port, outdir, layers=1, depth=1):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -55,58 +73,56 @@ def _worker(rank, world, n_attn, port, outdir, layers=1):
     for l in range(layers):
         wg, w1, w3, w2 = _weights(l)
         weights.append({"wg": torch.from_numpy(wg), "w13": interleave_w13(bf(w1), bf(w3)), "w2": bf(w2)})
-    topo = Topology(world, n_attn, E)
+    topo = Topology(world, n_attn, E, depth)
     r = AFPipeRank(MoEShape(T, H, E, K, DE), topo, rank, MB, torch.device("cpu"), stages=CpuStages(),
                    weights=weights, layers=layers)
     r.init_groups()
     if r.role == "A":
-        for i, (b, ob) in enumerate(zip(r.bufs, r.out_bufs)):
-            x, dy = _inputs(r.idx, i)
-            b.x.copy_(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16))
-            ob.dy.copy_(bf(dy))
+        for i in range(MB):
+            x, dy = _inputs(r.member, i)
+            if r.has_input:
+                r.input(i).copy_(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16))
+            if r.has_output:
+                r.out_bufs[i].dy.copy_(bf(dy))
     r.run_iteration()
-    out = {"role": r.role, "idx": r.idx}
-    if r.role == "A":
-        out["dx"] = [b.dx.float().numpy() for b in r.bufs]
-        out["xs"] = [[r.lbufs[l][i].x.view(torch.int16).numpy().view(np.uint16) for l in range(1, layers)]
-                     for i in range(MB)]
-        out["y"] = [b.y.float().numpy() for b in r.out_bufs]
-        out["dwg"] = [rt.dwg.numpy() for rt in r.routers]
-    else:
-        out["lo"], out["hi"] = r.lo, r.hi
-        out["dw13"] = [ex.dw13.numpy() for ex in r.expert_layers]
-        out["dw2"] = [ex.dw2.numpy() for ex in r.expert_layers]
-    torch.save(out, os.path.join(outdir, f"rank{rank}.pt"))
+    torch.save(collect(r), os.path.join(outdir, f"rank{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def check_against_oracle(outs, n_attn, layers, tol=1e-2):
+def check_against_oracle(outs, n_streams, layers, tol=1e-2):
     """Compare gathered rank outputs with the oracle residual stack (layers == 1: the
-    plain MoE layer), summing parameter gradients over A ranks and micro-batches."""
+    plain MoE layer), summing parameter gradients over streams and micro-batches.
+    Stream j's layer-0 input/gradient, its layer inputs and its output may live on
+    different ranks (pipeline groups): they are joined by (member, layer)."""
     from oracle import oracle as O
 
     ws = [_weights(l) for l in range(layers)]
     acc = [{k: 0 for k in ("dwg", "dw1", "dw3", "dw2")} for _ in range(layers)]
-    for a in range(n_attn):
-        got = next(o for o in outs if o["role"] == "A" and o["idx"] == a)
+    a_outs = [o for o in outs if o["role"] == "A"]
+    for j in range(n_streams):
+        mine = [o for o in a_outs if o["member"] == j]
+        dx_got = next(o["dx"] for o in mine if "dx" in o)
+        y_got = next(o["y"] for o in mine if "y" in o)
+        xin = {l: v for o in mine for l, v in o["xin"].items()}
         for i in range(MB):
-            x, dy = _inputs(a, i)
+            x, dy = _inputs(j, i)
             if layers == 1:
                 f = O.moe_forward(x, *ws[0], K)
                 b = O.moe_backward(f, x, *ws[0], dy)
                 y, dx, bs = f.y, b.dx, [b]
             else:
-                y, dx, _, bs, xs = O.moe_stack(x, ws, K, dy, inputs=got["xs"][i])
-                for a_got, a_ref in zip(got["xs"][i], xs[1:]):
+                inputs = [xin[l][i] for l in range(1, layers)]
+                y, dx, _, bs, xs = O.moe_stack(x, ws, K, dy, inputs=inputs)
+                for a_got, a_ref in zip(inputs, xs[1:]):
                     assert O.normwise_rel_err(O.bf16_bits_to_f32(a_got), O.bf16_bits_to_f32(a_ref)) < tol
-            assert O.normwise_rel_err(got["y"][i], y) < tol
-            assert O.normwise_rel_err(got["dx"][i], dx) < tol
+            assert O.normwise_rel_err(y_got[i], y) < tol
+            assert O.normwise_rel_err(dx_got[i], dx) < tol
             for l in range(layers):
                 for k in acc[l]:
                     acc[l][k] = acc[l][k] + getattr(bs[l], k)
     for o in outs:
-        for l in range(layers):
+        for l in o["layers"]:
             if o["role"] == "A":
                 assert O.normwise_rel_err(o["dwg"][l], acc[l]["dwg"]) < tol  # all-reduced over the A group
             else:
@@ -119,12 +135,15 @@ def check_against_oracle(outs, n_attn, layers, tol=1e-2):
                 assert O.normwise_rel_err(o["dw2"][l], acc[l]["dw2"][lo:hi]) < tol
 
 
-@pytest.mark.parametrize("world,n_attn,layers", [(2, 1, 1), (3, 1, 1), (3, 2, 1), (4, 2, 1), (2, 1, 2), (3, 1, 3)])
-def test_afpipe_runtime_matches_oracle(world, n_attn, layers):
+@pytest.mark.parametrize("world,n_attn,layers,depth", [
+    (2, 1, 1, 1), (3, 1, 1, 1), (3, 2, 1, 1), (4, 2, 1, 1), (2, 1, 2, 1), (3, 1, 3, 1),
+    (4, 2, 2, 2), (4, 2, 4, 2),   # pipeline_depth 2: layers alternate between two A+F groups
+])
+def test_afpipe_runtime_matches_oracle(world, n_attn, layers, depth):
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers, depth), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
-    check_against_oracle(outs, n_attn, layers)
+    check_against_oracle(outs, n_attn // depth, layers)
 
 
 def test_topology_blocks_match_reference_balanced_blocks():
@@ -141,7 +160,7 @@ def test_topology_blocks_match_reference_balanced_blocks():
         Topology(10, 1, 8)
 
 
-def _attn_worker(rank, world, n_attn, port, outdir, layers):
+def _attn_worker(rank, world, n_attn, port, outdir, layers, depth=1):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -151,24 +170,25 @@ def _attn_worker(rank, world, n_attn, port, outdir, layers):
     from paper_2605_11005_b200.runtime import AFPipeRank, Topology
 
     weights = _attn_weights(layers)
-    r = AFPipeRank(MoEShape(T, H, E, K, DE), Topology(world, n_attn, E), rank, MB, torch.device("cpu"),
+    r = AFPipeRank(MoEShape(T, H, E, K, DE), Topology(world, n_attn, E, depth), rank, MB, torch.device("cpu"),
                    stages=CpuStages(), weights=weights, layers=layers, attention=True, seq_len=T)
     r.init_groups()
-    out = {"role": r.role, "idx": r.idx}
+    out = {"role": r.role, "member": r.member, "layers": r.my_layers}
     if r.role == "A":
         for i in range(MB):
-            x, dy = _attn_inputs(r.idx, i)
-            r.input(i).copy_(x)
-            r.out_bufs[i].dy.copy_(dy)
+            x, dy = _attn_inputs(r.member, i)
+            if r.has_input:
+                r.input(i).copy_(x)
+            if r.has_output:
+                r.out_bufs[i].dy.copy_(dy)
     r.run_iteration()
     if r.role == "A":
-        out["y"] = [b.y.float() for b in r.out_bufs]
-        out["dx"] = [r.input_grad(i).float() for i in range(MB)]
-        out["dwg"] = [rt.dwg.clone() for rt in r.routers]
-        out["dqkv"] = [a.dw_qkv.clone() for a in r.attn]
-    else:
-        out["lo"], out["hi"] = r.lo, r.hi
-        out["dw2"] = [ex.dw2.clone() for ex in r.expert_layers]
+        if r.has_output:
+            out["y"] = [b.y.float() for b in r.out_bufs]
+        if r.has_input:
+            out["dx"] = [r.input_grad(i).float() for i in range(MB)]
+        out["dwg"] = {l: rt.dwg.clone() for l, rt in r.routers.items()}
+        out["dqkv"] = {l: a.dw_qkv.clone() for l, a in r.attn.items()}
     torch.save(out, os.path.join(outdir, f"rank{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
@@ -235,15 +255,15 @@ def _sequential_reference(n_attn, layers):
     return res
 
 
-@pytest.mark.parametrize("world,n_attn,layers", [(2, 1, 2), (3, 2, 1)])
-def test_afpipe_runtime_with_attention_matches_sequential(world, n_attn, layers):
+@pytest.mark.parametrize("world,n_attn,layers,depth", [(2, 1, 2, 1), (3, 2, 1, 1), (4, 2, 2, 2)])
+def test_afpipe_runtime_with_attention_matches_sequential(world, n_attn, layers, depth):
     """A-side attention inside the AF-Pipe schedule (attention.py): the distributed run
     reproduces a single-process sequential execution of the same blocks; attention and
     router gradients are all-reduced over the A group."""
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_attn_worker, args=(world, n_attn, _free_port(), d, layers), nprocs=world, join=True)
+        mp.spawn(_attn_worker, args=(world, n_attn, _free_port(), d, layers, depth), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
-    ref = _sequential_reference(n_attn, layers)
+    ref = _sequential_reference(n_attn // depth, layers)
     from oracle import oracle as O
 
     tot_dwg = [sum(ref[a]["dwg"][l] for a in ref) for l in range(layers)]
@@ -251,10 +271,12 @@ def test_afpipe_runtime_with_attention_matches_sequential(world, n_attn, layers)
     for o in outs:
         if o["role"] != "A":
             continue
-        r = ref[o["idx"]]
+        r = ref[o["member"]]
         for i in range(MB):
-            assert O.normwise_rel_err(o["y"][i].numpy(), r["y"][i].numpy()) < 1e-2
-            assert O.normwise_rel_err(o["dx"][i].numpy(), r["dx"][i].numpy()) < 1e-2
-        for l in range(layers):
+            if "y" in o:
+                assert O.normwise_rel_err(o["y"][i].numpy(), r["y"][i].numpy()) < 1e-2
+            if "dx" in o:
+                assert O.normwise_rel_err(o["dx"][i].numpy(), r["dx"][i].numpy()) < 1e-2
+        for l in o["layers"]:
             assert O.normwise_rel_err(o["dwg"][l].numpy(), tot_dwg[l].numpy()) < 1e-2
             assert O.normwise_rel_err(o["dqkv"][l].numpy(), tot_qkv[l].numpy()) < 1e-2

@@ -21,12 +21,14 @@ sys.path.insert(0, str(ROOT / "tests"))
 from test_runtime_gloo import E, K, MB, T, DE, H, _free_port, _inputs, _weights, check_against_oracle  # noqa: E402
 
 
-def _worker(rank, world, n_attn, port, outdir, layers):
+def _worker(rank, world, n_attn, port, outdir, layers, depth=1):
     sys.path.insert(0, str(ROOT))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
     dev = torch.device("cuda", rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    from test_runtime_gloo import collect
+
     from oracle import oracle as O
     from paper_2605_11005_b200.moe import MoEShape, interleave_w13
     from paper_2605_11005_b200.runtime import AFPipeRank, Topology
@@ -36,42 +38,33 @@ def _worker(rank, world, n_attn, port, outdir, layers):
     for l in range(layers):
         wg, w1, w3, w2 = _weights(l)
         weights.append({"wg": torch.from_numpy(wg), "w13": interleave_w13(bf(w1), bf(w3)), "w2": bf(w2)})
-    r = AFPipeRank(MoEShape(T, H, E, K, DE), Topology(world, n_attn, E), rank, MB, dev, weights=weights,
+    r = AFPipeRank(MoEShape(T, H, E, K, DE), Topology(world, n_attn, E, depth), rank, MB, dev, weights=weights,
                    record_events=True, layers=layers)
     r.init_groups()
     if r.role == "A":
-        for i, (b, ob) in enumerate(zip(r.bufs, r.out_bufs)):
-            x, dy = _inputs(r.idx, i)
-            b.x.copy_(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16))
-            ob.dy.copy_(bf(dy))
+        for i in range(MB):
+            x, dy = _inputs(r.member, i)
+            if r.has_input:
+                r.input(i).copy_(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16))
+            if r.has_output:
+                r.out_bufs[i].dy.copy_(bf(dy))
     for _ in range(2):  # second iteration re-uses every buffer (stream-ordering check)
         r.run_iteration()
     torch.cuda.synchronize()
-    out = {"role": r.role, "idx": r.idx}
-    if r.role == "A":
-        out["dx"] = [b.dx.float().cpu().numpy() for b in r.bufs]
-        out["xs"] = [[r.lbufs[l][i].x.view(torch.int16).cpu().numpy().view(np.uint16) for l in range(1, layers)]
-                     for i in range(MB)]
-        out["y"] = [b.y.float().cpu().numpy() for b in r.out_bufs]
-        out["dwg"] = [rt.dwg.cpu().numpy() for rt in r.routers]
-    else:
-        out["lo"], out["hi"] = r.lo, r.hi
-        out["dw13"] = [ex.dw13.cpu().numpy() for ex in r.expert_layers]
-        out["dw2"] = [ex.dw2.cpu().numpy() for ex in r.expert_layers]
-    torch.save(out, os.path.join(outdir, f"rank{rank}.pt"))
+    torch.save(collect(r, lambda t: t.cpu().numpy()), os.path.join(outdir, f"rank{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n_attn,layers", [(2, 1, 1), (2, 1, 2), (4, 2, 1), (4, 1, 1), (4, 3, 1),
-                                                 (4, 2, 2)])
-def test_afpipe_runtime_gpu_matches_oracle(world, n_attn, layers):
+@pytest.mark.parametrize("world,n_attn,layers,depth", [(2, 1, 1, 1), (2, 1, 2, 1), (4, 2, 1, 1), (4, 1, 1, 1),
+                                                       (4, 3, 1, 1), (4, 2, 2, 1), (4, 2, 2, 2), (4, 2, 4, 2)])
+def test_afpipe_runtime_gpu_matches_oracle(world, n_attn, layers, depth):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers, depth), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
-    check_against_oracle(outs, n_attn, layers)
+    check_against_oracle(outs, n_attn // depth, layers)
 
 
 def _attn_worker(rank, world, n_attn, port, outdir, layers):
@@ -99,8 +92,8 @@ def _attn_worker(rank, world, n_attn, port, outdir, layers):
     if r.role == "A":
         out["y"] = [b.y.float().cpu() for b in r.out_bufs]
         out["dx"] = [r.input_grad(i).float().cpu() for i in range(MB)]
-        out["dqkv"] = [a.dw_qkv.cpu() for a in r.attn]
-        out["dwg"] = [rt.dwg.cpu() for rt in r.routers]
+        out["dqkv"] = [r.attn[l].dw_qkv.cpu() for l in range(layers)]
+        out["dwg"] = [r.routers[l].dwg.cpu() for l in range(layers)]
     torch.save(out, os.path.join(outdir, f"rank{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
