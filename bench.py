@@ -576,6 +576,12 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
         f_flops = mb * L * (shape.gemm_flops_fwd() + shape.gemm_flops_bwd()) * topo.streams
         achieved = f_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
         peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        # HBM-bound when streaming each F rank's weights per micro-batch dominates (fine-grained MoE)
+        import dataclasses
+
+        f_bytes = L * dataclasses.replace(shape, T=shape.T * topo.streams).gemm_hbm_bytes(mb)
+        hbm_bound = f_bytes / (peaks["hbm_gbs"] * 1e9) > f_flops / (peak_tf * 1e12)
+        achieved_gbs = f_bytes / (gemm_ms / 1e3) / 1e9 if gemm_ms > 0 else None
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
@@ -594,6 +600,12 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                 "wgrad": "fp32, deferred per iteration on F ranks",
             },
             "roofline": {
+                "bound": "hbm", "kernel": "grouped expert GEMMs on F ranks (F_f + F_b + W tasks)",
+                "achieved": round(achieved_gbs, 1) if achieved_gbs else None, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved_gbs / peaks["hbm_gbs"], 4) if achieved_gbs else None,
+                "traffic": None, "tensor_frac": round(achieved / peak_tf, 4) if achieved else None,
+                "peak_kind": f"{peak_kind} HBM, per F GPU (algorithmic GEMM bytes / sum of F compute time)",
+            } if hbm_bound else {
                 "bound": "tensor", "kernel": "grouped expert GEMMs on F ranks (F_f + F_b + W tasks)",
                 "achieved": round(achieved, 1) if achieved else None, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_tf, 4) if achieved else None, "traffic": None,
