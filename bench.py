@@ -172,7 +172,10 @@ def run_reference(args, shape, exp):
     value = statistics.median(s["value"] for s in samples)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": warm, "ms_per_step": None, "higher_is_better": True,
+        "steps": steps, "warmup": warm,
+        # one full step (mb micro-batches of T tokens per layer) at the sampled rate
+        "ms_per_step": round(exp.workload.num_microbatches * shape.T / value * 1e3, 1),
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E,
                    "k": shape.k, "D_e": shape.De, "layers": exp.model.layers,
