@@ -67,7 +67,7 @@ def test_afpipe_runtime_gpu_matches_oracle(world, n_attn, layers, depth):
     check_against_oracle(outs, n_attn // depth, layers)
 
 
-def _attn_worker(rank, world, n_attn, port, outdir, layers):
+def _attn_worker(rank, world, n_attn, port, outdir, layers, depth=1):
     sys.path.insert(0, str(ROOT))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
@@ -78,32 +78,37 @@ def _attn_worker(rank, world, n_attn, port, outdir, layers):
     from paper_2605_11005_b200.moe import MoEShape
     from paper_2605_11005_b200.runtime import AFPipeRank, Topology
 
-    r = AFPipeRank(MoEShape(T, H, E, K, DE), Topology(world, n_attn, E), rank, MB, dev,
+    r = AFPipeRank(MoEShape(T, H, E, K, DE), Topology(world, n_attn, E, depth), rank, MB, dev,
                    weights=_attn_weights(layers), layers=layers, attention=True, seq_len=T)
     r.init_groups()
     if r.role == "A":
         for i in range(MB):
-            x, dy = _attn_inputs(r.idx, i)
-            r.input(i).copy_(x)
-            r.out_bufs[i].dy.copy_(dy)
+            x, dy = _attn_inputs(r.member, i)
+            if r.has_input:
+                r.input(i).copy_(x)
+            if r.has_output:
+                r.out_bufs[i].dy.copy_(dy)
     r.run_iteration()
     torch.cuda.synchronize()
-    out = {"role": r.role, "idx": r.idx}
+    out = {"role": r.role, "member": r.member, "layers": r.my_layers}
     if r.role == "A":
-        out["y"] = [b.y.float().cpu() for b in r.out_bufs]
-        out["dx"] = [r.input_grad(i).float().cpu() for i in range(MB)]
-        out["dqkv"] = [r.attn[l].dw_qkv.cpu() for l in range(layers)]
-        out["dwg"] = [r.routers[l].dwg.cpu() for l in range(layers)]
+        if r.has_output:
+            out["y"] = [b.y.float().cpu() for b in r.out_bufs]
+        if r.has_input:
+            out["dx"] = [r.input_grad(i).float().cpu() for i in range(MB)]
+        out["dqkv"] = {l: r.attn[l].dw_qkv.cpu() for l in r.my_layers}
+        out["dwg"] = {l: r.routers[l].dwg.cpu() for l in r.my_layers}
     torch.save(out, os.path.join(outdir, f"rank{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_afpipe_attention_gpu_matches_fused_stack():
-    """1A+1F over NCCL with A-side attention (2 layers) == the fused single-GPU stack
-    (MoEStack with attention) on the same weights and inputs."""
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
+@pytest.mark.parametrize("world,n_attn,depth", [(2, 1, 1), (4, 2, 2)])
+def test_afpipe_attention_gpu_matches_fused_stack(world, n_attn, depth):
+    """A-side attention over NCCL (2 layers; 1A+1F, or two 1A+1F pipeline groups) == the
+    fused single-GPU stack (MoEStack with attention) on the same weights and inputs."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
     from test_runtime_gloo import _attn_inputs, _attn_weights
 
     from oracle import oracle as O
@@ -112,8 +117,13 @@ def test_afpipe_attention_gpu_matches_fused_stack():
 
     layers = 2
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_attn_worker, args=(2, 1, _free_port(), d, layers), nprocs=2, join=True)
-        got = torch.load(os.path.join(d, "rank0.pt"), weights_only=False)
+        mp.spawn(_attn_worker, args=(world, n_attn, _free_port(), d, layers, depth), nprocs=world, join=True)
+        outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
+    a_outs = [o for o in outs if o["role"] == "A" and o["member"] == 0]
+    y_got = next(o["y"] for o in a_outs if "y" in o)
+    dx_got = next(o["dx"] for o in a_outs if "dx" in o)
+    dqkv = {l: v for o in a_outs for l, v in o["dqkv"].items()}
+    dwg = {l: v for o in a_outs for l, v in o["dwg"].items()}
     dev = torch.device("cuda", 0)
     shape = MoEShape(T, H, E, K, DE)
     ws = _attn_weights(layers)
@@ -126,8 +136,8 @@ def test_afpipe_attention_gpu_matches_fused_stack():
     stack.iteration()
     torch.cuda.synchronize()
     for i in range(MB):
-        assert O.normwise_rel_err(got["y"][i].numpy(), stack.output(i).float().cpu().numpy()) < 1e-2
-        assert O.normwise_rel_err(got["dx"][i].numpy(), stack.input_grad(i).float().cpu().numpy()) < 1e-2
+        assert O.normwise_rel_err(y_got[i].numpy(), stack.output(i).float().cpu().numpy()) < 1e-2
+        assert O.normwise_rel_err(dx_got[i].numpy(), stack.input_grad(i).float().cpu().numpy()) < 1e-2
     for l in range(layers):
-        assert O.normwise_rel_err(got["dqkv"][l].numpy(), stack.attn[l].dw_qkv.cpu().numpy()) < 1e-2
-        assert O.normwise_rel_err(got["dwg"][l].numpy(), stack.layers[l].router.dwg.cpu().numpy()) < 1e-2
+        assert O.normwise_rel_err(dqkv[l].numpy(), stack.attn[l].dw_qkv.cpu().numpy()) < 1e-2
+        assert O.normwise_rel_err(dwg[l].numpy(), stack.layers[l].router.dwg.cpu().numpy()) < 1e-2
