@@ -32,8 +32,10 @@
  *   - Permuted buffers are expert-contiguous with every expert block padded to
  *     DM_ROW_ALIGN rows (zero-filled); pad_off[E+1] holds the block offsets and
  *     dm_capacity_rows() bounds their total, so no host sync is ever needed.
- *   - W13 is [E, 2*D_e, H] with gate/up rows interleaved in blocks of 128
- *     (rows 256b..256b+127 = gate rows 128b.., next 128 = up rows 128b..);
+ *   - W13 is [E, 2*D_e, H] with gate/up rows interleaved in blocks of DM_GLU_BLOCK
+ *     = 64 (rows 128b..128b+63 = gate rows 64b.., next 64 = up rows 64b..), so each
+ *     64-column half of a 128-column accumulator slice holds a gate block and its
+ *     up block; h13 / dh13 columns follow the same interleave;
  *     W2 is [E, H, D_e]; router weight W_g is fp32 [E, H].
  */
 #ifndef DM_MOE_H_
@@ -62,6 +64,7 @@ extern "C" {
 #define DM_ABI_VERSION 1
 #define DM_CHUNK_TOKENS 32      /* tokens per histogram chunk (stable sort unit) */
 #define DM_ROW_ALIGN 128        /* expert block alignment in permuted buffers   */
+#define DM_GLU_BLOCK 64         /* gate/up interleave block of W13 / h13 / dh13 */
 #define DM_MAX_TOPK 16
 #define DM_MAX_EXPERTS 1024
 
@@ -231,7 +234,7 @@ DM_API int dm_permute_bwd_f32(const float* dx_perm, const int32_t* row_map, cons
 DM_API int dm_router_wgrad_sorted_f32(const float* x, const int32_t* src_token, const float* dl_perm,
                                       const int32_t* counts, const int32_t* pad_off, int T, int H, int E,
                                       float* dwg, float beta, void* stream);
-/* act3 [rows, 3De] = split-3(silu(gate) * up) of fp32 h13 [rows, 2De] (128-col blocks). */
+/* act3 [rows, 3De] = split-3(silu(gate) * up) of fp32 h13 [rows, 2De] (DM_GLU_BLOCK interleave). */
 DM_API int dm_swiglu_fwd_split(const float* h13, int rows, int De, void* act3, void* stream);
 /* dh13_3 [rows, 6De] = split-3 of the SwiGLU backward of fp32 d_act [rows, De]. */
 DM_API int dm_swiglu_bwd_split(const float* d_act, const float* h13, int rows, int De, void* dh13_3,

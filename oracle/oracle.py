@@ -154,8 +154,11 @@ def dispatch_numpy(idx: np.ndarray, E: int, align: int = ROW_ALIGN):
 # ------------------------------------------------------------------ layer math
 
 
-def interleave_w13(w1: np.ndarray, w3: np.ndarray, block: int = 128) -> np.ndarray:
-    """[E, D_e, H] gate/up -> the kernels' [E, 2*D_e, H] 128-row block interleave."""
+GLU_BLOCK = 64   # include/dm_moe.h DM_GLU_BLOCK
+
+
+def interleave_w13(w1: np.ndarray, w3: np.ndarray, block: int = GLU_BLOCK) -> np.ndarray:
+    """[E, D_e, H] gate/up -> the kernels' [E, 2*D_e, H] DM_GLU_BLOCK-row block interleave."""
     E, De, H = w1.shape
     out = np.empty((E, 2 * De, H), w1.dtype)
     v = out.reshape(E, De // block, 2, block, H)
@@ -164,7 +167,7 @@ def interleave_w13(w1: np.ndarray, w3: np.ndarray, block: int = 128) -> np.ndarr
     return out
 
 
-def deinterleave_cols(h: np.ndarray, block: int = 128):
+def deinterleave_cols(h: np.ndarray, block: int = GLU_BLOCK):
     """[R, 2*D_e] interleaved columns -> (gate [R, D_e], up [R, D_e])."""
     R, two = h.shape
     De = two // 2

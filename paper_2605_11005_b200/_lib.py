@@ -16,6 +16,7 @@ LIB_PATH = _PKG / "libdm_moe.so"
 
 DM_CHUNK_TOKENS = 32
 DM_ROW_ALIGN = 128
+DM_GLU_BLOCK = 64      # gate/up interleave block of W13 / h13 / dh13 (dm_moe.h)
 DM_MAX_TOPK = 16
 DM_MAX_EXPERTS = 1024
 

@@ -278,18 +278,18 @@ router_wgrad_sorted_f32_kernel(const float* __restrict__ x, const int32_t* __res
 }
 
 // ------------------------------------------------------------------ SwiGLU
-// h13 fp32 [rows, 2De] (128-column gate/up blocks, dm_moe.h) -> act3 split-3 [rows, 3De].
+// h13 fp32 [rows, 2De] (DM_GLU_BLOCK-column gate/up blocks, dm_moe.h) -> act3 split-3 [rows, 3De].
 __global__ void __launch_bounds__(256)
 swiglu_fwd_split_kernel(const float* __restrict__ h13, int rows, int De, __nv_bfloat16* __restrict__ act3) {
   const int per_row = De >> 3;
   const size_t n = (size_t)rows * per_row;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / per_row), c = (int)(i % per_row) * 8;
-    const int blk = c >> 7, off = c & 127;
-    const float* hr = h13 + (size_t)r * 2 * De + blk * 256 + off;
+    const int blk = c / DM_GLU_BLOCK, off = c % DM_GLU_BLOCK;
+    const float* hr = h13 + (size_t)r * 2 * De + blk * 2 * DM_GLU_BLOCK + off;
     float g[8], u[8], a[8];
     ld8(hr, g);
-    ld8(hr + 128, u);
+    ld8(hr + DM_GLU_BLOCK, u);
 #pragma unroll
     for (int q = 0; q < 8; ++q) a[q] = g[q] / (1.0f + expf(-g[q])) * u[q];
     st_split3_act(act3 + (size_t)r * 3 * De, De, c, a);
@@ -305,11 +305,11 @@ swiglu_bwd_split_kernel(const float* __restrict__ d_act, const float* __restrict
   const size_t n = (size_t)rows * per_row;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / per_row), c = (int)(i % per_row) * 8;
-    const int blk = c >> 7, off = c & 127;
-    const float* hr = h13 + (size_t)r * 2 * De + blk * 256 + off;
+    const int blk = c / DM_GLU_BLOCK, off = c % DM_GLU_BLOCK;
+    const float* hr = h13 + (size_t)r * 2 * De + blk * 2 * DM_GLU_BLOCK + off;
     float g[8], u[8], d[8], dg[8], du[8];
     ld8(hr, g);
-    ld8(hr + 128, u);
+    ld8(hr + DM_GLU_BLOCK, u);
     ld8(d_act + (size_t)r * De + c, d);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -318,8 +318,8 @@ swiglu_bwd_split_kernel(const float* __restrict__ d_act, const float* __restrict
       du[q] = d[q] * g[q] * s;
     }
     __nv_bfloat16* row = dh13_3 + (size_t)r * 6 * De;
-    st_split3_act(row, 2 * De, blk * 256 + off, dg);
-    st_split3_act(row, 2 * De, blk * 256 + 128 + off, du);
+    st_split3_act(row, 2 * De, blk * 2 * DM_GLU_BLOCK + off, dg);
+    st_split3_act(row, 2 * De, blk * 2 * DM_GLU_BLOCK + DM_GLU_BLOCK + off, du);
   }
 }
 
@@ -452,6 +452,7 @@ int dm_router_wgrad_sorted_f32(const float* x, const int32_t* src_token, const f
 
 int dm_swiglu_fwd_split(const float* h13, int rows, int De, void* act3, void* stream) {
   if (rows < 0 || De % 128 || De < 128) return set_error(DM_ERR_SHAPE, "swiglu_fwd_split: D_e %d not a multiple of 128", De);
+  static_assert(DM_GLU_BLOCK % 8 == 0 && 128 % DM_GLU_BLOCK == 0, "GLU block must tile 128 columns");
   if (rows == 0) return DM_OK;
   swiglu_fwd_split_kernel<<<grid_for((long long)rows * (De / 8), 256), 256, 0, (cudaStream_t)stream>>>(
       h13, rows, De, reinterpret_cast<__nv_bfloat16*>(act3));

@@ -129,15 +129,16 @@ __device__ __forceinline__ void epilogue_row(const TileInfo& ti, uint32_t trow, 
       for (int i = 0; i < 4; ++i) st_v4(out + c + 8 * i, o[i]);
     }
   } else if constexpr (EPI == EPI_SWIGLU_FWD) {
-    // Tile columns [0,128) are gate rows of W13, [128,256) the matching up rows.
+    // Tile columns alternate DM_GLU_BLOCK gate rows of W13 and the matching up rows.
     const long long row = ti.m0 + r;
     __nv_bfloat16* hout = a.aux + row * a.ld_aux + ti.n0;
     __nv_bfloat16* aout = reinterpret_cast<__nv_bfloat16*>(a.C) + row * a.ldc + (ti.n0 >> 1);
 #pragma unroll 1
-    for (int c = 0; c < GBN / 2; c += 16) {
+    for (int c = 0; c < GBN / 2; c += 16) {   // c: act column within the tile
+      const int gc = (c / DM_GLU_BLOCK) * 2 * DM_GLU_BLOCK + c % DM_GLU_BLOCK;
       uint32_t g[16], u[16];
-      tmem_ld16(trow + c, g);
-      tmem_ld16(trow + 128 + c, u);
+      tmem_ld16(trow + gc, g);
+      tmem_ld16(trow + gc + DM_GLU_BLOCK, u);
       tmem_wait_ld();
       int4 hg[2], hu[2], ao[2];
       uint32_t* hgp = reinterpret_cast<uint32_t*>(hg);
@@ -151,13 +152,13 @@ __device__ __forceinline__ void epilogue_row(const TileInfo& ti, uint32_t trow, 
         hup[i] = pack_bf16(u0, u1);
         aop[i] = pack_bf16(silu_f(g0) * u0, silu_f(g1) * u1);
       }
-      st_v4(hout + c, hg[0]);       st_v4(hout + c + 8, hg[1]);
-      st_v4(hout + 128 + c, hu[0]); st_v4(hout + 128 + c + 8, hu[1]);
-      st_v4(aout + c, ao[0]);       st_v4(aout + c + 8, ao[1]);
+      st_v4(hout + gc, hg[0]);                st_v4(hout + gc + 8, hg[1]);
+      st_v4(hout + gc + DM_GLU_BLOCK, hu[0]); st_v4(hout + gc + DM_GLU_BLOCK + 8, hu[1]);
+      st_v4(aout + c, ao[0]);                 st_v4(aout + c + 8, ao[1]);
     }
   } else if constexpr (EPI == EPI_SWIGLU_BWD) {
     // Accumulator = d_act for D_e columns [n0, n0+256); gate/up live in the
-    // 128-block-interleaved h13 layout: d -> (d/128)*256 + d%128 (+128 for up).
+    // DM_GLU_BLOCK-interleaved h13 layout: d -> (d/B)*2B + d%B (+B for up).
     const long long row = ti.m0 + r;
     const __nv_bfloat16* hin = a.aux_in + row * a.ld_aux_in;
     __nv_bfloat16* dhout = a.aux + row * a.ld_aux;
@@ -166,10 +167,10 @@ __device__ __forceinline__ void epilogue_row(const TileInfo& ti, uint32_t trow, 
       uint32_t d[16];
       tmem_ld16(trow + c, d);
       const int dcol = ti.n0 + c;
-      const long long gcol = (long long)(dcol >> 7) * 256 + (dcol & 127);
+      const long long gcol = (long long)(dcol / DM_GLU_BLOCK) * 2 * DM_GLU_BLOCK + dcol % DM_GLU_BLOCK;
       int4 gv[2], uv[2];
-      gv[0] = ld_v4(hin + gcol);       gv[1] = ld_v4(hin + gcol + 8);
-      uv[0] = ld_v4(hin + gcol + 128); uv[1] = ld_v4(hin + gcol + 136);
+      gv[0] = ld_v4(hin + gcol);                uv[0] = ld_v4(hin + gcol + DM_GLU_BLOCK);
+      gv[1] = ld_v4(hin + gcol + 8);            uv[1] = ld_v4(hin + gcol + DM_GLU_BLOCK + 8);
       tmem_wait_ld();
       const uint32_t* gp = reinterpret_cast<const uint32_t*>(gv);
       const uint32_t* up = reinterpret_cast<const uint32_t*>(uv);
@@ -192,8 +193,8 @@ __device__ __forceinline__ void epilogue_row(const TileInfo& ti, uint32_t trow, 
         dgp[i] = pack_bf16(rg[0], rg[1]);
         dup[i] = pack_bf16(ru[0], ru[1]);
       }
-      st_v4(dhout + gcol, dg[0]);       st_v4(dhout + gcol + 8, dg[1]);
-      st_v4(dhout + gcol + 128, du[0]); st_v4(dhout + gcol + 136, du[1]);
+      st_v4(dhout + gcol, dg[0]);                st_v4(dhout + gcol + 8, dg[1]);
+      st_v4(dhout + gcol + DM_GLU_BLOCK, du[0]); st_v4(dhout + gcol + DM_GLU_BLOCK + 8, du[1]);
     }
   } else {  // EPI_F32 (wgrad): C_g[m, n] = acc + beta * C_g[m, n]
     float* out = reinterpret_cast<float*>(a.C) + (long long)ti.g * a.c_group_stride +
@@ -492,13 +493,15 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
       }
     }
   } else if constexpr (EPI == EPI_SWIGLU_FWD) {
-    // accumulator columns [0,128) = gate rows of W13, [128,256) = the matching up rows
+    // accumulator columns alternate DM_GLU_BLOCK gate rows of W13 and the matching
+    // up rows; c walks the tile's 128 act columns in 64-column boxes
     const int row0 = ti.m0 + q * 32;
 #pragma unroll 1
     for (int c = 0; c < 128; c += 64) {
+      const int gc = (c / DM_GLU_BLOCK) * 2 * DM_GLU_BLOCK + c % DM_GLU_BLOCK;
       uint32_t g[64], u[64];
-      tmem_ld64(tacc + c, g);
-      tmem_ld64(tacc + 128 + c, u);
+      tmem_ld64(tacc + gc, g);
+      tmem_ld64(tacc + gc + DM_GLU_BLOCK, u);
       tmem_wait_ld();
       if (c > 0) {
         if (lane == 0) bulk_wait_read<0>();
@@ -515,25 +518,25 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(tmAux, stg, ti.n0 + c, row0);
-        tma_store_2d(tmAux, stg + BOX_BYTES, ti.n0 + 128 + c, row0);
+        tma_store_2d(tmAux, stg, ti.n0 + gc, row0);
+        tma_store_2d(tmAux, stg + BOX_BYTES, ti.n0 + gc + DM_GLU_BLOCK, row0);
         tma_store_2d(tmC, stg + 2 * BOX_BYTES, (ti.n0 >> 1) + c, row0);
         bulk_commit();
       }
     }
   } else if constexpr (EPI == EPI_SWIGLU_BWD) {
     // accumulator = d_act for D_e columns [n0, n0+256); g/u come from the
-    // 128-block-interleaved h13 (d -> (d/128)*256 + d%128, +128 for up)
+    // DM_GLU_BLOCK-interleaved h13 (d -> (d/B)*2B + d%B, +B for up)
     const int row0 = ti.m0 + q * 32;
     const uint32_t in_g = s0 + 2 * BOX_BYTES, in_u = s0 + 3 * BOX_BYTES;
     auto gcol_of = [&](int c) {
       const int dcol = ti.n0 + c * 64;
-      return (dcol >> 7) * 256 + (dcol & 127);
+      return (dcol / DM_GLU_BLOCK) * 2 * DM_GLU_BLOCK + dcol % DM_GLU_BLOCK;
     };
     if (lane == 0) {
       mbar_expect_tx(ibar, 2 * BOX_BYTES);
       tma_load_2d(stg + 2 * BOX_BYTES, tmIn, ibar, gcol_of(0), row0);
-      tma_load_2d(stg + 3 * BOX_BYTES, tmIn, ibar, gcol_of(0) + 128, row0);
+      tma_load_2d(stg + 3 * BOX_BYTES, tmIn, ibar, gcol_of(0) + DM_GLU_BLOCK, row0);
     }
 #pragma unroll 1
     for (int c = 0; c < 4; ++c) {
@@ -556,7 +559,7 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
         fence_proxy_async_smem();
         mbar_expect_tx(ibar, 2 * BOX_BYTES);
         tma_load_2d(stg + 2 * BOX_BYTES, tmIn, ibar, gcol_of(c + 1), row0);
-        tma_load_2d(stg + 3 * BOX_BYTES, tmIn, ibar, gcol_of(c + 1) + 128, row0);
+        tma_load_2d(stg + 3 * BOX_BYTES, tmIn, ibar, gcol_of(c + 1) + DM_GLU_BLOCK, row0);
       }
       // d[i] <- dg (bf16-pair packed later), reuse gu/uu for du
 #pragma unroll
@@ -587,7 +590,7 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
       __syncwarp();
       if (lane == 0) {
         tma_store_2d(tmAux, stg, gcol, row0);
-        tma_store_2d(tmAux, stg + BOX_BYTES, gcol + 128, row0);
+        tma_store_2d(tmAux, stg + BOX_BYTES, gcol + DM_GLU_BLOCK, row0);
         bulk_commit();
       }
     }

@@ -91,8 +91,8 @@ class MoEShape:
                    k=m.topk, De=m.moe_hidden)
 
 
-def interleave_w13(w1: torch.Tensor, w3: torch.Tensor, block: int = 128) -> torch.Tensor:
-    """[E, D_e, H] gate + up -> [E, 2*D_e, H] with 128-row gate/up blocks (dm_moe.h)."""
+def interleave_w13(w1: torch.Tensor, w3: torch.Tensor, block: int = _lib.DM_GLU_BLOCK) -> torch.Tensor:
+    """[E, D_e, H] gate + up -> [E, 2*D_e, H] with DM_GLU_BLOCK-row gate/up blocks (dm_moe.h)."""
     E, De, H = w1.shape
     out = torch.empty(E, 2 * De, H, dtype=w1.dtype, device=w1.device)
     v = out.view(E, De // block, 2, block, H)
@@ -101,7 +101,7 @@ def interleave_w13(w1: torch.Tensor, w3: torch.Tensor, block: int = 128) -> torc
     return out
 
 
-def split_w13(w13: torch.Tensor, block: int = 128) -> tuple[torch.Tensor, torch.Tensor]:
+def split_w13(w13: torch.Tensor, block: int = _lib.DM_GLU_BLOCK) -> tuple[torch.Tensor, torch.Tensor]:
     E, two_de, H = w13.shape
     v = w13.view(E, two_de // (2 * block), 2, block, H)
     return v[:, :, 0].reshape(E, two_de // 2, H), v[:, :, 1].reshape(E, two_de // 2, H)

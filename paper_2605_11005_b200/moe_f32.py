@@ -26,7 +26,7 @@ BF16, F32, I32 = torch.bfloat16, torch.float32, torch.int32
 
 
 class ExpertParamsF32:
-    """fp32 master weights W13 [E, 2D_e, H] (128-row gate/up blocks) and W2 [E, H, D_e],
+    """fp32 master weights W13 [E, 2D_e, H] (DM_GLU_BLOCK-row gate/up blocks) and W2 [E, H, D_e],
     their fp32 gradients, and the split-3 bf16 copies the GEMMs read (refreshed by
     `prepare()` after every weight update)."""
 

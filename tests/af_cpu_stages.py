@@ -21,18 +21,21 @@ def _silu(g):
     return g / (1 + torch.exp(-g))
 
 
+B = 64   # DM_GLU_BLOCK: gate/up column interleave of h13 / dh13
+
+
 def _split(h: torch.Tensor):
     R, two = h.shape
-    v = h.view(R, two // 256, 2, 128)
+    v = h.view(R, two // (2 * B), 2, B)
     return v[:, :, 0].reshape(R, two // 2), v[:, :, 1].reshape(R, two // 2)
 
 
 def _join(g: torch.Tensor, u: torch.Tensor) -> torch.Tensor:
     R, De = g.shape
     out = torch.empty(R, 2 * De, dtype=g.dtype)
-    v = out.view(R, De // 128, 2, 128)
-    v[:, :, 0] = g.view(R, De // 128, 128)
-    v[:, :, 1] = u.view(R, De // 128, 128)
+    v = out.view(R, De // B, 2, B)
+    v[:, :, 0] = g.view(R, De // B, B)
+    v[:, :, 1] = u.view(R, De // B, B)
     return out
 
 

@@ -127,7 +127,8 @@ def check_against_oracle(outs, n_streams, layers, tol=1e-2):
                 assert O.normwise_rel_err(o["dwg"][l], acc[l]["dwg"]) < tol  # all-reduced over the A group
             else:
                 lo, hi = o["lo"], o["hi"]
-                v = o["dw13"][l].reshape(hi - lo, DE // 128, 2, 128, H)
+                G = 64   # DM_GLU_BLOCK
+                v = o["dw13"][l].reshape(hi - lo, DE // G, 2, G, H)
                 g1 = v[:, :, 0].reshape(hi - lo, DE, H)
                 g3 = v[:, :, 1].reshape(hi - lo, DE, H)
                 assert O.normwise_rel_err(g1, acc[l]["dw1"][lo:hi]) < tol
