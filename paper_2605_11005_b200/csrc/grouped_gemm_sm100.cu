@@ -52,6 +52,10 @@ struct GemmArgs {
   const int* seg_off;
   int nseg;
   int seg_stride_rows;
+  // diagnostic only (env DM_GEMM_DIAG=1, results invalid): load the A tile of the
+  // first k-block of every tile only, so the mainloop streams half the bytes. Used to
+  // tell operand-supply-bound from MMA-bound mainloops; never set on the product path.
+  int diag_skip_a;
   // optional instrumentation (dm_debug_gemm_profile): u64 cycle counters
   // [0] producer waits on empty, [1] MMA waits on tempty, [2] MMA waits on full,
   // [3] epilogue waits on tfull (lane 0 of each epilogue warp), [4] CTA lifetime
@@ -71,6 +75,7 @@ struct GemmArgs {
 
 struct TileInfo {
   int g, m0, n0, kb_count, row_base;
+  int half;   // 2-SM ragged-M tail tile with 128 valid rows: M = 128 MMA, 64 rows per CTA
 };
 
 template <int RAGGED_K>
@@ -83,6 +88,7 @@ __device__ __forceinline__ TileInfo decode_tile(int t, const int* tile_start, co
   }
   TileInfo ti;
   ti.g = lo;
+  ti.half = 0;
   const int local = t - tile_start[lo];
   const int row_off = RAGGED_K ? 0 : off[lo];
   const int rows = RAGGED_K ? 0 : off[lo + 1] - row_off;
@@ -415,15 +421,21 @@ __device__ __forceinline__ TileInfo decode_tile_2sm(int t, const int* tile_start
   TileInfo ti;
   ti.g = lo;
   const int local = t - tile_start[lo];
+  ti.half = 0;
   if (!RAGGED_K) {
     const int row_off = off[lo];
     const int rows = off[lo + 1] - row_off;
     const int mt = (rows + 255) / 256;
-    ti.m0 = row_off + (local % mt) * 256 + 128 * rank;   // this CTA's first row
+    const int tm0 = row_off + (local % mt) * 256;
+    // Groups are 128-row aligned, so a tile has 256 or (the group's tail) 128 valid
+    // rows. A tail tile runs as an M = 128 pair MMA (64 rows per CTA) instead of an
+    // M = 256 MMA with an idle half: the padding-to-256 MMA work disappears.
+    ti.half = (row_off + rows - tm0) <= 128;
+    ti.m0 = tm0 + (ti.half ? 64 : 128) * (int)rank;   // this CTA's first row
     ti.n0 = (local / mt) * GBN;
     ti.kb_count = a.K / GBK;
     ti.row_base = row_off;
-    active = ti.m0 < row_off + rows;
+    active = true;
   } else {
     // Rasterise along the smaller output dimension so concurrent tiles share the
     // larger operand's tile (streamed once) while the smaller operand stays in L2:
@@ -467,16 +479,25 @@ __device__ __forceinline__ void box_row_bf16(uint32_t box, int lane, const uint3
 // Epilogue of one epilogue warp (TMEM lane quarter q = rows q*32 .. q*32+31 of
 // this CTA's 128-row half). `stg` is the warp's private staging area; only lane 0
 // issues TMA and owns the bulk groups.
+//
+// TMEM geometry of the warp's accumulator slice. Full tiles (M = 256 pair MMA): lane =
+// row, all 256 columns. Half tiles (M = 128 pair MMA, 64 rows per CTA): the "2x2"
+// data-path layout, lanes 0-63 hold rows 0-63 x tile columns [0,128) and lanes 64-127
+// the same rows x columns [128,256), both at TMEM columns [0,128); so warp q drains
+// rows (q&1)*32.. of the 128-column half (q>>1) — each warp still owns whole SwiGLU
+// pairs because gate/up blocks are DM_GLU_BLOCK = 64 wide.
 template <int EPI>
 __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, int q, int lane,
                                              const GemmArgs& a, const CUtensorMap* tmC,
                                              const CUtensorMap* tmAux, const CUtensorMap* tmIn,
                                              uint8_t* stg, uint64_t* ibar, uint32_t& iphase) {
   const uint32_t s0 = smem_u32(stg);
+  const int row0 = ti.m0 + (ti.half ? (q & 1) : q) * 32;   // first row of this warp
+  const int col0 = ti.n0 + (ti.half ? (q >> 1) * 128 : 0);  // first tile column it holds
+  const int ncols = ti.half ? 128 : GBN;
   if constexpr (EPI == EPI_BF16) {
-    const int row0 = ti.m0 + q * 32;
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < ncols / 64; ++c) {
       uint32_t v[64];
       tmem_ld64(tacc + c * 64, v);
       tmem_wait_ld();
@@ -488,16 +509,15 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(tmC, stg + (c & 1) * BOX_BYTES, ti.n0 + c * 64, row0);
+        tma_store_2d(tmC, stg + (c & 1) * BOX_BYTES, col0 + c * 64, row0);
         bulk_commit();
       }
     }
   } else if constexpr (EPI == EPI_SWIGLU_FWD) {
     // accumulator columns alternate DM_GLU_BLOCK gate rows of W13 and the matching
-    // up rows; c walks the tile's 128 act columns in 64-column boxes
-    const int row0 = ti.m0 + q * 32;
+    // up rows; c walks the warp's act columns (ncols / 2) in 64-column boxes
 #pragma unroll 1
-    for (int c = 0; c < 128; c += 64) {
+    for (int c = 0; c < ncols / 2; c += 64) {
       const int gc = (c / DM_GLU_BLOCK) * 2 * DM_GLU_BLOCK + c % DM_GLU_BLOCK;
       uint32_t g[64], u[64];
       tmem_ld64(tacc + gc, g);
@@ -518,19 +538,19 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(tmAux, stg, ti.n0 + gc, row0);
-        tma_store_2d(tmAux, stg + BOX_BYTES, ti.n0 + gc + DM_GLU_BLOCK, row0);
-        tma_store_2d(tmC, stg + 2 * BOX_BYTES, (ti.n0 >> 1) + c, row0);
+        tma_store_2d(tmAux, stg, col0 + gc, row0);
+        tma_store_2d(tmAux, stg + BOX_BYTES, col0 + gc + DM_GLU_BLOCK, row0);
+        tma_store_2d(tmC, stg + 2 * BOX_BYTES, (col0 >> 1) + c, row0);
         bulk_commit();
       }
     }
   } else if constexpr (EPI == EPI_SWIGLU_BWD) {
-    // accumulator = d_act for D_e columns [n0, n0+256); g/u come from the
-    // DM_GLU_BLOCK-interleaved h13 (d -> (d/B)*2B + d%B, +B for up)
-    const int row0 = ti.m0 + q * 32;
+    // accumulator = d_act for this warp's D_e columns [col0, col0 + ncols); g/u come
+    // from the DM_GLU_BLOCK-interleaved h13 (d -> (d/B)*2B + d%B, +B for up)
+    const int nch = ncols / 64;
     const uint32_t in_g = s0 + 2 * BOX_BYTES, in_u = s0 + 3 * BOX_BYTES;
     auto gcol_of = [&](int c) {
-      const int dcol = ti.n0 + c * 64;
+      const int dcol = col0 + c * 64;
       return (dcol / DM_GLU_BLOCK) * 2 * DM_GLU_BLOCK + dcol % DM_GLU_BLOCK;
     };
     if (lane == 0) {
@@ -539,7 +559,7 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
       tma_load_2d(stg + 3 * BOX_BYTES, tmIn, ibar, gcol_of(0) + DM_GLU_BLOCK, row0);
     }
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < nch; ++c) {
       const int gcol = gcol_of(c);
       uint32_t d[64];
       tmem_ld64(tacc + c * 64, d);
@@ -555,7 +575,7 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
       }
       tmem_wait_ld();
       __syncwarp();
-      if (c + 1 < 4 && lane == 0) {  // inputs consumed: prefetch the next chunk's g/u
+      if (c + 1 < nch && lane == 0) {  // inputs consumed: prefetch the next chunk's g/u
         fence_proxy_async_smem();
         mbar_expect_tx(ibar, 2 * BOX_BYTES);
         tma_load_2d(stg + 2 * BOX_BYTES, tmIn, ibar, gcol_of(c + 1), row0);
@@ -594,12 +614,13 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
         bulk_commit();
       }
     }
-  } else {  // EPI_F32: dW_g rows (g*M + m) of a [G*M, N] fp32 matrix; beta in {0, 1}
-    const int grow0 = ti.g * a.M + ti.m0 + q * 32;
+  } else {  // EPI_F32: dW_g rows (g*M + m) of a [G*M, N] fp32 matrix (ragged K, a.M > 0) or
+            // C rows m (ragged M, a.M = 0); beta in {0, 1}
+    const int grow0 = ti.g * a.M + row0;
     const bool empty = ti.kb_count == 0;
     if (empty && a.beta != 0.0f) return;  // adding zeros
 #pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < ncols / 32; ++c) {
       uint32_t v[32];
       if (!empty) {
         tmem_ld16(tacc + c * 32, *reinterpret_cast<uint32_t(*)[16]>(v));
@@ -619,8 +640,8 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (a.beta != 0.0f) tma_reduce_add_2d(tmC, stg + (c & 1) * BOX_BYTES, ti.n0 + c * 32, grow0);
-        else tma_store_2d(tmC, stg + (c & 1) * BOX_BYTES, ti.n0 + c * 32, grow0);
+        if (a.beta != 0.0f) tma_reduce_add_2d(tmC, stg + (c & 1) * BOX_BYTES, col0 + c * 32, grow0);
+        else tma_store_2d(tmC, stg + (c & 1) * BOX_BYTES, col0 + c * 32, grow0);
         bulk_commit();
       }
     }
@@ -719,10 +740,12 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
             kcoord = kb * GBK;
           }
           DM_PROF_WAIT(0, mbar_wait(&empty[stage], phase ^ 1));
-          if (leader) mbar_expect_tx(&full[stage], 2 * (G2_A_BYTES + G2_B_BYTES));
+          const bool load_a = !args.diag_skip_a || kb < STAGES;
+          if (leader) mbar_expect_tx(&full[stage], 2 * ((load_a ? G2_A_BYTES : 0) + G2_B_BYTES));
           uint8_t* a_dst = sA + stage * G2_A_BYTES;
           uint8_t* b_dst = sB + stage * G2_B_BYTES;
-          if (!A_MN) {
+          if (!load_a) {
+          } else if (!A_MN) {
             tma_load_2d_2sm(a_dst, &tmA, &full[stage], kcoord, ti.m0, pol_a);
           } else {
             tma_load_2d_2sm(a_dst, &tmA, &full[stage], ti.m0, kcoord, pol_a);
@@ -742,7 +765,8 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader)
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(256, GBN, A_MN, B_MN);
+      constexpr uint32_t idesc_full = make_idesc_bf16(256, GBN, A_MN, B_MN);
+      constexpr uint32_t idesc_half = make_idesc_bf16(128, GBN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -754,6 +778,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
         DM_PROF_WAIT(1, mbar_wait(&tempty[as], aphase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * GBN;
+        const uint32_t idesc = ti.half ? idesc_half : idesc_full;
         for (int kb = 0; kb < ti.kb_count; ++kb) {
           DM_PROF_WAIT(2, mbar_wait(&full[stage], phase));
           tc_fence_after();
@@ -906,6 +931,12 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const EpiTe
     grid &= ~1;
     GemmArgs a2 = args;
     a2.prof = g_gemm_prof;
+    static int diag = -1;
+    if (diag < 0) {
+      const char* e = getenv("DM_GEMM_DIAG");
+      diag = (e && e[0] == '1') ? 1 : 0;
+    }
+    a2.diag_skip_a = diag;
     kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, tc, tx, ti, a2);
   } else {
     auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
