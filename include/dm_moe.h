@@ -233,7 +233,7 @@ DM_API int dm_permute_bwd_f32(const float* dx_perm, const int32_t* row_map, cons
                               float* dx, void* stream);
 DM_API int dm_router_wgrad_sorted_f32(const float* x, const int32_t* src_token, const float* dl_perm,
                                       const int32_t* counts, const int32_t* pad_off, int T, int H, int E,
-                                      float* dwg, float beta, void* stream);
+                                      float* partial_ws, float* dwg, float beta, void* stream);
 /* act3 [rows, 3De] = split-3(silu(gate) * up) of fp32 h13 [rows, 2De] (DM_GLU_BLOCK interleave). */
 DM_API int dm_swiglu_fwd_split(const float* h13, int rows, int De, void* act3, void* stream);
 /* dh13_3 [rows, 6De] = split-3 of the SwiGLU backward of fp32 d_act [rows, De]. */

@@ -75,7 +75,7 @@ SIGNATURES: dict[str, tuple] = {
     "dm_combine_bwd_f32": (_i, [_f32p, _f32p, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _i, _vp, _f32p,
                                 _f32p, _f32p, _vp]),
     "dm_permute_bwd_f32": (_i, [_f32p, _i32p, _i32p, _f32p, _f32p, _i, _i, _i, _i, _f32p, _f32p, _vp]),
-    "dm_router_wgrad_sorted_f32": (_i, [_f32p, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _f32p, _f, _vp]),
+    "dm_router_wgrad_sorted_f32": (_i, [_f32p, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _f32p, _f32p, _f, _vp]),
     "dm_swiglu_fwd_split": (_i, [_f32p, _i, _i, _vp, _vp]),
     "dm_swiglu_bwd_split": (_i, [_f32p, _f32p, _i, _i, _vp, _vp]),
     "dm_split3": (_i, [_f32p, _i, _i, _i, _i, _vp, _vp]),

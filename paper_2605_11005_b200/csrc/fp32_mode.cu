@@ -251,17 +251,23 @@ permute_bwd_f32_kernel(const float* __restrict__ dx_perm, const int32_t* __restr
   }
 }
 
-// dW_g[e,:] = sum over expert e's permuted rows r (ascending) of dl_perm[r] * x[src_token[r], :]
+// dW_g[e,:] = sum over expert e's permuted rows r (ascending) of dl_perm[r] * x[src_token[r], :];
+// with nseg > 1 each (expert, row segment) writes a partial reduced in segment order by
+// router_wgrad_reduce_f32_kernel (deterministic), as in combine.cu's bf16 version.
 __global__ void __launch_bounds__(128)
 router_wgrad_sorted_f32_kernel(const float* __restrict__ x, const int32_t* __restrict__ src_token,
                                const float* __restrict__ dl_perm, const int32_t* __restrict__ counts,
-                               const int32_t* __restrict__ pad_off, int H, float* __restrict__ dwg, float beta) {
-  const int e = blockIdx.y;
+                               const int32_t* __restrict__ pad_off, int H, int E, int nseg,
+                               float* __restrict__ partial, float* __restrict__ dwg, float beta) {
+  const int e = blockIdx.y, seg = blockIdx.z;
   const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (col >= H) return;
-  const int beg = pad_off[e], n = counts[e];
+  const int n = counts[e];
+  const int r0 = pad_off[e] + (int)((long long)n * seg / nseg);
+  const int r1 = pad_off[e] + (int)((long long)n * (seg + 1) / nseg);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int r = beg; r < beg + n; ++r) {
+#pragma unroll 4
+  for (int r = r0; r < r1; ++r) {
     const float d = dl_perm[r];
     const float4 v = __ldg(reinterpret_cast<const float4*>(x + (size_t)src_token[r] * H + col));
     acc.x = __fmaf_rn(d, v.x, acc.x);
@@ -269,12 +275,35 @@ router_wgrad_sorted_f32_kernel(const float* __restrict__ x, const int32_t* __res
     acc.z = __fmaf_rn(d, v.z, acc.z);
     acc.w = __fmaf_rn(d, v.w, acc.w);
   }
+  if (nseg > 1) {
+    *reinterpret_cast<float4*>(partial + ((size_t)seg * E + e) * H + col) = acc;
+    return;
+  }
   float4* o = reinterpret_cast<float4*>(dwg + (size_t)e * H + col);
   if (beta != 0.0f) {
     const float4 p = *o;
     acc.x += beta * p.x; acc.y += beta * p.y; acc.z += beta * p.z; acc.w += beta * p.w;
   }
   *o = acc;
+}
+
+__global__ void router_wgrad_reduce_f32_kernel(const float* __restrict__ partial, int nseg, size_t EH,
+                                               float* __restrict__ dwg, float beta) {
+  for (size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < EH;
+       i += (size_t)gridDim.x * blockDim.x * 4) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int q = 0; q < nseg; ++q) {
+      const float4 v = *reinterpret_cast<const float4*>(partial + (size_t)q * EH + i);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    float4* o = reinterpret_cast<float4*>(dwg + i);
+    if (beta != 0.0f) {
+      const float4 old = *o;
+      s.x += beta * old.x; s.y += beta * old.y; s.z += beta * old.z; s.w += beta * old.w;
+    }
+    *o = s;
+  }
 }
 
 // ------------------------------------------------------------------ SwiGLU
@@ -441,13 +470,26 @@ int dm_permute_bwd_f32(const float* dx_perm, const int32_t* row_map, const int32
 }
 
 int dm_router_wgrad_sorted_f32(const float* x, const int32_t* src_token, const float* dl_perm,
-                               const int32_t* counts, const int32_t* pad_off, int T, int H, int E, float* dwg,
-                               float beta, void* stream) {
+                               const int32_t* counts, const int32_t* pad_off, int T, int H, int E,
+                               float* partial_ws, float* dwg, float beta, void* stream) {
   if (T < 1 || H % 8 || E < 1 || E > DM_MAX_EXPERTS) return set_error(DM_ERR_SHAPE, "router_wgrad_sorted_f32 bad shape");
-  dim3 grid((H / 4 + 127) / 128, E);
-  router_wgrad_sorted_f32_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(x, src_token, dl_perm, counts, pad_off, H,
-                                                                         dwg, beta);
-  return finish("router_wgrad_sorted_f32 launch");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int gx = (H / 4 + 127) / 128;
+  int nseg = 1;
+  if (partial_ws) {
+    const int tbt = dm_router_wgrad_token_block(E);
+    const int cap_seg = (T + tbt - 1) / tbt;
+    nseg = (4 * num_sms_current() + gx * E - 1) / (gx * E);
+    if (nseg > cap_seg) nseg = cap_seg;
+    if (nseg < 1) nseg = 1;
+  }
+  router_wgrad_sorted_f32_kernel<<<dim3(gx, E, nseg), 128, 0, st>>>(x, src_token, dl_perm, counts, pad_off, H, E,
+                                                                     nseg, partial_ws, dwg, beta);
+  int rc = finish("router_wgrad_sorted_f32 launch");
+  if (rc || nseg == 1) return rc;
+  const size_t EH = (size_t)E * H;
+  router_wgrad_reduce_f32_kernel<<<grid_for((long long)(EH / 4), 64), 64, 0, st>>>(partial_ws, nseg, EH, dwg, beta);
+  return finish("router_wgrad_reduce_f32 launch");
 }
 
 int dm_swiglu_fwd_split(const float* h13, int rows, int De, void* act3, void* stream) {

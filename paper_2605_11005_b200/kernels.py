@@ -249,11 +249,11 @@ def permute_bwd_f32(dx_perm, row_map, idx, dlogit, wg, dx, stream=None, resid=No
               _ptr(resid), _ptr(dx), _stream(stream))
 
 
-def router_wgrad_sorted_f32(x, src_token, dl_perm, counts, pad_off, dwg, beta=0.0, stream=None):
+def router_wgrad_sorted_f32(x, src_token, dl_perm, counts, pad_off, dwg, beta=0.0, stream=None, partial_ws=None):
     T, H = x.shape
     E = dwg.shape[0]
     _lib.call("dm_router_wgrad_sorted_f32", _ptr(x), _ptr(src_token), _ptr(dl_perm), _ptr(counts), _ptr(pad_off),
-              T, H, E, _ptr(dwg), float(beta), _stream(stream))
+              T, H, E, _ptr(partial_ws), _ptr(dwg), float(beta), _stream(stream))
 
 
 def swiglu_fwd_split(h13, act3, stream=None):

@@ -92,6 +92,7 @@ class BuffersF32:
         self.src = z(slab.cap, dt=I32)
         self.dl_perm = z(slab.cap)
         self.route_ws = z(_lib.route_workspace_size(s.T, s.H, s.E, s.k), dt=torch.uint8)
+        self.wgrad_ws = z(_lib.router_wgrad_workspace_size(s.T, s.H, s.E) // 4)
         self.pad_off = slab.pad_off[index]
         r = slab.rows(index)
         for name in ("x3", "h13", "act3", "y_perm", "dy3", "d_act", "dh13_3", "dx_perm"):
@@ -158,7 +159,7 @@ class MoELayerF32:
 
     def stage_router_wgrad(self, b: BuffersF32, accumulate: bool, stream=None) -> None:
         K.router_wgrad_sorted_f32(b.x, b.src, b.dl_perm, b.counts, b.pad_off, self.dwg,
-                                  1.0 if accumulate else 0.0, stream)
+                                  1.0 if accumulate else 0.0, stream, partial_ws=b.wgrad_ws)
 
     def forward(self, b: BuffersF32, stream=None) -> None:
         self.stage_dispatch(b, stream)
