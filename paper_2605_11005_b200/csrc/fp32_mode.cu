@@ -61,6 +61,7 @@ __device__ __forceinline__ void st_split3_act(__nv_bfloat16* row, int K, int c, 
 // the 8-element chunks c = p mod 32, even/odd element chains, xor butterfly).
 // Warp per token, W_g rows of an expert block staged in smem.
 constexpr int RF_WARPS = 8;
+constexpr int RF_EB = 8;    // experts per register block (each x chunk is loaded once per block)
 
 __global__ void __launch_bounds__(RF_WARPS * 32)
 router_logits_f32_kernel(const float* __restrict__ x, const float* __restrict__ wg, float* __restrict__ logits,
@@ -77,18 +78,28 @@ router_logits_f32_kernel(const float* __restrict__ x, const float* __restrict__ 
     __syncthreads();
     for (int t = blockIdx.x * RF_WARPS + warp; t < T; t += gridDim.x * RF_WARPS) {
       const float* xr = x + (size_t)t * H;
-      for (int e = 0; e < ecur; ++e) {
-        float2 acc = make_float2(0.f, 0.f);
+      for (int eb = 0; eb < ecur; eb += RF_EB) {
+        float2 acc[RF_EB];
+#pragma unroll
+        for (int e = 0; e < RF_EB; ++e) acc[e] = make_float2(0.f, 0.f);
         for (int c = lane; c < nch; c += 32) {
           float xv[8];
           ld8(xr + c * 8, xv);
-          const float* wr = sw + (size_t)e * H + c * 8;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc = ffma2(make_float2(xv[2 * i], xv[2 * i + 1]),
-                                                   make_float2(wr[2 * i], wr[2 * i + 1]), acc);
+          for (int e = 0; e < RF_EB; ++e) {
+            if (eb + e < ecur) {
+              const float* wr = sw + (size_t)(eb + e) * H + c * 8;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) acc[e] = ffma2(make_float2(xv[2 * i], xv[2 * i + 1]),
+                                                          make_float2(wr[2 * i], wr[2 * i + 1]), acc[e]);
+            }
+          }
         }
-        const float v = warp_sum_butterfly(__fadd_rn(acc.x, acc.y));
-        if (lane == 0) logits[(size_t)t * E + e0 + e] = v;
+#pragma unroll
+        for (int e = 0; e < RF_EB; ++e) {
+          const float v = warp_sum_butterfly(__fadd_rn(acc[e].x, acc[e].y));
+          if (lane == 0 && eb + e < ecur) logits[(size_t)t * E + e0 + eb + e] = v;
+        }
       }
     }
   }

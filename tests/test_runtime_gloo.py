@@ -139,6 +139,7 @@ def check_against_oracle(outs, n_streams, layers, tol=1e-2):
 @pytest.mark.parametrize("world,n_attn,layers,depth", [
     (2, 1, 1, 1), (3, 1, 1, 1), (3, 2, 1, 1), (4, 2, 1, 1), (2, 1, 2, 1), (3, 1, 3, 1),
     (4, 2, 2, 2), (4, 2, 4, 2),   # pipeline_depth 2: layers alternate between two A+F groups
+    (8, 4, 1, 1), (8, 4, 2, 2),   # the 8-GPU 4A:4F split of BASELINE configs[1] (protocol on CPU)
 ])
 def test_afpipe_runtime_matches_oracle(world, n_attn, layers, depth):
     with tempfile.TemporaryDirectory() as d:
