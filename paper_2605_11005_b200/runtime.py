@@ -45,7 +45,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .afpipe import COMPUTE, RECV, SEND, LayerDurations, issue_order, plan_layer
+from .afpipe import COMPUTE, SEND, LayerDurations, issue_order, plan_layer
 from .moe import ActivationSlab, ExpertParams, MicroBatchBuffers, MoEShape, RouterParams, link_residual_stack
 
 BF16, F32, I32 = torch.bfloat16, torch.float32, torch.int32
