@@ -56,6 +56,8 @@ struct GemmArgs {
   // first k-block of every tile only, so the mainloop streams half the bytes. Used to
   // tell operand-supply-bound from MMA-bound mainloops; never set on the product path.
   int diag_skip_a;
+  // 1: warp 0 streams A and warp 3 streams B (two issuers); 0: warp 0 issues both
+  int dual_producer;
   // optional instrumentation (dm_debug_gemm_profile): u64 cycle counters
   // [0] producer waits on empty, [1] MMA waits on tempty, [2] MMA waits on full,
   // [3] epilogue waits on tfull (lane 0 of each epilogue warp), [4] CTA lifetime
@@ -709,13 +711,18 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = s_tile[G];
 
-  if (warp == 0) {
-    // ------------------------------------------- TMA producer (both CTAs)
+  if (warp == 0 || (warp == 3 && args.dual_producer)) {
+    // ------------------------------------------- TMA producers (both CTAs)
+    // warp 0 streams the A operand, warp 3 the B operand: two independent issuing
+    // threads per CTA (the MN-major wgrad operands need two 64-column boxes each and a
+    // single issuer starved the MMA). Both walk the same tile/k schedule and ring; the
+    // A producer posts the stage's expected bytes (complete_tx may land first).
     if (lane == 0) {
       // L2 policy: evict-last/evict-first hints on the re-read/streamed operand
       // were measured slower than the default policy on every variant.
-      const uint64_t pol_a = L2_EVICT_NORMAL;
-      const uint64_t pol_b = L2_EVICT_NORMAL;
+      const uint64_t pol = L2_EVICT_NORMAL;
+      const bool is_a = warp == 0;
+      const bool do_a = is_a, do_b = !is_a || !args.dual_producer;
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
@@ -739,23 +746,28 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
           } else {
             kcoord = kb * GBK;
           }
-          DM_PROF_WAIT(0, mbar_wait(&empty[stage], phase ^ 1));
+          if (is_a) DM_PROF_WAIT(0, mbar_wait(&empty[stage], phase ^ 1));
+          else mbar_wait(&empty[stage], phase ^ 1);
           const bool load_a = !args.diag_skip_a || kb < STAGES;
-          if (leader) mbar_expect_tx(&full[stage], 2 * ((load_a ? G2_A_BYTES : 0) + G2_B_BYTES));
-          uint8_t* a_dst = sA + stage * G2_A_BYTES;
-          uint8_t* b_dst = sB + stage * G2_B_BYTES;
-          if (!load_a) {
-          } else if (!A_MN) {
-            tma_load_2d_2sm(a_dst, &tmA, &full[stage], kcoord, ti.m0, pol_a);
-          } else {
-            tma_load_2d_2sm(a_dst, &tmA, &full[stage], ti.m0, kcoord, pol_a);
-            tma_load_2d_2sm(a_dst + 8192, &tmA, &full[stage], ti.m0 + 64, kcoord, pol_a);
+          if (do_a) {
+            if (leader) mbar_expect_tx(&full[stage], 2 * ((load_a ? G2_A_BYTES : 0) + G2_B_BYTES));
+            uint8_t* a_dst = sA + stage * G2_A_BYTES;
+            if (!load_a) {
+            } else if (!A_MN) {
+              tma_load_2d_2sm(a_dst, &tmA, &full[stage], kcoord, ti.m0, pol);
+            } else {
+              tma_load_2d_2sm(a_dst, &tmA, &full[stage], ti.m0, kcoord, pol);
+              tma_load_2d_2sm(a_dst + 8192, &tmA, &full[stage], ti.m0 + 64, kcoord, pol);
+            }
           }
-          if (!B_MN) {
-            tma_load_2d_2sm(b_dst, &tmB, &full[stage], kcoord, b_gofs + nb0, pol_b);
-          } else {
-            tma_load_2d_2sm(b_dst, &tmB, &full[stage], nb0, b_gofs + kcoord, pol_b);
-            tma_load_2d_2sm(b_dst + 8192, &tmB, &full[stage], nb0 + 64, b_gofs + kcoord, pol_b);
+          if (do_b) {
+            uint8_t* b_dst = sB + stage * G2_B_BYTES;
+            if (!B_MN) {
+              tma_load_2d_2sm(b_dst, &tmB, &full[stage], kcoord, b_gofs + nb0, pol);
+            } else {
+              tma_load_2d_2sm(b_dst, &tmB, &full[stage], nb0, b_gofs + kcoord, pol);
+              tma_load_2d_2sm(b_dst + 8192, &tmB, &full[stage], nb0 + 64, b_gofs + kcoord, pol);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -937,6 +949,12 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const EpiTe
       diag = (e && e[0] == '1') ? 1 : 0;
     }
     a2.diag_skip_a = diag;
+    static int dual = -1;
+    if (dual < 0) {
+      const char* e = getenv("DM_GEMM_DUAL");
+      dual = (e && e[0] == '0') ? 0 : 1;
+    }
+    a2.dual_producer = dual;
     kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, tc, tx, ti, a2);
   } else {
     auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;

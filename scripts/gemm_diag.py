@@ -27,13 +27,19 @@ def main(E=8, rows_per=1024, H=4096, De=14336):
     dh13 = torch.empty_like(h13)
     dx = torch.empty_like(y)
     flops = 2 * cap * H * De
+    so4 = torch.stack([po] * 4)  # 4 micro-batches stacked (deferred wgrad shape)
+    x4, act4, y4, dh4 = (t.repeat(4, 1) for t in (x, act, y, dh13))
+    dW2 = torch.empty(E, H, De, device=dev)
+    dW13 = torch.empty(E, 2 * De, H, device=dev)
     ops = {
         "w13_fwd": (lambda: K.w13_swiglu_fwd(x, w13, po, h13, act), 2 * flops),
         "w2_fwd": (lambda: K.w2_fwd(act, w2, po, y), flops),
         "w2_dgrad": (lambda: K.w2_dgrad_swiglu_bwd(y, w2, h13, po, dh13), flops),
         "w13_dgrad": (lambda: K.w13_dgrad(dh13, w13, po, dx), 2 * flops),
+        "wgrad2_x4": (lambda: K.wgrad(y4, act4, so4, dW2), 4 * flops),
+        "wgrad13_x4": (lambda: K.wgrad(dh4, x4, so4, dW13), 8 * flops),
     }
-    out = {"diag": os.environ.get("DM_GEMM_DIAG", "0")}
+    out = {"diag": os.environ.get("DM_GEMM_DIAG", "0"), "dual": os.environ.get("DM_GEMM_DUAL", "1")}
     for name, (fn, fl) in ops.items():
         for _ in range(3):
             fn()
@@ -50,4 +56,7 @@ def main(E=8, rows_per=1024, H=4096, De=14336):
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "dsv3":
+        main(E=256, rows_per=128, H=7168, De=2048)
+    else:
+        main()

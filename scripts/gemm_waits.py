@@ -61,4 +61,7 @@ def main(E=8, rows_per=1024, H=4096, De=14336):
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "dsv3":   # E=256 experts of ~128 rows, H=7168, D_e=2048
+        main(E=256, rows_per=128, H=7168, De=2048)
+    else:
+        main()
