@@ -624,6 +624,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
             "link": {"mean_GB/s": round(statistics.mean(link), 1) if link else None,
                      "max_GB/s": round(max(link), 1) if link else None,
                      "peak_GB/s": 900.0, "note": "bytes / (data ready -> send complete), per transfer group"},
+            "reference_model": _reference_model(exp, topo, shape, mb, L, f_flops, link, peaks, achieved),
             "gpu_launches": int(lsum.item()),
             "clocks": clocks,
             "memory": {
@@ -678,6 +679,29 @@ def isolated_stage_ms(fns: dict, dev, reps: int = 10) -> dict:
                 fn()
         out[name] = max(timed(g) - base, 1e-6) / reps
     return out
+
+
+def _reference_model(exp, topo, shape, mb, L, f_flops, link, peaks, achieved_tf):
+    """The reference's analytic roofline (costs.py:117-144) next to the measured figures:
+    intensities, the NVLink turning points for this A:F split, the attainable FFN
+    throughput at the measured link bandwidth, and this run's FFN FLOPs per exchanged byte."""
+    from paper_2605_11005_b200.profile import reference_intensities, reference_turning_points, roofline_attainable
+
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * 1e12
+    link_bw = (statistics.mean(link) if link else 900.0) * 1e9
+    i_attn, i_ffn = reference_intensities(exp)
+    i_hat, i_attn_eff, i_ffn_eff = reference_turning_points(peak, link_bw, topo.n_attn, topo.n_ffn)
+    moved = 4 * shape.T * shape.k * shape.H * exp.model.bytes_per_element * mb * L * topo.streams
+    return {
+        "I_attn": round(i_attn, 1), "I_ffn": round(i_ffn, 1),
+        "turning_point_system": round(i_hat, 1), "turning_point_ffn_effective": round(i_ffn_eff, 1),
+        "ffn_attainable_TFLOPs_at_measured_link": round(roofline_attainable(i_ffn, peak, link_bw) / 1e12, 1),
+        "ffn_flops_per_exchanged_byte_measured_run": round(f_flops / moved, 1),
+        "ffn_achieved_TFLOPs_per_gpu": round(achieved_tf, 1) if achieved_tf else None,
+        "note": "reference costs.arithmetic_intensities / turning_points / roofline_attainable with P = measured "
+                "sustained bf16 and B = this run's mean link GB/s; I_ffn >> turning point means the F side is "
+                "compute-bound, the exchange hides behind it",
+    }
 
 
 def run_e2e(args, stack, shape, mb, dev, world, graphs=None):

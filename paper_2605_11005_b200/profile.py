@@ -192,3 +192,28 @@ def reference_memory_estimate(exp, component: str, n_attn: int, n_ffn: int) -> f
     hidden = m.bytes_per_element * w.micro_batch * w.seq_len * h
     in_flight = min(w.num_microbatches, max(1, 2 * p * layers - first_visit))
     return param_bytes + optimizer_bytes + float(layers * hidden * in_flight)
+
+
+def reference_intensities(exp) -> tuple[float, float]:
+    """(I_attn, I_ffn) FLOPs per exchanged byte of the reference cost model
+    (restated from `costs.arithmetic_intensities`, costs.py:117-122): I_attn =
+    ((2(g+1)/g)·H + 4s) / (2k), I_ffn = 2·D_e."""
+    from fractions import Fraction
+
+    m, w = exp.model, exp.workload
+    g = m.gqa_group
+    i_attn = Fraction(Fraction(2 * (g + 1), g) * m.hidden + 4 * w.seq_len, 2 * m.topk)
+    return float(i_attn), float(2 * m.moe_hidden)
+
+
+def reference_turning_points(peak_flops: float, bandwidth: float, attn_nodes: int, ffn_nodes: int):
+    """(I_hat, I_attn_eff, I_ffn_eff) of `costs.turning_points` (costs.py:125-139):
+    the system turning point P/B split by node share, 2m/(m+n)·I_hat and its complement."""
+    i_hat = peak_flops / bandwidth
+    i_attn = 2.0 * attn_nodes / (attn_nodes + ffn_nodes) * i_hat
+    return i_hat, i_attn, 2.0 * i_hat - i_attn
+
+
+def roofline_attainable(intensity: float, peak_flops: float, bandwidth: float) -> float:
+    """min(P, I·B) (`costs.roofline_attainable`, costs.py:142-144)."""
+    return min(float(peak_flops), float(intensity) * float(bandwidth))

@@ -97,3 +97,22 @@ def test_reference_memory_estimate_restatement_matches_reference():
                 plan = assign_layers(ref.model.layers, ref.pipeline_depth, comp)
                 want = memory_estimate(plan, ref.model, ref.workload, alloc).total
                 assert reference_memory_estimate(ours, comp, n_attn, n_ffn) == pytest.approx(want, rel=1e-12)
+
+
+@pytest.mark.skipif(not REF.exists(), reason="reference not mounted")
+def test_reference_roofline_restatements_match_reference():
+    sys.path.insert(0, str(REF))
+    from afpipe import costs
+    from afpipe.config import load_experiment as ref_load
+
+    from paper_2605_11005_b200.profile import reference_intensities, reference_turning_points, roofline_attainable
+
+    for cfg in ("tiny.yaml", "mixtral_layer.yaml", "dsv3_layer.yaml"):
+        path = str(ROOT / "configs" / cfg)
+        ours, ref = load_experiment(path), ref_load(path)
+        ia, if_ = costs.arithmetic_intensities(ref.model, ref.workload)
+        assert reference_intensities(ours) == pytest.approx((float(ia), float(if_)), rel=1e-15)
+        for m, n in ((1, 1), (2, 6), (4, 4)):
+            assert reference_turning_points(ref.cluster.gpu_peak, ref.cluster.ib_bw, m, n) == pytest.approx(
+                costs.turning_points(ref.cluster, m, n), rel=1e-15)
+        assert roofline_attainable(float(if_), 1.683e15, 9e11) == costs.roofline_attainable(if_, 1.683e15, 9e11)
