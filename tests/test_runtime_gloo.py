@@ -26,17 +26,20 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
+SKEW = 0.0   # > 0: routing biased onto experts 0..K-1 (oracle.make_inputs), so some F ranks get no rows
+
+
 def _weights(layer: int = 0):
     from oracle import oracle as O
 
-    _, wg, w1, w3, w2, _ = O.make_inputs(T, H, E, K, DE, seed=7 + 31 * layer)
+    _, wg, w1, w3, w2, _ = O.make_inputs(T, H, E, K, DE, seed=7 + 31 * layer, skew=SKEW)
     return wg, w1, w3, w2
 
 
 def _inputs(a: int, i: int):
     from oracle import oracle as O
 
-    x, _, _, _, _, dy = O.make_inputs(T, H, E, K, DE, seed=100 + 10 * a + i)
+    x, _, _, _, _, dy = O.make_inputs(T, H, E, K, DE, seed=100 + 10 * a + i, skew=SKEW)
     return x, dy
 
 
@@ -58,7 +61,9 @@ def collect(r, to_np=lambda t: t.numpy()):
     return out
 
 
-def _worker(rank, world, n_attn, port, outdir, layers=1, depth=1):
+def _worker(rank, world, n_attn, port, outdir, layers=1, depth=1, skew=0.0):
+    global SKEW
+    SKEW = skew
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -146,6 +151,22 @@ def test_afpipe_runtime_matches_oracle(world, n_attn, layers, depth):
         mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers, depth), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
     check_against_oracle(outs, n_attn // depth, layers)
+
+
+def test_afpipe_runtime_skewed_routing_empty_f_ranks():
+    """Routing biased onto experts 0..K-1: the F rank owning experts 2..3 receives no rows
+    (empty slices are skipped symmetrically on both ends) and still returns zero grads."""
+    global SKEW
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(3, 1, _free_port(), d, 1, 1, 40.0), nprocs=3, join=True)
+        outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(3)]
+    SKEW = 40.0
+    try:
+        check_against_oracle(outs, 1, 1)
+    finally:
+        SKEW = 0.0
+    f_hi = next(o for o in outs if o["role"] == "F" and o["lo"] == 2)
+    assert np.abs(f_hi["dw2"][0]).max() == 0.0
 
 
 def test_topology_blocks_match_reference_balanced_blocks():

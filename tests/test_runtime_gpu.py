@@ -21,7 +21,10 @@ sys.path.insert(0, str(ROOT / "tests"))
 from test_runtime_gloo import E, K, MB, T, DE, H, _free_port, _inputs, _weights, check_against_oracle  # noqa: E402
 
 
-def _worker(rank, world, n_attn, port, outdir, layers, depth=1):
+def _worker(rank, world, n_attn, port, outdir, layers, depth=1, skew=0.0):
+    import test_runtime_gloo as G
+
+    G.SKEW = skew
     sys.path.insert(0, str(ROOT))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
@@ -65,6 +68,22 @@ def test_afpipe_runtime_gpu_matches_oracle(world, n_attn, layers, depth):
         mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers, depth), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
     check_against_oracle(outs, n_attn // depth, layers)
+
+
+def test_afpipe_runtime_gpu_skewed_routing():
+    """All tokens routed to experts 0..1: the F rank owning experts 2..3 gets empty slices."""
+    if torch.cuda.device_count() < 3:
+        pytest.skip("needs 3 GPUs")
+    import test_runtime_gloo as G
+
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(3, 1, _free_port(), d, 1, 1, 40.0), nprocs=3, join=True)
+        outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(3)]
+    G.SKEW = 40.0
+    try:
+        check_against_oracle(outs, 1, 1)
+    finally:
+        G.SKEW = 0.0
 
 
 def _attn_worker(rank, world, n_attn, port, outdir, layers, depth=1):
