@@ -332,6 +332,54 @@ expert_scan_kernel(const int32_t* __restrict__ hist, int nchunk, int E, int32_t*
   }
 }
 
+// Scan for many experts (E >= 64): thread per expert, so every pass over the
+// [nchunk][E] histogram is coalesced across threads; the padded per-expert sizes
+// are prefix-summed with a block scan (warp shuffles + warp totals).
+__global__ void __launch_bounds__(1024)
+expert_scan_wide_kernel(const int32_t* __restrict__ hist, int nchunk, int E, int32_t* __restrict__ counts,
+                        int32_t* __restrict__ pad_off, int32_t* __restrict__ chunk_base) {
+  __shared__ int s_warp[32];
+  const int e = threadIdx.x, lane = e & 31, warp = e >> 5;
+  int tot = 0;
+  if (e < E) {
+#pragma unroll 8
+    for (int c = 0; c < nchunk; ++c) tot += hist[(size_t)c * E + e];
+    counts[e] = tot;
+  }
+  const int padded = (tot + DM_ROW_ALIGN - 1) / DM_ROW_ALIGN * DM_ROW_ALIGN;
+  int incl = padded;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    int w = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += o;
+    }
+    s_warp[lane] = w;   // inclusive prefix of warp totals
+  }
+  __syncthreads();
+  const int excl = incl - padded + (warp > 0 ? s_warp[warp - 1] : 0);
+  if (e < E) {
+    pad_off[e] = excl;
+    if (e == E - 1) pad_off[E] = excl + padded;
+    int run = excl;
+#pragma unroll 8
+    for (int c = 0; c < nchunk; ++c) {
+      const int v = hist[(size_t)c * E + e];
+      chunk_base[(size_t)c * E + e] = run;
+      run += v;
+    }
+  }
+}
+
 // Permute (scatter-copy), warp per token: pos(t, j) = chunk_base[chunk(t), e] +
 // rank[t, j]; x[t] is read once with 8-deep 128-bit loads and written to its k
 // expert rows. Every warp then helps zero the padding rows (they feed the
@@ -617,7 +665,11 @@ int dm_expert_scan(const int32_t* chunk_hist, int T, int E, int32_t* counts, int
   int rc = check_route_shape(T, 8, E, 1);
   if (rc) return rc;
   const int nchunk = dm_num_chunks(T);
-  expert_scan_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(chunk_hist, nchunk, E, counts, pad_off, chunk_base);
+  if (E >= 64)
+    expert_scan_wide_kernel<<<1, (E + 31) / 32 * 32, 0, (cudaStream_t)stream>>>(chunk_hist, nchunk, E, counts,
+                                                                                pad_off, chunk_base);
+  else
+    expert_scan_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(chunk_hist, nchunk, E, counts, pad_off, chunk_base);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "expert_scan launch");
   note_launch();

@@ -1,4 +1,7 @@
-"""One warm-up + N profiled steps of the fused Mixtral layer (for ncu launch lists)."""
+"""One warm-up + N profiled steps of the fused MoE layer (for ncu launch lists).
+
+The measured steps are bracketed by cudaProfilerStart/Stop, so run ncu with
+`--profile-from-start off` to capture exactly one iteration's launches."""
 import argparse
 import sys
 from pathlib import Path
@@ -21,7 +24,12 @@ layer = MoELayer.random(shape, device="cuda", seed=1, num_buffers=mb)
 for b in layer.buffers:
     b.x.normal_()
     b.dy.normal_()
-for s in range(a.warmup + a.steps):
+for _ in range(a.warmup):
     layer.iteration(mb)
 torch.cuda.synchronize()
+torch.cuda.profiler.start()
+for _ in range(a.steps):
+    layer.iteration(mb)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok")

@@ -16,9 +16,9 @@ runN 2 --config configs/tiny.yaml > $O/bench_tiny_n2_afpipe_2layers.json
 runN 4 > $O/bench_mixtral_n4_2a2f.json
 runN 4 --n-attn 1 > $O/bench_mixtral_n4_1a3f.json
 runN 4 --n-attn 1 --config configs/dsv3_layer.yaml --steps 5 > $O/bench_dsv3_n4_1a3f.json
-timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
   --log-file $O/launches_mixtral_step.csv python scripts/profile_step.py > $O/ncu1.log 2>&1
-timeout 500 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv \
+timeout 500 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
   --log-file $O/launches_dsv3_step.csv python scripts/profile_step.py --config configs/dsv3_layer.yaml > $O/ncu2.log 2>&1
 for f in $O/*.json; do python -c "
 import json,sys
