@@ -687,7 +687,8 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
 #pragma unroll
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * 128); }
+    // tempty: one arrival per epilogue warp of both CTAs (lane 0 after a __syncwarp)
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * 4); }
 #pragma unroll
     for (int s = 0; s < 4; ++s) mbar_init(&ibar[s], 1);
     fence_mbar_init();
@@ -828,9 +829,14 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
         const uint32_t tacc = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * GBN;
         epilogue_tma<EPI>(ti, tacc, q, lane, args, &tmC, &tmAux, &tmIn, stg, &ibar[q], iphase);
       }
+      // TMEM buffer drained: one (remote) arrival per warp instead of per thread — the
+      // per-thread cluster arrives cost ~10% of the epilogue on short-K (wgrad) tiles
       tc_fence_before();
-      if (leader) mbar_arrive(&tempty[as]);
-      else mbar_arrive_cluster(&tempty[as], 0);
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&tempty[as]);
+        else mbar_arrive_cluster(&tempty[as], 0);
+      }
     }
     if (lane == 0) bulk_wait_all();
     __syncwarp();
