@@ -26,8 +26,12 @@ def _ptr(t: torch.Tensor | None) -> int | None:
 
 
 def _stream(stream: torch.cuda.Stream | None = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    """cudaStream_t of `stream`, or of the current stream of the current device. The
+    raw-handle query avoids torch.cuda.current_stream()'s Python overhead (~10 us), which
+    dominated the host side of small-shape AF-Pipe iterations."""
+    if stream is not None:
+        return stream.cuda_stream
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def _check(t: torch.Tensor, dtype: torch.dtype, shape: tuple, name: str) -> None:
