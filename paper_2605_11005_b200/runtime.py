@@ -255,12 +255,15 @@ class GpuStages:
         K.w2_dgrad_swiglu_bwd(fb.dy_perm, experts.w2, fb.h13, group_off, fb.dh13)
         K.w13_dgrad(fb.dh13, experts.w13, group_off, fb.dx_perm)
 
-    def f_wgrad(self, slab: ActivationSlab, experts: ExpertParams, seg_off: torch.Tensor, accumulate: bool):
+    def f_wgrad(self, slab: ActivationSlab, experts: ExpertParams, seg_off: torch.Tensor, accumulate: bool,
+                seg_stride_rows: int = 0):
+        """seg_stride_rows 0: absolute segment rows; > 0: segment i's rows are relative
+        to i * seg_stride_rows (the fixed-size 1:1 exchange)."""
         from . import kernels as K
 
         beta = 1.0 if accumulate else 0.0
-        K.wgrad(slab.dy_perm, slab.act, seg_off, experts.dw2, beta, seg_stride_rows=0)
-        K.wgrad(slab.dh13, slab.x_perm, seg_off, experts.dw13, beta, seg_stride_rows=0)
+        K.wgrad(slab.dy_perm, slab.act, seg_off, experts.dw2, beta, seg_stride_rows=seg_stride_rows)
+        K.wgrad(slab.dh13, slab.x_perm, seg_off, experts.dw13, beta, seg_stride_rows=seg_stride_rows)
 
 
 @dataclass
@@ -314,6 +317,12 @@ class AFPipeRank:
         self.device = torch.device(device)
         self.role, self.idx = topo.role(rank)
         self.group, self.member = topo.group_of(rank)
+        # One A and one F rank per pipeline group: the F rank owns every expert, so the
+        # A rank's whole capacity buffer is the slice; exchanges are fixed-size (cap rows)
+        # and the received padded offsets are used on the device as the F-side group
+        # offsets directly — no host synchronisation anywhere in the iteration.
+        self.fixed = (topo.a_per_group == 1 and topo.f_per_group == 1
+                      and os.environ.get("DM_AFPIPE_FIXED", "1") != "0")
         self.my_layers = topo.layers_of(self.group, layers)
         self.stages = stages if stages is not None else GpuStages()
         self.st = _Streams(self.device)
@@ -504,10 +513,11 @@ class AFPipeRank:
                 self.attn[layer].forward(i, self._layer_input(layer, i), b.x, self.seq_len)
             self.stages.a_dispatch(b, self.routers[layer])
             done = self.st.event("compute")
-            with self.st.ctx("copy"):
-                self.st.wait("copy", done)
-                self.pad_host[layer][i].copy_(b.pad_off, non_blocking=self.st.cuda)
-                self.pad_ready[layer][i] = self.st.event("copy")
+            if not self.fixed:
+                with self.st.ctx("copy"):
+                    self.st.wait("copy", done)
+                    self.pad_host[layer][i].copy_(b.pad_off, non_blocking=self.st.cuda)
+                    self.pad_ready[layer][i] = self.st.event("copy")
             b.fwd_done = done
         elif name == "A_c":     # depth > 1: this layer's combine, then x_{l+1} leaves (A2A)
             self._wait_works(b, "N2M")
@@ -549,8 +559,10 @@ class AFPipeRank:
         if name in ("A2A", "A2A_b"):
             return self._a2a(name, i, layer, lane)
         b = self.lbufs[layer][i]
-        pad = self._a_pad(layer, i)
         g = self.group
+        if self.fixed:
+            return self._a_comm_fixed(name, i, b, self.topo.f_rank(0, g))
+        pad = self._a_pad(layer, i)
         ops = []
         if name == "M2N":
             with self.st.ctx("send"):
@@ -572,6 +584,22 @@ class AFPipeRank:
                 for f, r0, r1, lo, hi in self._a_slices(pad):
                     ops.append(("recv", dst[r0:r1], self.topo.f_rank(f, g)))
                 setattr(b, "works_" + name, _exchange(ops))
+
+    def _a_comm_fixed(self, name: str, i: int, b, peer: int):
+        """1:1 group: whole-capacity messages (the used rows are ~all of it when one F rank
+        holds every expert), header = the full padded offsets."""
+        if name == "M2N":
+            with self.st.ctx("send"):
+                self.st.wait("send", b.fwd_done)
+                b.works_M2N = self._xchg([("send", b.pad_off, peer), ("send", b.x_perm, peer)], name, i)
+        elif name == "M2N_b":
+            with self.st.ctx("send"):
+                self.st.wait("send", b.turn_done)
+                b.works_M2N_b = self._xchg([("send", b.dy_perm, peer)], name, i)
+        else:
+            dst = b.y_perm if name == "N2M" else b.dx_perm
+            with self.st.ctx("recv"):
+                setattr(b, "works_" + name, _exchange([("recv", dst, peer)]))
 
     def _a2a(self, name: str, i: int, layer: int, lane: str):
         """depth > 1: the residual stream between consecutive layers' A groups (same
@@ -612,6 +640,8 @@ class AFPipeRank:
         fm = self.lfmb[layer][i]
         n_a = self.n_src
         src_rank = lambda a: self.topo.a_rank(a, self.group)  # noqa: E731
+        if self.fixed:
+            return self._f_comm_fixed(name, i, layer, fm, src_rank(0))
         if name == "M2N":
             with self.st.ctx("recv"):
                 hw = _exchange([("recv", fm.headers[a], src_rank(a)) for a in range(n_a)])
@@ -660,6 +690,24 @@ class AFPipeRank:
                 ops = [("send", src[b0:b0 + r], src_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
                 fm.works[name] = self._xchg(ops, name, i)
 
+    def _f_comm_fixed(self, name: str, i: int, layer: int, fm, peer: int):
+        """1:1 group: the header lands in this micro-batch's wgrad segment row, which is
+        also the GEMM group-offset array (relative rows; wgrad strides by cap_f)."""
+        if name == "M2N":
+            seg = self.seg_offs[layer][i]
+            fm.group_off = seg
+            fm.slices = [(0, self.cap_f)]
+            with self.st.ctx("recv"):
+                fm.works["M2N"] = _exchange([("recv", seg, peer), ("recv", fm.x_perm, peer)])
+        elif name == "M2N_b":
+            with self.st.ctx("recv"):
+                fm.works["M2N_b"] = _exchange([("recv", fm.dy_perm, peer)])
+        else:
+            src = fm.y_perm if name == "N2M" else fm.dx_perm
+            with self.st.ctx("send"):
+                self.st.wait("send", fm.works.get(name + "_ready"))
+                fm.works[name] = self._xchg([("send", src, peer)], name, i)
+
     def f_task(self, name: str, i: int, layer: int):
         fm = self.lfmb[layer][i]
         experts = self.expert_layers[layer]
@@ -700,7 +748,8 @@ class AFPipeRank:
         if self.role == "F":
             def w_pass():
                 for l in self.my_layers:
-                    self.stages.f_wgrad(self.slabs[l], self.expert_layers[l], self.seg_offs[l], accumulate)
+                    self.stages.f_wgrad(self.slabs[l], self.expert_layers[l], self.seg_offs[l], accumulate,
+                                        self.cap_f if self.fixed else 0)
             self._compute("W", -1, w_pass)
             for l in self.my_layers:
                 for fm in self.lfmb[l]:

@@ -112,14 +112,15 @@ class CpuStages:
             fb.dh13[a:b] = _join(dg, du).to(BF16)
             fb.dx_perm[a:b] = (fb.dh13[a:b].float() @ experts.w13[e].float()).to(BF16)
 
-    def f_wgrad(self, slab, experts, seg_off, accumulate):
+    def f_wgrad(self, slab, experts, seg_off, accumulate, seg_stride_rows=0):
         if not accumulate:
             experts.dw13.zero_()
             experts.dw2.zero_()
         so = seg_off.tolist()
-        for row in so:
+        for i, row in enumerate(so):
+            base = i * seg_stride_rows
             for e in range(len(row) - 1):
-                a, b = row[e], row[e + 1]
+                a, b = base + row[e], base + row[e + 1]
                 if b > a:
                     experts.dw2[e] += slab.dy_perm[a:b].float().t() @ slab.act[a:b].float()
                     experts.dw13[e] += slab.dh13[a:b].float().t() @ slab.x_perm[a:b].float()
