@@ -131,7 +131,9 @@ class Topology:
 
 # ------------------------------------------------------------------ streams
 class _Streams:
-    """compute / send / recv / copy streams on CUDA; no-ops on CPU (gloo tests)."""
+    """compute / send / recv / copy streams on CUDA; no-ops on CPU (gloo tests). `copy`
+    carries the small count reads the exchange waits on, `h2d` / `d2h` the e2e mode's
+    activation copies, so a 32 MB input copy never delays a count read."""
 
     def __init__(self, device: torch.device):
         self.cuda = device.type == "cuda"
@@ -140,6 +142,8 @@ class _Streams:
             self.send = torch.cuda.Stream(device)
             self.recv = torch.cuda.Stream(device)
             self.copy = torch.cuda.Stream(device)
+            self.h2d = torch.cuda.Stream(device)
+            self.d2h = torch.cuda.Stream(device)
 
     def ctx(self, which: str):
         """Make stream `which` current; leaving returns to the compute stream (contexts are
@@ -407,6 +411,7 @@ class AFPipeRank:
         self.trace: list = []
         self.t0 = None
         self.host_io = None
+        self.x_free, self.dy_free = [], []   # per micro-batch: last reader of x / dy done (e2e)
 
     # ----------------------------------------------------------------- plan
     def _default_durations(self) -> LayerDurations:
@@ -463,6 +468,9 @@ class AFPipeRank:
         iteration start, y / dx copied back as each micro-batch finishes (e2e mode).
         Group 0 ranks use x / dx, the last layer's group y / dy."""
         self.host_io = (xs, dys, ys, dxs)
+        if len(self.x_free) != len(xs):   # first e2e iteration: wait for all earlier work
+            now = self.st.event("compute")
+            self.x_free, self.dy_free = [now] * len(xs), [now] * len(xs)
 
     @property
     def has_input(self) -> bool:
@@ -473,15 +481,24 @@ class AFPipeRank:
         return self.role == "A" and (self.L - 1) in self.my_layers
 
     def _h2d_inputs(self):
+        """Queue this iteration's input copies on the h2d stream. Micro-batch i's x (dy)
+        overwrites its buffer as soon as the previous iteration's last reader of it, A_b of
+        layer 0 (of the last layer), is done — not at the iteration boundary — so the copies
+        overlap the previous iteration's tail; A_f waits on x only, the turnaround on dy."""
         xs, dys, _, _ = self.host_io
-        self.h2d_ready = []
-        with self.st.ctx("copy"):
-            for i, (x, dy) in enumerate(zip(xs, dys)):
+        n = len(xs)
+        self.x_ready, self.dy_ready = [None] * n, [None] * n
+        with self.st.ctx("h2d"):
+            for i in range(n):
                 if self.has_input:
-                    self.input(i).copy_(x, non_blocking=True)
+                    self.st.wait("h2d", self.x_free[i])
+                    self.input(i).copy_(xs[i], non_blocking=True)
+                    self.x_ready[i] = self.st.event("h2d")
+            for i in range(n):
                 if self.has_output:
-                    self.out_bufs[i].dy.copy_(dy, non_blocking=True)
-                self.h2d_ready.append(self.st.event("copy"))
+                    self.st.wait("h2d", self.dy_free[i])
+                    self.out_bufs[i].dy.copy_(dys[i], non_blocking=True)
+                    self.dy_ready[i] = self.st.event("h2d")
 
     def input(self, i: int) -> torch.Tensor:
         """A rank of group 0: micro-batch i's input activations (before attention if any)."""
@@ -502,7 +519,7 @@ class AFPipeRank:
         if name == "A_f":
             if layer == 0:
                 if self.host_io is not None:
-                    self.st.wait("compute", self.h2d_ready[i])
+                    self.st.wait("compute", self.x_ready[i])
             elif self.p == 1:   # previous layer's combine writes this layer's input (residual fused)
                 prev = self.lbufs[layer - 1][i]
                 self._wait_works(prev, "N2M")
@@ -525,11 +542,15 @@ class AFPipeRank:
             b.comb_done = self.st.event("compute")
         elif name == "A_t":
             self._wait_works(b, "N2M")
+            if layer == self.L - 1 and self.host_io is not None:
+                self.st.wait("compute", self.dy_ready[i])
             self.stages.a_combine(b)
             self.stages.a_combine_bwd(b)
             b.turn_done = self.st.event("compute")
         elif name == "A_cb":    # depth > 1: dy_l arrived (A2A_b); this layer's combine backward
             self._wait_works(b, "A2A_b")
+            if layer == self.L - 1 and self.host_io is not None:
+                self.st.wait("compute", self.dy_ready[i])
             self.stages.a_combine_bwd(b)
             b.turn_done = self.st.event("compute")
         elif name == "A_b":
@@ -543,17 +564,18 @@ class AFPipeRank:
                 prev.turn_done = self.st.event("compute")
             else:
                 b.bwd_done = self.st.event("compute")
-            if layer == 0 and self.host_io is not None:
-                _, _, ys, dxs = self.host_io
+            if self.host_io is not None and layer in (0, self.L - 1):
                 done = self.st.event("compute")
-                with self.st.ctx("copy"):
-                    self.st.wait("copy", done)
-                    dxs[i].copy_(self.input_grad(i), non_blocking=True)
-            if layer == self.L - 1 and self.host_io is not None:
-                _, _, ys, _ = self.host_io
-                with self.st.ctx("copy"):
-                    self.st.wait("copy", b.turn_done)
-                    ys[i].copy_(self.out_bufs[i].y, non_blocking=True)
+                if layer == self.L - 1:   # y_i was final at the turnaround
+                    self.dy_free[i] = done
+                    with self.st.ctx("d2h"):
+                        self.st.wait("d2h", b.turn_done)
+                        self.host_io[2][i].copy_(self.out_bufs[i].y, non_blocking=True)
+                if layer == 0:            # x_i has no reader left this iteration; dx_i is final
+                    self.x_free[i] = done
+                    with self.st.ctx("d2h"):
+                        self.st.wait("d2h", done)
+                        self.host_io[3][i].copy_(self.input_grad(i), non_blocking=True)
 
     def a_comm(self, name: str, i: int, layer: int, lane: str):
         if name in ("A2A", "A2A_b"):
@@ -727,7 +749,7 @@ class AFPipeRank:
         # comm/copy streams must not touch this iteration's buffers before the
         # compute stream is done with the previous iteration's uses of them
         start = self.st.event("compute")
-        for which in ("send", "recv", "copy"):
+        for which in ("send", "recv", "copy", "d2h"):
             self.st.wait(which, start)
         self.trace = []
         self.t0 = self.st.event("compute", self.record_events)
@@ -761,8 +783,8 @@ class AFPipeRank:
                 for b in self.lbufs[l]:
                     for k in ("M2N", "M2N_b", "A2A_send", "A2A_b_send"):
                         self._wait_works(b, k)
-            if self.host_io is not None:
-                self.st.compute.wait_stream(self.st.copy) if self.st.cuda else None
+            if self.host_io is not None and self.st.cuda:   # the iteration ends with y / dx on the host
+                self.st.compute.wait_stream(self.st.d2h)
             if self.a_group is not None and self.topo.a_per_group > 1:
                 for l in self.my_layers:
                     dist.all_reduce(self.routers[l].dwg, group=self.a_group)

@@ -21,7 +21,7 @@ sys.path.insert(0, str(ROOT / "tests"))
 from test_runtime_gloo import E, K, MB, T, DE, H, _free_port, _inputs, _weights, check_against_oracle  # noqa: E402
 
 
-def _worker(rank, world, n_attn, port, outdir, layers, depth=1, skew=0.0):
+def _worker(rank, world, n_attn, port, outdir, layers, depth=1, skew=0.0, host_io=False):
     import test_runtime_gloo as G
 
     G.SKEW = skew
@@ -44,19 +44,66 @@ def _worker(rank, world, n_attn, port, outdir, layers, depth=1, skew=0.0):
     r = AFPipeRank(MoEShape(T, H, E, K, DE), Topology(world, n_attn, E, depth), rank, MB, dev, weights=weights,
                    record_events=True, layers=layers)
     r.init_groups()
-    if r.role == "A":
-        for i in range(MB):
-            x, dy = _inputs(r.member, i)
-            if r.has_input:
-                r.input(i).copy_(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16))
-            if r.has_output:
-                r.out_bufs[i].dy.copy_(bf(dy))
-    for _ in range(2):  # second iteration re-uses every buffer (stream-ordering check)
-        r.run_iteration()
+    if host_io:
+        _run_host_io(r, bf)
+    else:
+        if r.role == "A":
+            for i in range(MB):
+                x, dy = _inputs(r.member, i)
+                if r.has_input:
+                    r.input(i).copy_(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16))
+                if r.has_output:
+                    r.out_bufs[i].dy.copy_(bf(dy))
+        for _ in range(2):  # second iteration re-uses every buffer (stream-ordering check)
+            r.run_iteration()
     torch.cuda.synchronize()
     torch.save(collect(r, lambda t: t.cpu().numpy()), os.path.join(outdir, f"rank{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
+
+
+def _run_host_io(r, bf):
+    """e2e mode: pinned host inputs copied in and y / dx copied out by the runtime. Three
+    back-to-back iterations (real, other, real inputs) without a host sync, so the h2d
+    copies of one iteration overlap the tail of the previous one; the two real iterations
+    must produce bit-identical host outputs equal to the device buffers."""
+    pin = lambda t: t.contiguous().pin_memory()  # noqa: E731
+    empty = lambda: [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(MB)]  # noqa: E731
+    real, other = ([], []), ([], [])
+    for i in range(MB):
+        x, dy = _inputs(r.member, i)
+        real[0].append(pin(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16)))
+        real[1].append(pin(bf(dy)))
+        other[0].append(pin(torch.randn(T, H).to(torch.bfloat16)))
+        other[1].append(pin(torch.randn(T, H).to(torch.bfloat16)))
+    outs = []
+    for xs, dys in (real, other, real):
+        ys, dxs = empty(), empty()
+        if r.role == "A":
+            r.set_host_io(xs, dys, ys, dxs)
+        r.run_iteration()
+        outs.append((ys, dxs))
+    torch.cuda.synchronize()
+    if r.role == "A":
+        for i in range(MB):
+            if r.has_output:
+                assert torch.equal(outs[0][0][i], outs[2][0][i])
+                assert torch.equal(outs[2][0][i], r.out_bufs[i].y.cpu())
+            if r.has_input:
+                assert torch.equal(outs[0][1][i], outs[2][1][i])
+                assert torch.equal(outs[2][1][i], r.input_grad(i).cpu())
+
+
+@pytest.mark.parametrize("world,n_attn,layers,depth", [(2, 1, 2, 1), (4, 2, 2, 2), (4, 1, 1, 1)])
+def test_afpipe_runtime_gpu_host_io(world, n_attn, layers, depth):
+    """The e2e path bench.py times (set_host_io: h2d / d2h streams, per-micro-batch
+    buffer-free events) matches the oracle and is bit-reproducible across iterations."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers, depth, 0.0, True), nprocs=world, join=True)
+        outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
+    check_against_oracle(outs, n_attn // depth, layers)
 
 
 @pytest.mark.parametrize("world,n_attn,layers,depth", [(2, 1, 1, 1), (2, 1, 2, 1), (4, 2, 1, 1), (4, 1, 1, 1),
