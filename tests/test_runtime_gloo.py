@@ -61,7 +61,40 @@ def collect(r, to_np=lambda t: t.numpy()):
     return out
 
 
-def _worker(rank, world, n_attn, port, outdir, layers=1, depth=1, skew=0.0):
+def run_host_io(r, bf, pin=lambda t: t.contiguous()):
+    """e2e mode (set_host_io): host inputs copied in and y / dx copied out by the runtime,
+    three back-to-back iterations (real, other, real inputs); the two real iterations must
+    give identical host outputs equal to the device buffers. Shared with the NCCL test
+    (pinned buffers there, so the copies overlap the previous iteration's tail)."""
+    empty = lambda: [pin(torch.empty(T, H, dtype=torch.bfloat16)) for _ in range(MB)]  # noqa: E731
+    real, other = ([], []), ([], [])
+    g = torch.Generator().manual_seed(5)
+    for i in range(MB):
+        x, dy = _inputs(r.member, i)
+        real[0].append(pin(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16)))
+        real[1].append(pin(bf(dy)))
+        other[0].append(pin(torch.randn(T, H, generator=g).to(torch.bfloat16)))
+        other[1].append(pin(torch.randn(T, H, generator=g).to(torch.bfloat16)))
+    outs = []
+    for xs, dys in (real, other, real):
+        ys, dxs = empty(), empty()
+        if r.role == "A":
+            r.set_host_io(xs, dys, ys, dxs)
+        r.run_iteration()
+        outs.append((ys, dxs))
+    if r.device.type == "cuda":
+        torch.cuda.synchronize()
+    if r.role == "A":
+        for i in range(MB):
+            if r.has_output:
+                assert torch.equal(outs[0][0][i], outs[2][0][i])
+                assert torch.equal(outs[2][0][i], r.out_bufs[i].y.cpu())
+            if r.has_input:
+                assert torch.equal(outs[0][1][i], outs[2][1][i])
+                assert torch.equal(outs[2][1][i], r.input_grad(i).cpu())
+
+
+def _worker(rank, world, n_attn, port, outdir, layers=1, depth=1, skew=0.0, host_io=False):
     global SKEW
     SKEW = skew
     sys.path.insert(0, str(ROOT))
@@ -82,14 +115,17 @@ def _worker(rank, world, n_attn, port, outdir, layers=1, depth=1, skew=0.0):
     r = AFPipeRank(MoEShape(T, H, E, K, DE), topo, rank, MB, torch.device("cpu"), stages=CpuStages(),
                    weights=weights, layers=layers)
     r.init_groups()
-    if r.role == "A":
-        for i in range(MB):
-            x, dy = _inputs(r.member, i)
-            if r.has_input:
-                r.input(i).copy_(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16))
-            if r.has_output:
-                r.out_bufs[i].dy.copy_(bf(dy))
-    r.run_iteration()
+    if host_io:
+        run_host_io(r, bf)
+    else:
+        if r.role == "A":
+            for i in range(MB):
+                x, dy = _inputs(r.member, i)
+                if r.has_input:
+                    r.input(i).copy_(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16))
+                if r.has_output:
+                    r.out_bufs[i].dy.copy_(bf(dy))
+        r.run_iteration()
     torch.save(collect(r), os.path.join(outdir, f"rank{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
@@ -149,6 +185,15 @@ def check_against_oracle(outs, n_streams, layers, tol=1e-2):
 def test_afpipe_runtime_matches_oracle(world, n_attn, layers, depth):
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers, depth), nprocs=world, join=True)
+        outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
+    check_against_oracle(outs, n_attn // depth, layers)
+
+
+@pytest.mark.parametrize("world,n_attn,layers,depth", [(2, 1, 2, 1), (4, 2, 2, 2)])
+def test_afpipe_runtime_host_io(world, n_attn, layers, depth):
+    """The e2e host-I/O path bench.py times (set_host_io), on CPU."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, n_attn, _free_port(), d, layers, depth, 0.0, True), nprocs=world, join=True)
         outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(world)]
     check_against_oracle(outs, n_attn // depth, layers)
 

@@ -45,7 +45,7 @@ def _worker(rank, world, n_attn, port, outdir, layers, depth=1, skew=0.0, host_i
                    record_events=True, layers=layers)
     r.init_groups()
     if host_io:
-        _run_host_io(r, bf)
+        G.run_host_io(r, bf, pin=lambda t: t.contiguous().pin_memory())
     else:
         if r.role == "A":
             for i in range(MB):
@@ -60,38 +60,6 @@ def _worker(rank, world, n_attn, port, outdir, layers, depth=1, skew=0.0, host_i
     torch.save(collect(r, lambda t: t.cpu().numpy()), os.path.join(outdir, f"rank{rank}.pt"))
     dist.barrier()
     dist.destroy_process_group()
-
-
-def _run_host_io(r, bf):
-    """e2e mode: pinned host inputs copied in and y / dx copied out by the runtime. Three
-    back-to-back iterations (real, other, real inputs) without a host sync, so the h2d
-    copies of one iteration overlap the tail of the previous one; the two real iterations
-    must produce bit-identical host outputs equal to the device buffers."""
-    pin = lambda t: t.contiguous().pin_memory()  # noqa: E731
-    empty = lambda: [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(MB)]  # noqa: E731
-    real, other = ([], []), ([], [])
-    for i in range(MB):
-        x, dy = _inputs(r.member, i)
-        real[0].append(pin(torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16)))
-        real[1].append(pin(bf(dy)))
-        other[0].append(pin(torch.randn(T, H).to(torch.bfloat16)))
-        other[1].append(pin(torch.randn(T, H).to(torch.bfloat16)))
-    outs = []
-    for xs, dys in (real, other, real):
-        ys, dxs = empty(), empty()
-        if r.role == "A":
-            r.set_host_io(xs, dys, ys, dxs)
-        r.run_iteration()
-        outs.append((ys, dxs))
-    torch.cuda.synchronize()
-    if r.role == "A":
-        for i in range(MB):
-            if r.has_output:
-                assert torch.equal(outs[0][0][i], outs[2][0][i])
-                assert torch.equal(outs[2][0][i], r.out_bufs[i].y.cpu())
-            if r.has_input:
-                assert torch.equal(outs[0][1][i], outs[2][1][i])
-                assert torch.equal(outs[2][1][i], r.input_grad(i).cpu())
 
 
 @pytest.mark.parametrize("world,n_attn,layers,depth", [(2, 1, 2, 1), (4, 2, 2, 2), (4, 1, 1, 1)])
