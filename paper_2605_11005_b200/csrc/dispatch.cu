@@ -113,7 +113,9 @@ __device__ __forceinline__ void chunk_ranks(const int* sel, int nslots, int* run
 // of a warp is 512 contiguous bytes. The even/odd element chains of the
 // canonical order run as packed fp32x2 FMAs (FFMA2) on naturally paired
 // registers. W_g rows e >= E are zero-filled, so the hot loop has no E checks.
-constexpr int FUSED_UNROLL = 4;
+// x loads are double-buffered two k-tiles deep (unroll 2 beats 4: fewer spills,
+// dispatch stage 52.2 -> 50.2 us cold-L2, scripts/dispatch_ab.py).
+constexpr int FUSED_UNROLL = 2;
 constexpr int FUSED_NT = 2;
 constexpr int FUSED_WARPS = DM_CHUNK_TOKENS / FUSED_NT;   // 16
 

@@ -41,7 +41,7 @@ def main(T=4096, H=4096, E=8, k=2, reps=50):
     ts.sort()
     h = hashlib.sha1()
     for t in (idx, rm, w, counts, pad, xp[: int(pad[-1])]):
-        h.update(t.cpu().numpy().tobytes())
+        h.update((t.view(torch.int16) if t.dtype == torch.bfloat16 else t).cpu().numpy().tobytes())
     nbytes = T * H * 2 + T * k * H * 2 + 8 * T * k
     med = ts[len(ts) // 2]
     print(json.dumps({"E": E, "median_us": round(med, 1), "min_us": round(ts[0], 1),
