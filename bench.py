@@ -115,10 +115,30 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "window_s": round(t1 - t0 - 0.2, 3)}
 
 
+_WEIGHTS = {}
+
+
+def _oracle_weights(H, E, De):
+    """Random-init layer weights for the CPU arms, generated once per shape (generating a
+    Mixtral layer's 1.4 G fp32 values takes longer than timing it)."""
+    import numpy as np
+
+    key = (H, E, De)
+    if key not in _WEIGHTS:
+        rng = np.random.default_rng(11)
+        _WEIGHTS[key] = ((rng.standard_normal((E, H), dtype=np.float32) * 0.02),
+                         (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02),
+                         (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02),
+                         (rng.standard_normal((E, H, De), dtype=np.float32) * 0.02))
+    return _WEIGHTS[key]
+
+
 def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: int | None = None,
-                 layers: int = 1):
+                 layers: int = 1, fixed_tokens: int | None = None):
     """Time the oracle port (numpy fp32 BLAS, all host threads) on a bounded token sample
-    of one layer; a stack of `layers` identical-shape layers costs `layers` times that."""
+    of one layer; a stack of `layers` identical-shape layers costs `layers` times that.
+    The sample doubles from 64 tokens until it takes tokens_budget_s / 4 (or is capped);
+    fixed_tokens times exactly that many."""
     import numpy as np
 
     from oracle import oracle as O
@@ -135,11 +155,8 @@ def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: i
         w2 = layer.experts.w2.float().cpu().numpy()
         wg = (layer.router.wg if hasattr(layer, "router") else layer.wg).float().cpu().numpy()
     else:
-        w1 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02)
-        w3 = (rng.standard_normal((E, De, H), dtype=np.float32) * 0.02)
-        w2 = (rng.standard_normal((E, H, De), dtype=np.float32) * 0.02)
-        wg = (rng.standard_normal((E, H), dtype=np.float32) * 0.02)
-    T = 64
+        wg, w1, w3, w2 = _oracle_weights(H, E, De)
+    T = fixed_tokens or 64
     best = None
     while True:
         x = O.f32_to_bf16_bits(rng.standard_normal((T, H), dtype=np.float32))
@@ -149,7 +166,7 @@ def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: i
         O.moe_backward(f, x, wg, w1, w3, w2, dy, dtype=np.float32)
         dt = time.perf_counter() - t0
         best = (T, dt)
-        if dt > tokens_budget_s / 4 or T >= (max_tokens or shape.T) or T * 2 > shape.T:
+        if fixed_tokens or dt > tokens_budget_s / 4 or T >= (max_tokens or shape.T) or T * 2 > shape.T:
             break
         T *= 2
     T, dt = best
@@ -164,9 +181,13 @@ def run_reference(args, shape, exp):
     if rank != 0:
         return 0
     steps, warm = args.steps, args.warmup
+    # the first warm-up step sizes the sample (doubling up to ~1 s of CPU work, at most 256
+    # tokens); every later step times that many tokens once, so K + W steps stay within minutes
+    tokens = None
     samples = []
     for i in range(warm + steps):
-        r = cpu_baseline(shape, tokens_budget_s=8.0, max_tokens=256, layers=exp.model.layers)
+        r = cpu_baseline(shape, tokens_budget_s=4.0, max_tokens=256, layers=exp.model.layers, fixed_tokens=tokens)
+        tokens = tokens or int(r["sample"].split()[0])
         if i >= warm:
             samples.append(r)
     value = statistics.median(s["value"] for s in samples)
