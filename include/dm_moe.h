@@ -248,6 +248,15 @@ DM_API int dm_grouped_wgrad_strided(const void* a_tok, int M, int lda, const voi
  * rows, 2: per group of `rows` rows, stacked [hi; lo; hi] (dst [groups*3*rows, cols]). */
 DM_API int dm_split3(const float* src, int groups, int rows, int cols, int layout, void* dst, void* stream);
 
+/* ---- A-side attention (reference cost C_a, costs.py:84-87) ----
+ * Causal GQA flash-attention forward, head_dim 128, tcgen05/TMEM/TMA. qkv is the bf16
+ * projection [T, (nh + 2*nkv) * 128] (q heads, then k heads, then v heads; T = batch *
+ * seq_len, sequences contiguous); out [T, nh * 128] bf16; lse [batch, nh, seq_len] fp32
+ * natural-log softmax normaliser of the scaled logits (scale 1/sqrt(128)).
+ * seq_len must be a multiple of 128. */
+DM_API int dm_attention_fwd(const void* qkv, int T, int seq_len, int nh, int nkv, int head_dim, void* out,
+                            float* lse, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,7 +24,7 @@ INCLUDE = ROOT / "include"
 BUILD = PKG / "_build"
 LIB = PKG / "libdm_moe.so"
 
-SOURCES = ["abi.cu", "dispatch.cu", "combine.cu", "grouped_gemm_sm100.cu", "fp32_mode.cu"]
+SOURCES = ["abi.cu", "dispatch.cu", "combine.cu", "grouped_gemm_sm100.cu", "fp32_mode.cu", "attention_fwd.cu"]
 HEADERS = ["dm_common.cuh", "dm_internal.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

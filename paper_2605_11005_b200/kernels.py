@@ -285,3 +285,15 @@ def wgrad_split3(a3, M, b3, N, seg_off, dW, beta=0.0, stream=None, seg_stride_ro
     for i, (pa, pb) in enumerate(((hi_a, hi_b), (hi_a, lo_b), (lo_a, hi_b))):
         _lib.call("dm_grouped_wgrad_strided", pa, M, 3 * M, pb, N, 3 * N, _ptr(so), nseg, E, total_rows, stride,
                   _ptr(dW), float(beta) if i == 0 else 1.0, _stream(stream))
+
+
+# ---------------------------------------------------------------- attention
+def attention_fwd(qkv, seq_len, nh, nkv, out, lse, stream=None):
+    """Causal GQA flash-attention forward (head_dim 128) on the packed projection
+    qkv [T, (nh + 2 nkv) * 128]: out [T, nh * 128] bf16, lse [T / seq_len, nh, seq_len]
+    fp32 (natural log, logits scaled by 1/sqrt(128))."""
+    T = qkv.shape[0]
+    _check(qkv, BF16, (T, (nh + 2 * nkv) * 128), "qkv")
+    _check(out, BF16, (T, nh * 128), "out")
+    _check(lse, F32, (T // seq_len, nh, seq_len), "lse")
+    _lib.call("dm_attention_fwd", _ptr(qkv), T, seq_len, nh, nkv, 128, _ptr(out), _ptr(lse), _stream(stream))
