@@ -2,18 +2,21 @@
 // attention of SURVEY.md §8f row 3, whose cost the reference only models,
 // C_a = b·(s·H²·(2+2/g) + 4·s²·H) (pkg/src/afpipe/costs.py:84-87).
 //
-// One CTA = one (sequence, query head, 128-query tile); head_dim 128. Warp roles:
-//   warp 0   TMA producer: the Q tile once, then K_j / V_j tiles through a 2-stage ring
-//   warp 1   MMA issuer (one thread): S_j = Q·K_jᵀ into one of two TMEM S buffers, then
-//            O += P_{j-1}·V_{j-1} into the TMEM O accumulator (P from smem, V MN-major)
-//   warp 2   TMEM allocator
-//   warps 4-7 softmax: thread r owns query row r (= TMEM lane r): reads its S row with
-//            tcgen05.ld, online softmax in the exp2 domain (running max m, sum l), rescales
-//            its O row in TMEM (tcgen05.ld/st) when the max moved, writes its P row (bf16)
-//            into the SWIZZLE_128B smem tile the next MMA reads; final O / l and the
-//            natural-log LSE go to global memory.
-// S_{j+1} is issued before PV_j, so the exponentials of tile j+1 overlap the P·V MMA of
-// tile j; the causal diagonal tile masks key > query. Query tiles run heaviest first.
+// One CTA = one (sequence, query head, pair of adjacent 128-query tiles A and B); head_dim
+// 128. Warp roles:
+//   warp 0    TMA: both Q tiles once, then K_j through a 2-stage ring
+//   warp 3    TMA: V_j (one stage; V_j is consumed by both tiles' P·V)
+//   warp 1    MMA issuer (one thread), per KV tile j in the ping-pong order
+//             S_A(j) = Q_A·K_jᵀ, O_B += P_B(j-1)·V_{j-1}, S_B(j) = Q_B·K_jᵀ, O_A += P_A(j)·V_j,
+//             so the tensor core works for one tile while the other tile's softmax runs
+//   warp 2    TMEM allocator (S_A, S_B, O_A, O_B: 4 x 128 fp32 columns)
+//   warps 4-7 / 8-11  softmax of tile A / B: thread r owns query row r (= TMEM lane r),
+//             reads its S row with tcgen05.ld, online softmax in the exp2 domain with a lazy
+//             running max, rescales its O row in TMEM (tcgen05.ld/st) when the max moved, and
+//             writes its P row (bf16) into the SWIZZLE_128B smem tile the P·V MMA reads; the
+//             final O / l and the natural-log LSE go to global memory.
+// Causal: tile A stops at its diagonal KV tile 2p, tile B at 2p+1 (both diagonals masked
+// key > query). Pairs run heaviest first.
 #include "dm_common.cuh"
 #include "dm_internal.h"
 
@@ -25,8 +28,9 @@ constexpr int AT_BN = 128;                              // keys per KV tile
 constexpr int AT_STAGES = 2;
 constexpr uint32_t AT_TILE = AT_BM * AT_D * 2;          // 32 KiB: one Q, K, V or P tile
 constexpr uint32_t AT_ATOM = AT_BM * 128;               // 16 KiB: 128 rows x 64 bf16 (SWIZZLE_128B)
-constexpr int AT_THREADS = 256;
-constexpr size_t AT_SMEM = 1024 + (size_t)AT_TILE * (2 + 2 * AT_STAGES) + 256;
+constexpr int AT_THREADS = 384;
+// Q_A, Q_B | P_A, P_B | K ring (AT_STAGES) | V
+constexpr size_t AT_SMEM = 1024 + (size_t)AT_TILE * (5 + AT_STAGES) + 256;
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -38,6 +42,15 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// The running max only moves when a row's new max exceeds it by more than 2^8 (log2
+// domain): P entries stay <= 256 (exact in fp32, representable in bf16) and the O rescale
+// (tcgen05.ld/st of the whole O row) is skipped on most tiles; m, l and O stay consistent.
+constexpr float AT_RESCALE_LOG2 = 8.0f;
 
 // K-major [128 rows x 128] bf16 tile stored as two 64-column SWIZZLE_128B atoms: k16 step kk.
 __device__ __forceinline__ uint64_t at_kmajor(uint32_t base, int kk) {
@@ -54,36 +67,43 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
-  uint8_t* sQ = smem;
-  uint8_t* sP = smem + AT_TILE;
-  uint8_t* sKV = smem + 2 * AT_TILE;                    // stage s: K at +2s·TILE, V at +(2s+1)·TILE
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)AT_TILE * (2 + 2 * AT_STAGES));
+  uint8_t* sQ = smem;                                   // tile t at +t·TILE
+  uint8_t* sP = smem + 2 * AT_TILE;                     // tile t at +t·TILE
+  uint8_t* sK = smem + 4 * AT_TILE;                     // stage s at +s·TILE
+  uint8_t* sV = smem + (4 + AT_STAGES) * AT_TILE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)AT_TILE * (5 + AT_STAGES));
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;                         // [AT_STAGES]
-  uint64_t* kv_empty = bars + 1 + AT_STAGES;            // [AT_STAGES]
-  uint64_t* s_full = bars + 1 + 2 * AT_STAGES;          // [2]
-  uint64_t* s_free = bars + 3 + 2 * AT_STAGES;          // [2]
-  uint64_t* p_full = bars + 5 + 2 * AT_STAGES;
-  uint64_t* pv_done = bars + 6 + 2 * AT_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * AT_STAGES);
+  uint64_t* k_full = bars + 1;                          // [AT_STAGES]
+  uint64_t* k_empty = bars + 1 + AT_STAGES;             // [AT_STAGES]
+  uint64_t* v_full = bars + 1 + 2 * AT_STAGES;
+  uint64_t* v_empty = bars + 2 + 2 * AT_STAGES;
+  uint64_t* s_full = bars + 3 + 2 * AT_STAGES;          // [2] per tile
+  uint64_t* s_free = bars + 5 + 2 * AT_STAGES;          // [2]
+  uint64_t* p_full = bars + 7 + 2 * AT_STAGES;          // [2]
+  uint64_t* pv_done = bars + 9 + 2 * AT_STAGES;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * AT_STAGES);
 
-  const int n_qt = seq_len / AT_BM;
-  const int qt = n_qt - 1 - (int)blockIdx.x;            // longest causal rows first
+  const int n_pairs = seq_len / (2 * AT_BM);
+  const int pair = n_pairs - 1 - (int)blockIdx.x;       // longest causal rows first
+  const int qt0 = 2 * pair;                             // tile A = qt0, tile B = qt0 + 1
+  const int nA = qt0 + 1, nB = qt0 + 2;                 // KV tiles each tile attends to
   const int h = blockIdx.y, b = blockIdx.z;
   const int hk = h / (nh / nkv);
   const int row0 = b * seq_len;
-  const int n_kv = qt + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < AT_STAGES; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_free[i], AT_BM); }
-    mbar_init(p_full, AT_BM);
-    mbar_init(pv_done, 1);
+    for (int s = 0; s < AT_STAGES; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1); mbar_init(&s_free[t], AT_BM);
+      mbar_init(&p_full[t], AT_BM); mbar_init(&pv_done[t], 1);
+    }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);            // S0 [0,128) S1 [128,256) O [256,384)
+  if (warp == 2) tmem_alloc(tmem_slot, 512);            // S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -92,21 +112,31 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
   if (warp == 0) {
     if (lane == 0) {
       tma_prefetch_desc(&tm);
-      const int qcol = h * AT_D, kcol = (nh + hk) * AT_D, vcol = (nh + nkv + hk) * AT_D;
-      mbar_expect_tx(q_full, AT_TILE);
-      tma_load_2d(sQ, &tm, q_full, qcol, row0 + qt * AT_BM);
-      tma_load_2d(sQ + AT_ATOM, &tm, q_full, qcol + 64, row0 + qt * AT_BM);
-      for (int j = 0; j < n_kv; ++j) {
+      const int qcol = h * AT_D, kcol = (nh + hk) * AT_D;
+      mbar_expect_tx(q_full, 2 * AT_TILE);
+      for (int t = 0; t < 2; ++t) {
+        const int r = row0 + (qt0 + t) * AT_BM;
+        tma_load_2d(sQ + t * AT_TILE, &tm, q_full, qcol, r);
+        tma_load_2d(sQ + t * AT_TILE + AT_ATOM, &tm, q_full, qcol + 64, r);
+      }
+      for (int j = 0; j < nB; ++j) {
         const int s = j % AT_STAGES;
-        mbar_wait(&kv_empty[s], ((j / AT_STAGES) & 1) ^ 1);
-        uint8_t* k = sKV + (size_t)s * 2 * AT_TILE;
-        uint8_t* v = k + AT_TILE;
-        const int r = row0 + j * AT_BN;
-        mbar_expect_tx(&kv_full[s], 2 * AT_TILE);
-        tma_load_2d(k, &tm, &kv_full[s], kcol, r);
-        tma_load_2d(k + AT_ATOM, &tm, &kv_full[s], kcol + 64, r);
-        tma_load_2d(v, &tm, &kv_full[s], vcol, r);
-        tma_load_2d(v + AT_ATOM, &tm, &kv_full[s], vcol + 64, r);
+        mbar_wait(&k_empty[s], ((j / AT_STAGES) & 1) ^ 1);
+        uint8_t* k = sK + (size_t)s * AT_TILE;
+        mbar_expect_tx(&k_full[s], AT_TILE);
+        tma_load_2d(k, &tm, &k_full[s], kcol, row0 + j * AT_BN);
+        tma_load_2d(k + AT_ATOM, &tm, &k_full[s], kcol + 64, row0 + j * AT_BN);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    if (lane == 0) {
+      const int vcol = (nh + nkv + hk) * AT_D;
+      for (int j = 0; j < nB; ++j) {
+        mbar_wait(v_empty, (j & 1) ^ 1);
+        mbar_expect_tx(v_full, AT_TILE);
+        tma_load_2d(sV, &tm, v_full, vcol, row0 + j * AT_BN);
+        tma_load_2d(sV + AT_ATOM, &tm, v_full, vcol + 64, row0 + j * AT_BN);
       }
     }
     __syncwarp();
@@ -114,86 +144,108 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(AT_BM, AT_BN, 0, 0);   // Q K-major, K K-major
       constexpr uint32_t idesc_o = make_idesc_bf16(AT_BM, AT_D, 0, 1);    // P K-major, V MN-major
-      const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP);
+      const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP), va = smem_u32(sV);
+      auto mma_s = [&](int t, uint32_t ka) {
+#pragma unroll
+        for (int kk = 0; kk < AT_D / 16; ++kk)
+          umma_bf16_ss(tmem + t * AT_BN, at_kmajor(qa + t * AT_TILE, kk), at_kmajor(ka, kk), idesc_s,
+                       kk > 0 ? 1u : 0u);
+        umma_commit(&s_full[t]);
+      };
+      auto mma_pv = [&](int t, int j) {
+#pragma unroll
+        for (int kk = 0; kk < AT_BN / 16; ++kk)
+          umma_bf16_ss(tmem + (2 + t) * AT_BN, at_kmajor(pa + t * AT_TILE, kk), at_mnmajor(va, kk), idesc_o,
+                       (j | kk) != 0 ? 1u : 0u);
+        umma_commit(&pv_done[t]);
+      };
       mbar_wait(q_full, 0);
-      tc_fence_after();
-      for (int j = 0; j <= n_kv; ++j) {
-        if (j < n_kv) {
-          const int s = j % AT_STAGES, sb = j & 1;
-          mbar_wait(&kv_full[s], (j / AT_STAGES) & 1);
-          if (j >= 2) mbar_wait(&s_free[sb], ((j - 2) >> 1) & 1);
+      for (int j = 0; j < nB; ++j) {
+        const int s = j % AT_STAGES;
+        const uint32_t ka = smem_u32(sK + (size_t)s * AT_TILE);
+        mbar_wait(&k_full[s], (j / AT_STAGES) & 1);
+        if (j < nA) {                                   // S_A(j)
+          if (j >= 1) mbar_wait(&s_free[0], (j - 1) & 1);
           tc_fence_after();
-          const uint32_t ka = smem_u32(sKV + (size_t)s * 2 * AT_TILE);
-#pragma unroll
-          for (int kk = 0; kk < AT_D / 16; ++kk)
-            umma_bf16_ss(tmem + sb * AT_BN, at_kmajor(qa, kk), at_kmajor(ka, kk), idesc_s, kk > 0 ? 1u : 0u);
-          umma_commit(&s_full[sb]);
+          mma_s(0, ka);
         }
-        if (j >= 1) {
-          const int jj = j - 1, s = jj % AT_STAGES;
-          mbar_wait(p_full, jj & 1);
+        if (j >= 1) {                                   // O_B += P_B(j-1)·V_{j-1}; V_{j-1} done
+          mbar_wait(&p_full[1], (j - 1) & 1);
           tc_fence_after();
-          const uint32_t va = smem_u32(sKV + (size_t)s * 2 * AT_TILE + AT_TILE);
-#pragma unroll
-          for (int kk = 0; kk < AT_BN / 16; ++kk)
-            umma_bf16_ss(tmem + 2 * AT_BN, at_kmajor(pa, kk), at_mnmajor(va, kk), idesc_o,
-                         (jj | kk) != 0 ? 1u : 0u);
-          umma_commit(pv_done);
-          umma_commit(&kv_empty[s]);
+          mma_pv(1, j - 1);
+          umma_commit(v_empty);
+        }
+        if (j >= 1) mbar_wait(&s_free[1], (j - 1) & 1); // S_B(j); K_j done
+        tc_fence_after();
+        mma_s(1, ka);
+        umma_commit(&k_empty[s]);
+        if (j < nA) {                                   // O_A += P_A(j)·V_j
+          mbar_wait(v_full, j & 1);
+          mbar_wait(&p_full[0], j & 1);
+          tc_fence_after();
+          mma_pv(0, j);
         }
       }
+      mbar_wait(v_full, (nB - 1) & 1);                  // O_B += P_B(last)·V_last
+      mbar_wait(&p_full[1], (nB - 1) & 1);
+      tc_fence_after();
+      mma_pv(1, nB - 1);
+      umma_commit(v_empty);
     }
     __syncwarp();
   } else if (warp >= 4) {
+    const int t = (warp - 4) >> 2;                      // 0: tile A, 1: tile B
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;                       // query row in the tile = TMEM lane
+    const int qt = qt0 + t, n = t ? nB : nA;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
-    const uint32_t prow = smem_u32(sP);
+    const uint32_t tS = trow + t * AT_BN, tO = trow + (2 + t) * AT_BN;
+    const uint32_t prow = smem_u32(sP) + t * AT_TILE;
     float m = -INFINITY, l = 0.0f;
-    for (int j = 0; j < n_kv; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
       uint32_t sv[AT_BN];
 #pragma unroll
       for (int c = 0; c < AT_BN / 16; ++c)
-        tmem_ld16(trow + sb * AT_BN + c * 16, *reinterpret_cast<uint32_t(*)[16]>(sv + c * 16));
+        tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(sv + c * 16));
       tmem_wait_ld();
       tc_fence_before();
-      mbar_arrive(&s_free[sb]);                         // the MMA may overwrite this S buffer
+      mbar_arrive(&s_free[t]);                          // the MMA may overwrite this S buffer
       if (j == qt) {                                    // diagonal tile: key > query is masked
 #pragma unroll
         for (int c = 0; c < AT_BN; ++c)
           if (c > r) sv[c] = __float_as_uint(-INFINITY);
       }
-      float mx = -INFINITY;
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < AT_BN; ++c) mx = fmaxf(mx, __uint_as_float(sv[c]));
-      const float m_new = fmaxf(m, mx * scale_log2);
-      const float alpha = exp2f(m - m_new);             // 0 on the first tile
-      float sum = 0.0f;
-      uint32_t pk[AT_BN / 2];
+      for (int c = 0; c < AT_BN; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(sv[c]));
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
+      const bool move = mx > m + AT_RESCALE_LOG2;       // always on the first tile (m = -inf)
+      const float m_new = move ? mx : m;
+      const float alpha = move ? ex2(m - m_new) : 1.0f; // 0 on the first tile
+      float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int c = 0; c < AT_BN / 2; ++c) {
-        const float p0 = exp2f(__fmaf_rn(__uint_as_float(sv[2 * c]), scale_log2, -m_new));
-        const float p1 = exp2f(__fmaf_rn(__uint_as_float(sv[2 * c + 1]), scale_log2, -m_new));
-        sum += p0 + p1;
-        pk[c] = pack_bf16(p0, p1);
+      for (int c = 0; c < AT_BN / 2; ++c) {             // P packed in place: sv[c] = bf16x2(p_2c, p_2c+1)
+        const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[2 * c]), scale_log2, -m_new));
+        const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[2 * c + 1]), scale_log2, -m_new));
+        sum4[c & 3] += p0 + p1;
+        sv[c] = pack_bf16(p0, p1);
       }
-      l = __fmaf_rn(l, alpha, sum);
+      l = __fmaf_rn(l, alpha, (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
       m = m_new;
       if (j >= 1) {
-        mbar_wait(pv_done, (j - 1) & 1);                // O holds tiles < j; P buffer is free
+        mbar_wait(&pv_done[t], (j - 1) & 1);            // O holds tiles < j; P buffer is free
         tc_fence_after();
         if (__any_sync(0xffffffffu, alpha != 1.0f)) {
 #pragma unroll 1
           for (int c = 0; c < AT_D / 16; ++c) {
             uint32_t o[16];
-            tmem_ld16(trow + 2 * AT_BN + c * 16, o);
+            tmem_ld16(tO + c * 16, o);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(trow + 2 * AT_BN + c * 16, o);
+            tmem_st16(tO + c * 16, o);
           }
           tmem_wait_st();
         }
@@ -202,21 +254,21 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const uint32_t* q = pk + a * 32 + c * 4;
+          const uint32_t* q = sv + a * 32 + c * 4;
           st_shared_v4(prow + a * AT_ATOM + sw128(r, c), q[0], q[1], q[2], q[3]);
         }
       fence_proxy_async_smem();                         // generic-proxy P writes -> tensor core
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[t]);
     }
-    mbar_wait(pv_done, (n_kv - 1) & 1);
+    mbar_wait(&pv_done[t], (n - 1) & 1);
     tc_fence_after();
     const float inv = 1.0f / l;
     __nv_bfloat16* orow = out + (size_t)(row0 + qt * AT_BM + r) * ld_out + (size_t)h * AT_D;
 #pragma unroll 1
     for (int c = 0; c < AT_D / 16; ++c) {
       uint32_t o[16];
-      tmem_ld16(trow + 2 * AT_BN + c * 16, o);
+      tmem_ld16(tO + c * 16, o);
       tmem_wait_ld();
       uint32_t w[8];
 #pragma unroll
@@ -241,8 +293,8 @@ using namespace dm;
 int dm_attention_fwd(const void* qkv, int T, int seq_len, int nh, int nkv, int head_dim, void* out, float* lse,
                      void* stream) {
   if (head_dim != AT_D) return set_error(DM_ERR_SHAPE, "attention_fwd: head_dim %d (only 128)", head_dim);
-  if (T < 1 || seq_len < AT_BM || seq_len % AT_BM || T % seq_len)
-    return set_error(DM_ERR_SHAPE, "attention_fwd: seq_len %d must be a multiple of 128 dividing T=%d", seq_len, T);
+  if (T < 1 || seq_len < 2 * AT_BM || seq_len % (2 * AT_BM) || T % seq_len)
+    return set_error(DM_ERR_SHAPE, "attention_fwd: seq_len %d must be a multiple of 256 dividing T=%d", seq_len, T);
   if (nh < 1 || nkv < 1 || nh % nkv) return set_error(DM_ERR_SHAPE, "attention_fwd: %d heads, %d kv heads", nh, nkv);
   if ((reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
     return set_error(DM_ERR_ALIGN, "attention_fwd: qkv/out not 16-byte aligned");
@@ -265,7 +317,7 @@ int dm_attention_fwd(const void* qkv, int T, int seq_len, int nh, int nkv, int h
     configured = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)AT_D);
-  dim3 grid(seq_len / AT_BM, nh, T / seq_len);
+  dim3 grid(seq_len / (2 * AT_BM), nh, T / seq_len);
   attn_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, (cudaStream_t)stream>>>(
       tm, seq_len, nh, nkv, nh * AT_D, reinterpret_cast<__nv_bfloat16*>(out), lse, scale_log2);
   cudaError_t e = cudaGetLastError();
