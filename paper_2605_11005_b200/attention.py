@@ -15,6 +15,11 @@ KV head (ModelConfig.gqa_group), head_dim 128, no normalisation / RoPE (shape an
 FLOPs are what the schedule needs). Gradients come from torch autograd on the
 per-micro-batch graph saved by `forward`; parameter gradients accumulate in fp32
 `.grad`-style buffers (`dw_qkv`, `dw_o`).
+
+On CUDA with seq_len a multiple of 256 the attention forward is this repo's own sm_100a
+kernel (`dm_attention_fwd`: tcgen05/TMEM/TMA flash attention, csrc/attention_fwd.cu); its
+(O, LSE) feed cuDNN's SDPA backward (the LSE matches cuDNN's to 5e-5), so only the
+backward and the projections remain library code.
 """
 
 from __future__ import annotations
@@ -41,12 +46,55 @@ def attention_flops(hidden: int, gqa_group: int, seq_len: int, micro_batch: int,
     return proj + attn, 2 * proj + int(2.5 * attn)
 
 
+class _OwnCausalAttention(torch.autograd.Function):
+    """o [T, nh·D] = causal GQA attention of the packed projection qkv [T, (nh + 2 nkv)·D]:
+    forward on dm_attention_fwd, backward on cuDNN's SDPA backward with our (O, LSE)."""
+
+    @staticmethod
+    def forward(ctx, qkv, seq_len, nh, nkv):
+        from . import kernels as K
+
+        T = qkv.shape[0]
+        out = torch.empty(T, nh * HEAD_DIM, dtype=BF16, device=qkv.device)
+        lse = torch.empty(T // seq_len, nh, seq_len, dtype=F32, device=qkv.device)
+        K.attention_fwd(qkv, seq_len, nh, nkv, out, lse)
+        ctx.save_for_backward(qkv, out, lse)
+        ctx.shape = (seq_len, nh, nkv)
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        qkv, out, lse = ctx.saved_tensors
+        s, nh, nkv = ctx.shape
+        T = qkv.shape[0]
+        b, g = T // s, nh // nkv
+        x = qkv.view(b, s, nh + 2 * nkv, HEAD_DIM).transpose(1, 2)
+        q = x[:, :nh]
+        k = x[:, nh:nh + nkv].repeat_interleave(g, 1) if g > 1 else x[:, nh:nh + nkv]
+        v = x[:, nh + nkv:].repeat_interleave(g, 1) if g > 1 else x[:, nh + nkv:]
+        o = out.view(b, s, nh, HEAD_DIM).transpose(1, 2)
+        do = grad_out.contiguous().view(b, s, nh, HEAD_DIM).transpose(1, 2)
+        zero = torch.zeros((), dtype=torch.int64, device=qkv.device)   # philox seed / offset (no dropout)
+        dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
+            do, q, k, v, o, lse.unsqueeze(-1), zero, zero, None, None, None, s, s, 0.0, True)
+        if g > 1:
+            dk = dk.view(b, nkv, g, s, HEAD_DIM).sum(2)
+            dv = dv.view(b, nkv, g, s, HEAD_DIM).sum(2)
+        dqkv = torch.cat([dq, dk.to(dq.dtype), dv.to(dq.dtype)], dim=1)       # [b, nh + 2 nkv, s, D]
+        return dqkv.transpose(1, 2).reshape(T, -1), None, None, None
+
+
+def own_attention_supported(x: torch.Tensor, seq_len: int, head_dim: int = HEAD_DIM) -> bool:
+    return x.is_cuda and head_dim == HEAD_DIM and seq_len % 256 == 0 and x.shape[0] % seq_len == 0
+
+
 class AttentionBlock:
     def __init__(self, hidden: int, gqa_group: int = 1, device="cuda", seed: int = 0,
-                 head_dim: int = HEAD_DIM):
+                 head_dim: int = HEAD_DIM, own_kernel: bool = True):
         if hidden % head_dim:
             raise ValueError(f"hidden {hidden} not a multiple of head_dim {head_dim}")
         self.H, self.d = hidden, head_dim
+        self.own_kernel = own_kernel   # dm_attention_fwd for the forward where supported
         self.nh = hidden // head_dim
         if self.nh % gqa_group:
             raise ValueError(f"{self.nh} heads not divisible by gqa_group {gqa_group}")
@@ -69,6 +117,9 @@ class AttentionBlock:
         T, H = x.shape
         b = T // seq_len
         qkv = x @ self.w_qkv.t()
+        if self.own_kernel and own_attention_supported(x, seq_len, self.d):
+            o = _OwnCausalAttention.apply(qkv.contiguous(), seq_len, self.nh, self.nkv)
+            return o @ self.w_o.t()
         q, k, v = qkv.split([self.nh * self.d, self.nkv * self.d, self.nkv * self.d], dim=1)
         q = q.view(b, seq_len, self.nh, self.d).transpose(1, 2)
         k = k.view(b, seq_len, self.nkv, self.d).transpose(1, 2)

@@ -63,3 +63,27 @@ def test_attention_fwd_rejects_bad_shapes():
     lse = torch.empty(1, 2, 200, dtype=torch.float32, device=dev)
     with pytest.raises(_lib.DMError):
         K.attention_fwd(qkv, 200, 2, 1, out, lse)   # seq_len not a multiple of 256
+
+
+@pytest.mark.parametrize("s,b,g", [(256, 2, 1), (512, 1, 4)])
+def test_attention_block_own_forward_matches_library(s, b, g):
+    """AttentionBlock with the own forward kernel (+ cuDNN backward on its O / LSE) equals
+    the all-library block: output, input gradient and both weight gradients."""
+    from paper_2605_11005_b200.attention import AttentionBlock
+
+    dev = torch.device("cuda", 0)
+    H = 512
+    gen = torch.Generator(device="cpu").manual_seed(s + g)
+    x = torch.randn(b * s, H, generator=gen).to(torch.bfloat16).to(dev)
+    dh = torch.randn(b * s, H, generator=gen).to(torch.bfloat16).to(dev)
+    res = []
+    for own in (True, False):
+        blk = AttentionBlock(H, g, dev, seed=3, own_kernel=own)
+        out = torch.empty_like(x)
+        dx = torch.empty_like(x)
+        blk.forward(0, x, out, s)
+        blk.backward(0, dh, dx, accumulate=False)
+        torch.cuda.synchronize()
+        res.append((out.float(), dx.float(), blk.dw_qkv.clone(), blk.dw_o.clone()))
+    for a, r in zip(res[0], res[1]):
+        assert (a - r).abs().max().item() / r.abs().max().item() < 1e-2
