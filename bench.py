@@ -446,7 +446,9 @@ def run_ours(args, shape, exp):
         fa, fb = attn[0].flops(exp.workload.seq_len, exp.workload.micro_batch)
         line["attention"] = {
             "ms_per_microbatch_layer": round(a_ms, 4), "TFLOP/s": round((fa + fb) / (a_ms / 1e3) / 1e12, 1),
-            "impl": "library stopgap (SURVEY §8f-3): cuBLAS projections + torch SDPA (cuDNN/flash), autograd",
+            "impl": ("own sm_100a flash-attention forward (dm_attention_fwd) + cuDNN SDPA backward on its O/LSE; "
+                     "cuBLAS projections, autograd" if attn[0].own_kernel and exp.workload.seq_len % 256 == 0
+                     else "library: cuBLAS projections + torch SDPA (cuDNN/flash), autograd"),
             "gqa_group": exp.model.gqa_group, "seq_len": exp.workload.seq_len}
         line["config"]["layer"] = "attention + residual MoE block"
         line["config"]["launch"] = "CUDA graphs" if graphs is not None else "eager"
@@ -617,7 +619,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                 "parallelism": f"AF-Pipe {topo.n_attn}A:{topo.n_ffn}F" + (f" x {topo.depth} pipeline groups"
                                                                            if topo.depth > 1 else "") + " (A: DP "
                                + ("attention + " if args.attention else "") + "routing/combine, F: EP experts)",
-                "layer": "attention + residual MoE block (attention: library stopgap)" if args.attention
+                "layer": "attention + residual MoE block (attention: own forward kernel, library backward)" if args.attention
                          else "MoE block",
                 "transport": "NCCL send/recv (torch.distributed P2P) over NVLink",
                 "weights": "random-init", "l2": "inputs+weights larger than L2",
@@ -811,7 +813,7 @@ def main(argv=None):
     ap.add_argument("--eager", action="store_true", help="N=1: launch kernels eagerly instead of CUDA graphs")
     ap.add_argument("--no-isolated", action="store_true", help="skip the isolated A-side kernel timing")
     ap.add_argument("--attention", action="store_true",
-                    help="add the A-side causal attention block to every layer (library stopgap; sweeps)")
+                    help="add the A-side causal attention block to every layer (own forward kernel, cuDNN backward; sweeps)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
