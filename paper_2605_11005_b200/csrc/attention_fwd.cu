@@ -47,6 +47,23 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Packed fp32 pairs (FADD2) and three-input max (FMNMX3): the softmax warps are issue-bound
+// (an FMA-pipe exp2 polynomial for part of the row measured slower), so the row reductions
+// and the exp2 argument FMAs run two elements per instruction.
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long ra, rb, rc;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(rc) : "l"(ra), "l"(rb));
+  float2 d;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rc));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 // The running max only moves when a row's new max exceeds it by more than 2^8 (log2
 // domain): P entries stay <= 256 (exact in fp32, representable in bf16) and the O rescale
 // (tcgen05.ld/st of the whole O row) is skipped on most tiles; m, l and O stay consistent.
@@ -219,20 +236,23 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
       }
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < AT_BN; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(sv[c]));
-      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
+      for (int c = 0; c < AT_BN / 2; ++c)
+        mx4[c & 3] = fmax3(mx4[c & 3], __uint_as_float(sv[2 * c]), __uint_as_float(sv[2 * c + 1]));
+      const float mx = fmax3(mx4[0], mx4[1], fmaxf(mx4[2], mx4[3])) * scale_log2;
       const bool move = mx > m + AT_RESCALE_LOG2;       // always on the first tile (m = -inf)
       const float m_new = move ? mx : m;
       const float alpha = move ? ex2(m - m_new) : 1.0f; // 0 on the first tile
-      float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      float2 sum2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_new, -m_new);
 #pragma unroll
       for (int c = 0; c < AT_BN / 2; ++c) {             // P packed in place: sv[c] = bf16x2(p_2c, p_2c+1)
-        const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[2 * c]), scale_log2, -m_new));
-        const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[2 * c + 1]), scale_log2, -m_new));
-        sum4[c & 3] += p0 + p1;
-        sv[c] = pack_bf16(p0, p1);
+        const float2 x = ffma2(make_float2(__uint_as_float(sv[2 * c]), __uint_as_float(sv[2 * c + 1])), sc2, nm2);
+        const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+        sum2[c & 3] = fadd2(sum2[c & 3], pp);
+        sv[c] = pack_bf16(pp.x, pp.y);
       }
-      l = __fmaf_rn(l, alpha, (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
+      const float2 s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
+      l = __fmaf_rn(l, alpha, s01.x + s01.y);
       m = m_new;
       if (j >= 1) {
         mbar_wait(&pv_done[t], (j - 1) & 1);            // O holds tiles < j; P buffer is free
