@@ -6,9 +6,10 @@
 // 128. Warp roles:
 //   warp 0    TMA: both Q tiles once, then K_j through a 2-stage ring
 //   warp 3    TMA: V_j (one stage; V_j is consumed by both tiles' P·V)
-//   warp 1    MMA issuer (one thread), per KV tile j in the ping-pong order
-//             S_A(j) = Q_A·K_jᵀ, O_B += P_B(j-1)·V_{j-1}, S_B(j) = Q_B·K_jᵀ, O_A += P_A(j)·V_j,
-//             so the tensor core works for one tile while the other tile's softmax runs
+//   warp 1    MMA issuer (one thread), per KV tile j: S_A(j) = Q_A·K_jᵀ, S_B(j) = Q_B·K_jᵀ,
+//             O_A += P_A(j-1)·V_{j-1}, O_B += P_B(j-1)·V_{j-1}: each tile's softmax of KV tile j
+//             overlaps the other MMAs of the step, so the tensor core works for one tile
+//             while the other tile's softmax runs
 //   warp 2    TMEM allocator (S_A, S_B, O_A, O_B: 4 x 128 fp32 columns)
 //   warps 4-7 / 8-11  softmax of tile A / B: thread r owns query row r (= TMEM lane r),
 //             reads its S row with tcgen05.ld, online softmax in the exp2 domain with a lazy
@@ -177,37 +178,38 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
         umma_commit(&pv_done[t]);
       };
       mbar_wait(q_full, 0);
-      for (int j = 0; j < nB; ++j) {
-        const int s = j % AT_STAGES;
-        const uint32_t ka = smem_u32(sK + (size_t)s * AT_TILE);
-        mbar_wait(&k_full[s], (j / AT_STAGES) & 1);
-        if (j < nA) {                                   // S_A(j)
-          if (j >= 1) mbar_wait(&s_free[0], (j - 1) & 1);
+      // iteration j: S_A(j), S_B(j), then O_A += P_A(j-1)·V_{j-1}, O_B += P_B(j-1)·V_{j-1}.
+      // Both P·V of a KV tile run back to back, so V_j has two S MMAs of slack to land and
+      // each tile's softmax has the other three MMAs of the step to hide behind.
+      for (int j = 0; j <= nB; ++j) {
+        if (j < nB) {
+          const int s = j % AT_STAGES;
+          const uint32_t ka = smem_u32(sK + (size_t)s * AT_TILE);
+          mbar_wait(&k_full[s], (j / AT_STAGES) & 1);
+          if (j < nA) {
+            if (j >= 1) mbar_wait(&s_free[0], (j - 1) & 1);
+            tc_fence_after();
+            mma_s(0, ka);
+          }
+          if (j >= 1) mbar_wait(&s_free[1], (j - 1) & 1);
           tc_fence_after();
-          mma_s(0, ka);
+          mma_s(1, ka);
+          umma_commit(&k_empty[s]);
         }
-        if (j >= 1) {                                   // O_B += P_B(j-1)·V_{j-1}; V_{j-1} done
-          mbar_wait(&p_full[1], (j - 1) & 1);
+        if (j >= 1) {
+          const int jj = j - 1;
+          mbar_wait(v_full, jj & 1);
+          if (jj < nA) {
+            mbar_wait(&p_full[0], jj & 1);
+            tc_fence_after();
+            mma_pv(0, jj);
+          }
+          mbar_wait(&p_full[1], jj & 1);
           tc_fence_after();
-          mma_pv(1, j - 1);
+          mma_pv(1, jj);
           umma_commit(v_empty);
         }
-        if (j >= 1) mbar_wait(&s_free[1], (j - 1) & 1); // S_B(j); K_j done
-        tc_fence_after();
-        mma_s(1, ka);
-        umma_commit(&k_empty[s]);
-        if (j < nA) {                                   // O_A += P_A(j)·V_j
-          mbar_wait(v_full, j & 1);
-          mbar_wait(&p_full[0], j & 1);
-          tc_fence_after();
-          mma_pv(0, j);
-        }
       }
-      mbar_wait(v_full, (nB - 1) & 1);                  // O_B += P_B(last)·V_last
-      mbar_wait(&p_full[1], (nB - 1) & 1);
-      tc_fence_after();
-      mma_pv(1, nB - 1);
-      umma_commit(v_empty);
     }
     __syncwarp();
   } else if (warp >= 4) {
