@@ -253,7 +253,7 @@ DM_API int dm_split3(const float* src, int groups, int rows, int cols, int layou
  * projection [T, (nh + 2*nkv) * 128] (q heads, then k heads, then v heads; T = batch *
  * seq_len, sequences contiguous); out [T, nh * 128] bf16; lse [batch, nh, seq_len] fp32
  * natural-log softmax normaliser of the scaled logits (scale 1/sqrt(128)).
- * seq_len must be a multiple of 128. */
+ * seq_len must be a multiple of 128 (of 256 when nh / nkv is odd). */
 DM_API int dm_attention_fwd(const void* qkv, int T, int seq_len, int nh, int nkv, int head_dim, void* out,
                             float* lse, void* stream);
 

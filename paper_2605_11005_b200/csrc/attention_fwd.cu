@@ -16,8 +16,9 @@
 //             running max, rescales its O row in TMEM (tcgen05.ld/st) when the max moved, and
 //             writes its P row (bf16) into the SWIZZLE_128B smem tile the P·V MMA reads; the
 //             final O / l and the natural-log LSE go to global memory.
-// Causal: tile A stops at its diagonal KV tile 2p, tile B at 2p+1 (both diagonals masked
-// key > query). Pairs run heaviest first.
+// Tiles A and B are two query heads of one KV group on the same rows (GQA with an even
+// group size: each K/V tile serves both) or two adjacent row tiles of one head. Causal:
+// each tile stops at its diagonal KV tile (masked key > query). Heaviest rows first.
 #include "dm_common.cuh"
 #include "dm_internal.h"
 
@@ -81,7 +82,7 @@ __device__ __forceinline__ uint64_t at_mnmajor(uint32_t base, int kk) {
 
 __global__ void __launch_bounds__(AT_THREADS, 1)
 attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int nkv, int ld_out,
-                __nv_bfloat16* __restrict__ out, float* __restrict__ lse, float scale_log2) {
+                __nv_bfloat16* __restrict__ out, float* __restrict__ lse, float scale_log2, int head_pairs) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
@@ -101,12 +102,22 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
   uint64_t* pv_done = bars + 9 + 2 * AT_STAGES;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * AT_STAGES);
 
-  const int n_pairs = seq_len / (2 * AT_BM);
-  const int pair = n_pairs - 1 - (int)blockIdx.x;       // longest causal rows first
-  const int qt0 = 2 * pair;                             // tile A = qt0, tile B = qt0 + 1
-  const int nA = qt0 + 1, nB = qt0 + 2;                 // KV tiles each tile attends to
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int hk = h / (nh / nkv);
+  // Tile pairing. GQA (an even number of query heads per KV head): tiles A and B are two
+  // query heads of one KV group on the same 128 rows, so every K/V tile loaded serves both.
+  // Otherwise: two adjacent 128-row tiles of one head (B attends to one more KV tile).
+  int qtA, qtB, hA, hB;
+  if (head_pairs) {
+    qtA = qtB = (int)gridDim.x - 1 - (int)blockIdx.x;   // longest causal rows first
+    hA = 2 * blockIdx.y;
+    hB = hA + 1;
+  } else {
+    qtA = 2 * ((int)gridDim.x - 1 - (int)blockIdx.x);
+    qtB = qtA + 1;
+    hA = hB = blockIdx.y;
+  }
+  const int nA = qtA + 1, nB = qtB + 1;                 // KV tiles each tile attends to
+  const int b = blockIdx.z;
+  const int hk = hA / (nh / nkv);
   const int row0 = b * seq_len;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -130,10 +141,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
   if (warp == 0) {
     if (lane == 0) {
       tma_prefetch_desc(&tm);
-      const int qcol = h * AT_D, kcol = (nh + hk) * AT_D;
+      const int kcol = (nh + hk) * AT_D;
       mbar_expect_tx(q_full, 2 * AT_TILE);
       for (int t = 0; t < 2; ++t) {
-        const int r = row0 + (qt0 + t) * AT_BM;
+        const int r = row0 + (t ? qtB : qtA) * AT_BM, qcol = (t ? hB : hA) * AT_D;
         tma_load_2d(sQ + t * AT_TILE, &tm, q_full, qcol, r);
         tma_load_2d(sQ + t * AT_TILE + AT_ATOM, &tm, q_full, qcol + 64, r);
       }
@@ -216,7 +227,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
     const int t = (warp - 4) >> 2;                      // 0: tile A, 1: tile B
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;                       // query row in the tile = TMEM lane
-    const int qt = qt0 + t, n = t ? nB : nA;
+    const int qt = t ? qtB : qtA, n = t ? nB : nA, h = t ? hB : hA;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     const uint32_t tS = trow + t * AT_BN, tO = trow + (2 + t) * AT_BN;
     const uint32_t prow = smem_u32(sP) + t * AT_TILE;
@@ -315,9 +326,11 @@ using namespace dm;
 int dm_attention_fwd(const void* qkv, int T, int seq_len, int nh, int nkv, int head_dim, void* out, float* lse,
                      void* stream) {
   if (head_dim != AT_D) return set_error(DM_ERR_SHAPE, "attention_fwd: head_dim %d (only 128)", head_dim);
-  if (T < 1 || seq_len < 2 * AT_BM || seq_len % (2 * AT_BM) || T % seq_len)
-    return set_error(DM_ERR_SHAPE, "attention_fwd: seq_len %d must be a multiple of 256 dividing T=%d", seq_len, T);
   if (nh < 1 || nkv < 1 || nh % nkv) return set_error(DM_ERR_SHAPE, "attention_fwd: %d heads, %d kv heads", nh, nkv);
+  const int row_tile = (nh / nkv) % 2 == 0 ? AT_BM : 2 * AT_BM;   // head pairs vs adjacent row tiles
+  if (T < 1 || seq_len < row_tile || seq_len % row_tile || T % seq_len)
+    return set_error(DM_ERR_SHAPE, "attention_fwd: seq_len %d must be a multiple of %d dividing T=%d", seq_len,
+                     row_tile, T);
   if ((reinterpret_cast<uintptr_t>(qkv) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
     return set_error(DM_ERR_ALIGN, "attention_fwd: qkv/out not 16-byte aligned");
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
@@ -339,9 +352,10 @@ int dm_attention_fwd(const void* qkv, int T, int seq_len, int nh, int nkv, int h
     configured = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)AT_D);
-  dim3 grid(seq_len / (2 * AT_BM), nh, T / seq_len);
+  const int head_pairs = (nh / nkv) % 2 == 0;
+  dim3 grid(head_pairs ? seq_len / AT_BM : seq_len / (2 * AT_BM), head_pairs ? nh / 2 : nh, T / seq_len);
   attn_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, (cudaStream_t)stream>>>(
-      tm, seq_len, nh, nkv, nh * AT_D, reinterpret_cast<__nv_bfloat16*>(out), lse, scale_log2);
+      tm, seq_len, nh, nkv, nh * AT_D, reinterpret_cast<__nv_bfloat16*>(out), lse, scale_log2, head_pairs);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "attention_fwd launch");
   note_launch();

@@ -30,7 +30,7 @@ def _reference(qkv, b, s, nh, nkv):
     return o.transpose(1, 2).reshape(b * s, nh * D), lse
 
 
-@pytest.mark.parametrize("b,s,nh,nkv", [(1, 256, 2, 1), (2, 256, 4, 2), (3, 512, 2, 2), (1, 1024, 8, 8), (1, 2048, 4, 1)])
+@pytest.mark.parametrize("b,s,nh,nkv", [(1, 256, 2, 1), (2, 256, 4, 2), (3, 512, 2, 2), (1, 1024, 8, 8), (1, 2048, 4, 1), (2, 384, 8, 2)])
 def test_attention_fwd_matches_fp32_reference(b, s, nh, nkv):
     from paper_2605_11005_b200 import kernels as K
 
@@ -62,7 +62,7 @@ def test_attention_fwd_rejects_bad_shapes():
     out = torch.empty(200, 2 * D, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(1, 2, 200, dtype=torch.float32, device=dev)
     with pytest.raises(_lib.DMError):
-        K.attention_fwd(qkv, 200, 2, 1, out, lse)   # seq_len not a multiple of 256
+        K.attention_fwd(qkv, 200, 2, 1, out, lse)   # seq_len not a multiple of 128
 
 
 @pytest.mark.parametrize("s,b,g", [(256, 2, 1), (512, 1, 4)])
