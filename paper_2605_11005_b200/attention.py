@@ -67,21 +67,20 @@ class _OwnCausalAttention(torch.autograd.Function):
         qkv, out, lse = ctx.saved_tensors
         s, nh, nkv = ctx.shape
         T = qkv.shape[0]
-        b, g = T // s, nh // nkv
-        x = qkv.view(b, s, nh + 2 * nkv, HEAD_DIM).transpose(1, 2)
-        q = x[:, :nh]
-        k = x[:, nh:nh + nkv].repeat_interleave(g, 1) if g > 1 else x[:, nh:nh + nkv]
-        v = x[:, nh + nkv:].repeat_interleave(g, 1) if g > 1 else x[:, nh + nkv:]
+        b = T // s
+        x = qkv.view(b, s, nh + 2 * nkv, HEAD_DIM).transpose(1, 2)        # [b, heads, s, D] views
+        q, k, v = x[:, :nh], x[:, nh:nh + nkv], x[:, nh + nkv:]            # GQA handled by cuDNN
         o = out.view(b, s, nh, HEAD_DIM).transpose(1, 2)
         do = grad_out.contiguous().view(b, s, nh, HEAD_DIM).transpose(1, 2)
         zero = torch.zeros((), dtype=torch.int64, device=qkv.device)   # philox seed / offset (no dropout)
         dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
             do, q, k, v, o, lse.unsqueeze(-1), zero, zero, None, None, None, s, s, 0.0, True)
-        if g > 1:
-            dk = dk.view(b, nkv, g, s, HEAD_DIM).sum(2)
-            dv = dv.view(b, nkv, g, s, HEAD_DIM).sum(2)
-        dqkv = torch.cat([dq, dk.to(dq.dtype), dv.to(dq.dtype)], dim=1)       # [b, nh + 2 nkv, s, D]
-        return dqkv.transpose(1, 2).reshape(T, -1), None, None, None
+        dqkv = torch.empty_like(qkv)
+        d = dqkv.view(b, s, nh + 2 * nkv, HEAD_DIM)
+        d[:, :, :nh].copy_(dq.transpose(1, 2))
+        d[:, :, nh:nh + nkv].copy_(dk.transpose(1, 2))
+        d[:, :, nh + nkv:].copy_(dv.transpose(1, 2))
+        return dqkv, None, None, None
 
 
 def own_attention_supported(x: torch.Tensor, seq_len: int, head_dim: int = HEAD_DIM) -> bool:
