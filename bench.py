@@ -393,12 +393,19 @@ def run_ours(args, shape, exp):
             hbm[name]["isolated_frac"] = round(gbs / peaks["hbm_gbs"], 3)
     # measured DRAM bytes of one iteration's GEMM launches (ncu; scripts/gemm_traffic.py),
     # per step like `achieved`, when a capture for this workload is committed
-    traffic = None
+    traffic, traffic_info = None, None
     for tfile in sorted((ROOT / "profiles").glob(f"*/gemm_traffic_{Path(args.config).stem}.json")):
         try:
-            traffic = json.loads(tfile.read_text()).get("bytes_per_iteration")
+            tj = json.loads(tfile.read_text())
+            traffic = tj.get("bytes_per_iteration")
+            n_l = len(tj.get("launches", [])) or None
+            traffic_info = {"unit": "DRAM bytes per step (all GEMM launches of one iteration, ncu)",
+                            "launches_per_step": n_l,
+                            "per_launch_avg": round(traffic / n_l) if traffic and n_l else None,
+                            "algorithmic_bytes_per_step": tj.get("algorithmic_bytes_per_iteration"),
+                            "ratio_to_algorithmic": tj.get("ratio"), "source": str(tfile.relative_to(ROOT))}
         except (ValueError, OSError):
-            traffic = None
+            traffic, traffic_info = None, None
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
@@ -416,9 +423,9 @@ def run_ours(args, shape, exp):
             "stage_breakdown": "separate eager pass with CUDA events per stage (not the timed region)",
         },
         "roofline": ({
-            "bound": "hbm", "kernel": "grouped expert GEMMs (K4/K5/K8, 6 launches per micro-batch)",
+            "bound": "hbm", "kernel": "grouped expert GEMMs (K4/K5/K8: 4 launches per micro-batch + 2 deferred wgrad launches per step)",
             "achieved": round(achieved_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(achieved_gbs / peaks["hbm_gbs"], 4), "traffic": traffic,
+            "frac": round(achieved_gbs / peaks["hbm_gbs"], 4), "traffic": traffic, "traffic_detail": traffic_info,
             "peak_kind": f"{peak_kind} HBM copy bandwidth (MEASURED_PEAKS.json)",
             "algorithmic_bytes_per_step": gemm_bytes // args.steps,
             "tensor_achieved_tflops": round(achieved_tf, 1), "tensor_frac": round(achieved_tf / peak_tf, 4),
@@ -426,9 +433,9 @@ def run_ours(args, shape, exp):
                    f"{ideal_tensor_ms / args.steps:.2f} ms/step (weights streamed per micro-batch)",
             "gemm_ms_per_microbatch_layer": round(gemm_ms / (args.steps * mb * L), 4),
         } if hbm_bound else {
-            "bound": "tensor", "kernel": "grouped expert GEMMs (K4/K5/K8, 6 launches per micro-batch)",
+            "bound": "tensor", "kernel": "grouped expert GEMMs (K4/K5/K8: 4 launches per micro-batch + 2 deferred wgrad launches per step)",
             "achieved": round(achieved_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
-            "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
+            "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic, "traffic_detail": traffic_info,
             "peak_kind": f"{peak_kind} sustained bf16 (MEASURED_PEAKS.json)",
             "gemm_ms_per_microbatch_layer": round(gemm_ms / (args.steps * mb * L), 4),
             "frac_of_burst": round(achieved_tf / peaks["bf16_tflops"], 4),
