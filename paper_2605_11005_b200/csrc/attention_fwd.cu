@@ -80,9 +80,38 @@ __device__ __forceinline__ uint64_t at_mnmajor(uint32_t base, int kk) {
   return make_sdesc_sw128(base + kk * 2048, AT_ATOM, 1024);
 }
 
+// One work item = two 128-query tiles (A, B): two query heads of one KV group on the same
+// rows (GQA with an even group: each K/V tile serves both) or two adjacent row tiles of one
+// head. Items are numbered heaviest (longest causal rows) first.
+struct AtItem {
+  int qtA, qtB, hA, hB, b;
+};
+__device__ __forceinline__ AtItem at_item(int i, int head_pairs, int n_qt, int nh, int nb) {
+  AtItem it;
+  if (head_pairs) {
+    const int per = (nh / 2) * nb, rt = i / per, rem = i % per;
+    it.qtA = it.qtB = n_qt - 1 - rt;
+    it.hA = 2 * (rem % (nh / 2));
+    it.hB = it.hA + 1;
+    it.b = rem / (nh / 2);
+  } else {
+    const int per = nh * nb, rt = i / per, rem = i % per;
+    it.qtA = 2 * (n_qt / 2 - 1 - rt);
+    it.qtB = it.qtA + 1;
+    it.hA = it.hB = rem % nh;
+    it.b = rem / nh;
+  }
+  return it;
+}
+
+// Persistent: one CTA per SM walks the items i = blockIdx.x, +gridDim.x, ...; TMEM, barriers
+// and the K/V rings live across items (phases from running counters), the next item's Q
+// load waits only for the last S MMAs of the previous one, and its first P·V waits for the
+// previous epilogue to drain O — prologue and epilogue overlap the neighbouring items.
 __global__ void __launch_bounds__(AT_THREADS, 1)
 attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int nkv, int ld_out,
-                __nv_bfloat16* __restrict__ out, float* __restrict__ lse, float scale_log2, int head_pairs) {
+                __nv_bfloat16* __restrict__ out, float* __restrict__ lse, float scale_log2, int head_pairs,
+                int nb) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
@@ -100,35 +129,25 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
   uint64_t* s_free = bars + 5 + 2 * AT_STAGES;          // [2]
   uint64_t* p_full = bars + 7 + 2 * AT_STAGES;          // [2]
   uint64_t* pv_done = bars + 9 + 2 * AT_STAGES;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12 + 2 * AT_STAGES);
+  uint64_t* o_free = bars + 11 + 2 * AT_STAGES;         // [2] epilogue drained O
+  uint64_t* q_empty = bars + 13 + 2 * AT_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14 + 2 * AT_STAGES);
 
-  // Tile pairing. GQA (an even number of query heads per KV head): tiles A and B are two
-  // query heads of one KV group on the same 128 rows, so every K/V tile loaded serves both.
-  // Otherwise: two adjacent 128-row tiles of one head (B attends to one more KV tile).
-  int qtA, qtB, hA, hB;
-  if (head_pairs) {
-    qtA = qtB = (int)gridDim.x - 1 - (int)blockIdx.x;   // longest causal rows first
-    hA = 2 * blockIdx.y;
-    hB = hA + 1;
-  } else {
-    qtA = 2 * ((int)gridDim.x - 1 - (int)blockIdx.x);
-    qtB = qtA + 1;
-    hA = hB = blockIdx.y;
-  }
-  const int nA = qtA + 1, nB = qtB + 1;                 // KV tiles each tile attends to
-  const int b = blockIdx.z;
-  const int hk = hA / (nh / nkv);
-  const int row0 = b * seq_len;
+  const int n_qt = seq_len / AT_BM;
+  const int n_items = head_pairs ? n_qt * (nh / 2) * nb : (n_qt / 2) * nh * nb;
+  const int g = nh / nkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int s = 0; s < AT_STAGES; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
     mbar_init(v_full, 1);
     mbar_init(v_empty, 1);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1); mbar_init(&s_free[t], AT_BM);
       mbar_init(&p_full[t], AT_BM); mbar_init(&pv_done[t], 1);
+      mbar_init(&o_free[t], AT_BM);
     }
     fence_mbar_init();
   }
@@ -141,31 +160,40 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
   if (warp == 0) {
     if (lane == 0) {
       tma_prefetch_desc(&tm);
-      const int kcol = (nh + hk) * AT_D;
-      mbar_expect_tx(q_full, 2 * AT_TILE);
-      for (int t = 0; t < 2; ++t) {
-        const int r = row0 + (t ? qtB : qtA) * AT_BM, qcol = (t ? hB : hA) * AT_D;
-        tma_load_2d(sQ + t * AT_TILE, &tm, q_full, qcol, r);
-        tma_load_2d(sQ + t * AT_TILE + AT_ATOM, &tm, q_full, qcol + 64, r);
-      }
-      for (int j = 0; j < nB; ++j) {
-        const int s = j % AT_STAGES;
-        mbar_wait(&k_empty[s], ((j / AT_STAGES) & 1) ^ 1);
-        uint8_t* k = sK + (size_t)s * AT_TILE;
-        mbar_expect_tx(&k_full[s], AT_TILE);
-        tma_load_2d(k, &tm, &k_full[s], kcol, row0 + j * AT_BN);
-        tma_load_2d(k + AT_ATOM, &tm, &k_full[s], kcol + 64, row0 + j * AT_BN);
+      int gk = 0, it = 0;
+      for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++it) {
+        const AtItem w = at_item(i, head_pairs, n_qt, nh, nb);
+        const int row0 = w.b * seq_len, kcol = (nh + w.hA / g) * AT_D, nB = w.qtB + 1;
+        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);   // previous item's S MMAs are done with Q
+        mbar_expect_tx(q_full, 2 * AT_TILE);
+        for (int t = 0; t < 2; ++t) {
+          const int r = row0 + (t ? w.qtB : w.qtA) * AT_BM, qcol = (t ? w.hB : w.hA) * AT_D;
+          tma_load_2d(sQ + t * AT_TILE, &tm, q_full, qcol, r);
+          tma_load_2d(sQ + t * AT_TILE + AT_ATOM, &tm, q_full, qcol + 64, r);
+        }
+        for (int j = 0; j < nB; ++j, ++gk) {
+          const int s = gk % AT_STAGES;
+          mbar_wait(&k_empty[s], ((gk / AT_STAGES) & 1) ^ 1);
+          uint8_t* k = sK + (size_t)s * AT_TILE;
+          mbar_expect_tx(&k_full[s], AT_TILE);
+          tma_load_2d(k, &tm, &k_full[s], kcol, row0 + j * AT_BN);
+          tma_load_2d(k + AT_ATOM, &tm, &k_full[s], kcol + 64, row0 + j * AT_BN);
+        }
       }
     }
     __syncwarp();
   } else if (warp == 3) {
     if (lane == 0) {
-      const int vcol = (nh + nkv + hk) * AT_D;
-      for (int j = 0; j < nB; ++j) {
-        mbar_wait(v_empty, (j & 1) ^ 1);
-        mbar_expect_tx(v_full, AT_TILE);
-        tma_load_2d(sV, &tm, v_full, vcol, row0 + j * AT_BN);
-        tma_load_2d(sV + AT_ATOM, &tm, v_full, vcol + 64, row0 + j * AT_BN);
+      int gv = 0;
+      for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+        const AtItem w = at_item(i, head_pairs, n_qt, nh, nb);
+        const int row0 = w.b * seq_len, vcol = (nh + nkv + w.hA / g) * AT_D, nB = w.qtB + 1;
+        for (int j = 0; j < nB; ++j, ++gv) {
+          mbar_wait(v_empty, (gv & 1) ^ 1);
+          mbar_expect_tx(v_full, AT_TILE);
+          tma_load_2d(sV, &tm, v_full, vcol, row0 + j * AT_BN);
+          tma_load_2d(sV + AT_ATOM, &tm, v_full, vcol + 64, row0 + j * AT_BN);
+        }
       }
     }
     __syncwarp();
@@ -174,51 +202,52 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
       constexpr uint32_t idesc_s = make_idesc_bf16(AT_BM, AT_BN, 0, 0);   // Q K-major, K K-major
       constexpr uint32_t idesc_o = make_idesc_bf16(AT_BM, AT_D, 0, 1);    // P K-major, V MN-major
       const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP), va = smem_u32(sV);
-      auto mma_s = [&](int t, uint32_t ka) {
+      int gk = 0, gv = 0, it = 0;
+      int gs[2] = {0, 0}, gp[2] = {0, 0};
+      for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++it) {
+        const AtItem w = at_item(i, head_pairs, n_qt, nh, nb);
+        const int nA = w.qtA + 1, nB = w.qtB + 1;
+        mbar_wait(q_full, it & 1);
+        // step j: S_A(j), S_B(j), then O_A += P_A(j-1)·V_{j-1}, O_B += P_B(j-1)·V_{j-1}: each
+        // tile's softmax hides behind the other MMAs of the step and V_j has two S MMAs of slack
+        for (int j = 0; j <= nB; ++j) {
+          if (j < nB) {
+            const int s = gk % AT_STAGES;
+            const uint32_t ka = smem_u32(sK + (size_t)s * AT_TILE);
+            mbar_wait(&k_full[s], (gk / AT_STAGES) & 1);
+            for (int t = 0; t < 2; ++t) {
+              if (t == 0 && j >= nA) continue;
+              if (gs[t] >= 1) mbar_wait(&s_free[t], (gs[t] - 1) & 1);
+              tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < AT_D / 16; ++kk)
-          umma_bf16_ss(tmem + t * AT_BN, at_kmajor(qa + t * AT_TILE, kk), at_kmajor(ka, kk), idesc_s,
-                       kk > 0 ? 1u : 0u);
-        umma_commit(&s_full[t]);
-      };
-      auto mma_pv = [&](int t, int j) {
+              for (int kk = 0; kk < AT_D / 16; ++kk)
+                umma_bf16_ss(tmem + t * AT_BN, at_kmajor(qa + t * AT_TILE, kk), at_kmajor(ka, kk), idesc_s,
+                             kk > 0 ? 1u : 0u);
+              umma_commit(&s_full[t]);
+              ++gs[t];
+            }
+            umma_commit(&k_empty[s]);
+            ++gk;
+            if (j == nB - 1) umma_commit(q_empty);      // this item's Q is no longer read
+          }
+          if (j >= 1) {
+            const int jj = j - 1;
+            mbar_wait(v_full, gv & 1);
+            for (int t = 0; t < 2; ++t) {
+              if (t == 0 && jj >= nA) continue;
+              if (jj == 0 && it > 0) mbar_wait(&o_free[t], (it - 1) & 1);   // previous O drained
+              mbar_wait(&p_full[t], gp[t] & 1);
+              tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < AT_BN / 16; ++kk)
-          umma_bf16_ss(tmem + (2 + t) * AT_BN, at_kmajor(pa + t * AT_TILE, kk), at_mnmajor(va, kk), idesc_o,
-                       (j | kk) != 0 ? 1u : 0u);
-        umma_commit(&pv_done[t]);
-      };
-      mbar_wait(q_full, 0);
-      // iteration j: S_A(j), S_B(j), then O_A += P_A(j-1)·V_{j-1}, O_B += P_B(j-1)·V_{j-1}.
-      // Both P·V of a KV tile run back to back, so V_j has two S MMAs of slack to land and
-      // each tile's softmax has the other three MMAs of the step to hide behind.
-      for (int j = 0; j <= nB; ++j) {
-        if (j < nB) {
-          const int s = j % AT_STAGES;
-          const uint32_t ka = smem_u32(sK + (size_t)s * AT_TILE);
-          mbar_wait(&k_full[s], (j / AT_STAGES) & 1);
-          if (j < nA) {
-            if (j >= 1) mbar_wait(&s_free[0], (j - 1) & 1);
-            tc_fence_after();
-            mma_s(0, ka);
+              for (int kk = 0; kk < AT_BN / 16; ++kk)
+                umma_bf16_ss(tmem + (2 + t) * AT_BN, at_kmajor(pa + t * AT_TILE, kk), at_mnmajor(va, kk), idesc_o,
+                             (jj | kk) != 0 ? 1u : 0u);
+              umma_commit(&pv_done[t]);
+              ++gp[t];
+            }
+            umma_commit(v_empty);
+            ++gv;
           }
-          if (j >= 1) mbar_wait(&s_free[1], (j - 1) & 1);
-          tc_fence_after();
-          mma_s(1, ka);
-          umma_commit(&k_empty[s]);
-        }
-        if (j >= 1) {
-          const int jj = j - 1;
-          mbar_wait(v_full, jj & 1);
-          if (jj < nA) {
-            mbar_wait(&p_full[0], jj & 1);
-            tc_fence_after();
-            mma_pv(0, jj);
-          }
-          mbar_wait(&p_full[1], jj & 1);
-          tc_fence_after();
-          mma_pv(1, jj);
-          umma_commit(v_empty);
         }
       }
     }
@@ -227,91 +256,100 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
     const int t = (warp - 4) >> 2;                      // 0: tile A, 1: tile B
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;                       // query row in the tile = TMEM lane
-    const int qt = t ? qtB : qtA, n = t ? nB : nA, h = t ? hB : hA;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     const uint32_t tS = trow + t * AT_BN, tO = trow + (2 + t) * AT_BN;
     const uint32_t prow = smem_u32(sP) + t * AT_TILE;
-    float m = -INFINITY, l = 0.0f;
-    for (int j = 0; j < n; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      uint32_t sv[AT_BN];
-#pragma unroll
-      for (int c = 0; c < AT_BN / 16; ++c)
-        tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(sv + c * 16));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&s_free[t]);                          // the MMA may overwrite this S buffer
-      if (j == qt) {                                    // diagonal tile: key > query is masked
-#pragma unroll
-        for (int c = 0; c < AT_BN; ++c)
-          if (c > r) sv[c] = __float_as_uint(-INFINITY);
-      }
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < AT_BN / 2; ++c)
-        mx4[c & 3] = fmax3(mx4[c & 3], __uint_as_float(sv[2 * c]), __uint_as_float(sv[2 * c + 1]));
-      const float mx = fmax3(mx4[0], mx4[1], fmaxf(mx4[2], mx4[3])) * scale_log2;
-      const bool move = mx > m + AT_RESCALE_LOG2;       // always on the first tile (m = -inf)
-      const float m_new = move ? mx : m;
-      const float alpha = move ? ex2(m - m_new) : 1.0f; // 0 on the first tile
-      float2 sum2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_new, -m_new);
-#pragma unroll
-      for (int c = 0; c < AT_BN / 2; ++c) {             // P packed in place: sv[c] = bf16x2(p_2c, p_2c+1)
-        const float2 x = ffma2(make_float2(__uint_as_float(sv[2 * c]), __uint_as_float(sv[2 * c + 1])), sc2, nm2);
-        const float2 pp = make_float2(ex2(x.x), ex2(x.y));
-        sum2[c & 3] = fadd2(sum2[c & 3], pp);
-        sv[c] = pack_bf16(pp.x, pp.y);
-      }
-      const float2 s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
-      l = __fmaf_rn(l, alpha, s01.x + s01.y);
-      m = m_new;
-      if (j >= 1) {
-        mbar_wait(&pv_done[t], (j - 1) & 1);            // O holds tiles < j; P buffer is free
+    int base = 0;                                       // S / P·V count of this tile before the item
+    for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+      const AtItem w = at_item(i, head_pairs, n_qt, nh, nb);
+      const int qt = t ? w.qtB : w.qtA, n = qt + 1, h = t ? w.hB : w.hA;
+      float m = -INFINITY, l = 0.0f;
+      for (int j = 0; j < n; ++j) {
+        mbar_wait(&s_full[t], (base + j) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.0f)) {
-#pragma unroll 1
-          for (int c = 0; c < AT_D / 16; ++c) {
-            uint32_t o[16];
-            tmem_ld16(tO + c * 16, o);
-            tmem_wait_ld();
+        uint32_t sv[AT_BN];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(tO + c * 16, o);
+        for (int c = 0; c < AT_BN / 16; ++c)
+          tmem_ld16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(sv + c * 16));
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&s_free[t]);                        // the MMA may overwrite this S buffer
+        if (j == qt) {                                  // diagonal tile: key > query is masked
+#pragma unroll
+          for (int c = 0; c < AT_BN; ++c)
+            if (c > r) sv[c] = __float_as_uint(-INFINITY);
+        }
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < AT_BN / 2; ++c)
+          mx4[c & 3] = fmax3(mx4[c & 3], __uint_as_float(sv[2 * c]), __uint_as_float(sv[2 * c + 1]));
+        const float mx = fmax3(mx4[0], mx4[1], fmaxf(mx4[2], mx4[3])) * scale_log2;
+        const bool move = mx > m + AT_RESCALE_LOG2;     // always on the first tile (m = -inf)
+        const float m_new = move ? mx : m;
+        const float alpha = move ? ex2(m - m_new) : 1.0f;
+        float2 sum2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};
+        const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_new, -m_new);
+#pragma unroll
+        for (int c = 0; c < AT_BN / 2; ++c) {           // P packed in place: sv[c] = bf16x2(p_2c, p_2c+1)
+          const float2 x = ffma2(make_float2(__uint_as_float(sv[2 * c]), __uint_as_float(sv[2 * c + 1])), sc2, nm2);
+          const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+          sum2[c & 3] = fadd2(sum2[c & 3], pp);
+          sv[c] = pack_bf16(pp.x, pp.y);
+        }
+        const float2 s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
+        l = __fmaf_rn(l, alpha, s01.x + s01.y);
+        m = m_new;
+        if (j >= 1) {
+          mbar_wait(&pv_done[t], (base + j - 1) & 1);   // O holds tiles < j; P buffer is free
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+#pragma unroll 1
+            for (int c = 0; c < AT_D / 16; ++c) {
+              uint32_t o[16];
+              tmem_ld16(tO + c * 16, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int q = 0; q < 16; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * alpha);
+              tmem_st16(tO + c * 16, o);
+            }
+            tmem_wait_st();
           }
-          tmem_wait_st();
         }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t* q = sv + a * 32 + c * 4;
+            st_shared_v4(prow + a * AT_ATOM + sw128(r, c), q[0], q[1], q[2], q[3]);
+          }
+        fence_proxy_async_smem();                       // generic-proxy P writes -> tensor core
+        tc_fence_before();
+        mbar_arrive(&p_full[t]);
       }
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t* q = sv + a * 32 + c * 4;
-          st_shared_v4(prow + a * AT_ATOM + sw128(r, c), q[0], q[1], q[2], q[3]);
-        }
-      fence_proxy_async_smem();                         // generic-proxy P writes -> tensor core
-      tc_fence_before();
-      mbar_arrive(&p_full[t]);
-    }
-    mbar_wait(&pv_done[t], (n - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.0f / l;
-    __nv_bfloat16* orow = out + (size_t)(row0 + qt * AT_BM + r) * ld_out + (size_t)h * AT_D;
+      mbar_wait(&pv_done[t], (base + n - 1) & 1);
+      tc_fence_after();
+      base += n;
+      const float inv = 1.0f / l;
+      const int row0 = w.b * seq_len;
+      __nv_bfloat16* orow = out + (size_t)(row0 + qt * AT_BM + r) * ld_out + (size_t)h * AT_D;
 #pragma unroll 1
-    for (int c = 0; c < AT_D / 16; ++c) {
-      uint32_t o[16];
-      tmem_ld16(tO + c * 16, o);
-      tmem_wait_ld();
-      uint32_t w[8];
+      for (int c = 0; c < AT_D / 16; ++c) {
+        uint32_t o[16];
+        tmem_ld16(tO + c * 16, o);
+        tmem_wait_ld();
+        uint32_t v8[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        w[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-      int4* dst = reinterpret_cast<int4*>(orow + c * 16);
-      dst[0] = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
-      dst[1] = make_int4((int)w[4], (int)w[5], (int)w[6], (int)w[7]);
+        for (int q = 0; q < 8; ++q)
+          v8[q] = pack_bf16(__uint_as_float(o[2 * q]) * inv, __uint_as_float(o[2 * q + 1]) * inv);
+        int4* dst = reinterpret_cast<int4*>(orow + c * 16);
+        dst[0] = make_int4((int)v8[0], (int)v8[1], (int)v8[2], (int)v8[3]);
+        dst[1] = make_int4((int)v8[4], (int)v8[5], (int)v8[6], (int)v8[7]);
+      }
+      tc_fence_before();
+      mbar_arrive(&o_free[t]);                          // the next item's first P·V may overwrite O
+      lse[((size_t)w.b * nh + h) * seq_len + qt * AT_BM + r] = (m + log2f(l)) * 0.69314718055994531f;
     }
-    lse[((size_t)b * nh + h) * seq_len + qt * AT_BM + r] = (m + log2f(l)) * 0.69314718055994531f;
   }
   tc_fence_before();
   __syncthreads();
@@ -352,10 +390,11 @@ int dm_attention_fwd(const void* qkv, int T, int seq_len, int nh, int nkv, int h
     configured = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)AT_D);
-  const int head_pairs = (nh / nkv) % 2 == 0;
-  dim3 grid(head_pairs ? seq_len / AT_BM : seq_len / (2 * AT_BM), head_pairs ? nh / 2 : nh, T / seq_len);
+  const int head_pairs = (nh / nkv) % 2 == 0, nb = T / seq_len;
+  const int n_items = head_pairs ? (seq_len / AT_BM) * (nh / 2) * nb : (seq_len / (2 * AT_BM)) * nh * nb;
+  const int grid = n_items < num_sms_current() ? n_items : num_sms_current();
   attn_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, (cudaStream_t)stream>>>(
-      tm, seq_len, nh, nkv, nh * AT_D, reinterpret_cast<__nv_bfloat16*>(out), lse, scale_log2, head_pairs);
+      tm, seq_len, nh, nkv, nh * AT_D, reinterpret_cast<__nv_bfloat16*>(out), lse, scale_log2, head_pairs, nb);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "attention_fwd launch");
   note_launch();
