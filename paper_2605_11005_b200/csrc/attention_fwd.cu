@@ -2,9 +2,9 @@
 // attention of SURVEY.md §8f row 3, whose cost the reference only models,
 // C_a = b·(s·H²·(2+2/g) + 4·s²·H) (pkg/src/afpipe/costs.py:84-87).
 //
-// One CTA = one (sequence, query head, pair of adjacent 128-query tiles A and B); head_dim
-// 128. Warp roles:
-//   warp 0    TMA: both Q tiles once, then K_j through a 2-stage ring
+// Persistent CTAs (one per SM) walk work items of two 128-query tiles A and B; head_dim 128.
+// Warp roles:
+//   warp 0    TMA: the item's two Q tiles, then K_j through a 2-stage ring
 //   warp 3    TMA: V_j (one stage; V_j is consumed by both tiles' P·V)
 //   warp 1    MMA issuer (one thread), per KV tile j: S_A(j) = Q_A·K_jᵀ, S_B(j) = Q_B·K_jᵀ,
 //             O_A += P_A(j-1)·V_{j-1}, O_B += P_B(j-1)·V_{j-1}: each tile's softmax of KV tile j
@@ -18,7 +18,7 @@
 //             final O / l and the natural-log LSE go to global memory.
 // Tiles A and B are two query heads of one KV group on the same rows (GQA with an even
 // group size: each K/V tile serves both) or two adjacent row tiles of one head. Causal:
-// each tile stops at its diagonal KV tile (masked key > query). Heaviest rows first.
+// each tile stops at its diagonal KV tile (masked key > query). Items run heaviest first.
 #include "dm_common.cuh"
 #include "dm_internal.h"
 
