@@ -104,7 +104,16 @@ __device__ __forceinline__ AtItem at_item(int i, int head_pairs, int n_qt, int n
   return it;
 }
 
-// Persistent: one CTA per SM walks the items i = blockIdx.x, +gridDim.x, ...; TMEM, barriers
+// Round r of the persistent walk: CTA k takes item r·G + k on even rounds and r·G + G-1-k on
+// odd ones (snake order over the heaviest-first list, so every CTA's total work is close to
+// the mean); -1 when the last, partial round has nothing for this CTA.
+__device__ __forceinline__ int at_snake(int r, int n_items) {
+  const int G = gridDim.x, k = blockIdx.x;
+  const int i = r * G + ((r & 1) ? G - 1 - k : k);
+  return i < n_items ? i : -1;
+}
+
+// Persistent: one CTA per SM walks the items in snake order (at_snake); TMEM, barriers
 // and the K/V rings live across items (phases from running counters), the next item's Q
 // load waits only for the last S MMAs of the previous one, and its first P·V waits for the
 // previous epilogue to drain O — prologue and epilogue overlap the neighbouring items.
@@ -161,7 +170,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
     if (lane == 0) {
       tma_prefetch_desc(&tm);
       int gk = 0, it = 0;
-      for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++it) {
+      for (int rd = 0; rd * (int)gridDim.x < n_items; ++rd) {
+        const int i = at_snake(rd, n_items);
+        if (i < 0) continue;
         const AtItem w = at_item(i, head_pairs, n_qt, nh, nb);
         const int row0 = w.b * seq_len, kcol = (nh + w.hA / g) * AT_D, nB = w.qtB + 1;
         if (it > 0) mbar_wait(q_empty, (it - 1) & 1);   // previous item's S MMAs are done with Q
@@ -179,13 +190,16 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
           tma_load_2d(k, &tm, &k_full[s], kcol, row0 + j * AT_BN);
           tma_load_2d(k + AT_ATOM, &tm, &k_full[s], kcol + 64, row0 + j * AT_BN);
         }
+        ++it;
       }
     }
     __syncwarp();
   } else if (warp == 3) {
     if (lane == 0) {
       int gv = 0;
-      for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+      for (int rd = 0; rd * (int)gridDim.x < n_items; ++rd) {
+        const int i = at_snake(rd, n_items);
+        if (i < 0) continue;
         const AtItem w = at_item(i, head_pairs, n_qt, nh, nb);
         const int row0 = w.b * seq_len, vcol = (nh + nkv + w.hA / g) * AT_D, nB = w.qtB + 1;
         for (int j = 0; j < nB; ++j, ++gv) {
@@ -204,7 +218,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
       const uint32_t qa = smem_u32(sQ), pa = smem_u32(sP), va = smem_u32(sV);
       int gk = 0, gv = 0, it = 0;
       int gs[2] = {0, 0}, gp[2] = {0, 0};
-      for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++it) {
+      for (int rd = 0; rd * (int)gridDim.x < n_items; ++rd) {
+        const int i = at_snake(rd, n_items);
+        if (i < 0) continue;
         const AtItem w = at_item(i, head_pairs, n_qt, nh, nb);
         const int nA = w.qtA + 1, nB = w.qtB + 1;
         mbar_wait(q_full, it & 1);
@@ -249,6 +265,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
             ++gv;
           }
         }
+        ++it;
       }
     }
     __syncwarp();
@@ -260,7 +277,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm, int seq_len, int nh, int
     const uint32_t tS = trow + t * AT_BN, tO = trow + (2 + t) * AT_BN;
     const uint32_t prow = smem_u32(sP) + t * AT_TILE;
     int base = 0;                                       // S / P·V count of this tile before the item
-    for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+    for (int rd = 0; rd * (int)gridDim.x < n_items; ++rd) {
+      const int i = at_snake(rd, n_items);
+      if (i < 0) continue;
       const AtItem w = at_item(i, head_pairs, n_qt, nh, nb);
       const int qt = t ? w.qtB : w.qtA, n = qt + 1, h = t ? w.hB : w.hA;
       float m = -INFINITY, l = 0.0f;
