@@ -454,7 +454,8 @@ def run_ours(args, shape, exp):
         line["attention"] = {
             "ms_per_microbatch_layer": round(a_ms, 4), "TFLOP/s": round((fa + fb) / (a_ms / 1e3) / 1e12, 1),
             "impl": ("own sm_100a flash-attention forward (dm_attention_fwd) + cuDNN SDPA backward on its O/LSE; "
-                     "cuBLAS projections, autograd" if attn[0].own_kernel and exp.workload.seq_len % 256 == 0
+                     "cuBLAS projections, autograd" if attn[0].own_kernel
+                     and exp.workload.seq_len % (128 if exp.model.gqa_group % 2 == 0 else 256) == 0
                      else "library: cuBLAS projections + torch SDPA (cuDNN/flash), autograd"),
             "gqa_group": exp.model.gqa_group, "seq_len": exp.workload.seq_len}
         line["config"]["layer"] = "attention + residual MoE block"

@@ -16,7 +16,7 @@ FLOPs are what the schedule needs). Gradients come from torch autograd on the
 per-micro-batch graph saved by `forward`; parameter gradients accumulate in fp32
 `.grad`-style buffers (`dw_qkv`, `dw_o`).
 
-On CUDA with seq_len a multiple of 256 the attention forward is this repo's own sm_100a
+On CUDA with seq_len a multiple of 128 (256 for an odd GQA group) the attention forward is this repo's own sm_100a
 kernel (`dm_attention_fwd`: tcgen05/TMEM/TMA flash attention, csrc/attention_fwd.cu); its
 (O, LSE) feed cuDNN's SDPA backward (the LSE matches cuDNN's to 5e-5), so only the
 backward and the projections remain library code.
@@ -83,8 +83,11 @@ class _OwnCausalAttention(torch.autograd.Function):
         return dqkv, None, None, None
 
 
-def own_attention_supported(x: torch.Tensor, seq_len: int, head_dim: int = HEAD_DIM) -> bool:
-    return x.is_cuda and head_dim == HEAD_DIM and seq_len % 256 == 0 and x.shape[0] % seq_len == 0
+def own_attention_supported(x: torch.Tensor, seq_len: int, head_dim: int = HEAD_DIM, gqa_group: int = 1) -> bool:
+    """dm_attention_fwd's shape contract: head_dim 128, whole sequences, seq_len a multiple of
+    128 (pairs of query heads share a tile pair) or 256 (odd GQA group: adjacent row tiles)."""
+    row_tile = 128 if gqa_group % 2 == 0 else 256
+    return x.is_cuda and head_dim == HEAD_DIM and seq_len % row_tile == 0 and x.shape[0] % seq_len == 0
 
 
 class AttentionBlock:
@@ -116,7 +119,7 @@ class AttentionBlock:
         T, H = x.shape
         b = T // seq_len
         qkv = x @ self.w_qkv.t()
-        if self.own_kernel and own_attention_supported(x, seq_len, self.d):
+        if self.own_kernel and own_attention_supported(x, seq_len, self.d, self.nh // self.nkv):
             o = _OwnCausalAttention.apply(qkv.contiguous(), seq_len, self.nh, self.nkv)
             return o @ self.w_o.t()
         q, k, v = qkv.split([self.nh * self.d, self.nkv * self.d, self.nkv * self.d], dim=1)
