@@ -73,7 +73,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             list(ex.map(lambda j: _compile(*j), jobs))
     if force or jobs or _stale(LIB, objs):
         tmp = LIB.with_suffix(".so.tmp")
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
+        # -cudart shared: use the process's libcudart (the one torch loads) instead of a
+        # static copy, so the library shares one runtime instance with its host
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "shared", "-o", str(tmp), *map(str, objs)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")

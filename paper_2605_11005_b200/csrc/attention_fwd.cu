@@ -402,12 +402,7 @@ int dm_attention_fwd(const void* qkv, int T, int seq_len, int nh, int nkv, int h
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(DM_ERR_DRIVER, "attention_fwd: cuTensorMapEncodeTiled failed (%d)", (int)r);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AT_SMEM);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(attn_fwd)");
-    configured = true;
-  }
+  if (int rc = ensure_smem_attr((const void*)attn_fwd_kernel, (int)AT_SMEM, "cudaFuncSetAttribute(attn_fwd)")) return rc;
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)AT_D);
   const int head_pairs = (nh / nkv) % 2 == 0, nb = T / seq_len;
   const int n_items = head_pairs ? (seq_len / AT_BM) * (nh / 2) * nb : (seq_len / (2 * AT_BM)) * nh * nb;

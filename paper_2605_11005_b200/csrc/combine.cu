@@ -480,8 +480,7 @@ int dm_permute_bwd(const void* dx_perm, const int32_t* row_map, const int32_t* i
   const __nv_bfloat16* dxp = reinterpret_cast<const __nv_bfloat16*>(dx_perm);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(dx);
   if (E <= PBWD_MAX_E) {
-    static int occ = 0;
-    if (!occ) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, permute_bwd_smem_kernel<2>, 256, 0);
+    const int occ = max_active_blocks((const void*)permute_bwd_smem_kernel<2>, 256, 0);
     const int gx = (H + 255) / 256;
     int gy = ((occ > 0 ? occ : 2) * num_sms_current() + gx - 1) / gx;
     const int groups = (T + 8 * PBWD_TG - 1) / (8 * PBWD_TG);
@@ -516,19 +515,12 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
   int ntb = (T + tbt - 1) / tbt;   // the workspace holds this many partial blocks
   cudaStream_t st = (cudaStream_t)stream;
   if (E <= 16) {
-    static bool cfg = false;
-    static int occ8 = 1, occ16 = 1;
-    if (!cfg) {
-      cudaError_t e1 = cudaFuncSetAttribute(router_wgrad_reg_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            8 * 8 * 8 * 32 * 4);
-      cudaError_t e2 = cudaFuncSetAttribute(router_wgrad_reg_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            4 * 16 * 8 * 32 * 4);
-      if (e1 != cudaSuccess) return set_cuda_error(e1, "cudaFuncSetAttribute(router_wgrad_reg)");
-      if (e2 != cudaSuccess) return set_cuda_error(e2, "cudaFuncSetAttribute(router_wgrad_reg)");
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ8, router_wgrad_reg_kernel<8>, 256, 8 * 8 * 8 * 32 * 4);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ16, router_wgrad_reg_kernel<16>, 128, 4 * 16 * 8 * 32 * 4);
-      cfg = true;
-    }
+    if (int rc = ensure_smem_attr((const void*)router_wgrad_reg_kernel<8>, 8 * 8 * 8 * 32 * 4,
+                                  "cudaFuncSetAttribute(router_wgrad_reg)")) return rc;
+    if (int rc = ensure_smem_attr((const void*)router_wgrad_reg_kernel<16>, 4 * 16 * 8 * 32 * 4,
+                                  "cudaFuncSetAttribute(router_wgrad_reg)")) return rc;
+    const int occ8 = max_active_blocks((const void*)router_wgrad_reg_kernel<8>, 256, 8 * 8 * 8 * 32 * 4);
+    const int occ16 = max_active_blocks((const void*)router_wgrad_reg_kernel<16>, 128, 4 * 16 * 8 * 32 * 4);
     // One wave: as many token blocks as the resident CTA slots allow per column chunk
     // (never more than the workspace's ntb), each a contiguous run of tbt tokens.
     const int gx = (H / 8 + 31) / 32;
@@ -551,13 +543,8 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
     int cw = 128;
     while (cw > 32 && (size_t)E * cw * sizeof(float) > 96 * 1024) cw >>= 1;
     const size_t smem = (size_t)E * cw * sizeof(float);
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(router_wgrad_partial_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
-      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router_wgrad)");
-      configured = true;
-    }
+    if (int rc = ensure_smem_attr((const void*)router_wgrad_partial_kernel, 128 * 1024,
+                                  "cudaFuncSetAttribute(router_wgrad)")) return rc;
     dim3 grid((H + cw - 1) / cw, ntb);
     router_wgrad_partial_kernel<<<grid, cw, smem, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
                                                        T, H, E, k, tbt, partial_ws);

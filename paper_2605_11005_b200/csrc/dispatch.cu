@@ -549,13 +549,8 @@ int router_logits_launch(const void* x, const float* wg, float* logits, int T, i
                          cudaStream_t stream) {
   if (E > 16) {
     constexpr size_t rt_smem = (size_t)RT_STAGES * RT_STAGE_INT4 * sizeof(int4);
-    static bool rt_cfg = false;
-    if (!rt_cfg) {
-      cudaError_t e = cudaFuncSetAttribute(router_logits_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)rt_smem);
-      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router_tiled)");
-      rt_cfg = true;
-    }
+    if (int rc = ensure_smem_attr((const void*)router_logits_tiled_kernel, (int)rt_smem,
+                                  "cudaFuncSetAttribute(router_tiled)")) return rc;
     dim3 grid((T + RT_TOK - 1) / RT_TOK, (E + RT_EXP - 1) / RT_EXP);
     router_logits_tiled_kernel<<<grid, RT_THREADS, rt_smem, stream>>>(reinterpret_cast<const __nv_bfloat16*>(x), wg,
                                                                 logits, T, H, E);
@@ -569,13 +564,8 @@ int router_logits_launch(const void* x, const float* wg, float* logits, int T, i
   if (ec < 1) return set_error(DM_ERR_SHAPE, "router: hidden %d too large for one smem row", H);
   if (ec > E) ec = E;
   const size_t smem = (size_t)ec * row_bytes;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(router_logits_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ROUTER_SMEM_BUDGET);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router)");
-    configured = true;
-  }
+  if (int rc = ensure_smem_attr((const void*)router_logits_kernel, ROUTER_SMEM_BUDGET, "cudaFuncSetAttribute(router)"))
+    return rc;
   const int per_cta = ROUTER_WARPS * ROUTER_NT;
   int grid = (T + per_cta - 1) / per_cta;
   const int cap = num_sms_current();
@@ -596,16 +586,10 @@ int router_fused_launch(const void* x, const float* wg, int T, int H, int E, int
   const size_t smem = (size_t)(E <= 8 ? 8 : 16) * NI * 64 * sizeof(float4);
   if (E > 16 || smem > (size_t)ROUTER_SMEM_BUDGET) return -1;
   if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(wg) & 15) return -1;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e1 = cudaFuncSetAttribute(router_fused_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          ROUTER_SMEM_BUDGET);
-    cudaError_t e2 = cudaFuncSetAttribute(router_fused_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          ROUTER_SMEM_BUDGET);
-    if (e1 != cudaSuccess) return set_cuda_error(e1, "cudaFuncSetAttribute(router_fused)");
-    if (e2 != cudaSuccess) return set_cuda_error(e2, "cudaFuncSetAttribute(router_fused)");
-    configured = true;
-  }
+  if (int rc = ensure_smem_attr((const void*)router_fused_kernel<8>, ROUTER_SMEM_BUDGET,
+                                "cudaFuncSetAttribute(router_fused)")) return rc;
+  if (int rc = ensure_smem_attr((const void*)router_fused_kernel<16>, ROUTER_SMEM_BUDGET,
+                                "cudaFuncSetAttribute(router_fused)")) return rc;
   const int nchunk = dm_num_chunks(T);
   const int grid = nchunk < num_sms_current() ? nchunk : num_sms_current();
   const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);

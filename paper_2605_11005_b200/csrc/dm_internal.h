@@ -21,6 +21,12 @@ int num_sms_current();
 // cuTensorMapEncodeTiled resolved once through the runtime's driver entry point.
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 
+// Raises `func`'s dynamic shared-memory limit to `bytes` on the current device, once per
+// (kernel, device), thread-safe (cudaFuncSetAttribute is per device).
+int ensure_smem_attr(const void* func, int bytes, const char* what);
+// Cached cudaOccupancyMaxActiveBlocksPerMultiprocessor per (kernel, device); >= 1.
+int max_active_blocks(const void* func, int threads, size_t smem);
+
 // Counts kernel launches issued through the ABI (reported by dm_launch_count()).
 void note_launch();
 

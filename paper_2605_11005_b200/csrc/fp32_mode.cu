@@ -433,13 +433,8 @@ int dm_route_and_dispatch_f32(const float* x, const float* wg, int T, int H, int
   int ec = (int)((160 * 1024) / row_bytes);
   if (ec < 1) return set_error(DM_ERR_SHAPE, "router_f32: hidden %d too large for one smem row", H);
   if (ec > E) ec = E;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(router_logits_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         160 * 1024);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router_f32)");
-    configured = true;
-  }
+  if (int rc = ensure_smem_attr((const void*)router_logits_f32_kernel, 160 * 1024, "cudaFuncSetAttribute(router_f32)"))
+    return rc;
   int grid = (T + RF_WARPS - 1) / RF_WARPS;
   if (grid > num_sms_current()) grid = num_sms_current();
   router_logits_f32_kernel<<<grid, RF_WARPS * 32, (size_t)ec * row_bytes, st>>>(x, wg, ws.logits, T, H, E, ec);

@@ -853,13 +853,15 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
 
 static unsigned long long* g_gemm_prof = nullptr;
 
+// Environment switches, read once (thread-safe static initialisation).
+static int env_flag(const char* name, char on, int if_on, int otherwise) {
+  const char* e = getenv(name);
+  return (e && e[0] == on) ? if_on : otherwise;
+}
+
 static bool use_2sm() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DM_GEMM_1SM");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
+  static const bool v = env_flag("DM_GEMM_1SM", '1', 0, 1) == 1;
+  return v;
 }
 
 static int make_tmap_2d(CUtensorMap* tm, const void* base, bool fp32, uint64_t inner, uint64_t outer,
@@ -940,37 +942,18 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const EpiTe
     auto kern = grouped_gemm_2sm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
     const size_t smem = g2_smem_bytes<EPI>() + 2 * ((size_t)args.num_groups + 1) * sizeof(int);
     if (smem > 232448) return set_error(DM_ERR_SHAPE, "too many groups (%d) for the GEMM smem budget", args.num_groups);
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm2 smem)");
-      configured = true;
-    }
+    if ((rc = ensure_smem_attr((const void*)kern, 232448, "cudaFuncSetAttribute(gemm2 smem)"))) return rc;
     grid &= ~1;
     GemmArgs a2 = args;
     a2.prof = g_gemm_prof;
-    static int diag = -1;
-    if (diag < 0) {
-      const char* e = getenv("DM_GEMM_DIAG");
-      diag = (e && e[0] == '1') ? 1 : 0;
-    }
+    static const int diag = env_flag("DM_GEMM_DIAG", '1', 1, 0);
+    static const int dual = env_flag("DM_GEMM_DUAL", '0', 0, 1);
     a2.diag_skip_a = diag;
-    static int dual = -1;
-    if (dual < 0) {
-      const char* e = getenv("DM_GEMM_DUAL");
-      dual = (e && e[0] == '0') ? 0 : 1;
-    }
     a2.dual_producer = dual;
     kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, tc, tx, ti, a2);
   } else {
     auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
-    static bool configured = false;  // per instantiation
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)GEMM_SMEM_BYTES);
-      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm smem)");
-      configured = true;
-    }
+    if ((rc = ensure_smem_attr((const void*)kern, (int)GEMM_SMEM_BYTES, "cudaFuncSetAttribute(gemm smem)"))) return rc;
     kern<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(ta, tb, args);
   }
   cudaError_t e = cudaGetLastError();

@@ -42,11 +42,11 @@ import os
 from dataclasses import dataclass, field
 
 import torch
-import torch.distributed as dist
 
 from . import _lib
 from .afpipe import COMPUTE, SEND, LayerDurations, issue_order, plan_layer
 from .moe import ActivationSlab, ExpertParams, MicroBatchBuffers, MoEShape, RouterParams, link_residual_stack
+from .transport import AF, NcclTransport, direction_of
 
 BF16, F32, I32 = torch.bfloat16, torch.float32, torch.int32
 
@@ -188,36 +188,19 @@ class _Null:
         return False
 
 
-_FAST_P2P = [None]   # ProcessGroup with NCCL-style coalescing, resolved on first use
+def _exchange(ops: list[tuple[str, torch.Tensor, int]], direction: str = AF):
+    """One coalesced group of P2P ops on the default NCCL/gloo transport (kept for callers
+    outside AFPipeRank; the runtime itself goes through its `transport`)."""
+    return _default_transport().exchange(ops, direction)
 
 
-def _exchange(ops: list[tuple[str, torch.Tensor, int]]):
-    """One coalesced group of P2P ops on the current stream; returns the works.
+_DEFAULT_TX = []
 
-    On CUDA tensors the group is issued straight on the default ProcessGroup
-    (_start_coalescing / send / recv / _end_coalescing — what batch_isend_irecv does,
-    without its per-op Python validation, which dominated small-shape iterations);
-    other backends (gloo in the CPU tests) use the public batch_isend_irecv."""
-    ops = [o for o in ops if o[1].numel() > 0]
-    if not ops:
-        return []
-    dev = ops[0][1].device
-    if dev.type == "cuda":
-        pg = _FAST_P2P[0]
-        if pg is None:
-            pg = dist.distributed_c10d._get_default_group()
-            ok = hasattr(pg, "_start_coalescing") and pg._get_backend(dev).supports_coalescing
-            _FAST_P2P[0] = pg = pg if ok else False
-        if pg:
-            pg._start_coalescing(dev)
-            for k, t, peer in ops:
-                if k == "send":
-                    pg.send([t], peer, 0)
-                else:
-                    pg.recv([t], peer, 0)
-            return [pg._end_coalescing(dev)]
-    p2p = [dist.P2POp(dist.isend if k == "send" else dist.irecv, t, peer) for k, t, peer in ops]
-    return dist.batch_isend_irecv(p2p)
+
+def _default_transport() -> NcclTransport:
+    if not _DEFAULT_TX:
+        _DEFAULT_TX.append(NcclTransport())
+    return _DEFAULT_TX[0]
 
 
 # ------------------------------------------------------------------ stages
@@ -307,8 +290,11 @@ class AFPipeRank:
     def __init__(self, shape: MoEShape, topo: Topology, rank: int, microbatches: int, device,
                  stages=None, seed: int = 0, weights=None, durations: LayerDurations | None = None,
                  record_events: bool = False, layers: int = 1, residual: bool | None = None,
-                 attention: bool = False, seq_len: int | None = None, gqa_group: int = 1):
+                 attention: bool = False, seq_len: int | None = None, gqa_group: int = 1, transport=None):
         shape.validate() if device.type == "cuda" else None
+        # NcclTransport (one process per GPU) or transport.LoopbackTransport (ranks as
+        # threads of one process on one device)
+        self.tx = transport if transport is not None else _default_transport()
         if layers < 1:
             raise ValueError(f"layers must be >= 1, got {layers}")
         if topo.depth > layers:
@@ -435,7 +421,7 @@ class AFPipeRank:
         events on the send stream ([data ready, transfer complete])."""
         sending = any(k == "send" for k, _, _ in ops)
         ev0 = self.st.event("send", True) if (self.record_events and sending) else None
-        works = _exchange(ops)
+        works = self.tx.exchange(ops, direction_of(name))
         if ev0 is not None:
             for w in works:
                 w.wait()
@@ -605,7 +591,7 @@ class AFPipeRank:
             with self.st.ctx("recv"):
                 for f, r0, r1, lo, hi in self._a_slices(pad):
                     ops.append(("recv", dst[r0:r1], self.topo.f_rank(f, g)))
-                setattr(b, "works_" + name, _exchange(ops))
+                setattr(b, "works_" + name, self.tx.exchange(ops, direction_of(name)))
 
     def _a_comm_fixed(self, name: str, i: int, b, peer: int):
         """1:1 group: whole-capacity messages (the used rows are ~all of it when one F rank
@@ -621,7 +607,7 @@ class AFPipeRank:
         else:
             dst = b.y_perm if name == "N2M" else b.dx_perm
             with self.st.ctx("recv"):
-                setattr(b, "works_" + name, _exchange([("recv", dst, peer)]))
+                setattr(b, "works_" + name, self.tx.exchange([("recv", dst, peer)], direction_of(name)))
 
     def _a2a(self, name: str, i: int, layer: int, lane: str):
         """depth > 1: the residual stream between consecutive layers' A groups (same
@@ -638,7 +624,7 @@ class AFPipeRank:
                 nb = self.lbufs[layer + 1][i]
                 peer = self.topo.a_rank(j, layer % p)
                 with self.st.ctx("recv"):
-                    nb.works_A2A = _exchange([("recv", self._layer_input(layer + 1, i), peer)])
+                    nb.works_A2A = self.tx.exchange([("recv", self._layer_input(layer + 1, i), peer)], direction_of(name))
         else:                   # "A2A_b": task layer = l - 1 (the consumer); producer layer l
             if lane == SEND:
                 src = self.lbufs[layer + 1][i]
@@ -651,7 +637,7 @@ class AFPipeRank:
                 b = self.lbufs[layer][i]
                 peer = self.topo.a_rank(j, (layer + 1) % p)
                 with self.st.ctx("recv"):
-                    b.works_A2A_b = _exchange([("recv", b.dy, peer)])
+                    b.works_A2A_b = self.tx.exchange([("recv", b.dy, peer)], direction_of(name))
 
     def _wait_works(self, obj, name):
         for w in getattr(obj, "works_" + name, []) or []:
@@ -666,7 +652,7 @@ class AFPipeRank:
             return self._f_comm_fixed(name, i, layer, fm, src_rank(0))
         if name == "M2N":
             with self.st.ctx("recv"):
-                hw = _exchange([("recv", fm.headers[a], src_rank(a)) for a in range(n_a)])
+                hw = self.tx.exchange([("recv", fm.headers[a], src_rank(a)) for a in range(n_a)], AF)
                 for w in hw:
                     w.wait()
             with self.st.ctx("copy"):
@@ -699,11 +685,11 @@ class AFPipeRank:
             self.seg_offs[layer][i * n_a:(i + 1) * n_a].copy_(seg, non_blocking=self.st.cuda)
             with self.st.ctx("recv"):
                 ops = [("recv", fm.x_perm[b0:b0 + r], src_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
-                fm.works["M2N"] = _exchange(ops)
+                fm.works["M2N"] = self.tx.exchange(ops, AF)
         elif name == "M2N_b":
             with self.st.ctx("recv"):
                 ops = [("recv", fm.dy_perm[b0:b0 + r], src_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
-                fm.works["M2N_b"] = _exchange(ops)
+                fm.works["M2N_b"] = self.tx.exchange(ops, AF)
         elif name in ("N2M", "N2M_b"):
             src = fm.y_perm if name == "N2M" else fm.dx_perm
             ready = fm.works.get(name + "_ready")
@@ -720,10 +706,10 @@ class AFPipeRank:
             fm.group_off = seg
             fm.slices = [(0, self.cap_f)]
             with self.st.ctx("recv"):
-                fm.works["M2N"] = _exchange([("recv", seg, peer), ("recv", fm.x_perm, peer)])
+                fm.works["M2N"] = self.tx.exchange([("recv", seg, peer), ("recv", fm.x_perm, peer)], AF)
         elif name == "M2N_b":
             with self.st.ctx("recv"):
-                fm.works["M2N_b"] = _exchange([("recv", fm.dy_perm, peer)])
+                fm.works["M2N_b"] = self.tx.exchange([("recv", fm.dy_perm, peer)], AF)
         else:
             src = fm.y_perm if name == "N2M" else fm.dx_perm
             with self.st.ctx("send"):
@@ -787,17 +773,19 @@ class AFPipeRank:
                 self.st.compute.wait_stream(self.st.d2h)
             if self.a_group is not None and self.topo.a_per_group > 1:
                 for l in self.my_layers:
-                    dist.all_reduce(self.routers[l].dwg, group=self.a_group)
+                    self.tx.all_reduce(self.routers[l].dwg, self.a_group)
                 for blk in (self.attn or {}).values():
                     for g in blk.grads():
-                        dist.all_reduce(g, group=self.a_group)
+                        self.tx.all_reduce(g, self.a_group)
 
     def init_groups(self):
-        """Create the per-pipeline-group A communicators (collective: every rank calls
-        new_group for every group, in the same order)."""
+        """Create the transport's two direction communicators and the per-pipeline-group
+        A communicators (collective: every rank calls new_group for every group, in the
+        same order)."""
+        self.tx.setup(self.topo.world)
         for g in range(self.topo.depth):
             ranks = [self.topo.a_rank(j, g) for j in range(self.topo.a_per_group)]
-            pg = dist.new_group(ranks)
+            pg = self.tx.new_group(ranks)
             if self.role == "A" and self.group == g:
                 self.a_group = pg
 
