@@ -34,8 +34,10 @@ enum { EPI_BF16 = 0, EPI_SWIGLU_FWD = 1, EPI_SWIGLU_BWD = 2, EPI_F32 = 3 };
 struct GemmArgs {
   int num_groups;
   const int* group_off;          // [G+1], 128-aligned, device
-  int M;                         // ragged-K: rows of C per group (multiple of 128)
-  int N;                         // multiple of 256
+  int M;                         // ragged-K: rows of C per group (multiple of 128; a partial
+                                 //   last 256-row tile is clipped by the 3-D C map)
+  int N;                         // multiple of 128 (2-SM path; a partial last 256-column tile
+                                 //   reads zero-filled / discarded B rows, its stores are clipped)
   int K;                         // ragged-M: reduction length (multiple of 64)
   int b_group_rows;              // ragged-M: rows of the B tensor owned by one weight matrix
   int b_groups;                  // ragged-M: group g multiplies weight matrix g % b_groups
@@ -442,7 +444,7 @@ __device__ __forceinline__ TileInfo decode_tile_2sm(int t, const int* tile_start
     // Rasterise along the smaller output dimension so concurrent tiles share the
     // larger operand's tile (streamed once) while the smaller operand stays in L2:
     // dW13 (M = 2*D_e >> N = H) goes n-fastest, dW2 (M = H < N = D_e) m-fastest.
-    const int mt = a.M / 256, nt = a.N / GBN;
+    const int mt = (a.M + 255) / 256, nt = (a.N + GBN - 1) / GBN;
     if (a.M >= a.N) {
       ti.m0 = (local / nt) * 256 + 128 * rank;
       ti.n0 = (local % nt) * GBN;
@@ -618,7 +620,8 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
     }
   } else {  // EPI_F32: dW_g rows (g*M + m) of a [G*M, N] fp32 matrix (ragged K, a.M > 0) or
             // C rows m (ragged M, a.M = 0); beta in {0, 1}
-    const int grow0 = ti.g * a.M + row0;
+    // ragged K (a.M > 0): the 3-D map [G][M][N] clips this group's rows/cols; ragged M:
+    // 2-D [rows, N] map
     const bool empty = ti.kb_count == 0;
     if (empty && a.beta != 0.0f) return;  // adding zeros
 #pragma unroll 1
@@ -642,8 +645,14 @@ __device__ __forceinline__ void epilogue_tma(const TileInfo& ti, uint32_t tacc, 
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        if (a.beta != 0.0f) tma_reduce_add_2d(tmC, stg + (c & 1) * BOX_BYTES, col0 + c * 32, grow0);
-        else tma_store_2d(tmC, stg + (c & 1) * BOX_BYTES, col0 + c * 32, grow0);
+        uint8_t* box = stg + (c & 1) * BOX_BYTES;
+        if (a.M > 0) {
+          if (a.beta != 0.0f) tma_reduce_add_3d(tmC, box, col0 + c * 32, row0, ti.g);
+          else tma_store_3d(tmC, box, col0 + c * 32, row0, ti.g);
+        } else {
+          if (a.beta != 0.0f) tma_reduce_add_2d(tmC, box, col0 + c * 32, row0);
+          else tma_store_2d(tmC, box, col0 + c * 32, row0);
+        }
         bulk_commit();
       }
     }
@@ -702,7 +711,8 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
     for (int g = 0; g < G; ++g) {
       s_tile[g] = acc;
       const int rows = RAGGED_K ? 0 : s_off[g + 1] - s_off[g];
-      acc += RAGGED_K ? (args.M / 256) * (args.N / GBN) : ((rows + 255) / 256) * (args.N / GBN);
+      const int nt = (args.N + GBN - 1) / GBN;   // last column tile may be partial (N % 256 == 128)
+      acc += RAGGED_K ? ((args.M + 255) / 256) * nt : ((rows + 255) / 256) * nt;
     }
     s_tile[G] = acc;
   }
@@ -864,18 +874,20 @@ static bool use_2sm() {
   return v;
 }
 
+// groups > 0: a rank-3 map [groups][outer][inner] of back-to-back [outer, inner] blocks
+// (box depth 1), so every group's edges clip independently.
 static int make_tmap_2d(CUtensorMap* tm, const void* base, bool fp32, uint64_t inner, uint64_t outer,
-                       uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer) {
+                       uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer, uint64_t groups = 0) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   if (!enc) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled entry point unavailable");
   const uint64_t esz = fp32 ? 4 : 2;
   if ((reinterpret_cast<uintptr_t>(base) & 15) || ((row_stride_elems * esz) & 15))
     return set_error(DM_ERR_ALIGN, "TMA operand base/stride not 16-byte aligned");
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {row_stride_elems * esz};
-  cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(tm, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  cuuint64_t dims[3] = {inner, outer, groups};
+  cuuint64_t strides[2] = {row_stride_elems * esz, row_stride_elems * esz * outer};
+  cuuint32_t box[3] = {box_inner, box_outer, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(tm, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, groups ? 3 : 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -903,6 +915,7 @@ struct EpiTensor {
   const void* base = nullptr;
   bool fp32 = false;
   uint64_t cols = 0, rows = 0, ld = 0;
+  uint64_t groups = 0;   // > 0: rank-3 map, `groups` blocks of [rows, cols]
 };
 
 struct EpiTensors {
@@ -920,7 +933,7 @@ static int make_epi_map(CUtensorMap* tm, const EpiTensor& t, const CUtensorMap& 
     *tm = dummy;
     return DM_OK;
   }
-  return make_tmap_2d(tm, t.base, t.fp32, t.cols, t.rows, t.ld, t.fp32 ? 32 : 64, 32);
+  return make_tmap_2d(tm, t.base, t.fp32, t.cols, t.rows, t.ld, t.fp32 ? 32 : 64, 32, t.groups);
 }
 
 template <int A_MN, int B_MN, int RAGGED_K, int EPI>
@@ -952,6 +965,8 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const EpiTe
     a2.dual_producer = dual;
     kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, tc, tx, ti, a2);
   } else {
+    if (args.N % GBN || (RAGGED_K && args.M % 256))
+      return set_error(DM_ERR_SHAPE, "the 1-SM debug GEMM path needs full 256-wide tiles (N=%d, M=%d)", args.N, args.M);
     auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
     if ((rc = ensure_smem_attr((const void*)kern, (int)GEMM_SMEM_BYTES, "cudaFuncSetAttribute(gemm smem)"))) return rc;
     kern<<<grid, GEMM_THREADS, GEMM_SMEM_BYTES, stream>>>(ta, tb, args);
@@ -996,8 +1011,8 @@ int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* group_off,
                       int cap_rows, int H, int De, void* y_perm, void* stream) {
   int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
-  if (H % GBN || De % GBK)
-    return set_error(DM_ERR_SHAPE, "w2 fwd needs H %% 256 == 0 and D_e %% 64 == 0 (H=%d, D_e=%d)", H, De);
+  if (H % 128 || H < 128 || De % GBK || De < GBK)
+    return set_error(DM_ERR_SHAPE, "w2 fwd needs H %% 128 == 0 and D_e %% 64 == 0 (H=%d, D_e=%d)", H, De);
   const GemmOperand A{act, (uint64_t)De, (uint64_t)cap_rows, (uint64_t)De, false, false};
   const GemmOperand B{w2, (uint64_t)De, (uint64_t)E * H, (uint64_t)De, false, true};
   GemmArgs a{};
@@ -1013,8 +1028,8 @@ int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const vo
                                    void* dh13, void* stream) {
   int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
-  if (H % GBK || De % GBN)
-    return set_error(DM_ERR_SHAPE, "w2 dgrad needs H %% 64 == 0 and D_e %% 256 == 0 (H=%d, D_e=%d)", H, De);
+  if (H % GBK || H < GBK || De % 128 || De < 128)
+    return set_error(DM_ERR_SHAPE, "w2 dgrad needs H %% 64 == 0 and D_e %% 128 == 0 (H=%d, D_e=%d)", H, De);
   const GemmOperand A{dy_perm, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H, false, false};
   const GemmOperand B{w2, (uint64_t)De, (uint64_t)E * H, (uint64_t)De, true, true};
   GemmArgs a{};
@@ -1031,8 +1046,8 @@ int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* group
                          int cap_rows, int H, int De, void* dx_perm, void* stream) {
   int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
-  if (H % GBN || De % 128)
-    return set_error(DM_ERR_SHAPE, "w13 dgrad needs H %% 256 == 0 and D_e %% 128 == 0 (H=%d, D_e=%d)", H, De);
+  if (H % 128 || H < 128 || De % 128 || De < 128)
+    return set_error(DM_ERR_SHAPE, "w13 dgrad needs H %% 128 == 0 and D_e %% 128 == 0 (H=%d, D_e=%d)", H, De);
   const GemmOperand A{dh13, (uint64_t)2 * De, (uint64_t)cap_rows, (uint64_t)2 * De, false, false};
   const GemmOperand B{w13, (uint64_t)H, (uint64_t)E * 2 * De, (uint64_t)H, true, true};
   GemmArgs a{};
@@ -1048,8 +1063,8 @@ int dm_grouped_wgrad_strided(const void* a_tok, int M, int lda, const void* b_to
                              float* dW, float beta, void* stream) {
   int rc = check_groups(E, E, total_rows);
   if (rc) return rc;
-  if (M % 256 || N % GBN || M <= 0 || N <= 0)
-    return set_error(DM_ERR_SHAPE, "wgrad needs M %% 256 == 0 and N %% 256 == 0 (M=%d, N=%d)", M, N);
+  if (M % 128 || N % 128 || M <= 0 || N <= 0)
+    return set_error(DM_ERR_SHAPE, "wgrad needs M %% 128 == 0 and N %% 128 == 0 (M=%d, N=%d)", M, N);
   if (lda < M || ldb < N || lda % 8 || ldb % 8)
     return set_error(DM_ERR_SHAPE, "wgrad row strides (lda=%d, ldb=%d) must be >= M/N and multiples of 8", lda, ldb);
   if (nseg < 1 || nseg > 64) return set_error(DM_ERR_SHAPE, "wgrad segments %d outside [1, 64]", nseg);
@@ -1063,7 +1078,8 @@ int dm_grouped_wgrad_strided(const void* a_tok, int M, int lda, const void* b_to
   a.C = dW; a.ldc = N; a.c_group_stride = (long long)M * N; a.beta = beta;
   a.seg_off = seg_off; a.nseg = nseg; a.seg_stride_rows = seg_stride_rows;
   EpiTensors et;
-  et.c = {dW, true, (uint64_t)N, (uint64_t)E * M, (uint64_t)N};
+  et.c = {dW, true, (uint64_t)N, (uint64_t)M, (uint64_t)N};
+  et.c.groups = (uint64_t)E;
   return launch_gemm<1, 1, 1, EPI_F32>(A, B, et, a, (cudaStream_t)stream);
 }
 
@@ -1078,8 +1094,8 @@ int dm_grouped_gemm_f32(const void* a3, const void* b3, int b_mn_major, const in
                         int cap_rows, int N, int K3, float* c, void* stream) {
   int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
-  if (K3 % GBK || K3 < GBK || N % GBN || N < GBN)
-    return set_error(DM_ERR_SHAPE, "gemm_f32 needs K3 %% 64 == 0 and N %% 256 == 0 (K3=%d, N=%d)", K3, N);
+  if (K3 % GBK || K3 < GBK || N % 128 || N < 128)
+    return set_error(DM_ERR_SHAPE, "gemm_f32 needs K3 %% 64 == 0 and N %% 128 == 0 (K3=%d, N=%d)", K3, N);
   if (reinterpret_cast<uintptr_t>(c) & 15) return set_error(DM_ERR_ALIGN, "C not 16-byte aligned");
   const GemmOperand A{a3, (uint64_t)K3, (uint64_t)cap_rows, (uint64_t)K3, false, false};
   GemmArgs a{};

@@ -48,8 +48,10 @@ class MoEShape:
         return _lib.capacity_rows(self.T, self.E, self.k)
 
     def validate(self) -> None:
-        if self.H % 256 or self.De % 256:
-            raise ValueError(f"hidden ({self.H}) and moe_hidden ({self.De}) must be multiples of 256")
+        # 128-column tiles: the expert GEMMs run 256-wide tiles and clip a 128-wide tail
+        # (deepseek_moe.yaml: moe_hidden 1408 = 11 x 128)
+        if self.H % 128 or self.De % 128 or self.H < 128 or self.De < 128:
+            raise ValueError(f"hidden ({self.H}) and moe_hidden ({self.De}) must be multiples of 128")
         if not (1 <= self.k <= min(self.E, _lib.DM_MAX_TOPK)):
             raise ValueError(f"topk {self.k} out of range for E={self.E}")
         if self.E > _lib.DM_MAX_EXPERTS:

@@ -90,3 +90,17 @@ def test_repo_configs_parse(name):
     exp = load_experiment(str(Path(__file__).resolve().parents[1] / "configs" / name))
     assert exp.schedule_kind is ScheduleKind.AFPIPE
     assert exp.model.bytes_per_element == 2
+
+
+def test_reference_deepseek_experiment_is_a_valid_hot_path_shape():
+    """The layer of the reference's own shipped experiment (pkg/configs/deepseek_moe.yaml:
+    hidden 2048, 64 experts top-4, moe_hidden 1408) maps to a hot-path shape the kernels
+    accept (128-wide GEMM tails; GPU parity in test_gpu_parity.py
+    deepseek_moe_yaml_De1408 / deepseek_moe_yaml_layer)."""
+    from paper_2605_11005_b200.moe import MoEShape
+
+    shape = MoEShape.from_experiment(parse_experiment(DEEPSEEK_DOC))
+    assert (shape.H, shape.E, shape.k, shape.De) == (2048, 64, 4, 1408)
+    shape.validate()
+    with pytest.raises(ValueError):
+        MoEShape(T=8, H=2048, E=64, k=4, De=1400).validate()
