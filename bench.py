@@ -58,8 +58,8 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
+    def __init__(self, gpu):
+        self.gpu = gpu   # nvidia-smi --id: ordinal or "GPU-<uuid>"
         self.proc = None
         self.lines: list[str] = []
         self._t = None
@@ -133,19 +133,22 @@ def _oracle_weights(H, E, De):
     return _WEIGHTS[key]
 
 
-def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: int | None = None,
-                 layers: int = 1, fixed_tokens: int | None = None):
-    """Time the oracle port (numpy fp32 BLAS, all host threads) on a bounded token sample
-    of one layer; a stack of `layers` identical-shape layers costs `layers` times that.
-    The sample doubles from 64 tokens until it takes tokens_budget_s / 4 (or is capped);
-    fixed_tokens times exactly that many."""
+CPU_SAMPLE_TOKENS = 1024
+
+
+def cpu_baseline(shape, tokens: int | None = None, layer=None, layers: int = 1, seed: int = 7):
+    """Time the oracle port (numpy fp32 BLAS, all host threads) on a sample of `tokens`
+    tokens (default min(T, 1024)) of one micro-batch: the full fwd + bwd of every one of
+    `layers` identical-shape layers, measured once — no extrapolation. The oracle reuses
+    the fp32 weights in place (no per-call copies), so a 1024-token sample is dominated by
+    the GEMMs, not by fixed per-call costs."""
     import numpy as np
 
     from oracle import oracle as O
 
     threads = O.cpu_threads()
     H, E, k, De = shape.H, shape.E, shape.k, shape.De
-    rng = np.random.default_rng(7)
+    rng = np.random.default_rng(seed)
     if layer is not None:
         from paper_2605_11005_b200.moe import split_w13
 
@@ -156,53 +159,50 @@ def cpu_baseline(shape, tokens_budget_s: float = 15.0, layer=None, max_tokens: i
         wg = (layer.router.wg if hasattr(layer, "router") else layer.wg).float().cpu().numpy()
     else:
         wg, w1, w3, w2 = _oracle_weights(H, E, De)
-    T = fixed_tokens or 64
-    best = None
-    while True:
-        x = O.f32_to_bf16_bits(rng.standard_normal((T, H), dtype=np.float32))
-        dy = O.round_bf16(rng.standard_normal((T, H), dtype=np.float32))
-        t0 = time.perf_counter()
+    T = min(shape.T, tokens or CPU_SAMPLE_TOKENS)
+    x = O.f32_to_bf16_bits(rng.standard_normal((T, H), dtype=np.float32))
+    dy = O.round_bf16(rng.standard_normal((T, H), dtype=np.float32))
+    t0 = time.perf_counter()
+    for _ in range(layers):
         f = O.moe_forward(x, wg, w1, w3, w2, k, dtype=np.float32)
         O.moe_backward(f, x, wg, w1, w3, w2, dy, dtype=np.float32)
-        dt = time.perf_counter() - t0
-        best = (T, dt)
-        if fixed_tokens or dt > tokens_budget_s / 4 or T >= (max_tokens or shape.T) or T * 2 > shape.T:
-            break
-        T *= 2
-    T, dt = best
-    return {"value": T / dt / layers, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{T} tokens of the {shape.T}-token micro-batch, full layer fwd+bwd "
-                      f"(H={H}, E={E}, k={k}, D_e={De}), numpy fp32 BLAS oracle, {dt:.2f} s"
-                      + (f"; x{layers} layers" if layers > 1 else "")}
+    dt = time.perf_counter() - t0
+    return {"value": T / dt, "unit": UNIT, "cores": threads, "kind": "port", "tokens": T, "seconds": round(dt, 3),
+            "sample": f"{T} of the {shape.T} tokens of one micro-batch, full fwd+bwd of {layers} layer(s) "
+                      f"(H={H}, E={E}, k={k}, D_e={De}), numpy fp32 BLAS oracle on {threads} threads, "
+                      f"measured {dt:.2f} s (no extrapolation)"}
 
 
 def run_reference(args, shape, exp):
+    """The reference arm: the reference has no MoE arithmetic, so this times
+    the oracle port (oracle/oracle.py) on the host cores. One step = one sample of
+    min(T, 1024) tokens through every layer's fwd + bwd; value = tokens / measured time
+    of that sample, ms_per_step = that measured time (the timed work IS the step)."""
     rank = _env_int("RANK", 0)
     if rank != 0:
         return 0
     steps, warm = args.steps, args.warmup
-    # the first warm-up step sizes the sample (doubling up to ~1 s of CPU work, at most 256
-    # tokens); every later step times that many tokens once, so K + W steps stay within minutes
-    tokens = None
     samples = []
+    t_run = time.perf_counter()
     for i in range(warm + steps):
-        r = cpu_baseline(shape, tokens_budget_s=4.0, max_tokens=256, layers=exp.model.layers, fixed_tokens=tokens)
-        tokens = tokens or int(r["sample"].split()[0])
+        r = cpu_baseline(shape, layers=exp.model.layers, seed=7 + i)
         if i >= warm:
             samples.append(r)
-    value = statistics.median(s["value"] for s in samples)
+    t_run = time.perf_counter() - t_run
+    secs = [s["seconds"] for s in samples]
+    tokens = samples[-1]["tokens"]
+    ms = statistics.median(secs) * 1e3
+    value = tokens / (ms / 1e3)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": warm,
-        # one full step (mb micro-batches of T tokens per layer) at the sampled rate
-        "ms_per_step": round(exp.workload.num_microbatches * shape.T / value * 1e3, 1),
-        "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": round(ms, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": Path(args.config).stem, "T": shape.T, "H": shape.H, "E": shape.E,
                    "k": shape.k, "D_e": shape.De, "layers": exp.model.layers,
-                   "microbatches": exp.workload.num_microbatches},
-        "cpu_baseline": {**samples[-1], "value": value},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "microbatches": exp.workload.num_microbatches, "tokens_per_step": tokens},
+        "cpu_baseline": {**{kk: v for kk, v in samples[-1].items() if kk != "seconds"}, "value": round(value, 3)},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "consistency": {"timed_s": round(sum(secs), 2), "run_s": round(t_run, 2)},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -219,6 +219,11 @@ def run_ours(args, shape, exp):
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 under torchrun, or without "
+                         f"WORLD_SIZE set so that bench.py starts the {args.gpus} ranks itself")
+    if args.attention and exp.model.bytes_per_element == 4:
+        raise SystemExit("--attention runs bf16 attention blocks; fp32 mode (bytes_per_element 4) is MoE-only")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -311,7 +316,7 @@ def run_ours(args, shape, exp):
         else:
             step()
 
-    sampler = ClockSampler(dev.index) if rank == 0 else None
+    sampler = ClockSampler(_clock_target(dev)) if rank == 0 else None
     if sampler:
         sampler.start()
     for _ in range(args.warmup):
@@ -453,10 +458,7 @@ def run_ours(args, shape, exp):
         fa, fb = attn[0].flops(exp.workload.seq_len, exp.workload.micro_batch)
         line["attention"] = {
             "ms_per_microbatch_layer": round(a_ms, 4), "TFLOP/s": round((fa + fb) / (a_ms / 1e3) / 1e12, 1),
-            "impl": ("own sm_100a flash-attention forward (dm_attention_fwd) + cuDNN SDPA backward on its O/LSE; "
-                     "cuBLAS projections, autograd" if attn[0].own_kernel
-                     and exp.workload.seq_len % (128 if exp.model.gqa_group % 2 == 0 else 256) == 0
-                     else "library: cuBLAS projections + torch SDPA (cuDNN/flash), autograd"),
+            "impl": _attention_impl_label(attn[0].last_path),
             "gqa_group": exp.model.gqa_group, "seq_len": exp.workload.seq_len}
         line["config"]["layer"] = "attention + residual MoE block"
         line["config"]["launch"] = "CUDA graphs" if graphs is not None else "eager"
@@ -496,6 +498,38 @@ def _uncovered(a, b):
     return tot
 
 
+def _attention_impl_label(path) -> str:
+    """Which attention path actually ran (AttentionBlock.last_path), for the bench line."""
+    if path == "own":
+        return ("own sm_100a flash-attention forward (dm_attention_fwd) + cuDNN SDPA backward on its O/LSE; "
+                "cuBLAS projections, autograd")
+    return "library: cuBLAS projections + torch SDPA (cuDNN/flash), autograd"
+
+
+def _clock_target(dev) -> str:
+    """nvidia-smi --id for a torch device: its UUID (robust to CUDA_VISIBLE_DEVICES remaps)."""
+    import torch
+
+    try:
+        return f"GPU-{torch.cuda.get_device_properties(dev).uuid}"
+    except Exception:  # noqa: BLE001 - older torch: fall back to the ordinal
+        return str(dev.index)
+
+
+def _merge_clocks(per_rank: list[dict], roles: list[str]) -> dict:
+    """Bench-line clocks for N>1: the F ranks (where the expert GEMMs run) — the lowest
+    median SM clock among them and the union of their throttle reasons — plus every rank's
+    own record."""
+    f = [c for c, r in zip(per_rank, roles) if r == "F" and c and c.get("sm_mhz")] or \
+        [c for c in per_rank if c and c.get("sm_mhz")]
+    out = {"sm_mhz": min(c["sm_mhz"] for c in f) if f else None,
+           "sm_max_mhz": max(c["sm_max_mhz"] for c in f) if f else None,
+           "reasons": sorted({x for c in f for x in c.get("reasons", [])}),
+           "source": "F ranks (expert GEMMs): min of per-rank medians, union of reasons"}
+    out["per_rank"] = [{"rank": i, "role": r, **(c or {})} for i, (c, r) in enumerate(zip(per_rank, roles))]
+    return out
+
+
 def run_afpipe(args, shape, exp, world, rank, local, dev):
     """N>1: A:F-split AF-Pipe runtime (one process per GPU, NCCL over NVLink)."""
     import torch
@@ -520,9 +554,8 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                 r.input(i).normal_()
             if r.has_output:
                 r.out_bufs[i].dy.normal_()
-    sampler = ClockSampler(dev.index) if rank == 0 else None
-    if sampler:
-        sampler.start()
+    sampler = ClockSampler(_clock_target(dev))   # every rank samples its own GPU
+    sampler.start()
     for _ in range(args.warmup):
         r.run_iteration()
     torch.cuda.synchronize()
@@ -547,7 +580,10 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
     ms = tt[0].item()
     lsum = torch.tensor([float(launches)], device=dev)
     dist.all_reduce(lsum)
-    clocks = sampler.stop() if sampler else None
+    clk_all = [None] * world
+    dist.all_gather_object(clk_all, sampler.stop())
+    roles = [topo.role(q)[0] for q in range(world)]
+    clocks = _merge_clocks(clk_all, roles)
 
     # measured peak device memory per rank vs the reference's memory model
     mem_all = [None] * world
@@ -802,6 +838,20 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
                      "MoEStack.forward_backward") + " with pinned host x/dy in, y/dx out (copy stream overlapped)"}
 
 
+def _self_launch(n: int, argv: list) -> int:
+    """`python bench.py --gpus N` without torchrun: start the N ranks the way the driver
+    does (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1) and pass
+    rank 0's JSON line through."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv]
+    return subprocess.run(cmd).returncode
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -838,8 +888,10 @@ def main(argv=None):
         exp = dataclasses.replace(exp, workload=wl, model=md,
                                   virtual_stages=md.layers if args.layers else exp.virtual_stages)
     shape = MoEShape.from_experiment(exp)
-    if args.impl == "reference":
+    if args.impl == "reference":   # CPU arm: rank 0 only, no GPU ranks to start
         return run_reference(args, shape, exp)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _self_launch(args.gpus, argv if argv is not None else sys.argv[1:])
     return run_ours(args, shape, exp)
 
 

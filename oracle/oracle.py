@@ -219,13 +219,13 @@ def moe_forward(x_bits, wg, w1, w3, w2, k, dtype=np.float64) -> Forward:
         if n == 0:
             continue
         xe = x[src[a:a + n]]
-        g[a:a + n] = xe @ w1[e].astype(dtype).T
-        u[a:a + n] = xe @ w3[e].astype(dtype).T
+        g[a:a + n] = xe @ w1[e].astype(dtype, copy=False).T
+        u[a:a + n] = xe @ w3[e].astype(dtype, copy=False).T
     act = _silu(g) * u
     for e in range(E):
         a, n = pad_off[e], counts[e]
         if n:
-            y_perm[a:a + n] = act[a:a + n] @ w2[e].astype(dtype).T
+            y_perm[a:a + n] = act[a:a + n] @ w2[e].astype(dtype, copy=False).T
     y = np.einsum("tk,tkh->th", w.astype(dtype), y_perm[row_map])
     return Forward(logits, idx, w, counts, pad_off, row_map, src, g, u, act, y_perm, y)
 
@@ -267,11 +267,11 @@ def moe_backward(fwd: Forward, x_bits, wg, w1, w3, w2, dy, dtype=np.float64) -> 
             continue
         sl = slice(a, a + n)
         g, u, act = fwd.g[sl], fwd.u[sl], fwd.act[sl]
-        d_act = dy_perm[sl] @ w2[e].astype(dtype)
+        d_act = dy_perm[sl] @ w2[e].astype(dtype, copy=False)
         sg = 1.0 / (1.0 + np.exp(-g))
         dg = d_act * u * sg * (1.0 + g * (1.0 - sg))
         du = d_act * g * sg
-        dx_perm[sl] = dg @ w1[e].astype(dtype) + du @ w3[e].astype(dtype)
+        dx_perm[sl] = dg @ w1[e].astype(dtype, copy=False) + du @ w3[e].astype(dtype, copy=False)
         xe = x[fwd.src[sl]]
         dw1[e] = dg.T @ xe
         dw3[e] = du.T @ xe

@@ -111,6 +111,7 @@ class AttentionBlock:
         self.dw_qkv = torch.zeros(rows, hidden, dtype=F32, device=dev)
         self.dw_o = torch.zeros(hidden, hidden, dtype=F32, device=dev)
         self._saved: dict = {}
+        self.last_path = None   # "own" / "library": which attention path the last forward took
 
     def flops(self, seq_len: int, micro_batch: int) -> tuple[int, int]:
         return attention_flops(self.H, self.nh // self.nkv, seq_len, micro_batch, self.d)
@@ -120,8 +121,10 @@ class AttentionBlock:
         b = T // seq_len
         qkv = x @ self.w_qkv.t()
         if self.own_kernel and own_attention_supported(x, seq_len, self.d, self.nh // self.nkv):
+            self.last_path = "own"
             o = _OwnCausalAttention.apply(qkv.contiguous(), seq_len, self.nh, self.nkv)
             return o @ self.w_o.t()
+        self.last_path = "library"
         q, k, v = qkv.split([self.nh * self.d, self.nkv * self.d, self.nkv * self.d], dim=1)
         q = q.view(b, seq_len, self.nh, self.d).transpose(1, 2)
         k = k.view(b, seq_len, self.nkv, self.d).transpose(1, 2)

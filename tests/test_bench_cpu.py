@@ -37,3 +37,24 @@ def test_reference_arm_other_ranks_exit_quietly():
     res = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}, "--gpus", "2")
     assert res.returncode == 0, res.stderr[-2000:]
     assert not [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_reference_arm_time_is_measured_not_extrapolated():
+    """ms_per_step is the measured time of the step's own sample: steps x ms_per_step fits
+    inside the arm's wall time, and value x ms_per_step recovers the sampled token count."""
+    res = _run(None, "--steps", "2", "--warmup", "1")
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    c = line["consistency"]
+    assert line["steps"] * line["ms_per_step"] / 1e3 <= c["timed_s"] * 1.01 + 1e-3
+    assert c["timed_s"] <= c["run_s"]
+    assert abs(line["value"] * line["ms_per_step"] / 1e3 - line["config"]["tokens_per_step"]) < 0.01 * line["config"]["tokens_per_step"]
+    assert "no extrapolation" in line["cpu_baseline"]["sample"]
+
+
+def test_gpus_must_match_world_size():
+    env = {**os.environ, "RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0"}
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config",
+                          str(ROOT / "configs" / "tiny.yaml")], capture_output=True, text=True, timeout=600,
+                         env=env, cwd=ROOT)
+    assert res.returncode != 0
+    assert "WORLD_SIZE" in res.stderr
