@@ -70,6 +70,12 @@ extern "C" {
 
 static inline int dm_num_chunks(int T) { return (T + DM_CHUNK_TOKENS - 1) / DM_CHUNK_TOKENS; }
 
+/* dm_route_and_dispatch's streaming router (E <= 16) sorts in units of
+ * DM_ROUTE_UNIT_TOKENS tokens (one warp's tokens); its workspace holds one histogram
+ * row per unit, which also covers the DM_CHUNK_TOKENS chunks of the two-pass path. */
+#define DM_ROUTE_UNIT_TOKENS 4
+static inline int dm_num_route_units(int T) { return (T + DM_ROUTE_UNIT_TOKENS - 1) / DM_ROUTE_UNIT_TOKENS; }
+
 /* Upper bound on sum_e roundup(count_e, DM_ROW_ALIGN) for T tokens, top-k. */
 static inline int dm_capacity_rows(int T, int E, int k) {
   long long r = (long long)T * k + (long long)E * (DM_ROW_ALIGN - 1);
@@ -78,30 +84,34 @@ static inline int dm_capacity_rows(int T, int E, int k) {
 
 typedef struct dm_route_ws {
   float* logits;        /* [T, E] fp32 */
-  int32_t* chunk_hist;  /* [nchunk, E] */
-  int32_t* chunk_base;  /* [nchunk, E] */
+  int32_t* chunk_hist;  /* [nunit, E] (two-pass path: [nchunk, E]) */
+  int32_t* chunk_base;  /* [nunit, E] (two-pass path: [nchunk, E]) */
   int32_t* rank;        /* [T, k] stable rank of (t, j) among its chunk's slots of the same expert */
+  uint32_t* done;       /* CTA completion counters of the streaming router (4 KB): zero when
+                           the workspace is first used (allocate it zeroed); left zero */
 } dm_route_ws;
 
 static inline size_t dm_align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 static inline size_t dm_route_workspace_size(int T, int H, int E, int k) {
   (void)H;
-  size_t nchunk = (size_t)dm_num_chunks(T);
-  return dm_align256((size_t)T * E * 4) + 2 * dm_align256(nchunk * E * 4) + dm_align256((size_t)T * k * 4);
+  size_t nunit = (size_t)dm_num_route_units(T);
+  return dm_align256((size_t)T * E * 4) + 2 * dm_align256(nunit * E * 4) + dm_align256((size_t)T * k * 4) + 4096;
 }
 
 static inline void dm_route_workspace_layout(int T, int H, int E, int k, void* ws, dm_route_ws* out) {
-  (void)H; (void)k;
+  (void)H;
   char* p = (char*)ws;
-  size_t nchunk = (size_t)dm_num_chunks(T);
+  size_t nunit = (size_t)dm_num_route_units(T);
   out->logits = (float*)p;
   p += dm_align256((size_t)T * E * 4);
   out->chunk_hist = (int32_t*)p;
-  p += dm_align256(nchunk * E * 4);
+  p += dm_align256(nunit * E * 4);
   out->chunk_base = (int32_t*)p;
-  p += dm_align256(nchunk * E * 4);
+  p += dm_align256(nunit * E * 4);
   out->rank = (int32_t*)p;
+  p += dm_align256((size_t)T * k * 4);
+  out->done = (uint32_t*)p;
 }
 
 /* Tokens per router-wgrad partial block: small blocks (more parallelism) when the
@@ -178,6 +188,9 @@ DM_API int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, 
 
 /* Debug: route 2-SM GEMM wait-cycle counters into a device u64[5] buffer (NULL = off). */
 DM_API int dm_debug_gemm_profile(void* buf);
+/* Debug: per-CTA globaltimer timeline of the streaming router (>= 64 u64 per CTA, zeroed;
+ * NULL turns it off). */
+DM_API int dm_debug_route_profile(void* buf);
 
 /* ---- combine (A side) ------------------------------------------------- */
 /* y[t] = resid[t] + sum_j w[t,j] * y_perm[row_map[t,j]]  (fp32 accumulation; resid may be

@@ -61,6 +61,7 @@ SIGNATURES: dict[str, tuple] = {
     "dm_grouped_w13_dgrad": (_i, [_vp, _vp, _i32p, _i, _i, _i, _i, _i, _vp, _vp]),
     "dm_grouped_wgrad": (_i, [_vp, _i, _vp, _i, _i32p, _i, _i, _i, _i, _f32p, _f, _vp]),
     "dm_debug_gemm_profile": (_i, [_vp]),
+    "dm_debug_route_profile": (_i, [_vp]),
     "dm_combine_fwd": (_i, [_vp, _i32p, _f32p, _i, _i, _i, _vp, _vp, _vp]),
     "dm_combine_bwd": (_i, [_vp, _vp, _i32p, _f32p, _i32p, _i32p, _i, _i, _i, _i, _vp, _f32p,
                             _f32p, _f32p, _vp]),
@@ -134,10 +135,15 @@ def num_chunks(T: int) -> int:
     return (T + DM_CHUNK_TOKENS - 1) // DM_CHUNK_TOKENS
 
 
+DM_ROUTE_UNIT_TOKENS = 4
+
+
 def route_workspace_size(T: int, H: int, E: int, k: int) -> int:
+    """Mirror of dm_route_workspace_size (include/dm_moe.h); the last 4 KB hold the
+    streaming router's completion counters, which must be zero on first use."""
     a = lambda v: (v + 255) & ~255  # noqa: E731
-    nch = num_chunks(T)
-    return a(T * E * 4) + 2 * a(nch * E * 4) + a(T * k * 4)
+    nunit = (T + DM_ROUTE_UNIT_TOKENS - 1) // DM_ROUTE_UNIT_TOKENS
+    return a(T * E * 4) + 2 * a(nunit * E * 4) + a(T * k * 4) + 4096
 
 
 def router_wgrad_token_block(E: int) -> int:

@@ -16,6 +16,8 @@
 //   chunk with j % 2 == s (ascending); v[p] = partial[p][0] + partial[p][1]; then
 //   an xor butterfly 16,8,4,2,1 of round-to-nearest fp32 adds. Two chains per
 //   lane map onto packed fp32x2 FMAs (FFMA2), bit-identical to scalar fmaf.
+#include <stdlib.h>
+
 #include "dm_common.cuh"
 #include "dm_internal.h"
 
@@ -87,18 +89,19 @@ router_logits_kernel(const __nv_bfloat16* __restrict__ x, const float* __restric
 // Stable within-chunk ranks (warp 0): sel[] holds the chunk's expert ids in
 // token-major (t, j) order; rank[s] = number of earlier slots of the chunk that
 // chose the same expert. run[] (E ints, zeroed) ends as the chunk histogram.
-__device__ __forceinline__ void chunk_ranks(const int* sel, int nslots, int* run, int32_t* rank_out, int lane) {
+template <typename SelT, typename RunT = int>
+__device__ __forceinline__ void chunk_ranks(const SelT* sel, int nslots, RunT* run, int32_t* rank_out, int lane) {
   for (int base = 0; base < nslots; base += 32) {
     const int s = base + lane;
     const bool valid = s < nslots;
-    const int e = valid ? sel[s] : -1 - lane;
+    const int e = valid ? (int)sel[s] : -1 - lane;
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     const int r = __popc(peers & ((1u << lane) - 1u));
     const int prior = valid ? run[e] : 0;
     __syncwarp();
     if (valid) {
       rank_out[s] = prior + r;
-      if (r == 0) run[e] = prior + __popc(peers);
+      if (r == 0) run[e] = (RunT)(prior + __popc(peers));
     }
     __syncwarp();
   }
@@ -238,6 +241,339 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
     if (threadIdx.x < E) chunk_hist[(size_t)chunk * E + threadIdx.x] = run[threadIdx.x];
   }
 }
+
+// ------------------------------------------------------------------------
+// Streaming dispatch (E <= 16, H % 256 == 0, k <= 8): dm_route_and_dispatch in ONE
+// cooperative launch — route, grid barrier, offset scan, permute. Same canonical-order
+// logits, top-k, softmax weights and stable permutation as the three-launch path
+// (router_fused_kernel / expert_scan / permute_kernel, kept for other shapes and for A/B
+// runs with DM_DISPATCH_LEGACY=1). Shaped by per-CTA globaltimer timelines
+// (dm_debug_route_profile, scripts/rs_probe.py) of four designs:
+//   * work unit = RS_NT = DM_ROUTE_UNIT_TOKENS tokens (one warp); CTA b owns the contiguous
+//     units [b*upc, (b+1)*upc), so T = 4096 keeps all 148 SMs busy (7 units each) where
+//     32-token chunks left 20 SMs idle;
+//   * W_g (fp32, the whole [E, H] gate) arrives by TMA in SWIZZLE_128B boxes: a lane's 32-byte
+//     chunk of a 1 KB k-tile sits at granules (2(l&3)+h) ^ (l>>2) of 128-byte row l>>2, which
+//     makes the lane-strided 128-bit reads conflict-free without a transposing fill (register
+//     / cp.async fills took 5.8 / 9.8 us of L2 latency per CTA; the TMA fill 1.3-1.8 us);
+//   * x is read straight from global memory into registers two k-tiles ahead, so all 8 warps
+//     compute at once (a bulk-copy ring next to W_g held 3 units: 3 warps, 2-3x slower);
+//   * 4 tokens per warp share every W_g read; the k-tile's W_g pairs are loaded before its
+//     FFMA2s, which run element pair j outermost (independent chains back to back). The
+//     route phase is fp32-FMA bound (T*E*H FMAs in the canonical fmaf order; ~11 us of math
+//     for Mixtral's 134 M FMAs), not HBM bound;
+//   * histogram offsets: each CTA prefix-sums its own units in smem, publishes its totals,
+//     and after a grid barrier (fire-and-forget reductions on a monotonic counter: returning
+//     same-address atomics from 148 SMs serialise to ~10 us) every CTA scans the CTA totals
+//     (~1.2k ints) itself — no serial last-CTA tail;
+//   * permute: each CTA copies its own token rows (x still L2-resident) to their k expert
+//     rows, warp per row, and zeroes a share of the padding rows. This phase is bound by the
+//     write path: 64 MB of x_perm at the measured pure-write rate (scripts/hbm_probe.py,
+//     3.83 TB/s) is ~17 us.
+constexpr int RS_NT = DM_ROUTE_UNIT_TOKENS;
+constexpr int RS_WARPS = 8;
+constexpr int RS_THREADS = RS_WARPS * 32;
+constexpr int RS_MAX_UPC = 64;                      // units per CTA (grid grows past #SMs beyond)
+constexpr int RS_SMEM_BUDGET = 227 * 1024;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// optional per-CTA timeline (dm_debug_route_profile): [cta][0..63] globaltimer ns
+__device__ unsigned long long* g_rs_prof = nullptr;
+
+template <int EM>
+__global__ void __launch_bounds__(RS_THREADS, 1)
+dispatch_stream_kernel(const __grid_constant__ CUtensorMap tmW, const __nv_bfloat16* __restrict__ x, int T, int H,
+                       int E, int k, int upc, int w_boxes, int w_box_rows, int32_t* __restrict__ idx,
+                       float* __restrict__ w, int32_t* __restrict__ rank, int32_t* __restrict__ cta_tot,
+                       uint32_t* __restrict__ gbar, int32_t* __restrict__ counts, int32_t* __restrict__ pad_off,
+                       int32_t* __restrict__ row_map, int32_t* __restrict__ src_token,
+                       __nv_bfloat16* __restrict__ x_perm) {
+  extern __shared__ uint8_t rs_raw[];
+  __shared__ uint64_t wbar;
+  __shared__ int8_t sel[RS_WARPS][RS_NT * 8];              // expert ids < 16; RS_NT * k <= 32
+  __shared__ int16_t run[RS_WARPS][EM];
+  __shared__ int16_t s_uh[RS_MAX_UPC][EM];                 // unit histograms -> within-CTA bases
+  __shared__ int s_pad[EM + 1], s_cnt[EM];
+  __shared__ unsigned long long s_target;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NI = H >> 8;                                    // 256-element k-tiles (H % 256 == 0)
+  const uint32_t pad = (1024u - (smem_u32(rs_raw) & 1023u)) & 1023u;
+  uint8_t* sW = rs_raw + pad;                               // [EM][H] fp32, SWIZZLE_128B rows
+  const int nunit = (T + RS_NT - 1) / RS_NT;
+  const int ub = blockIdx.x * upc;
+  const int nmine = max(0, min(upc, nunit - ub));
+  unsigned long long* prof = g_rs_prof ? g_rs_prof + (size_t)blockIdx.x * 64 : nullptr;
+  if (prof && tid == 0) prof[0] = gtimer();
+  if (tid == 0) {
+    // grid barrier target: the arrival counter's value once every CTA of THIS launch arrived
+    s_target = *reinterpret_cast<volatile unsigned long long*>(gbar + 32) + gridDim.x;
+    mbar_init(&wbar, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmW);
+    mbar_expect_tx(&wbar, (uint32_t)(w_boxes * w_box_rows * 128));
+    for (int b = 0; b < w_boxes; ++b) tma_load_2d(sW + (size_t)b * w_box_rows * 128, &tmW, &wbar, 0, b * w_box_rows);
+  }
+  {   // W_g rows e >= E are zero (the hot loop has no E checks)
+    const int4 z = make_int4(0, 0, 0, 0);
+    for (size_t o = (size_t)E * H * 4 + tid * 16; o < (size_t)EM * H * 4; o += RS_THREADS * 16)
+      *reinterpret_cast<int4*>(sW + o) = z;
+  }
+  __syncthreads();
+  // this lane's two 16-byte W_g granules inside every 1 KB k-tile (see the header comment)
+  const uint32_t wrow = (uint32_t)(lane >> 2) * 128u;
+  const uint32_t wof0 = wrow + ((((uint32_t)(lane & 3) << 1) ^ (uint32_t)(lane >> 2)) << 4);
+  const uint32_t wof1 = wrow + (((((uint32_t)(lane & 3) << 1) | 1u) ^ (uint32_t)(lane >> 2)) << 4);
+  const uint32_t sWa = smem_u32(sW);
+  bool w_ready = false;
+  for (int i = warp; i < nmine; i += RS_WARPS) {
+    const int u = ub + i;
+    const int t0 = u * RS_NT;
+    // this unit's token rows (rows past T read row T-1; their results are dropped)
+    const __nv_bfloat16* xr[RS_NT];
+#pragma unroll
+    for (int t = 0; t < RS_NT; ++t) xr[t] = x + (size_t)min(t0 + t, T - 1) * H + lane * 8;
+    auto ldx = [&](int it, int4 (&xv)[RS_NT]) {
+#pragma unroll
+      for (int t = 0; t < RS_NT; ++t) xv[t] = it < NI ? ld_nc_v4(xr[t] + it * 256) : make_int4(0, 0, 0, 0);
+    };
+    int4 x0[RS_NT], x1[RS_NT];
+    ldx(0, x0);
+    ldx(1, x1);
+    if (!w_ready) {
+      mbar_wait(&wbar, 0);
+      w_ready = true;
+      if (prof && tid == 0) prof[1] = gtimer();
+    }
+    float2 acc[RS_NT][EM];   // {even-element chain, odd-element chain}
+#pragma unroll
+    for (int t = 0; t < RS_NT; ++t)
+#pragma unroll
+      for (int e = 0; e < EM; ++e) acc[t][e] = make_float2(0.f, 0.f);
+#pragma unroll 1
+    for (int it = 0; it < NI; ++it) {
+      int4 x2[RS_NT];
+      ldx(it + 2, x2);   // two k-tiles ahead
+      float4 wv[EM][2];
+#pragma unroll
+      for (int e = 0; e < EM; ++e) {
+        const uint32_t tb = sWa + (uint32_t)((size_t)e * H * 4) + (uint32_t)it * 1024u;
+        const int4 a = ld_shared_v4(tb + wof0), b = ld_shared_v4(tb + wof1);
+        wv[e][0] = make_float4(__int_as_float(a.x), __int_as_float(a.y), __int_as_float(a.z), __int_as_float(a.w));
+        wv[e][1] = make_float4(__int_as_float(b.x), __int_as_float(b.y), __int_as_float(b.z), __int_as_float(b.w));
+      }
+      // element pair j outermost: each chain (t, e) still takes its pairs in ascending order
+      // (the canonical order); consecutive FFMA2s are independent
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        float2 xp[RS_NT];
+#pragma unroll
+        for (int t = 0; t < RS_NT; ++t) {
+          const uint32_t q = reinterpret_cast<const uint32_t*>(&x0[t])[jj];
+          xp[t] = make_float2(bf16lo(q), bf16hi(q));
+        }
+#pragma unroll
+        for (int e = 0; e < EM; ++e) {
+          const float4 wq = wv[e][jj >> 1];
+          const float2 wj = (jj & 1) ? make_float2(wq.z, wq.w) : make_float2(wq.x, wq.y);
+#pragma unroll
+          for (int t = 0; t < RS_NT; ++t) acc[t][e] = ffma2(xp[t], wj, acc[t][e]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RS_NT; ++t) { x0[t] = x1[t]; x1[t] = x2[t]; }
+    }
+    if (prof && lane == 0 && i < 24) prof[16 + i] = gtimer();
+    // butterflies of the RS_NT x EM logits (independent shuffle chains interleave)
+    float lgs[RS_NT][EM];
+#pragma unroll
+    for (int t = 0; t < RS_NT; ++t)
+#pragma unroll
+      for (int e = 0; e < EM; ++e) lgs[t][e] = __fadd_rn(acc[t][e].x, acc[t][e].y);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int t = 0; t < RS_NT; ++t)
+#pragma unroll
+        for (int e = 0; e < EM; ++e) lgs[t][e] = __fadd_rn(lgs[t][e], __shfl_xor_sync(0xffffffffu, lgs[t][e], off));
+    // top-k: lane (t, j) = (lane / k, lane % k) produces pick j of token t; ties -> lower
+    // expert id
+    {
+      const int t = lane / k, j = lane - t * k;
+      const bool act = lane < RS_NT * k && t0 + t < T;
+      float lgt[EM];
+#pragma unroll
+      for (int e = 0; e < EM; ++e) {
+        float v = lgs[0][e];
+#pragma unroll
+        for (int tt = 1; tt < RS_NT; ++tt) v = (t == tt) ? lgs[tt][e] : v;
+        lgt[e] = v;
+      }
+      // the k sequential arg-max passes of router_fused_kernel, run by each lane for its
+      // own token, keeping pick j (same results for any input, NaN included)
+      unsigned taken = 0;
+      int mine = -1;
+      float v0 = 0.f, vsel = 0.f, ssum = 0.f;
+      for (int jj = 0; jj < k; ++jj) {
+        float bv = -INFINITY;
+        int be = -1;
+#pragma unroll
+        for (int e = 0; e < EM; ++e)
+          if (e < E && !((taken >> e) & 1u) && (be < 0 || lgt[e] > bv)) { bv = lgt[e]; be = e; }
+        taken |= 1u << be;
+        if (jj == 0) v0 = bv;
+        ssum += expf(bv - v0);
+        if (jj == j) { mine = be; vsel = bv; }
+      }
+      const float vmax = v0;
+      if (act) {
+        const int tok = t0 + t;
+        idx[(size_t)tok * k + j] = mine;
+        w[(size_t)tok * k + j] = expf(vsel - vmax) / ssum;
+        sel[warp][t * k + j] = (int8_t)mine;
+      }
+    }
+    if (lane < EM) run[warp][lane] = 0;
+    __syncwarp();
+    chunk_ranks(sel[warp], min(RS_NT, T - t0) * k, run[warp], rank + (size_t)t0 * k, lane);
+    __syncwarp();
+    if (lane < EM) s_uh[i][lane] = run[warp][lane];
+    __syncwarp();
+  }
+  if (prof && tid == 0) prof[2] = gtimer();
+  // within-CTA exclusive prefix over the units (thread e walks expert e), CTA totals out
+  __syncthreads();
+  if (tid < E) {
+    int acc = 0;
+    for (int i = 0; i < nmine; ++i) {
+      const int v = s_uh[i][tid];
+      s_uh[i][tid] = (int16_t)acc;
+      acc += v;
+    }
+    cta_tot[(size_t)blockIdx.x * E + tid] = acc;
+  }
+  // ------------------------------------------------------------ grid barrier
+  // (cooperative launch: all CTAs are resident). Arrivals are fire-and-forget reductions on a
+  // monotonic 64-bit counter (no returning atomics: 148 returning same-address atomics
+  // serialise to ~10 us); each CTA spins until the counter reaches this launch's target;
+  // CTA 0 then publishes the next launch's base.
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(gbar);
+    fence_acq_rel_gpu();
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" :: "l"(ctr) : "memory");
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+      if (v < s_target) __nanosleep(32);
+    } while (v < s_target);
+    if (blockIdx.x == 0) *reinterpret_cast<volatile unsigned long long*>(gbar + 32) = s_target;
+  }
+  __syncthreads();
+  fence_acq_rel_gpu();
+  if (prof && tid == 0) prof[3] = gtimer();
+  // ------------------------------------------------- scan of the CTA totals
+  // every CTA: s_base [nb][E] (exclusive over CTAs, in the dynamic smem), s_cnt, s_pad
+  const int nb = gridDim.x;
+  const int row_bytes = H * 2;
+  int* s_base = reinterpret_cast<int*>(rs_raw);
+  for (int q = tid; q < nb * E; q += RS_THREADS) s_base[q] = __ldcg(cta_tot + q);
+  __syncthreads();
+  for (int e = warp; e < E; e += RS_WARPS) {
+    int carry = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int b = b0 + lane;
+      const int v = b < nb ? s_base[b * E + e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+      }
+      if (b < nb) s_base[b * E + e] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_cnt[e] = carry;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      s_pad[e] = acc;
+      acc += (s_cnt[e] + DM_ROW_ALIGN - 1) / DM_ROW_ALIGN * DM_ROW_ALIGN;
+    }
+    s_pad[E] = acc;
+    if (blockIdx.x == 0) {
+      for (int e = 0; e < E; ++e) { counts[e] = s_cnt[e]; pad_off[e] = s_pad[e]; }
+      pad_off[E] = acc;
+    }
+  }
+  __syncthreads();
+  // ------------------------------------------------------- permute (scatter)
+  // positions of this CTA's (token, slot)s: row_map, src_token, and a smem copy
+  const int tok0 = ub * RS_NT;
+  const int ntok = max(0, min(nmine * RS_NT, T - tok0));
+  const int myb = blockIdx.x;
+  int* s_posn = s_base + nb * E;                            // [ntok * k]
+  for (int q = tid; q < ntok * k; q += RS_THREADS) {
+    const int t = tok0 + q / k;
+    const int e = idx[(size_t)t * k + q % k];
+    const int pos = s_pad[e] + s_base[myb * E + e] + s_uh[(t / RS_NT) - ub][e] + rank[(size_t)t * k + q % k];
+    s_posn[q] = pos;
+    row_map[(size_t)t * k + q % k] = pos;
+    src_token[pos] = t;
+  }
+  __syncthreads();
+  // copy: warp per token row (x just streamed through L2 by the route phase), the whole row
+  // in flight per warp (16 x 16 B per lane at H = 4096), k stores per vector; then the
+  // padding rows [s_pad[e] + s_cnt[e], s_pad[e+1]) are zeroed (they feed the ragged-K wgrad)
+  // and marked src_token = -1, spread over every CTA's warps
+  {
+    const int nvec = H >> 3;
+    for (int r = warp; r < ntok; r += RS_WARPS) {
+      const __nv_bfloat16* src = x + (size_t)(tok0 + r) * H;
+      int pj[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pj[j] = j < k ? s_posn[r * k + j] : 0;
+      for (int c0 = lane; c0 < nvec; c0 += 32 * 16) {
+        int4 v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int c = c0 + 32 * q;
+          v[q] = c < nvec ? ld_nc_v4(src + c * 8) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j >= k) break;
+          __nv_bfloat16* dst = x_perm + (size_t)pj[j] * H;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int c = c0 + 32 * q;
+            if (c < nvec) st_v4(dst + c * 8, v[q]);
+          }
+        }
+      }
+    }
+    const int end = s_pad[E];
+    const int4 z = make_int4(0, 0, 0, 0);
+    for (int r = myb * RS_WARPS + warp; r < end; r += nb * RS_WARPS) {
+      int lo = 0, hi = E;   // largest e with s_pad[e] <= r
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_pad[mid] <= r) lo = mid; else hi = mid;
+      }
+      if (r < s_pad[lo] + s_cnt[lo]) continue;
+      if (lane == 0) src_token[r] = -1;
+      __nv_bfloat16* row = x_perm + (size_t)r * H;
+      for (int c = lane; c < nvec; c += 32) st_v4(row + c * 8, z);
+    }
+  }
+  if (prof && tid == 0) prof[4] = gtimer();
+}
+
 
 // Generic top-k (any E): warp per token over the logits row; ties -> lower expert
 // id; weights = softmax over the selected logits. CTA per chunk also produces the
@@ -391,20 +727,21 @@ __global__ void __launch_bounds__(256)
 permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
                const int32_t* __restrict__ rank, const int32_t* __restrict__ chunk_base,
                const int32_t* __restrict__ counts, const int32_t* __restrict__ pad_off, int T, int H,
-               int E, int k_rt, int32_t* __restrict__ row_map, int32_t* __restrict__ src_token,
-               __nv_bfloat16* __restrict__ x_perm) {
+               int E, int k_rt, int chunk_tokens, int rel_base, const int32_t* __restrict__ cta_base, int upc,
+               int32_t* __restrict__ row_map, int32_t* __restrict__ src_token, __nv_bfloat16* __restrict__ x_perm) {
   const int k = KT ? KT : k_rt;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int nvec = H >> 3;
   for (int t = gwarp; t < T; t += nwarps) {
-    const int c = t / DM_CHUNK_TOKENS;
+    const int c = t / chunk_tokens;
     int p[KT ? KT : DM_MAX_TOPK];
 #pragma unroll
     for (int j = 0; j < k; ++j) {
       const int e = idx[(size_t)t * k + j];
-      p[j] = chunk_base[(size_t)c * E + e] + rank[(size_t)t * k + j];
+      p[j] = chunk_base[(size_t)c * E + e] + rank[(size_t)t * k + j] + (rel_base ? pad_off[e] : 0) +
+             (cta_base ? cta_base[(size_t)(c / upc) * E + e] : 0);
     }
     if (lane < k) {
       int pj = p[0];
@@ -447,11 +784,6 @@ permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ 
 constexpr int RT_TOK = 32, RT_EXP = 16, RT_THREADS = 256, RT_STAGES = 3;
 constexpr int RT_STAGE_INT4 = RT_TOK * 32 + RT_EXP * 2 * 32;  // 16 KB x + 16 KB W_g
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(valid ? 16 : 0)
-               : "memory");
-}
 
 __global__ void __launch_bounds__(RT_THREADS, 1)
 router_logits_tiled_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg,
@@ -611,6 +943,95 @@ static int token_grid_dispatch(int T) {
   return blocks < cap ? blocks : cap;
 }
 
+static int permute_launch(const void* x, const int32_t* idx, const int32_t* rank, const int32_t* chunk_base,
+                          const int32_t* counts, const int32_t* pad_off, int T, int H, int E, int k,
+                          int chunk_tokens, int rel_base, const int32_t* cta_base, int upc, int32_t* row_map,
+                          int32_t* src_token, void* x_perm, cudaStream_t st) {
+  const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  __nv_bfloat16* xp = reinterpret_cast<__nv_bfloat16*>(x_perm);
+  const int grid = token_grid_dispatch(T);
+#define DM_PERM(KTV) permute_kernel<KTV><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, \
+                                                                 chunk_tokens, rel_base, cta_base, upc, row_map, src_token, xp)
+  switch (k) {
+    case 1: DM_PERM(1); break;
+    case 2: DM_PERM(2); break;
+    case 4: DM_PERM(4); break;
+    case 8: DM_PERM(8); break;
+    default: DM_PERM(0); break;
+  }
+#undef DM_PERM
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "permute launch");
+  note_launch();
+  return DM_OK;
+}
+
+// Returns -1 when the streaming dispatch does not apply (E > 16, H % 256 != 0, k > 8, W_g
+// over the shared-memory budget, more than RS_MAX_UPC units per resident CTA, or no
+// cooperative launch). One cooperative launch: route, grid barrier, scan, permute.
+static int dispatch_stream_launch(const void* x, const float* wg, int T, int H, int E, int k, int32_t* idx, float* w,
+                                  int32_t* rank, int32_t* cta_tot, uint32_t* gbar, int32_t* counts, int32_t* pad_off,
+                                  int32_t* row_map, int32_t* src_token, void* x_perm, cudaStream_t stream) {
+  if (E > 16 || H % 256 || RS_NT * k > 32) return -1;   // one lane per (token, slot) in the top-k
+  if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(wg) & 15 ||
+      reinterpret_cast<uintptr_t>(x_perm) & 15) return -1;
+  const int EM = E <= 8 ? 8 : 16;
+  const size_t smem = 1024 /* alignment slack */ + (size_t)EM * H * 4;
+  if (smem + 4096 /* static */ > (size_t)RS_SMEM_BUDGET) return -1;
+  const int nunit = (T + RS_NT - 1) / RS_NT;
+  const void* kern = EM == 8 ? (const void*)dispatch_stream_kernel<8> : (const void*)dispatch_stream_kernel<16>;
+  if (int rc = ensure_smem_attr(kern, (int)smem, "cudaFuncSetAttribute(dispatch_stream)")) return rc;
+  const int resident = num_sms_current() * max_active_blocks(kern, RS_THREADS, smem);
+  int grid = nunit < resident ? nunit : resident;
+  const int upc = (nunit + grid - 1) / grid;
+  if (upc > RS_MAX_UPC) return -1;
+  grid = (nunit + upc - 1) / upc;
+  // phase 2/3 scratch in the dynamic smem: CTA-total table, positions, >= 2 staging rows
+  const size_t scratch = (((size_t)grid * E + (size_t)upc * RS_NT * k) * 4 + 1023) & ~(size_t)1023;
+  if (scratch + 2 * (size_t)H * 2 > (size_t)EM * H * 4) return -1;
+  // W_g as [E*H/32, 32] fp32 rows of 128 B, SWIZZLE_128B boxes of w_box_rows rows
+  const int rows_per_expert = H / 32;
+  int w_box_rows = 8;
+  for (int r = 256; r >= 8; r -= 8)
+    if (rows_per_expert % r == 0) { w_box_rows = r; break; }
+  const int w_boxes = E * rows_per_expert / w_box_rows;
+  CUtensorMap tmW;
+  {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled entry point unavailable");
+    cuuint64_t dims[2] = {32, (cuuint64_t)E * rows_per_expert};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {32, (cuuint32_t)w_box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&tmW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(wg), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled(W_g) failed (%d)", (int)r);
+  }
+  const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  __nv_bfloat16* xp = reinterpret_cast<__nv_bfloat16*>(x_perm);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(RS_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;   // the grid barrier needs every CTA resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (EM == 8)
+    e = cudaLaunchKernelEx(&cfg, dispatch_stream_kernel<8>, tmW, xb, T, H, E, k, upc, w_boxes, w_box_rows, idx, w, rank,
+                           cta_tot, gbar, counts, pad_off, row_map, src_token, xp);
+  else
+    e = cudaLaunchKernelEx(&cfg, dispatch_stream_kernel<16>, tmW, xb, T, H, E, k, upc, w_boxes, w_box_rows, idx, w,
+                           rank, cta_tot, gbar, counts, pad_off, row_map, src_token, xp);
+  if (e != cudaSuccess) return set_cuda_error(e, "dispatch_stream launch");
+  note_launch();
+  return DM_OK;
+}
+
 }  // namespace dm
 
 using namespace dm;
@@ -624,6 +1045,15 @@ static int check_route_shape(int T, int H, int E, int k) {
 }
 
 extern "C" {
+
+/* Debug/profiling hook: when `buf` (device, >= 64 u64 per CTA, zeroed) is non-NULL the
+ * streaming router records a per-CTA globaltimer timeline: [0..7] start, W_g staged,
+ * warp 0's units done, local prefix, group ticket, ticket, scan done, all units done;
+ * [8+i] unit i issued (i < 8); [16+2i], [17+2i] unit i data ready / math done (i < 24). */
+int dm_debug_route_profile(void* buf) {
+  cudaError_t e = cudaMemcpyToSymbol(g_rs_prof, &buf, sizeof(buf));
+  return e == cudaSuccess ? DM_OK : set_cuda_error(e, "cudaMemcpyToSymbol(g_rs_prof)");
+}
 
 int dm_router_logits(const void* x, const float* wg, float* logits, int T, int H, int E, void* stream) {
   int rc = check_route_shape(T, H, E, 1);
@@ -669,21 +1099,8 @@ int dm_permute(const void* x, const int32_t* idx, const int32_t* rank, const int
   if (rc) return rc;
   if (reinterpret_cast<uintptr_t>(x) & 15 || reinterpret_cast<uintptr_t>(x_perm) & 15)
     return set_error(DM_ERR_ALIGN, "permute rows must be 16-byte aligned");
-  const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
-  __nv_bfloat16* xp = reinterpret_cast<__nv_bfloat16*>(x_perm);
-  const int grid = token_grid_dispatch(T);
-  cudaStream_t st = (cudaStream_t)stream;
-  switch (k) {
-    case 1: permute_kernel<1><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
-    case 2: permute_kernel<2><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
-    case 4: permute_kernel<4><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
-    case 8: permute_kernel<8><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
-    default: permute_kernel<0><<<grid, 256, 0, st>>>(xb, idx, rank, chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, xp); break;
-  }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_cuda_error(e, "permute launch");
-  note_launch();
-  return DM_OK;
+  return permute_launch(x, idx, rank, chunk_base, counts, pad_off, T, H, E, k, DM_CHUNK_TOKENS, 0, nullptr, 1,
+                        row_map, src_token, x_perm, (cudaStream_t)stream);
 }
 
 int dm_route_and_dispatch(const void* x, const float* wg, int T, int H, int E, int k, void* workspace,
@@ -693,6 +1110,17 @@ int dm_route_and_dispatch(const void* x, const float* wg, int T, int H, int E, i
   if (rc) return rc;
   dm_route_ws ws;
   dm_route_workspace_layout(T, H, E, k, workspace, &ws);
+  if (reinterpret_cast<uintptr_t>(x_perm) & 15) return set_error(DM_ERR_ALIGN, "x_perm must be 16-byte aligned");
+  // streaming dispatch: ONE cooperative launch (route, grid barrier, scan, permute).
+  // Workspace: CTA totals in chunk_hist, grid-barrier counters in done.
+  // (DM_DISPATCH_LEGACY=1: the three-launch router_fused / scan / permute path, for A/B runs)
+  static const bool legacy = [] {
+    const char* e = getenv("DM_DISPATCH_LEGACY");
+    return e && e[0] == '1';
+  }();
+  if (!legacy && (rc = dispatch_stream_launch(x, wg, T, H, E, k, idx, w, ws.rank, ws.chunk_hist, ws.done, counts, pad_off,
+                                   row_map, src_token, x_perm, (cudaStream_t)stream)) >= 0)
+    return rc;
   if ((rc = router_fused_launch(x, wg, T, H, E, k, ws.logits, idx, w, ws.rank, ws.chunk_hist,
                                 (cudaStream_t)stream)) > 0)
     return rc;

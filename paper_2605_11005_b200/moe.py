@@ -189,7 +189,8 @@ class MicroBatchBuffers:
             self.w = z(s.T, s.k, dt=F32)
             self.row_map = z(s.T, s.k, dt=I32)
             self.src = z(slab.cap, dt=I32)
-            self.route_ws = z(_lib.route_workspace_size(s.T, s.H, s.E, s.k), dt=torch.uint8)
+            # zeroed: the streaming router's completion counters live in its last 4 KB
+            self.route_ws = torch.zeros(_lib.route_workspace_size(s.T, s.H, s.E, s.k), dtype=torch.uint8, device=dev)
             self.wgrad_ws = z(_lib.router_wgrad_workspace_size(s.T, s.H, s.E) // 4, dt=F32)
             self.y = z(s.T, s.H)
             self.dy = z(s.T, s.H)
@@ -360,14 +361,35 @@ class MoELayer:
     launches_per_wgrad_pass = 2
 
     def launches_per_microbatch(self, deferred_wgrad: bool = False) -> int:
-        """dm kernel launches of one micro-batch: dispatch (fused router + scan + permute
-        = 3 when E <= 16 and W_g fits in smem, else logits + top-k + scan + permute = 4),
-        expert fwd 2, combine 1, combine bwd 1, dgrad 2, permute bwd 1, router wgrad 2,
-        plus 2 wgrad GEMMs unless deferred to the iteration's W pass."""
+        """dm kernel launches of one micro-batch: dispatch (one cooperative streaming
+        launch when E <= 16, H % 256 == 0, k <= 8 and W_g fits in smem; else the
+        32-token fused router + scan + permute = 3 when W_g fits in 160 KB; else
+        logits + top-k + scan + permute = 4), expert fwd 2, combine 1, combine bwd 1,
+        dgrad 2, permute bwd 1, router wgrad 1-2, plus 2 wgrad GEMMs unless deferred to
+        the iteration's W pass."""
         s = self.shape
-        fused = s.E <= 16 and s.E * s.H * 4 <= 160 * 1024
         router_wgrad = 2 if _router_wgrad_segments(s) > 1 else 1
-        return (3 if fused else 4) + 7 + router_wgrad + (0 if deferred_wgrad else 2)
+        return dispatch_launches(s) + 7 + router_wgrad + (0 if deferred_wgrad else 2)
+
+
+def dispatch_launches(s: MoEShape) -> int:
+    """Kernel launches of dm_route_and_dispatch (mirrors dispatch.cu's path choice)."""
+    ni = (s.H // 8 + 31) // 32
+    em = 8 if s.E <= 8 else 16
+    nunit = -(-s.T // _lib.DM_ROUTE_UNIT_TOKENS)
+    sms = _lib.load().dm_num_sms(torch.cuda.current_device())
+    grid = min(nunit, sms)
+    upc = -(-nunit // grid)
+    grid = -(-nunit // upc)
+    scratch = ((grid * s.E + upc * _lib.DM_ROUTE_UNIT_TOKENS * s.k) * 4 + 1023) // 1024 * 1024
+    import os
+
+    if (os.environ.get("DM_DISPATCH_LEGACY", "0") != "1" and s.E <= 16 and s.H % 256 == 0 and _lib.DM_ROUTE_UNIT_TOKENS * s.k <= 32
+            and 1024 + em * s.H * 4 + 4096 <= 227 * 1024 and upc <= 64 and scratch + 4 * s.H <= em * s.H * 4):
+        return 1   # one cooperative launch: route, grid barrier, scan, permute
+    if s.E <= 16 and em * ni * 64 * 16 <= 160 * 1024:
+        return 3
+    return 4
 
 
 def _router_wgrad_segments(s: MoEShape) -> int:

@@ -91,7 +91,7 @@ class BuffersF32:
         self.counts = z(s.E, dt=I32)
         self.src = z(slab.cap, dt=I32)
         self.dl_perm = z(slab.cap)
-        self.route_ws = z(_lib.route_workspace_size(s.T, s.H, s.E, s.k), dt=torch.uint8)
+        self.route_ws = torch.zeros(_lib.route_workspace_size(s.T, s.H, s.E, s.k), dtype=torch.uint8, device=dev)
         self.wgrad_ws = z(_lib.router_wgrad_workspace_size(s.T, s.H, s.E) // 4)
         self.pad_off = slab.pad_off[index]
         r = slab.rows(index)

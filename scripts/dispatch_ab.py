@@ -19,7 +19,7 @@ def main(T=4096, H=4096, E=8, k=2, reps=50):
     x = torch.randn(T, H, generator=g).to(torch.bfloat16).to(dev)
     wg = (torch.randn(E, H, generator=g) * 0.02).to(dev)
     cap = _lib.capacity_rows(T, E, k)
-    ws = torch.empty(_lib.route_workspace_size(T, H, E, k), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(_lib.route_workspace_size(T, H, E, k), dtype=torch.uint8, device=dev)
     i32 = lambda *s: torch.empty(*s, dtype=torch.int32, device=dev)  # noqa: E731
     idx, rm = i32(T, k), i32(T, k)
     w = torch.empty(T, k, device=dev)
