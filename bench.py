@@ -383,7 +383,7 @@ def run_ours(args, shape, exp):
         gbs = hb[name] / (t / 1e3) / 1e9
         hbm[name] = {"ms": round(t, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 3)}
     # A-side kernels in isolation: CUDA-graph replays of [L2 flush, stage] minus [L2 flush]
-    # (flush = 512 MB memset > 126 MB L2), i.e. cold-L2 kernel time at the live clocks,
+    # (flush = 160 MB memset > 126 MB L2), i.e. cold-L2 kernel time at the live clocks,
     # without the per-stage event overhead of the in-step numbers above
     iso = {}
     if world == 1 and not args.no_isolated:
@@ -448,7 +448,7 @@ def run_ours(args, shape, exp):
         }),
         "roofline_hbm": {"peak_GB/s": peaks["hbm_gbs"], **hbm,
                          "note": "ms/frac: in-step CUDA events around each stage; isolated_*: graph replay, "
-                                 "L2 flushed before every launch (flush time subtracted)"},
+                                 "median of 31 replays of graph [160 MB L2 flush, stage] minus median of [flush]"},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": e2e,
@@ -554,10 +554,14 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                 r.input(i).normal_()
             if r.has_output:
                 r.out_bufs[i].dy.normal_()
+    # 1A:1F per pipeline group (fixed-size exchange, no host sync): the whole iteration —
+    # kernels, NCCL P2P on the send/recv streams, W pass — replays as one CUDA graph per rank
+    graph = r.capture() if (r.capturable and not args.eager) else None
+    step = graph.replay if graph is not None else r.run_iteration
     sampler = ClockSampler(_clock_target(dev))   # every rank samples its own GPU
     sampler.start()
     for _ in range(args.warmup):
-        r.run_iteration()
+        step()
     torch.cuda.synchronize()
     dist.barrier()
     if sampler:
@@ -568,12 +572,12 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
     dist.barrier()
     t_s.record()
     for _ in range(args.steps):
-        r.run_iteration()
+        step()
     t_e.record()
     torch.cuda.synchronize()
     if sampler:
         sampler.mark("end")
-    launches = _lib.launch_count() - n0
+    launches = _lib.launch_count() - n0 + (r.graph_launches * args.steps if graph is not None else 0)
     ms = t_s.elapsed_time(t_e)
     tt = torch.tensor([ms, float(launches)], device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -665,7 +669,9 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                                + ("attention + " if args.attention else "") + "routing/combine, F: EP experts)",
                 "layer": "attention + residual MoE block (attention: own forward kernel, library backward)" if args.attention
                          else "MoE block",
-                "transport": "NCCL send/recv (torch.distributed P2P) over NVLink",
+                "transport": "NCCL send/recv (torch.distributed P2P) over NVLink, one communicator per direction",
+                "launch": ("one CUDA graph per rank per iteration (kernels + NCCL P2P + W pass)" if graph is not None
+                           else "eager (data-dependent message sizes: host reads the counts headers)"),
                 "weights": "random-init", "l2": "inputs+weights larger than L2",
                 "wgrad": "fp32, deferred per iteration on F ranks",
             },
@@ -709,42 +715,49 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                     "path": "AFPipeRank.run_iteration with pinned host x/dy in, y/dx out per micro-batch"},
         }
         print(json.dumps(line), flush=True)
+    del graph, step   # before the process group goes (a live graph holding NCCL work hangs teardown)
+    torch.cuda.synchronize()
     dist.barrier()
     dist.destroy_process_group()
     return 0
 
 
-def isolated_stage_ms(fns: dict, dev, reps: int = 10) -> dict:
-    """ms per launch of each stage with a cold L2: graph([flush, fn] x reps) - graph([flush] x reps)."""
+def isolated_stage_ms(fns: dict, dev, reps: int = 31) -> dict:
+    """ms per launch of each stage with a cold L2: the median over `reps` single replays of a
+    CUDA graph [160 MB write (> the 126 MB L2), stage] minus the median of [write] alone.
+    Medians of individually timed replays: one timing of a 10-flush graph (the earlier
+    method) left several us of flush-to-flush noise on 20-40 us stages."""
     import torch
 
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.empty(160 << 20, dtype=torch.uint8, device=dev)
     s = torch.cuda.Stream(dev)
 
-    def timed(g):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g.replay()
-        e0.record()
-        g.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1)
+    def median_replay(g):
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
 
     g0 = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g0, stream=s):
-        for _ in range(reps):
-            flush.zero_()
-    base = timed(g0)
+        flush.zero_()
+    g0.replay()
+    base = median_replay(g0)
     out = {}
     for name, fn in fns.items():
         fn()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            for _ in range(reps):
-                flush.zero_()
-                fn()
-        out[name] = max(timed(g) - base, 1e-6) / reps
+            flush.zero_()
+            fn()
+        g.replay()
+        out[name] = max(median_replay(g) - base, 1e-6)
     return out
 
 

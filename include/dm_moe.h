@@ -118,10 +118,14 @@ static inline void dm_route_workspace_layout(int T, int H, int E, int k, void* w
  * per-block partials are small, i.e. for few experts. */
 static inline int dm_router_wgrad_token_block(int E) { return E <= 16 ? 128 : 512; }
 
+/* Partial blocks [ntb][E][H] fp32, then the completion counters of dm_router_wgrad_sorted
+ * (one int per (1024-column chunk, expert)) and of dm_router_wgrad (one per 256-column
+ * chunk): zero when the workspace is first used (allocate it zeroed), left zero. */
 static inline size_t dm_router_wgrad_workspace_size(int T, int H, int E) {
   int tb = dm_router_wgrad_token_block(E);
   size_t ntb = (size_t)((T + tb - 1) / tb);
-  return ntb * (size_t)E * (size_t)H * 4;
+  size_t ctr = ((size_t)((H + 1023) / 1024) * (size_t)E + (size_t)((H + 255) / 256)) * 4;
+  return ntb * (size_t)E * (size_t)H * 4 + ((ctr + 255) & ~(size_t)255);
 }
 
 /* ---- library ---------------------------------------------------------- */
@@ -213,8 +217,9 @@ DM_API int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogi
                     int k, float* partial_ws, float* dwg, float beta, void* stream);
 
 /* dW_g[e,:] = sum over expert e's permuted rows r of dl_perm[r] * x[src_token[r], :]
- * (+ beta * dW_g), deterministic. partial_ws (dm_router_wgrad_workspace_size bytes, may be
- * NULL) lets few-expert layers split each expert's rows into segments reduced in order. */
+ * (+ beta * dW_g), deterministic. partial_ws (dm_router_wgrad_workspace_size bytes, zeroed
+ * before first use, may be NULL) lets few-expert layers split each expert's rows into
+ * segments; the last segment CTA of each (column chunk, expert) sums them in order. */
 DM_API int dm_router_wgrad_sorted(const void* x, const int32_t* src_token, const float* dl_perm,
                                   const int32_t* counts, const int32_t* pad_off, int T, int H, int E,
                                   float* partial_ws, float* dwg, float beta, void* stream);

@@ -151,6 +151,9 @@ def router_wgrad_token_block(E: int) -> int:
 
 
 def router_wgrad_workspace_size(T: int, H: int, E: int) -> int:
+    """Mirror of dm_router_wgrad_workspace_size: partial blocks, then the sorted kernel's
+    segment-completion counters (zero on first use)."""
     tb = router_wgrad_token_block(E)
     ntb = (T + tb - 1) // tb
-    return ntb * E * H * 4
+    ctr = ((H + 1023) // 1024 * E + (H + 255) // 256) * 4
+    return ntb * E * H * 4 + ((ctr + 255) & ~255)

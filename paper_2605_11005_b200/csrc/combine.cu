@@ -183,7 +183,7 @@ permute_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __r
 // per-token W_g reads of the generic kernel were L1-bound; holding all E rows in
 // registers cost 64-128 registers and capped occupancy at 25%). Warps stride over
 // groups of PBWD_TG tokens; the grid fills the resident CTA slots in one wave.
-constexpr int PBWD_TG = 4;
+constexpr int PBWD_TG = 8;
 constexpr int PBWD_MAX_E = 16;
 
 template <int KT>
@@ -264,46 +264,76 @@ permute_bwd_smem_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t
   }
 }
 
-// Router weight gradient, stage 1 (E <= 16): CTA per (256-column chunk, token
-// block); lane owns 8 columns and keeps acc[E][8] in registers, reading x with
-// 128-bit loads; the NW warps take interleaved tokens of the block and are then
-// reduced through smem in fixed warp order (deterministic). gw[e] = dlogit[t,j]
-// when idx[t,j] == e (each expert appears at most once per token).
-template <int EM>
-__global__ void __launch_bounds__(EM == 8 ? 256 : 128)
+// Router weight gradient (E <= 16): CTA per (256-column chunk, token block); lane owns 8
+// columns and keeps acc[E][8] in registers; every x row is read once (the expert-sorted
+// variant gathers it k times). The NW warps take interleaved tokens of the block with
+// RWR_DEPTH tokens of x / idx / dlogit in flight per warp (the previous loop kept one),
+// are reduced through smem in fixed warp order, and the CTA partial goes to
+// partial[tb][E][H]; the last token-block CTA of each column chunk to finish (ticket in
+// the workspace) sums the partials in token-block order (+ beta * dW_g) — deterministic,
+// one launch. gw[e] = dlogit[t,j] when idx[t,j] == e (each expert at most once per token).
+constexpr int RWR_DEPTH = 8;
+constexpr int RWR_MAX_TB = 512;   // token-block size bound (its idx / dlogit are staged in smem)
+
+template <int EM, int KT>
+__global__ void __launch_bounds__(EM == 8 ? 256 : 128, 2)
 router_wgrad_reg_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
-                        const float* __restrict__ dlogit, int T, int H, int E, int k, int tb_tokens,
-                        float* __restrict__ partial) {
+                        const float* __restrict__ dlogit, int T, int H, int E, int k_rt, int tb_tokens,
+                        float* __restrict__ partial, unsigned* __restrict__ tickets, float* __restrict__ dwg,
+                        float beta) {
   constexpr int NW = EM == 8 ? 8 : 4;
-  extern __shared__ float red[];   // [NW][EM][8][32]
+  extern __shared__ float red[];   // [NW][EM][8][32], then the block's idx / dlogit
+  __shared__ int s_last;
+  const int k = KT ? KT : k_rt;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = (blockIdx.x * 32 + lane) * 8;
   const bool live = col < H;
   const int tb = blockIdx.y;
   const int t_beg = tb * tb_tokens, t_end = min(T, t_beg + tb_tokens);
+  // the token block's expert ids and dlogits: one coalesced pass into smem
+  int* s_idx = reinterpret_cast<int*>(red + NW * EM * 8 * 32);
+  float* s_dl = reinterpret_cast<float*>(s_idx + RWR_MAX_TB * DM_MAX_TOPK);
+  for (int q = threadIdx.x; q < (t_end - t_beg) * k; q += blockDim.x) {
+    s_idx[q] = idx[(size_t)t_beg * k + q];
+    s_dl[q] = dlogit[(size_t)t_beg * k + q];
+  }
+  __syncthreads();
   float acc[EM][8];
 #pragma unroll
   for (int e = 0; e < EM; ++e)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[e][i] = 0.0f;
   if (live) {
-#pragma unroll 4
-    for (int t = t_beg + warp; t < t_end; t += NW) {
-      float xf[8];
-      unpack8(ld_nc_v4(x + (size_t)t * H + col), xf);
-      float gw[EM];
+    // ring of RWR_DEPTH prefetched x vectors (tokens warp, warp+NW, ...)
+    int4 xv[RWR_DEPTH];
 #pragma unroll
-      for (int e = 0; e < EM; ++e) gw[e] = 0.0f;
-      for (int j = 0; j < k; ++j) {
-        const int ej = idx[(size_t)t * k + j];
-        const float dl = dlogit[(size_t)t * k + j];
+    for (int d = 0; d < RWR_DEPTH; ++d) {
+      const int t = t_beg + warp + d * NW;
+      xv[d] = t < t_end ? ld_nc_v4(x + (size_t)t * H + col) : make_int4(0, 0, 0, 0);
+    }
+    for (int t0 = t_beg + warp; t0 < t_end; t0 += RWR_DEPTH * NW) {
 #pragma unroll
-        for (int e = 0; e < EM; ++e) gw[e] = (ej == e) ? dl : gw[e];
+      for (int d = 0; d < RWR_DEPTH; ++d) {
+        const int t = t0 + d * NW;
+        if (t >= t_end) break;
+        float xf[8];
+        unpack8(xv[d], xf);
+        const int tn = t + RWR_DEPTH * NW;
+        xv[d] = tn < t_end ? ld_nc_v4(x + (size_t)tn * H + col) : make_int4(0, 0, 0, 0);
+        // the token's k experts are warp-uniform: branch to the k accumulator rows instead
+        // of an E-wide select-and-FMA (4x fewer FMAs at E = 8, k = 2)
+        const int q0 = (t - t_beg) * k;
+        for (int j = 0; j < k; ++j) {
+          const int ej = s_idx[q0 + j];
+          const float dl = s_dl[q0 + j];
+#pragma unroll
+          for (int e = 0; e < EM; ++e)
+            if (ej == e) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[e][i] = __fmaf_rn(dl, xf[i], acc[e][i]);
+            }
+        }
       }
-#pragma unroll
-      for (int e = 0; e < EM; ++e)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[e][i] = __fmaf_rn(gw[e], xf[i], acc[e][i]);
     }
   }
 #pragma unroll
@@ -326,6 +356,33 @@ router_wgrad_reg_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __re
       dst[0] = make_float4(o[0], o[1], o[2], o[3]);
       dst[1] = make_float4(o[4], o[5], o[6], o[7]);
     }
+  }
+  if (!tickets) return;   // reduced by router_wgrad_reduce_kernel
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(tickets + blockIdx.x, 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;   // ready for the next launch
+  if (!live) return;
+  const int ntb = gridDim.y;
+  for (int e = warp; e < E; e += NW) {   // token-block order: router_wgrad_reduce_kernel's sums
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    for (int q = 0; q < ntb; ++q) {
+      const float4* p = reinterpret_cast<const float4*>(partial + ((size_t)q * E + e) * H + col);
+      const float4 pa = __ldcg(p), pb = __ldcg(p + 1);
+      a.x += pa.x; a.y += pa.y; a.z += pa.z; a.w += pa.w;
+      b.x += pb.x; b.y += pb.y; b.z += pb.z; b.w += pb.w;
+    }
+    float4* o = reinterpret_cast<float4*>(dwg + (size_t)e * H + col);
+    if (beta != 0.0f) {
+      const float4 oa = o[0], ob = o[1];
+      a.x += beta * oa.x; a.y += beta * oa.y; a.z += beta * oa.z; a.w += beta * oa.w;
+      b.x += beta * ob.x; b.y += beta * ob.y; b.z += beta * ob.z; b.w += beta * ob.w;
+    }
+    o[0] = a;
+    o[1] = b;
   }
 }
 
@@ -375,42 +432,81 @@ __global__ void router_wgrad_reduce_kernel(const float* __restrict__ partial, in
 // Router weight gradient over the expert-sorted rows: the rows of expert e in the
 // permuted layout are exactly the (t, j) slots with idx == e in ascending t, so
 // dW_g[e, :] = sum over the block of dl_perm[r] * x[src_token[r], :] (dl_perm =
-// dlogit scattered to permuted positions by combine_bwd). CTA per (1024-column
-// chunk, expert, row segment); x rows are gathered with 128-bit loads (x is
-// L2-resident after the forward). With nseg > 1 (few experts, long blocks) each
-// segment writes a partial [seg][E][H] that router_wgrad_reduce_kernel sums in
-// segment order, so the result is deterministic either way. 8 accumulators per
-// thread keep occupancy high enough to cover the gather latency.
+// dlogit scattered to permuted positions by combine_bwd) — R*H FMAs instead of the
+// T*E*H of a dense dlogit^T x. CTA per (1024-column chunk, expert, row segment): the
+// segment's row indices and weights are staged in smem, then every thread keeps
+// RWS_DEPTH x-row gathers (16 B each) in flight — the previous version walked
+// src_token -> x dependent loads 8 rows at a time and was latency bound (0.19 of HBM).
+// With nseg > 1 each segment writes a partial [seg][E][H]; the last segment CTA of its
+// (chunk, expert) to finish (ticket counter in the workspace) sums the partials in
+// segment order (+ beta * dW_g): deterministic, and no second launch.
+constexpr int RWS_ROWS = 128;    // rows staged per batch
+constexpr int RWS_DEPTH = 16;    // x gathers in flight per thread
+
 __global__ void __launch_bounds__(128)
 router_wgrad_sorted_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ src_token,
                            const float* __restrict__ dl_perm, const int32_t* __restrict__ counts,
                            const int32_t* __restrict__ pad_off, int H, int E, int nseg, float* __restrict__ partial,
-                           float* __restrict__ dwg, float beta) {
+                           unsigned* __restrict__ tickets, float* __restrict__ dwg, float beta) {
+  __shared__ int s_t[RWS_ROWS];
+  __shared__ float s_d[RWS_ROWS];
+  __shared__ int s_last;
   const int e = blockIdx.y, seg = blockIdx.z;
   const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (col >= H) return;
+  const bool live = col < H;
   const int n = counts[e];
   const int r0 = pad_off[e] + (int)((long long)n * seg / nseg);
   const int r1 = pad_off[e] + (int)((long long)n * (seg + 1) / nseg);
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-#pragma unroll 8
-  for (int r = r0; r < r1; ++r) {
-    const int t = src_token[r];
-    const float d = dl_perm[r];
-    float f[8];
-    unpack8(ld_nc_v4(x + (size_t)t * H + col), f);
+  for (int rb = r0; rb < r1; rb += RWS_ROWS) {
+    const int nr = min(RWS_ROWS, r1 - rb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) { s_t[i] = src_token[rb + i]; s_d[i] = dl_perm[rb + i]; }
+    __syncthreads();
+    if (!live) continue;
+    for (int i = 0; i < nr; i += RWS_DEPTH) {
+      int4 v[RWS_DEPTH];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(d, f[i], acc[i]);
+      for (int q = 0; q < RWS_DEPTH; ++q)
+        v[q] = i + q < nr ? ld_nc_v4(x + (size_t)s_t[i + q] * H + col) : make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int q = 0; q < RWS_DEPTH; ++q) {
+        if (i + q >= nr) break;
+        const float d = s_d[i + q];
+        float f[8];
+        unpack8(v[q], f);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = __fmaf_rn(d, f[c], acc[c]);
+      }
+    }
   }
   float4 a = make_float4(acc[0], acc[1], acc[2], acc[3]), b = make_float4(acc[4], acc[5], acc[6], acc[7]);
   if (nseg > 1) {
-    float4* o = reinterpret_cast<float4*>(partial + ((size_t)seg * E + e) * H + col);
-    o[0] = a;
-    o[1] = b;
-    return;
+    if (live) {
+      float4* o = reinterpret_cast<float4*>(partial + ((size_t)seg * E + e) * H + col);
+      o[0] = a;
+      o[1] = b;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(tickets + (size_t)blockIdx.x * E + e, 1u) == (unsigned)nseg - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) tickets[(size_t)blockIdx.x * E + e] = 0u;   // ready for the next launch
+    if (!live) return;
+    a = make_float4(0.f, 0.f, 0.f, 0.f);
+    b = a;
+    for (int s2 = 0; s2 < nseg; ++s2) {   // segment order: same sums as router_wgrad_reduce_kernel
+      const float4* p = reinterpret_cast<const float4*>(partial + ((size_t)s2 * E + e) * H + col);
+      const float4 pa = __ldcg(p), pb = __ldcg(p + 1);
+      a.x += pa.x; a.y += pa.y; a.z += pa.z; a.w += pa.w;
+      b.x += pb.x; b.y += pb.y; b.z += pb.z; b.w += pb.w;
+    }
   }
+  if (!live) return;
   float4* o = reinterpret_cast<float4*>(dwg + (size_t)e * H + col);
   if (beta != 0.0f) {
     const float4 oa = o[0], ob = o[1];
@@ -515,12 +611,15 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
   int ntb = (T + tbt - 1) / tbt;   // the workspace holds this many partial blocks
   cudaStream_t st = (cudaStream_t)stream;
   if (E <= 16) {
-    if (int rc = ensure_smem_attr((const void*)router_wgrad_reg_kernel<8>, 8 * 8 * 8 * 32 * 4,
-                                  "cudaFuncSetAttribute(router_wgrad_reg)")) return rc;
-    if (int rc = ensure_smem_attr((const void*)router_wgrad_reg_kernel<16>, 4 * 16 * 8 * 32 * 4,
-                                  "cudaFuncSetAttribute(router_wgrad_reg)")) return rc;
-    const int occ8 = max_active_blocks((const void*)router_wgrad_reg_kernel<8>, 256, 8 * 8 * 8 * 32 * 4);
-    const int occ16 = max_active_blocks((const void*)router_wgrad_reg_kernel<16>, 128, 4 * 16 * 8 * 32 * 4);
+    // segment tickets follow the partial blocks in the workspace (after the sorted kernel's)
+    unsigned* tickets = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(partial_ws) + (size_t)ntb * E * H * 4) +
+                        (size_t)((H + 1023) / 1024) * E;
+    const size_t stage = (size_t)RWR_MAX_TB * DM_MAX_TOPK * 8;   // idx + dlogit of a token block
+    const size_t sm8 = 8 * 8 * 8 * 32 * 4 + stage, sm16 = 4 * 16 * 8 * 32 * 4 + stage;
+    const void* k8 = (const void*)router_wgrad_reg_kernel<8, 2>;
+    const void* k16 = (const void*)router_wgrad_reg_kernel<16, 2>;
+    const int occ8 = max_active_blocks(k8, 256, sm8);
+    const int occ16 = max_active_blocks(k16, 128, sm16);
     // One wave: as many token blocks as the resident CTA slots allow per column chunk
     // (never more than the workspace's ntb), each a contiguous run of tbt tokens.
     const int gx = (H / 8 + 31) / 32;
@@ -530,15 +629,30 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
     if (want < ntb) {
       tbt = (T + want - 1) / want;
       tbt = (tbt + 7) & ~7;
+      if (tbt > RWR_MAX_TB) tbt = RWR_MAX_TB;   // long sequences: more than one wave of blocks
       ntb = (T + tbt - 1) / tbt;
     }
+    if (tbt > RWR_MAX_TB) return set_error(DM_ERR_SHAPE, "router_wgrad token block %d > %d", tbt, RWR_MAX_TB);
     dim3 grid(gx, ntb);
-    if (E <= 8)
-      router_wgrad_reg_kernel<8><<<grid, 256, 8 * 8 * 8 * 32 * 4, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
-                                                       T, H, E, k, tbt, partial_ws);
-    else
-      router_wgrad_reg_kernel<16><<<grid, 128, 4 * 16 * 8 * 32 * 4, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), idx, dlogit,
-                                                        T, H, E, k, tbt, partial_ws);
+    const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+#define DM_RWR(EMV, KTV, NT, SM)                                                                              \
+    do {                                                                                                    \
+      if (int rc = ensure_smem_attr((const void*)router_wgrad_reg_kernel<EMV, KTV>, (int)SM,               \
+                                    "cudaFuncSetAttribute(router_wgrad_reg)")) return rc;                  \
+      router_wgrad_reg_kernel<EMV, KTV><<<grid, NT, SM, st>>>(xb, idx, dlogit, T, H, E, k, tbt, partial_ws, \
+                                                              tickets, dwg, beta);                          \
+    } while (0)
+#define DM_RWR_K(EMV, NT, SM)                                                                \
+    switch (k) { case 1: DM_RWR(EMV, 1, NT, SM); break; case 2: DM_RWR(EMV, 2, NT, SM); break;  \
+                 case 4: DM_RWR(EMV, 4, NT, SM); break; case 8: DM_RWR(EMV, 8, NT, SM); break;  \
+                 default: DM_RWR(EMV, 0, NT, SM); break; }
+    if (E <= 8) { DM_RWR_K(8, 256, sm8); } else { DM_RWR_K(16, 128, sm16); }
+#undef DM_RWR_K
+#undef DM_RWR
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_reg launch");
+    note_launch();
+    return DM_OK;
   } else {
     int cw = 128;
     while (cw > 32 && (size_t)E * cw * sizeof(float) > 96 * 1024) cw >>= 1;
@@ -580,20 +694,15 @@ int dm_router_wgrad_sorted(const void* x, const int32_t* src_token, const float*
     if (nseg < 1) nseg = 1;
   }
   dim3 grid(gx, E, nseg);
+  // segment tickets follow the partial blocks in the workspace
+  const int tbt = dm_router_wgrad_token_block(E);
+  unsigned* tickets = partial_ws ? reinterpret_cast<unsigned*>(
+      reinterpret_cast<char*>(partial_ws) + (size_t)((T + tbt - 1) / tbt) * E * H * 4) : nullptr;
   router_wgrad_sorted_kernel<<<grid, 128, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), src_token, dl_perm,
-                                                   counts, pad_off, H, E, nseg, partial_ws, dwg, beta);
+                                                   counts, pad_off, H, E, nseg, partial_ws, tickets, dwg, beta);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_sorted launch");
   note_launch();
-  if (nseg > 1) {
-    const size_t EH = (size_t)E * H;
-    int rblocks = (int)((EH / 4 + 63) / 64);
-    if (rblocks > num_sms_current() * 8) rblocks = num_sms_current() * 8;
-    router_wgrad_reduce_kernel<<<rblocks, 64, 0, st>>>(partial_ws, nseg, EH, dwg, beta);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return set_cuda_error(e, "router_wgrad_sorted reduce launch");
-    note_launch();
-  }
   return DM_OK;
 }
 

@@ -191,7 +191,7 @@ class MicroBatchBuffers:
             self.src = z(slab.cap, dt=I32)
             # zeroed: the streaming router's completion counters live in its last 4 KB
             self.route_ws = torch.zeros(_lib.route_workspace_size(s.T, s.H, s.E, s.k), dtype=torch.uint8, device=dev)
-            self.wgrad_ws = z(_lib.router_wgrad_workspace_size(s.T, s.H, s.E) // 4, dt=F32)
+            self.wgrad_ws = torch.zeros(_lib.router_wgrad_workspace_size(s.T, s.H, s.E) // 4, dtype=F32, device=dev)
             self.y = z(s.T, s.H)
             self.dy = z(s.T, s.H)
             self.dw = z(s.T, s.k, dt=F32)
@@ -262,12 +262,16 @@ def a_permute_bwd(buf: MicroBatchBuffers, router: RouterParams, stream=None) -> 
 
 
 def a_router_wgrad(buf: MicroBatchBuffers, router: RouterParams, accumulate: bool, stream=None) -> None:
-    """dW_g (+)= dlogit^T x over the expert-sorted rows (dlogit scattered to them by
-    combine_bwd); few-expert layers split each expert's rows into segments whose
-    partials are reduced in a fixed order (deterministic)."""
+    """dW_g (+)= dlogit^T x, deterministic. Few experts (E <= 16): token blocks, every x
+    row read once, acc[E][8] per lane, partials reduced in token-block order by the last
+    CTA of each column chunk. Many experts: over the expert-sorted rows (dlogit scattered
+    to them by combine_bwd), R*H FMAs instead of T*E*H."""
     beta = 1.0 if accumulate else 0.0
-    K.router_wgrad_sorted(buf.x, buf.src, buf.dl_perm, buf.counts, buf.pad_off, router.dwg, beta, stream,
-                          partial_ws=buf.wgrad_ws)
+    if buf.shape.E <= 16:
+        K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws, router.dwg, beta, stream)
+    else:
+        K.router_wgrad_sorted(buf.x, buf.src, buf.dl_perm, buf.counts, buf.pad_off, router.dwg, beta, stream,
+                              partial_ws=buf.wgrad_ws)
 
 
 class MoELayer:
@@ -365,11 +369,10 @@ class MoELayer:
         launch when E <= 16, H % 256 == 0, k <= 8 and W_g fits in smem; else the
         32-token fused router + scan + permute = 3 when W_g fits in 160 KB; else
         logits + top-k + scan + permute = 4), expert fwd 2, combine 1, combine bwd 1,
-        dgrad 2, permute bwd 1, router wgrad 1-2, plus 2 wgrad GEMMs unless deferred to
-        the iteration's W pass."""
+        dgrad 2, permute bwd 1, router wgrad 1 (segments reduced in-kernel), plus 2 wgrad
+        GEMMs unless deferred to the iteration's W pass."""
         s = self.shape
-        router_wgrad = 2 if _router_wgrad_segments(s) > 1 else 1
-        return dispatch_launches(s) + 7 + router_wgrad + (0 if deferred_wgrad else 2)
+        return dispatch_launches(s) + 7 + 1 + (0 if deferred_wgrad else 2)
 
 
 def dispatch_launches(s: MoEShape) -> int:

@@ -92,7 +92,7 @@ class BuffersF32:
         self.src = z(slab.cap, dt=I32)
         self.dl_perm = z(slab.cap)
         self.route_ws = torch.zeros(_lib.route_workspace_size(s.T, s.H, s.E, s.k), dtype=torch.uint8, device=dev)
-        self.wgrad_ws = z(_lib.router_wgrad_workspace_size(s.T, s.H, s.E) // 4)
+        self.wgrad_ws = torch.zeros(_lib.router_wgrad_workspace_size(s.T, s.H, s.E) // 4, dtype=F32, device=dev)
         self.pad_off = slab.pad_off[index]
         r = slab.rows(index)
         for name in ("x3", "h13", "act3", "y_perm", "dy3", "d_act", "dh13_3", "dx_perm"):

@@ -731,6 +731,40 @@ class AFPipeRank:
             fm.works["N2M_b_ready"] = self.st.event("compute")
 
     # ------------------------------------------------------------ iteration
+    @property
+    def capturable(self) -> bool:
+        """The iteration has no host synchronisation (1 A + 1 F rank per pipeline group:
+        fixed-size messages, device-side offsets) and no host I/O or tracing."""
+        return self.st.cuda and self.fixed and self.host_io is None and not self.record_events
+
+    def capture(self, accumulate: bool = False):
+        """Record one iteration — kernels, the NCCL sends/receives on their streams, the W
+        pass and the dW_g all-reduce — as a CUDA graph (PAPER.md:266's non-blocking streams
+        with the host out of the loop); `graph.replay()` on the caller's stream runs it.
+        Every rank of the job captures once, in the same order, after the process groups
+        exist (one eager warm-up iteration initialises NCCL and the kernels). Drop the
+        graph before destroying the process group: a live graph holding NCCL work makes
+        the teardown hang."""
+        if not self.capturable:
+            raise RuntimeError("AF-Pipe iteration capture needs the fixed-size (1A:1F per group) exchange, "
+                               "no host I/O and no event tracing")
+        self.run_iteration(accumulate)
+        torch.cuda.synchronize(self.device)
+        outer = self.st.compute
+        side = torch.cuda.Stream(self.device)   # the legacy default stream cannot be captured
+        side.wait_stream(outer)
+        g = torch.cuda.CUDAGraph()
+        self.st.compute = side
+        c0 = _lib.launch_count() if self.st.cuda else 0
+        try:
+            with torch.cuda.graph(g, stream=side):
+                self.run_iteration(accumulate)
+        finally:
+            self.st.compute = outer
+        self.graph_launches = _lib.launch_count() - c0   # dm kernels per replay
+        outer.wait_stream(side)
+        return g
+
     def run_iteration(self, accumulate: bool = False) -> None:
         # comm/copy streams must not touch this iteration's buffers before the
         # compute stream is done with the previous iteration's uses of them

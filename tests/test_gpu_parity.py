@@ -278,13 +278,15 @@ def test_iteration_matches_oracle_sum_over_microbatches(cuda):
     assert O.normwise_rel_err(f32(layer.experts.dw2), dw2) < TOL_BF16
 
 
-def test_router_wgrad_sorted_matches_token_blocked(cuda):
-    """Large-E router gradient over expert-sorted rows == the token-blocked path,
-    is bit-deterministic across runs, and accumulates with beta=1."""
+@pytest.mark.parametrize("E,k", [(64, 6), (8, 2)])
+def test_router_wgrad_sorted_matches_token_blocked(cuda, E, k):
+    """The two router-gradient paths agree (the layer uses the expert-sorted one for E > 16,
+    the token-blocked one with its in-kernel ticket reduction for E <= 16); the layer's is
+    bit-deterministic across runs and accumulates with beta=1."""
     from paper_2605_11005_b200 import kernels as K
     from paper_2605_11005_b200.moe import MoELayer, MoEShape, a_router_wgrad
 
-    shape = MoEShape(T=1000, H=1024, E=64, k=6, De=256)
+    shape = MoEShape(T=1000, H=1024, E=E, k=k, De=256)
     layer = MoELayer.random(shape, device=cuda, seed=9)
     buf = layer.buffers[0]
     buf.x.normal_()
@@ -295,9 +297,13 @@ def test_router_wgrad_sorted_matches_token_blocked(cuda):
     # dl_perm is dlogit scattered to the permuted rows
     rm = buf.row_map.long().flatten()
     assert torch.equal(buf.dl_perm[rm], buf.dlogit.flatten())
-    sorted_dwg = layer.router.dwg.clone()
+    sorted_dwg = layer.router.dwg.clone()   # the layer's own path
     ref = torch.empty_like(sorted_dwg)
-    K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws, ref, 0.0)
+    if E > 16:
+        K.router_wgrad(buf.x, buf.idx, buf.dlogit, buf.wgrad_ws, ref, 0.0)
+    else:
+        K.router_wgrad_sorted(buf.x, buf.src, buf.dl_perm, buf.counts, buf.pad_off, ref, 0.0,
+                              partial_ws=buf.wgrad_ws)
     torch.cuda.synchronize()
     assert O.normwise_rel_err(f32(sorted_dwg), f32(ref)) < 1e-5
     a_router_wgrad(buf, layer.router, False)
