@@ -15,6 +15,8 @@
 //             m-tiles of one expert reuse each weight n-tile from L2.
 //   ragged-K  (wgrad):      C_e[M, N] = A_tok[rows_e, M]^T * B_tok[rows_e, N],
 //             K loop over the expert's (zero-padded) token rows.
+#include <stdlib.h>
+
 #include "dm_common.cuh"
 #include "dm_internal.h"
 
@@ -874,10 +876,26 @@ static bool use_2sm() {
   return v;
 }
 
+// TMA L2 promotion. K-major operand boxes and epilogue boxes keep 256 B (the next k-block
+// / column box follows); MN-major operand boxes (64 x 64, 128-byte rows) use none: at the
+// Mixtral w13 dgrad (MN-major W13, K = 28672) 256 B promotion read 4.38 GB of DRAM per
+// launch vs 3.76 GB without (algorithmic 2.35 GB), and ran 2.3% slower
+// (scripts/gemm_traffic_probe.sh). DM_GEMM_PROMO = 0 / 64 / 128 / 256 forces one setting.
+static CUtensorMapL2promotion l2_promotion(bool mn_major_operand) {
+  static const int forced = [] {
+    const char* e = getenv("DM_GEMM_PROMO");
+    return e ? atoi(e) : -1;
+  }();
+  const int v = forced >= 0 ? forced : (mn_major_operand ? 0 : 256);
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+       : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // groups > 0: a rank-3 map [groups][outer][inner] of back-to-back [outer, inner] blocks
 // (box depth 1), so every group's edges clip independently.
 static int make_tmap_2d(CUtensorMap* tm, const void* base, bool fp32, uint64_t inner, uint64_t outer,
-                       uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer, uint64_t groups = 0) {
+                       uint64_t row_stride_elems, uint32_t box_inner, uint32_t box_outer, uint64_t groups = 0,
+                       bool mn_major_operand = false) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   if (!enc) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled entry point unavailable");
   const uint64_t esz = fp32 ? 4 : 2;
@@ -889,7 +907,7 @@ static int make_tmap_2d(CUtensorMap* tm, const void* base, bool fp32, uint64_t i
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(tm, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, groups ? 3 : 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(mn_major_operand),
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return DM_OK;
@@ -923,7 +941,7 @@ struct EpiTensors {
 };
 
 static int make_operand_map(CUtensorMap* tm, const GemmOperand& o, bool two_sm) {
-  if (o.mn_major) return make_tmap_bf16_2d(tm, o.base, o.inner, o.outer, o.ld, 64, 64);
+  if (o.mn_major) return make_tmap_2d(tm, o.base, false, o.inner, o.outer, o.ld, 64, 64, 0, true);
   const uint32_t rows = (o.is_b && !two_sm) ? 256 : 128;
   return make_tmap_bf16_2d(tm, o.base, o.inner, o.outer, o.ld, 64, rows);
 }
