@@ -82,6 +82,7 @@ SIGNATURES: dict[str, tuple] = {
     "dm_split3": (_i, [_f32p, _i, _i, _i, _i, _vp, _vp]),
     "dm_grouped_wgrad_strided": (_i, [_vp, _i, _i, _vp, _i, _i, _i32p, _i, _i, _i, _i, _f32p, _f, _vp]),
     "dm_attention_fwd": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _f32p, _vp]),
+    "dm_attention_bwd": (_i, [_vp, _vp, _vp, _f32p, _i, _i, _i, _i, _i, _f32p, _vp, _vp]),
 }
 
 _lib = None

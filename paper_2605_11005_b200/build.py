@@ -24,8 +24,9 @@ INCLUDE = ROOT / "include"
 BUILD = PKG / "_build"
 LIB = PKG / "libdm_moe.so"
 
-SOURCES = ["abi.cu", "dispatch.cu", "combine.cu", "grouped_gemm_sm100.cu", "fp32_mode.cu", "attention_fwd.cu"]
-HEADERS = ["dm_common.cuh", "dm_internal.h"]
+SOURCES = ["abi.cu", "dispatch.cu", "combine.cu", "grouped_gemm_sm100.cu", "fp32_mode.cu", "attention_fwd.cu",
+           "attention_bwd.cu"]
+HEADERS = ["dm_common.cuh", "dm_internal.h", "attention_common.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

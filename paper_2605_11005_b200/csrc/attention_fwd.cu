@@ -19,36 +19,15 @@
 // Tiles A and B are two query heads of one KV group on the same rows (GQA with an even
 // group size: each K/V tile serves both) or two adjacent row tiles of one head. Causal:
 // each tile stops at its diagonal KV tile (masked key > query). Items run heaviest first.
-#include "dm_common.cuh"
-#include "dm_internal.h"
+#include "attention_common.cuh"
 
 namespace dm {
 
-constexpr int AT_D = 128;                               // head dim
-constexpr int AT_BM = 128;                              // query rows per CTA (= TMEM lanes)
-constexpr int AT_BN = 128;                              // keys per KV tile
 constexpr int AT_STAGES = 2;
-constexpr uint32_t AT_TILE = AT_BM * AT_D * 2;          // 32 KiB: one Q, K, V or P tile
-constexpr uint32_t AT_ATOM = AT_BM * 128;               // 16 KiB: 128 rows x 64 bf16 (SWIZZLE_128B)
 constexpr int AT_THREADS = 384;
 // Q_A, Q_B | P_A, P_B | K ring (AT_STAGES) | V
 constexpr size_t AT_SMEM = 1024 + (size_t)AT_TILE * (5 + AT_STAGES) + 256;
 
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-      :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
-         "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
-         "r"(r[15])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 // Packed fp32 pairs (FADD2) and three-input max (FMNMX3): the softmax warps are issue-bound
 // (an FMA-pipe exp2 polynomial for part of the row measured slower), so the row reductions
 // and the exp2 argument FMAs run two elements per instruction.
@@ -70,15 +49,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 // domain): P entries stay <= 256 (exact in fp32, representable in bf16) and the O rescale
 // (tcgen05.ld/st of the whole O row) is skipped on most tiles; m, l and O stay consistent.
 constexpr float AT_RESCALE_LOG2 = 8.0f;
-
-// K-major [128 rows x 128] bf16 tile stored as two 64-column SWIZZLE_128B atoms: k16 step kk.
-__device__ __forceinline__ uint64_t at_kmajor(uint32_t base, int kk) {
-  return make_sdesc_sw128(base + (kk >> 2) * AT_ATOM + (kk & 3) * 32, 16, 1024);
-}
-// V as the MN-major B operand of P·V: [128 keys (K) x 128 d (N)], two 64-d atoms.
-__device__ __forceinline__ uint64_t at_mnmajor(uint32_t base, int kk) {
-  return make_sdesc_sw128(base + kk * 2048, AT_ATOM, 1024);
-}
 
 // One work item = two 128-query tiles (A, B): two query heads of one KV group on the same
 // rows (GQA with an even group: each K/V tile serves both) or two adjacent row tiles of one

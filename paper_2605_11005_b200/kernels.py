@@ -297,3 +297,18 @@ def attention_fwd(qkv, seq_len, nh, nkv, out, lse, stream=None):
     _check(out, BF16, (T, nh * 128), "out")
     _check(lse, F32, (T // seq_len, nh, seq_len), "lse")
     _lib.call("dm_attention_fwd", _ptr(qkv), T, seq_len, nh, nkv, 128, _ptr(out), _ptr(lse), _stream(stream))
+
+
+def attention_bwd(qkv, out, dout, lse, seq_len, nh, nkv, dqkv, dl_ws=None, stream=None):
+    """Backward of attention_fwd: dqkv [T, (nh + 2 nkv) * 128] bf16 (dQ | dK | dV) from the
+    packed projection, the forward's out / lse and dout [T, nh * 128]."""
+    T = qkv.shape[0]
+    _check(qkv, BF16, (T, (nh + 2 * nkv) * 128), "qkv")
+    _check(out, BF16, (T, nh * 128), "out")
+    _check(dout, BF16, (T, nh * 128), "dout")
+    _check(lse, F32, (T // seq_len, nh, seq_len), "lse")
+    _check(dqkv, BF16, (T, (nh + 2 * nkv) * 128), "dqkv")
+    if dl_ws is None:
+        dl_ws = torch.empty(T // seq_len, nh, seq_len, dtype=F32, device=qkv.device)
+    _lib.call("dm_attention_bwd", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), T, seq_len, nh, nkv, 128,
+              _ptr(dl_ws), _ptr(dqkv), _stream(stream))
