@@ -501,8 +501,8 @@ def _uncovered(a, b):
 def _attention_impl_label(path) -> str:
     """Which attention path actually ran (AttentionBlock.last_path), for the bench line."""
     if path == "own":
-        return ("own sm_100a flash-attention forward (dm_attention_fwd) + cuDNN SDPA backward on its O/LSE; "
-                "cuBLAS projections, autograd")
+        return ("own sm_100a kernels only: flash-attention fwd/bwd (dm_attention_fwd/_bwd), projections and "
+                "their gradients on the grouped tcgen05 GEMM (dm_grouped_w2_fwd / w13_dgrad / wgrad)")
     return "library: cuBLAS projections + torch SDPA (cuDNN/flash), autograd"
 
 
@@ -667,7 +667,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                 "parallelism": f"AF-Pipe {topo.n_attn}A:{topo.n_ffn}F" + (f" x {topo.depth} pipeline groups"
                                                                            if topo.depth > 1 else "") + " (A: DP "
                                + ("attention + " if args.attention else "") + "routing/combine, F: EP experts)",
-                "layer": "attention + residual MoE block (attention: own forward kernel, library backward)" if args.attention
+                "layer": "attention + residual MoE block (attention: own kernels)" if args.attention
                          else "MoE block",
                 "transport": "NCCL send/recv (torch.distributed P2P) over NVLink, one communicator per direction",
                 "launch": ("one CUDA graph per rank per iteration (kernels + NCCL P2P + W pass)" if graph is not None
@@ -884,7 +884,7 @@ def main(argv=None):
     ap.add_argument("--eager", action="store_true", help="N=1: launch kernels eagerly instead of CUDA graphs")
     ap.add_argument("--no-isolated", action="store_true", help="skip the isolated A-side kernel timing")
     ap.add_argument("--attention", action="store_true",
-                    help="add the A-side causal attention block to every layer (own forward kernel, cuDNN backward; sweeps)")
+                    help="add the A-side causal attention block to every layer (own kernels where the shape allows; sweeps)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -4,22 +4,23 @@ The reference models attention only as a cost, C_a = bÂ·(sÂ·HÂ²Â·(2+2/g) + 4Â·sÂ
 (`pkg/src/afpipe/costs.py:84-87`), placed on the attention (A) GPU groups of the
 AF-Pipe schedule. This module gives the A ranks that work for real so the
 long-context (configs[3]) and A:F allocation (configs[4]) sweeps measure the
-overlap the paper is about. It is NOT part of the MoE hot path this repo
-rebuilds: it is the stopgap SURVEY.md Â§8f names â€” cuBLAS projections and torch's
-scaled_dot_product_attention restricted to the cuDNN / flash backends (cuDNN's
-Blackwell attention kernels, measured 1.3 PFLOP/s fwd+bwd at s = 16K on B200,
-scripts/probe_sdpa.py) â€” and is labelled as library code wherever it is timed.
+overlap the paper is about. It is not part of the MoE hot path itself.
 
 Block: h = x + W_o Â· attn(x W_q, x W_k, x W_v), causal, GQA with g query heads per
 KV head (ModelConfig.gqa_group), head_dim 128, no normalisation / RoPE (shape and
-FLOPs are what the schedule needs). Gradients come from torch autograd on the
-per-micro-batch graph saved by `forward`; parameter gradients accumulate in fp32
+FLOPs are what the schedule needs). Parameter gradients accumulate in fp32
 `.grad`-style buffers (`dw_qkv`, `dw_o`).
 
-On CUDA with seq_len a multiple of 128 (256 for an odd GQA group) the attention forward is this repo's own sm_100a
-kernel (`dm_attention_fwd`: tcgen05/TMEM/TMA flash attention, csrc/attention_fwd.cu); its
-(O, LSE) feed cuDNN's SDPA backward (the LSE matches cuDNN's to 5e-5), so only the
-backward and the projections remain library code.
+Own path (CUDA, seq_len a multiple of 128 â€” 256 for an odd GQA group â€”, H % 256 == 0 and an
+even head count, `own_path_supported`): every FLOP runs in this repo's sm_100a kernels, no
+autograd graph â€”
+  forward   qkv = xÂ·W_qkváµ€ and y = oÂ·W_oáµ€ on the grouped tcgen05 GEMM (`dm_grouped_w2_fwd`, one
+            group), o / LSE on `dm_attention_fwd`, h = x + y;
+  backward  dO = dhÂ·W_o and dx_attn = dqkvÂ·W_qkv on `dm_grouped_w13_dgrad`, dQ/dK/dV on
+            `dm_attention_bwd` (fed the forward's O / LSE), dW_o += dháµ€Â·o and
+            dW_qkv += dqkváµ€Â·x on the ragged-K wgrad (`dm_grouped_wgrad`, fp32 TMA reduce-add).
+Other shapes (and CPU, for the gloo tests) run the library block: torch projections and
+scaled_dot_product_attention (cuDNN / flash) under autograd, labelled "library".
 """
 
 from __future__ import annotations
@@ -46,48 +47,20 @@ def attention_flops(hidden: int, gqa_group: int, seq_len: int, micro_batch: int,
     return proj + attn, 2 * proj + int(2.5 * attn)
 
 
-class _OwnCausalAttention(torch.autograd.Function):
-    """o [T, nhÂ·D] = causal GQA attention of the packed projection qkv [T, (nh + 2 nkv)Â·D]:
-    forward on dm_attention_fwd, backward on cuDNN's SDPA backward with our (O, LSE)."""
-
-    @staticmethod
-    def forward(ctx, qkv, seq_len, nh, nkv):
-        from . import kernels as K
-
-        T = qkv.shape[0]
-        out = torch.empty(T, nh * HEAD_DIM, dtype=BF16, device=qkv.device)
-        lse = torch.empty(T // seq_len, nh, seq_len, dtype=F32, device=qkv.device)
-        K.attention_fwd(qkv, seq_len, nh, nkv, out, lse)
-        ctx.save_for_backward(qkv, out, lse)
-        ctx.shape = (seq_len, nh, nkv)
-        return out
-
-    @staticmethod
-    def backward(ctx, grad_out):
-        qkv, out, lse = ctx.saved_tensors
-        s, nh, nkv = ctx.shape
-        T = qkv.shape[0]
-        b = T // s
-        x = qkv.view(b, s, nh + 2 * nkv, HEAD_DIM).transpose(1, 2)        # [b, heads, s, D] views
-        q, k, v = x[:, :nh], x[:, nh:nh + nkv], x[:, nh + nkv:]            # GQA handled by cuDNN
-        o = out.view(b, s, nh, HEAD_DIM).transpose(1, 2)
-        do = grad_out.contiguous().view(b, s, nh, HEAD_DIM).transpose(1, 2)
-        zero = torch.zeros((), dtype=torch.int64, device=qkv.device)   # philox seed / offset (no dropout)
-        dq, dk, dv = torch.ops.aten._scaled_dot_product_cudnn_attention_backward(
-            do, q, k, v, o, lse.unsqueeze(-1), zero, zero, None, None, None, s, s, 0.0, True)
-        dqkv = torch.empty_like(qkv)
-        d = dqkv.view(b, s, nh + 2 * nkv, HEAD_DIM)
-        d[:, :, :nh].copy_(dq.transpose(1, 2))
-        d[:, :, nh:nh + nkv].copy_(dk.transpose(1, 2))
-        d[:, :, nh + nkv:].copy_(dv.transpose(1, 2))
-        return dqkv, None, None, None
-
-
 def own_attention_supported(x: torch.Tensor, seq_len: int, head_dim: int = HEAD_DIM, gqa_group: int = 1) -> bool:
-    """dm_attention_fwd's shape contract: head_dim 128, whole sequences, seq_len a multiple of
-    128 (pairs of query heads share a tile pair) or 256 (odd GQA group: adjacent row tiles)."""
+    """dm_attention_fwd / _bwd's shape contract: head_dim 128, whole sequences, seq_len a multiple
+    of 128 (pairs of query heads share a tile pair) or 256 (odd GQA group: adjacent row tiles)."""
     row_tile = 128 if gqa_group % 2 == 0 else 256
     return x.is_cuda and head_dim == HEAD_DIM and seq_len % row_tile == 0 and x.shape[0] % seq_len == 0
+
+
+def own_path_supported(x: torch.Tensor, seq_len: int, nh: int, nkv: int, head_dim: int = HEAD_DIM) -> bool:
+    """The whole block on own kernels: the attention contract plus the grouped GEMM's
+    (output and reduction widths multiples of 128: the dgrads contract over (nh + 2 nkv)Â·128
+    and H columns viewed as 2Â·D_e, so H % 256 == 0 and nh even)."""
+    H = x.shape[1]
+    return (own_attention_supported(x, seq_len, head_dim, nh // nkv) and H % 256 == 0 and nh % 2 == 0
+            and x.shape[0] % 128 == 0)
 
 
 class AttentionBlock:
@@ -96,7 +69,7 @@ class AttentionBlock:
         if hidden % head_dim:
             raise ValueError(f"hidden {hidden} not a multiple of head_dim {head_dim}")
         self.H, self.d = hidden, head_dim
-        self.own_kernel = own_kernel   # dm_attention_fwd for the forward where supported
+        self.own_kernel = own_kernel   # the own-kernel block where supported
         self.nh = hidden // head_dim
         if self.nh % gqa_group:
             raise ValueError(f"{self.nh} heads not divisible by gqa_group {gqa_group}")
@@ -111,20 +84,61 @@ class AttentionBlock:
         self.dw_qkv = torch.zeros(rows, hidden, dtype=F32, device=dev)
         self.dw_o = torch.zeros(hidden, hidden, dtype=F32, device=dev)
         self._saved: dict = {}
-        self.last_path = None   # "own" / "library": which attention path the last forward took
+        self._goff: dict = {}
+        self.last_path = None   # "own" / "library": which path the last forward took
 
     def flops(self, seq_len: int, micro_batch: int) -> tuple[int, int]:
         return attention_flops(self.H, self.nh // self.nkv, seq_len, micro_batch, self.d)
 
+    def _group_off(self, T: int, device) -> torch.Tensor:
+        key = (T, str(device))
+        if key not in self._goff:
+            self._goff[key] = torch.tensor([0, T], dtype=torch.int32, device=device)
+        return self._goff[key]
+
+    # ---------------------------------------------------------------- own kernels
+    def _forward_own(self, slot, x: torch.Tensor, out: torch.Tensor, seq_len: int) -> None:
+        from . import kernels as K
+
+        T, H = x.shape
+        go = self._group_off(T, x.device)
+        wq = self.w_qkv.detach().view(1, -1, H)
+        wo = self.w_o.detach().view(1, H, H)
+        qkv = torch.empty(T, wq.shape[1], dtype=BF16, device=x.device)
+        K.w2_fwd(x, wq, go, qkv)                                   # qkv = x W_qkv^T
+        o = torch.empty(T, self.nh * self.d, dtype=BF16, device=x.device)
+        lse = torch.empty(T // seq_len, self.nh, seq_len, dtype=F32, device=x.device)
+        K.attention_fwd(qkv, seq_len, self.nh, self.nkv, o, lse)
+        y = torch.empty(T, H, dtype=BF16, device=x.device)
+        K.w2_fwd(o, wo, go, y)                                     # y = o W_o^T
+        torch.add(x, y, out=out)
+        self._saved[slot] = ("own", x, qkv, o, lse, seq_len)
+
+    def _backward_own(self, saved, grad_h: torch.Tensor, dx_out: torch.Tensor, accumulate: bool) -> None:
+        from . import kernels as K
+
+        _, x, qkv, o, lse, seq_len = saved
+        T, H = x.shape
+        go = self._group_off(T, x.device)
+        seg = go.view(1, 2)
+        dh = grad_h.contiguous()
+        w13_o = self.w_o.detach().view(1, H, H)                    # dgrad: dO = dh W_o
+        do = torch.empty(T, H, dtype=BF16, device=x.device)
+        K.w13_dgrad(dh, w13_o, go, do)
+        K.wgrad(dh, o, seg, self.dw_o.view(1, H, H), beta=1.0 if accumulate else 0.0)   # dW_o (+)= dh^T o
+        dqkv = torch.empty_like(qkv)
+        K.attention_bwd(qkv, o, do, lse, seq_len, self.nh, self.nkv, dqkv)
+        R = qkv.shape[1]
+        K.wgrad(dqkv, x, seg, self.dw_qkv.view(1, R, H), beta=1.0 if accumulate else 0.0)
+        dxa = torch.empty(T, H, dtype=BF16, device=x.device)
+        K.w13_dgrad(dqkv, self.w_qkv.detach().view(1, R, H), go, dxa)   # dx_attn = dqkv W_qkv
+        torch.add(dh, dxa, out=dx_out)
+
+    # ----------------------------------------------------------- library block
     def _attend(self, x: torch.Tensor, seq_len: int) -> torch.Tensor:
         T, H = x.shape
         b = T // seq_len
         qkv = x @ self.w_qkv.t()
-        if self.own_kernel and own_attention_supported(x, seq_len, self.d, self.nh // self.nkv):
-            self.last_path = "own"
-            o = _OwnCausalAttention.apply(qkv.contiguous(), seq_len, self.nh, self.nkv)
-            return o @ self.w_o.t()
-        self.last_path = "library"
         q, k, v = qkv.split([self.nh * self.d, self.nkv * self.d, self.nkv * self.d], dim=1)
         q = q.view(b, seq_len, self.nh, self.d).transpose(1, 2)
         k = k.view(b, seq_len, self.nkv, self.d).transpose(1, 2)
@@ -135,16 +149,25 @@ class AttentionBlock:
         return o @ self.w_o.t()
 
     def forward(self, slot, x: torch.Tensor, out: torch.Tensor, seq_len: int) -> None:
-        """out = x + attn(x) (bf16 [T, H]); keeps the autograd graph under `slot`."""
+        """out = x + attn(x) (bf16 [T, H]); keeps what the backward needs under `slot`."""
+        if self.own_kernel and own_path_supported(x, seq_len, self.nh, self.nkv, self.d):
+            self.last_path = "own"
+            self._forward_own(slot, x.detach(), out, seq_len)
+            return
+        self.last_path = "library"
         with torch.enable_grad():
             xi = x.detach().requires_grad_(True)
             h = xi + self._attend(xi, seq_len)
         out.copy_(h.detach())
-        self._saved[slot] = (xi, h)
+        self._saved[slot] = ("library", xi, h)
 
     def backward(self, slot, grad_h: torch.Tensor, dx_out: torch.Tensor, accumulate: bool) -> None:
         """dx_out = dL/dx given dL/dh; parameter grads (+)= into dw_qkv / dw_o (fp32)."""
-        xi, h = self._saved.pop(slot)
+        saved = self._saved.pop(slot)
+        if saved[0] == "own":
+            self._backward_own(saved, grad_h, dx_out, accumulate)
+            return
+        _, xi, h = saved
         gx, gq, go = torch.autograd.grad(h, (xi, self.w_qkv, self.w_o), grad_outputs=grad_h)
         dx_out.copy_(gx)
         if accumulate:

@@ -8,22 +8,47 @@
 //   dV = Pᵀ dO,  dP = dO Vᵀ,  dS = P ∘ (dP - D),  dQ = scale·dS K,  dK = scale·dSᵀ Q.
 // Three launches, all deterministic (no atomics):
 //   attn_bwd_dot_kernel   D (warp per (token, head))
-//   attn_bwd_dkdv_kernel  CTA per (key tile j, KV head, sequence): dK_j, dV_j accumulate in
-//                         TMEM over the group's g query heads and the query tiles i >= j:
-//                         Sᵀ = K_j Q_iᵀ and dPᵀ = V_j dO_iᵀ (tcgen05, M = keys), the
-//                         elementwise warps (thread = key row = TMEM lane) form Pᵀ and dSᵀ
-//                         rows in bf16 (SWIZZLE_128B smem), then dV += Pᵀ dO_i, dK += dSᵀ Q_i
-//                         with dO_i / Q_i re-read as MN-major B operands of the same tiles
-//   attn_bwd_dq_kernel    CTA per (query tile i, query head, sequence): S = Q_i K_jᵀ and
-//                         dP = dO_i V_jᵀ, dS rows, dQ += dS K_j for the key tiles j <= i
-// Warp roles (256 threads): warp 0 TMA, warp 1 MMA issuer (one thread), warp 2 TMEM
-// allocator, warps 4-7 elementwise (thread r = tile row r). Tiles 128 x 128, head_dim 128.
+//   attn_bwd_dkdv_kernel  CTA per (128-key tile j, KV head, sequence): dK_j, dV_j accumulate in
+//                         TMEM over the group's g query heads and the 64-query tiles at or past
+//                         the diagonal: Sᵀ = K_j Q_iᵀ and dPᵀ = V_j dO_iᵀ (M = 128 keys, N = 64),
+//                         the elementwise warps form Pᵀ and dSᵀ rows in bf16 (SWIZZLE_128B smem),
+//                         then dV += Pᵀ dO_i, dK += dSᵀ Q_i with dO_i / Q_i re-read as MN-major
+//                         B operands of the same smem tiles
+//   attn_bwd_dq_kernel    CTA per (128-query tile i, query head, sequence): S = Q_i K_jᵀ and
+//                         dP = dO_i V_jᵀ over the 64-key tiles j up to the diagonal, dS rows,
+//                         dQ += dS K_j
+// Both main kernels are software-pipelined: the S/dP accumulators are double-buffered in TMEM
+// (2 x 2 x 64 columns) and the P/dS tiles in smem, the streamed operand (Q/dO, resp. K/V) has a
+// 3-deep TMA ring, and the single MMA thread issues S(it+1), dP(it+1) before the dV/dK (dQ)
+// MMAs of step it — so the tensor core works on the next step while the elementwise warps turn
+// step it's S/dP rows into P/dS. Warp roles (384 threads): warp 0 TMA, warp 1 MMA issuer (one
+// thread), warp 2 TMEM allocator, warps 4-11 elementwise (warp w: TMEM lanes 32·(w%4).., 32 of
+// the 64 columns by (w-4)/4).
 #include "attention_common.cuh"
 
 namespace dm {
 
-constexpr int AB_THREADS = 256;
+constexpr int AB_THREADS = 384;
+constexpr int AB_EW = 8;                                  // elementwise warps
+constexpr int AB_T = 64;                                  // streamed tile rows (queries / keys)
+constexpr int AB_STAGES = 3;                              // TMA ring depth of the streamed tiles
+constexpr uint32_t AB_ATOM64 = AB_T * 128;                // 8 KiB: 64 rows x 64 bf16 (SWIZZLE_128B)
+constexpr uint32_t AB_TILE64 = 2 * AB_ATOM64;             // 16 KiB: 64 rows x 128 d
+constexpr uint32_t AB_PT = AT_BM * 128;                   // 16 KiB: 128 rows x 64 bf16 (P / dS)
 constexpr float AB_LOG2E = 1.4426950408889634f;
+
+// K-major [64 rows x 128] tile (two 8 KiB atoms): k16 step kk of the 128-deep reduction
+__device__ __forceinline__ uint64_t ab_kmajor64(uint32_t base, int kk) {
+  return make_sdesc_sw128(base + (kk >> 2) * AB_ATOM64 + (kk & 3) * 32, 16, 1024);
+}
+// the same [64 rows x 128 d] tile as an MN-major B operand: K = its 64 rows, N = d
+__device__ __forceinline__ uint64_t ab_mnmajor64(uint32_t base, int kk) {
+  return make_sdesc_sw128(base + kk * 2048, AB_ATOM64, 1024);
+}
+// [128 rows x 64] single-atom tile (P / dS) as a K-major A operand: K = its 64 columns
+__device__ __forceinline__ uint64_t ab_kmajor_p(uint32_t base, int kk) {
+  return make_sdesc_sw128(base + kk * 32, 16, 1024);
+}
 
 // D[b][h][s] = sum_d dO[t, h, d] * O[t, h, d] (fp32): warp per (token, head)
 __global__ void __launch_bounds__(256)
@@ -44,94 +69,120 @@ attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __
   }
 }
 
-// Write 32 bf16-pair words (64 values, columns c0..c0+63 of row r) into a 128 x 128 bf16
-// SWIZZLE_128B tile (two 64-column atoms).
-__device__ __forceinline__ void ab_store_row64(uint32_t tile, int r, int c0, const uint32_t (&v)[32]) {
-  const uint32_t atom = tile + (c0 >> 6) * AT_ATOM;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) st_shared_v4(atom + sw128(r, c), v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-}
-
-// Elementwise step of one row: 128 (S, dP) accumulator columns in TMEM -> bf16 P and dS rows in
-// smem. lse2[c] / dd[c] give the per-column (key-major kernel) or per-row (query-major kernel,
-// uniform) log2-LSE and D; masked columns (causal) produce P = dS = 0.
+// Elementwise step of one thread = one accumulator row r (TMEM lane) over 32 columns
+// [c0, c0 + 32) of the 64-column S / dP buffers: bf16 P and dS into the row's four 16-byte
+// chunks c0/8 .. c0/8+3 of a [128 x 64] SWIZZLE_128B tile. Key-major kernel (COLS_ARE_QUERIES):
+// row = key, column = query, lse2c / ddc per column; query-major: row = query, one lse2r / ddr.
+// Causal mask: key > query, i.e. (row - col > off) key-major, (col - row > off) query-major,
+// off = the tiles' position difference; only tested when `diag`.
 template <bool COLS_ARE_QUERIES>
-__device__ __forceinline__ void ab_row(uint32_t tS, uint32_t tP, uint32_t sPt, uint32_t sDSt, int r, bool diag,
-                                       const float* lse2c, const float* ddc, float lse2r, float ddr,
-                                       float scale_log2) {
-#pragma unroll 1
-  for (int c0 = 0; c0 < AT_BN; c0 += 64) {
-    uint32_t pw[32], dw[32];
+__device__ __forceinline__ void ab_row32(uint32_t tS, uint32_t tP, uint32_t sPt, uint32_t sDS, int r, int c0, bool diag,
+                                         int off, const float* lse2c, const float* ddc, float lse2r, float ddr,
+                                         float scale_log2) {
+  uint32_t s32[32], d32[32];
+  tmem_ld16(tS + c0, *reinterpret_cast<uint32_t(*)[16]>(s32));
+  tmem_ld16(tS + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(s32 + 16));
+  tmem_ld16(tP + c0, *reinterpret_cast<uint32_t(*)[16]>(d32));
+  tmem_ld16(tP + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(d32 + 16));
+  tmem_wait_ld();
+  uint32_t pw[16], dw[16];
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      uint32_t s32[32], d32[32];
-      tmem_ld16(tS + c0 + half * 32, *reinterpret_cast<uint32_t(*)[16]>(s32));
-      tmem_ld16(tS + c0 + half * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(s32 + 16));
-      tmem_ld16(tP + c0 + half * 32, *reinterpret_cast<uint32_t(*)[16]>(d32));
-      tmem_ld16(tP + c0 + half * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(d32 + 16));
-      tmem_wait_ld();
+  for (int q = 0; q < 16; ++q) {
+    float p2[2], ds2[2];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        float p2[2], ds2[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int c = c0 + half * 32 + 2 * q + u;
-          const float l2 = COLS_ARE_QUERIES ? lse2c[c] : lse2r;
-          const float dv = COLS_ARE_QUERIES ? ddc[c] : ddr;
-          // causal: key > query is masked (key tile j == query tile i on the diagonal)
-          const bool masked = diag && (COLS_ARE_QUERIES ? (r > c) : (c > r));
-          const float p = masked ? 0.f : ex2(__fmaf_rn(__uint_as_float(s32[2 * q + u]), scale_log2, -l2));
-          p2[u] = p;
-          ds2[u] = p * (__uint_as_float(d32[2 * q + u]) - dv);
-        }
-        pw[half * 16 + q] = pack_bf16(p2[0], p2[1]);
-        dw[half * 16 + q] = pack_bf16(ds2[0], ds2[1]);
-      }
+    for (int u = 0; u < 2; ++u) {
+      const int c = c0 + 2 * q + u;
+      const float l2 = COLS_ARE_QUERIES ? lse2c[c] : lse2r;
+      const float dv = COLS_ARE_QUERIES ? ddc[c] : ddr;
+      const bool masked = diag && (COLS_ARE_QUERIES ? (r - c > off) : (c - r > off));
+      const float p = masked ? 0.f : ex2(__fmaf_rn(__uint_as_float(s32[2 * q + u]), scale_log2, -l2));
+      p2[u] = p;
+      ds2[u] = p * (__uint_as_float(d32[2 * q + u]) - dv);
     }
-    if (sPt) ab_store_row64(sPt, r, c0, pw);
-    ab_store_row64(sDSt, r, c0, dw);
+    pw[q] = pack_bf16(p2[0], p2[1]);
+    dw[q] = pack_bf16(ds2[0], ds2[1]);
+  }
+  const int ch = c0 >> 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (sPt) st_shared_v4(sPt + sw128(r, ch + q), pw[4 * q], pw[4 * q + 1], pw[4 * q + 2], pw[4 * q + 3]);
+    st_shared_v4(sDS + sw128(r, ch + q), dw[4 * q], dw[4 * q + 1], dw[4 * q + 2], dw[4 * q + 3]);
   }
 }
 
-// dK_j, dV_j: CTA (key tile j = blockIdx.x, KV head = blockIdx.y, sequence = blockIdx.z)
+// Accumulator rows r of a [128 x 128] fp32 TMEM block, columns [c0, c0 + 64) -> bf16 * sc
+__device__ __forceinline__ void ab_store_acc(uint32_t tacc, int c0, float sc, bool zero, __nv_bfloat16* dst) {
+#pragma unroll 1
+  for (int c = c0; c < c0 + 64; c += 16) {
+    uint32_t v[16];
+    tmem_ld16(tacc + c, v);
+    tmem_wait_ld();
+    uint32_t w8[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      w8[q] = zero ? 0u : pack_bf16(__uint_as_float(v[2 * q]) * sc, __uint_as_float(v[2 * q + 1]) * sc);
+    int4* o4 = reinterpret_cast<int4*>(dst + c);
+    o4[0] = make_int4((int)w8[0], (int)w8[1], (int)w8[2], (int)w8[3]);
+    o4[1] = make_int4((int)w8[4], (int)w8[5], (int)w8[6], (int)w8[7]);
+  }
+}
+
+// smem carve-up shared by both kernels' host sizing
+constexpr size_t AB_SMEM_DKDV = 1024 + 2 * (size_t)AT_TILE + AB_STAGES * 2 * (size_t)AB_TILE64 + 4 * (size_t)AB_PT +
+                                4 * AB_T * sizeof(float) + 256;
+constexpr size_t AB_SMEM_DQ = 1024 + 2 * (size_t)AT_TILE + AB_STAGES * 2 * (size_t)AB_TILE64 + 2 * (size_t)AB_PT + 256;
+
+// dK_j, dV_j: CTA (128-key tile j = blockIdx.x (heaviest first), KV head, sequence)
 __global__ void __launch_bounds__(AB_THREADS, 1)
-attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmdo,
-                     const float* __restrict__ lse, const float* __restrict__ dl, int seq_len, int nh, int nkv,
-                     float scale_log2, float scale, __nv_bfloat16* __restrict__ dqkv) {
+attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmkv, const __grid_constant__ CUtensorMap tmq,
+                     const __grid_constant__ CUtensorMap tmdo, const float* __restrict__ lse,
+                     const float* __restrict__ dl, int seq_len, int nh, int nkv, float scale_log2, float scale,
+                     __nv_bfloat16* __restrict__ dqkv) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
   uint8_t* sK = smem;
-  uint8_t* sV = smem + AT_TILE;
-  uint8_t* sQ = smem + 2 * AT_TILE;
-  uint8_t* sDO = smem + 3 * AT_TILE;
-  uint8_t* sPt = smem + 4 * AT_TILE;
-  uint8_t* sDSt = smem + 5 * AT_TILE;
-  float* s_lse = reinterpret_cast<float*>(smem + 6 * AT_TILE);   // [2][128] (parity double buffer)
-  float* s_dd = s_lse + 2 * AT_BM;                               // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dd + 2 * AT_BM);
+  uint8_t* sV = sK + AT_TILE;
+  uint8_t* sQ = sV + AT_TILE;                                   // [AB_STAGES] x 16 KiB
+  uint8_t* sDO = sQ + AB_STAGES * AB_TILE64;                    // [AB_STAGES] x 16 KiB
+  uint8_t* sPt = sDO + AB_STAGES * AB_TILE64;                   // [2] x 16 KiB
+  uint8_t* sDSt = sPt + 2 * AB_PT;                              // [2] x 16 KiB
+  float* s_lse = reinterpret_cast<float*>(sDSt + 2 * AB_PT);    // [2][64]
+  float* s_dd = s_lse + 2 * AB_T;                               // [2][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dd + 2 * AB_T);
   uint64_t* kv_full = bars;
-  uint64_t* ld_full = bars + 1;
-  uint64_t* st_full = bars + 2;
-  uint64_t* p_full = bars + 3;
-  uint64_t* acc_done = bars + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+  uint64_t* ld_full = bars + 1;                  // [AB_STAGES]
+  uint64_t* ld_empty = ld_full + AB_STAGES;      // [AB_STAGES]
+  uint64_t* st_full = ld_empty + AB_STAGES;      // [2] S^T / dP^T buffer b computed
+  uint64_t* tm_empty = st_full + 2;              // [2] ... read out of TMEM
+  uint64_t* p_full = tm_empty + 2;               // [2] P^T / dS^T smem buffer b written
+  uint64_t* ps_empty = p_full + 2;               // [2] ... consumed by the dV / dK MMAs
+  uint64_t* acc_done = ps_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int j = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
-  const int n_t = seq_len / AT_BM, g = nh / nkv;
-  const int per_head = n_t - j, n_it = g * per_head;
+  const int n_q = seq_len / AB_T, g = nh / nkv;
+  const int per_head = n_q - 2 * j, n_it = g * per_head;
   const int row0 = b * seq_len;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    mbar_init(ld_full, 1);
-    mbar_init(st_full, 1);
-    mbar_init(p_full, AT_BM);
+    for (int s = 0; s < AB_STAGES; ++s) {
+      mbar_init(&ld_full[s], 1);
+      mbar_init(&ld_empty[s], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&st_full[q], 1);
+      mbar_init(&tm_empty[q], AB_EW);
+      mbar_init(&p_full[q], AB_EW * 32);
+      mbar_init(&ps_empty[q], 1);
+    }
     mbar_init(acc_done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);   // S^T [0,128) dP^T [128,256) dV [256,384) dK [384,512)
+  // TMEM: S^T / dP^T buffer q at [128q, 128q + 64) / [128q + 64, 128q + 128); dV [256, 384), dK [384, 512)
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -139,99 +190,106 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
 
   if (warp == 0) {
     if (lane == 0) {
+      tma_prefetch_desc(&tmkv);
       tma_prefetch_desc(&tmq);
       tma_prefetch_desc(&tmdo);
       const int kcol = (nh + kvh) * AT_D, vcol = (nh + nkv + kvh) * AT_D, krow = row0 + j * AT_BN;
       mbar_expect_tx(kv_full, 2 * AT_TILE);
-      tma_load_2d(sK, &tmq, kv_full, kcol, krow);
-      tma_load_2d(sK + AT_ATOM, &tmq, kv_full, kcol + 64, krow);
-      tma_load_2d(sV, &tmq, kv_full, vcol, krow);
-      tma_load_2d(sV + AT_ATOM, &tmq, kv_full, vcol + 64, krow);
+      tma_load_2d(sK, &tmkv, kv_full, kcol, krow);
+      tma_load_2d(sK + AT_ATOM, &tmkv, kv_full, kcol + 64, krow);
+      tma_load_2d(sV, &tmkv, kv_full, vcol, krow);
+      tma_load_2d(sV + AT_ATOM, &tmkv, kv_full, vcol + 64, krow);
       for (int it = 0; it < n_it; ++it) {
-        const int qh = kvh * g + it / per_head, i = j + it % per_head;
-        if (it > 0) mbar_wait(acc_done, (it - 1) & 1);   // the previous Q_i / dO_i are read out
-        const int qrow = row0 + i * AT_BM;
-        mbar_expect_tx(ld_full, 2 * AT_TILE);
-        tma_load_2d(sQ, &tmq, ld_full, qh * AT_D, qrow);
-        tma_load_2d(sQ + AT_ATOM, &tmq, ld_full, qh * AT_D + 64, qrow);
-        tma_load_2d(sDO, &tmdo, ld_full, qh * AT_D, qrow);
-        tma_load_2d(sDO + AT_ATOM, &tmdo, ld_full, qh * AT_D + 64, qrow);
+        const int s = it % AB_STAGES;
+        if (it >= AB_STAGES) mbar_wait(&ld_empty[s], (uint32_t)((it / AB_STAGES - 1) & 1));
+        const int qh = kvh * g + it / per_head, i = 2 * j + it % per_head;
+        const int qrow = row0 + i * AB_T;
+        uint8_t* q = sQ + s * AB_TILE64;
+        uint8_t* d = sDO + s * AB_TILE64;
+        mbar_expect_tx(&ld_full[s], 2 * AB_TILE64);
+        tma_load_2d(q, &tmq, &ld_full[s], qh * AT_D, qrow);
+        tma_load_2d(q + AB_ATOM64, &tmq, &ld_full[s], qh * AT_D + 64, qrow);
+        tma_load_2d(d, &tmdo, &ld_full[s], qh * AT_D, qrow);
+        tma_load_2d(d + AB_ATOM64, &tmdo, &ld_full[s], qh * AT_D + 64, qrow);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc_kk = make_idesc_bf16(AT_BM, AT_BN, 0, 0);   // both operands K-major
-      constexpr uint32_t idesc_km = make_idesc_bf16(AT_BM, AT_D, 0, 1);    // A K-major, B MN-major
-      const uint32_t ka = smem_u32(sK), va = smem_u32(sV), qa = smem_u32(sQ), da = smem_u32(sDO);
-      const uint32_t pa = smem_u32(sPt), dsa = smem_u32(sDSt);
+      constexpr uint32_t idesc_s = make_idesc_bf16(AT_BN, AB_T, 0, 0);   // M = 128 keys, N = 64 queries
+      constexpr uint32_t idesc_a = make_idesc_bf16(AT_BN, AT_D, 0, 1);   // M = 128 keys, N = d, B MN-major
+      const uint32_t ka = smem_u32(sK), va = smem_u32(sV);
+      auto dvdk = [&](int q) {   // dV += P^T dO_q, dK += dS^T Q_q
+        const int s = q % AB_STAGES, pb = q & 1;
+        mbar_wait(&p_full[pb], (uint32_t)((q >> 1) & 1));
+        tc_fence_after();
+        const uint32_t pa = smem_u32(sPt + pb * AB_PT), dsa = smem_u32(sDSt + pb * AB_PT);
+        const uint32_t qa = smem_u32(sQ + s * AB_TILE64), da = smem_u32(sDO + s * AB_TILE64);
+#pragma unroll
+        for (int kk = 0; kk < AB_T / 16; ++kk)
+          umma_bf16_ss(tmem + 256, ab_kmajor_p(pa, kk), ab_mnmajor64(da, kk), idesc_a, (q | kk) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < AB_T / 16; ++kk)
+          umma_bf16_ss(tmem + 384, ab_kmajor_p(dsa, kk), ab_mnmajor64(qa, kk), idesc_a, (q | kk) ? 1u : 0u);
+        umma_commit(&ld_empty[s]);
+        umma_commit(&ps_empty[pb]);
+      };
       mbar_wait(kv_full, 0);
       for (int it = 0; it < n_it; ++it) {
-        mbar_wait(ld_full, it & 1);
+        const int s = it % AB_STAGES, tb = it & 1;
+        mbar_wait(&ld_full[s], (uint32_t)((it / AB_STAGES) & 1));
+        if (it >= 2) mbar_wait(&tm_empty[tb], (uint32_t)(((it >> 1) - 1) & 1));
         tc_fence_after();
+        const uint32_t qa = smem_u32(sQ + s * AB_TILE64), da = smem_u32(sDO + s * AB_TILE64);
+        const uint32_t ts = tmem + tb * 128;
 #pragma unroll
         for (int kk = 0; kk < AT_D / 16; ++kk)                             // S^T = K_j Q_i^T
-          umma_bf16_ss(tmem, at_kmajor(ka, kk), at_kmajor(qa, kk), idesc_kk, kk > 0 ? 1u : 0u);
+          umma_bf16_ss(ts, at_kmajor(ka, kk), ab_kmajor64(qa, kk), idesc_s, kk > 0 ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < AT_D / 16; ++kk)                             // dP^T = V_j dO_i^T
-          umma_bf16_ss(tmem + AT_BN, at_kmajor(va, kk), at_kmajor(da, kk), idesc_kk, kk > 0 ? 1u : 0u);
-        umma_commit(st_full);
-        mbar_wait(p_full, it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < AT_BM / 16; ++kk)                            // dV += P^T dO_i
-          umma_bf16_ss(tmem + 2 * AT_BN, at_kmajor(pa, kk), at_mnmajor(da, kk), idesc_km, (it | kk) ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < AT_BM / 16; ++kk)                            // dK += dS^T Q_i
-          umma_bf16_ss(tmem + 3 * AT_BN, at_kmajor(dsa, kk), at_mnmajor(qa, kk), idesc_km, (it | kk) ? 1u : 0u);
-        umma_commit(acc_done);
+          umma_bf16_ss(ts + 64, at_kmajor(va, kk), ab_kmajor64(da, kk), idesc_s, kk > 0 ? 1u : 0u);
+        umma_commit(&st_full[tb]);
+        if (it >= 1) dvdk(it - 1);
       }
+      if (n_it > 0) dvdk(n_it - 1);
+      umma_commit(acc_done);
     }
     __syncwarp();
   } else if (warp >= 4) {
-    const int q4 = warp & 3;
+    const int q4 = warp & 3, half = (warp - 4) >> 2;
     const int r = q4 * 32 + lane;                                           // key row = TMEM lane
+    const int et = (warp - 4) * 32 + lane;                                  // 0..255
     const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     for (int it = 0; it < n_it; ++it) {
-      const int qh = kvh * g + it / per_head, i = j + it % per_head;
-      float* l2 = s_lse + (it & 1) * AT_BM;
-      float* dd = s_dd + (it & 1) * AT_BM;
-      const size_t lrow = ((size_t)b * nh + qh) * seq_len + (size_t)i * AT_BM + r;
-      l2[r] = lse[lrow] * AB_LOG2E;                                        // query r of tile i
-      dd[r] = dl[lrow];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      mbar_wait(st_full, it & 1);
+      const int qh = kvh * g + it / per_head, i = 2 * j + it % per_head;
+      const int tb = it & 1;
+      float* l2 = s_lse + tb * AB_T;
+      float* dd = s_dd + tb * AB_T;
+      if (et < AB_T) {
+        const size_t lrow = ((size_t)b * nh + qh) * seq_len + (size_t)i * AB_T + et;
+        l2[et] = lse[lrow] * AB_LOG2E;                                      // query et of tile i
+        dd[et] = dl[lrow];
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mbar_wait(&st_full[tb], (uint32_t)((it >> 1) & 1));
       tc_fence_after();
-      if (it > 0) mbar_wait(acc_done, (it - 1) & 1);                       // P^T / dS^T smem free
-      ab_row<true>(trow, trow + AT_BN, smem_u32(sPt), smem_u32(sDSt), r, i == j, l2, dd, 0.f, 0.f, scale_log2);
-      fence_proxy_async_smem();
+      if (it >= 2) mbar_wait(&ps_empty[tb], (uint32_t)(((it >> 1) - 1) & 1));   // P^T / dS^T smem free
+      const int off = i * AB_T - j * AT_BN;                                 // query tile start - key tile start
+      ab_row32<true>(trow + tb * 128, trow + tb * 128 + 64, smem_u32(sPt + tb * AB_PT), smem_u32(sDSt + tb * AB_PT), r,
+                     half * 32, off < AT_BN, off, l2, dd, 0.f, 0.f, scale_log2);
       tc_fence_before();
-      mbar_arrive(p_full);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tm_empty[tb]);
+      fence_proxy_async_smem();
+      mbar_arrive(&p_full[tb]);
     }
     // dV and dK rows of key r -> bf16 (dK scaled by the softmax scale)
-    if (n_it > 0) mbar_wait(acc_done, (n_it - 1) & 1);
+    mbar_wait(acc_done, 0);
     tc_fence_after();
     const int ld = (nh + 2 * nkv) * AT_D;
     __nv_bfloat16* drow = dqkv + (size_t)(row0 + j * AT_BN + r) * ld;
-#pragma unroll 1
-    for (int which = 0; which < 2; ++which) {                               // 0: dV, 1: dK
-      const uint32_t tacc = trow + (2 + which) * AT_BN;
-      const float sc = which ? scale : 1.0f;
-      __nv_bfloat16* dst = drow + (size_t)(which ? (nh + kvh) : (nh + nkv + kvh)) * AT_D;
-#pragma unroll 1
-      for (int c = 0; c < AT_D; c += 16) {
-        uint32_t v[16];
-        tmem_ld16(tacc + c, v);
-        tmem_wait_ld();
-        uint32_t w8[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          w8[q] = n_it > 0 ? pack_bf16(__uint_as_float(v[2 * q]) * sc, __uint_as_float(v[2 * q + 1]) * sc) : 0u;
-        int4* o4 = reinterpret_cast<int4*>(dst + c);
-        o4[0] = make_int4((int)w8[0], (int)w8[1], (int)w8[2], (int)w8[3]);
-        o4[1] = make_int4((int)w8[4], (int)w8[5], (int)w8[6], (int)w8[7]);
-      }
-    }
+    ab_store_acc(trow + 256, half * 64, 1.0f, n_it == 0, drow + (size_t)(nh + nkv + kvh) * AT_D);
+    ab_store_acc(trow + 384, half * 64, scale, n_it == 0, drow + (size_t)(nh + kvh) * AT_D);
   }
   tc_fence_before();
   __syncthreads();
@@ -239,42 +297,54 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-// dQ_i: CTA (query tile i = n_t-1-blockIdx.x (heaviest first), query head, sequence)
+// dQ_i: CTA (128-query tile i = n_t-1-blockIdx.x (heaviest first), query head, sequence)
 __global__ void __launch_bounds__(AB_THREADS, 1)
 attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmdo,
-                   const float* __restrict__ lse, const float* __restrict__ dl, int seq_len, int nh, int nkv,
-                   float scale_log2, float scale, __nv_bfloat16* __restrict__ dqkv) {
+                   const __grid_constant__ CUtensorMap tmkv, const float* __restrict__ lse,
+                   const float* __restrict__ dl, int seq_len, int nh, int nkv, float scale_log2, float scale,
+                   __nv_bfloat16* __restrict__ dqkv) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   uint8_t* smem = smem_raw + pad;
   uint8_t* sQ = smem;
-  uint8_t* sDO = smem + AT_TILE;
-  uint8_t* sK = smem + 2 * AT_TILE;
-  uint8_t* sV = smem + 3 * AT_TILE;
-  uint8_t* sDS = smem + 4 * AT_TILE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 5 * AT_TILE);
+  uint8_t* sDO = sQ + AT_TILE;
+  uint8_t* sK = sDO + AT_TILE;                                  // [AB_STAGES] x 16 KiB
+  uint8_t* sV = sK + AB_STAGES * AB_TILE64;                     // [AB_STAGES] x 16 KiB
+  uint8_t* sDS = sV + AB_STAGES * AB_TILE64;                    // [2] x 16 KiB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + 2 * AB_PT);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* s_full = bars + 2;
-  uint64_t* p_full = bars + 3;
-  uint64_t* acc_done = bars + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+  uint64_t* kv_full = bars + 1;                  // [AB_STAGES]
+  uint64_t* kv_empty = kv_full + AB_STAGES;      // [AB_STAGES]
+  uint64_t* s_full = kv_empty + AB_STAGES;       // [2]
+  uint64_t* tm_empty = s_full + 2;               // [2]
+  uint64_t* p_full = tm_empty + 2;               // [2]
+  uint64_t* ds_empty = p_full + 2;               // [2]
+  uint64_t* acc_done = ds_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int n_t = seq_len / AT_BM;
   const int i = n_t - 1 - (int)blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int g = nh / nkv, kvh = h / g, nj = i + 1;
+  const int g = nh / nkv, kvh = h / g, nj = 2 * i + 2;          // 64-key tiles up to the diagonal
   const int row0 = b * seq_len;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    mbar_init(kv_full, 1);
-    mbar_init(s_full, 1);
-    mbar_init(p_full, AT_BM);
+    for (int s = 0; s < AB_STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&s_full[q], 1);
+      mbar_init(&tm_empty[q], AB_EW);
+      mbar_init(&p_full[q], AB_EW * 32);
+      mbar_init(&ds_empty[q], 1);
+    }
     mbar_init(acc_done, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);   // S [0,128) dP [128,256) dQ [256,384)
+  // TMEM: S / dP buffer q at [128q, 128q + 64) / [128q + 64, 128q + 128); dQ [256, 384)
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -284,6 +354,7 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
     if (lane == 0) {
       tma_prefetch_desc(&tmq);
       tma_prefetch_desc(&tmdo);
+      tma_prefetch_desc(&tmkv);
       const int qrow = row0 + i * AT_BM;
       mbar_expect_tx(q_full, 2 * AT_TILE);
       tma_load_2d(sQ, &tmq, q_full, h * AT_D, qrow);
@@ -291,74 +362,81 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
       tma_load_2d(sDO, &tmdo, q_full, h * AT_D, qrow);
       tma_load_2d(sDO + AT_ATOM, &tmdo, q_full, h * AT_D + 64, qrow);
       const int kcol = (nh + kvh) * AT_D, vcol = (nh + nkv + kvh) * AT_D;
-      for (int jj = 0; jj < nj; ++jj) {
-        if (jj > 0) mbar_wait(acc_done, (jj - 1) & 1);   // the previous K_j / V_j are read out
-        const int krow = row0 + jj * AT_BN;
-        mbar_expect_tx(kv_full, 2 * AT_TILE);
-        tma_load_2d(sK, &tmq, kv_full, kcol, krow);
-        tma_load_2d(sK + AT_ATOM, &tmq, kv_full, kcol + 64, krow);
-        tma_load_2d(sV, &tmq, kv_full, vcol, krow);
-        tma_load_2d(sV + AT_ATOM, &tmq, kv_full, vcol + 64, krow);
+      for (int jt = 0; jt < nj; ++jt) {
+        const int s = jt % AB_STAGES;
+        if (jt >= AB_STAGES) mbar_wait(&kv_empty[s], (uint32_t)((jt / AB_STAGES - 1) & 1));
+        const int krow = row0 + jt * AB_T;
+        uint8_t* k = sK + s * AB_TILE64;
+        uint8_t* v = sV + s * AB_TILE64;
+        mbar_expect_tx(&kv_full[s], 2 * AB_TILE64);
+        tma_load_2d(k, &tmkv, &kv_full[s], kcol, krow);
+        tma_load_2d(k + AB_ATOM64, &tmkv, &kv_full[s], kcol + 64, krow);
+        tma_load_2d(v, &tmkv, &kv_full[s], vcol, krow);
+        tma_load_2d(v + AB_ATOM64, &tmkv, &kv_full[s], vcol + 64, krow);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc_kk = make_idesc_bf16(AT_BM, AT_BN, 0, 0);
-      constexpr uint32_t idesc_km = make_idesc_bf16(AT_BM, AT_D, 0, 1);
-      const uint32_t qa = smem_u32(sQ), da = smem_u32(sDO), ka = smem_u32(sK), va = smem_u32(sV);
-      const uint32_t dsa = smem_u32(sDS);
-      mbar_wait(q_full, 0);
-      for (int jj = 0; jj < nj; ++jj) {
-        mbar_wait(kv_full, jj & 1);
+      constexpr uint32_t idesc_s = make_idesc_bf16(AT_BM, AB_T, 0, 0);   // M = 128 queries, N = 64 keys
+      constexpr uint32_t idesc_a = make_idesc_bf16(AT_BM, AT_D, 0, 1);   // dQ: N = d, B (K_j) MN-major
+      const uint32_t qa = smem_u32(sQ), da = smem_u32(sDO);
+      auto dq_step = [&](int q) {   // dQ += dS K_q
+        const int s = q % AB_STAGES, pb = q & 1;
+        mbar_wait(&p_full[pb], (uint32_t)((q >> 1) & 1));
         tc_fence_after();
+        const uint32_t dsa = smem_u32(sDS + pb * AB_PT), ka = smem_u32(sK + s * AB_TILE64);
+#pragma unroll
+        for (int kk = 0; kk < AB_T / 16; ++kk)
+          umma_bf16_ss(tmem + 256, ab_kmajor_p(dsa, kk), ab_mnmajor64(ka, kk), idesc_a, (q | kk) ? 1u : 0u);
+        umma_commit(&kv_empty[s]);
+        umma_commit(&ds_empty[pb]);
+      };
+      mbar_wait(q_full, 0);
+      for (int jt = 0; jt < nj; ++jt) {
+        const int s = jt % AB_STAGES, tb = jt & 1;
+        mbar_wait(&kv_full[s], (uint32_t)((jt / AB_STAGES) & 1));
+        if (jt >= 2) mbar_wait(&tm_empty[tb], (uint32_t)(((jt >> 1) - 1) & 1));
+        tc_fence_after();
+        const uint32_t ka = smem_u32(sK + s * AB_TILE64), va = smem_u32(sV + s * AB_TILE64);
+        const uint32_t ts = tmem + tb * 128;
 #pragma unroll
         for (int kk = 0; kk < AT_D / 16; ++kk)                             // S = Q_i K_j^T
-          umma_bf16_ss(tmem, at_kmajor(qa, kk), at_kmajor(ka, kk), idesc_kk, kk > 0 ? 1u : 0u);
+          umma_bf16_ss(ts, at_kmajor(qa, kk), ab_kmajor64(ka, kk), idesc_s, kk > 0 ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < AT_D / 16; ++kk)                             // dP = dO_i V_j^T
-          umma_bf16_ss(tmem + AT_BN, at_kmajor(da, kk), at_kmajor(va, kk), idesc_kk, kk > 0 ? 1u : 0u);
-        umma_commit(s_full);
-        mbar_wait(p_full, jj & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < AT_BN / 16; ++kk)                            // dQ += dS K_j
-          umma_bf16_ss(tmem + 2 * AT_BN, at_kmajor(dsa, kk), at_mnmajor(ka, kk), idesc_km, (jj | kk) ? 1u : 0u);
-        umma_commit(acc_done);
+          umma_bf16_ss(ts + 64, at_kmajor(da, kk), ab_kmajor64(va, kk), idesc_s, kk > 0 ? 1u : 0u);
+        umma_commit(&s_full[tb]);
+        if (jt >= 1) dq_step(jt - 1);
       }
+      dq_step(nj - 1);
+      umma_commit(acc_done);
     }
     __syncwarp();
   } else if (warp >= 4) {
-    const int q4 = warp & 3;
+    const int q4 = warp & 3, half = (warp - 4) >> 2;
     const int r = q4 * 32 + lane;                                           // query row = TMEM lane
     const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     const size_t lrow = ((size_t)b * nh + h) * seq_len + (size_t)i * AT_BM + r;
     const float l2 = lse[lrow] * AB_LOG2E, dd = dl[lrow];
-    for (int jj = 0; jj < nj; ++jj) {
-      mbar_wait(s_full, jj & 1);
+    for (int jt = 0; jt < nj; ++jt) {
+      const int tb = jt & 1;
+      mbar_wait(&s_full[tb], (uint32_t)((jt >> 1) & 1));
       tc_fence_after();
-      if (jj > 0) mbar_wait(acc_done, (jj - 1) & 1);                       // dS smem free
-      ab_row<false>(trow, trow + AT_BN, 0u, smem_u32(sDS), r, jj == i, nullptr, nullptr, l2, dd, scale_log2);
-      fence_proxy_async_smem();
+      if (jt >= 2) mbar_wait(&ds_empty[tb], (uint32_t)(((jt >> 1) - 1) & 1));   // dS smem free
+      const int off = i * AT_BM - jt * AB_T;                                // query tile start - key tile start
+      ab_row32<false>(trow + tb * 128, trow + tb * 128 + 64, 0u, smem_u32(sDS + tb * AB_PT), r, half * 32, off < AB_T,
+                      off, nullptr, nullptr, l2, dd, scale_log2);
       tc_fence_before();
-      mbar_arrive(p_full);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tm_empty[tb]);
+      fence_proxy_async_smem();
+      mbar_arrive(&p_full[tb]);
     }
-    mbar_wait(acc_done, (nj - 1) & 1);
+    mbar_wait(acc_done, 0);
     tc_fence_after();
     const int ld = (nh + 2 * nkv) * AT_D;
-    __nv_bfloat16* dst = dqkv + (size_t)(row0 + i * AT_BM + r) * ld + (size_t)h * AT_D;
-#pragma unroll 1
-    for (int c = 0; c < AT_D; c += 16) {
-      uint32_t v[16];
-      tmem_ld16(trow + 2 * AT_BN + c, v);
-      tmem_wait_ld();
-      uint32_t w8[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) w8[q] = pack_bf16(__uint_as_float(v[2 * q]) * scale, __uint_as_float(v[2 * q + 1]) * scale);
-      int4* o4 = reinterpret_cast<int4*>(dst + c);
-      o4[0] = make_int4((int)w8[0], (int)w8[1], (int)w8[2], (int)w8[3]);
-      o4[1] = make_int4((int)w8[4], (int)w8[5], (int)w8[6], (int)w8[7]);
-    }
+    ab_store_acc(trow + 256, half * 64, scale, false, dqkv + (size_t)(row0 + i * AT_BM + r) * ld + (size_t)h * AT_D);
   }
   tc_fence_before();
   __syncthreads();
@@ -366,12 +444,12 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-static int ab_map(CUtensorMap* tm, const void* base, uint64_t cols, uint64_t rows) {
+static int ab_map(CUtensorMap* tm, const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
   PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
   if (!enc) return set_error(DM_ERR_DRIVER, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, AT_BM};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -398,10 +476,13 @@ int dm_attention_bwd(const void* qkv, const void* out, const void* dout, const f
     return set_error(DM_ERR_ALIGN, "attention_bwd: operands not 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = T / seq_len, n_t = seq_len / AT_BM;
-  CUtensorMap tmq, tmdo;
+  const uint64_t qkv_cols = (uint64_t)(nh + 2 * nkv) * AT_D;
+  CUtensorMap tm128, tm64, tmdo128, tmdo64;
   int rc;
-  if ((rc = ab_map(&tmq, qkv, (uint64_t)(nh + 2 * nkv) * AT_D, (uint64_t)T))) return rc;
-  if ((rc = ab_map(&tmdo, dout, (uint64_t)nh * AT_D, (uint64_t)T))) return rc;
+  if ((rc = ab_map(&tm128, qkv, qkv_cols, (uint64_t)T, AT_BM))) return rc;
+  if ((rc = ab_map(&tm64, qkv, qkv_cols, (uint64_t)T, AB_T))) return rc;
+  if ((rc = ab_map(&tmdo128, dout, (uint64_t)nh * AT_D, (uint64_t)T, AT_BM))) return rc;
+  if ((rc = ab_map(&tmdo64, dout, (uint64_t)nh * AT_D, (uint64_t)T, AB_T))) return rc;
   int blocks = (T * nh + 7) / 8;
   if (blocks > num_sms_current() * 8) blocks = num_sms_current() * 8;
   attn_bwd_dot_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(out),
@@ -410,19 +491,17 @@ int dm_attention_bwd(const void* qkv, const void* out, const void* dout, const f
   if (e != cudaSuccess) return set_cuda_error(e, "attention_bwd dot launch");
   note_launch();
   const float scale = 1.0f / sqrtf((float)AT_D), scale_log2 = AB_LOG2E * scale;
-  const size_t smem_kv = 1024 + 6 * (size_t)AT_TILE + 4 * AT_BM * sizeof(float) + 64;
-  const size_t smem_q = 1024 + 5 * (size_t)AT_TILE + 64;
-  if ((rc = ensure_smem_attr((const void*)attn_bwd_dkdv_kernel, (int)smem_kv, "cudaFuncSetAttribute(attn_bwd_dkdv)")))
+  if ((rc = ensure_smem_attr((const void*)attn_bwd_dkdv_kernel, (int)AB_SMEM_DKDV, "cudaFuncSetAttribute(attn_bwd_dkdv)")))
     return rc;
-  if ((rc = ensure_smem_attr((const void*)attn_bwd_dq_kernel, (int)smem_q, "cudaFuncSetAttribute(attn_bwd_dq)")))
+  if ((rc = ensure_smem_attr((const void*)attn_bwd_dq_kernel, (int)AB_SMEM_DQ, "cudaFuncSetAttribute(attn_bwd_dq)")))
     return rc;
   __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dqkv);
-  attn_bwd_dkdv_kernel<<<dim3(n_t, nkv, nb), AB_THREADS, smem_kv, st>>>(tmq, tmdo, lse, dl_ws, seq_len, nh, nkv,
-                                                                       scale_log2, scale, d);
+  attn_bwd_dkdv_kernel<<<dim3(n_t, nkv, nb), AB_THREADS, AB_SMEM_DKDV, st>>>(tm128, tm64, tmdo64, lse, dl_ws, seq_len,
+                                                                              nh, nkv, scale_log2, scale, d);
   if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "attention_bwd dkdv launch");
   note_launch();
-  attn_bwd_dq_kernel<<<dim3(n_t, nh, nb), AB_THREADS, smem_q, st>>>(tmq, tmdo, lse, dl_ws, seq_len, nh, nkv, scale_log2,
-                                                                   scale, d);
+  attn_bwd_dq_kernel<<<dim3(n_t, nh, nb), AB_THREADS, AB_SMEM_DQ, st>>>(tm128, tmdo128, tm64, lse, dl_ws, seq_len, nh,
+                                                                         nkv, scale_log2, scale, d);
   if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "attention_bwd dq launch");
   note_launch();
   return DM_OK;

@@ -257,19 +257,25 @@ router_fused_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict
 //     makes the lane-strided 128-bit reads conflict-free without a transposing fill (register
 //     / cp.async fills took 5.8 / 9.8 us of L2 latency per CTA; the TMA fill 1.3-1.8 us);
 //   * x is read straight from global memory into registers two k-tiles ahead, so all 8 warps
-//     compute at once (a bulk-copy ring next to W_g held 3 units: 3 warps, 2-3x slower);
+//     compute at once (a bulk-copy ring next to W_g held 3 units: 3 warps, 2-3x slower), with
+//     an L2 evict_last policy so the permute phase re-reads x from L2 (scripts/rs_probe.py:
+//     45 -> 41 us; an up-front cp.async.bulk.prefetch.L2 of the CTA's rows bought nothing more);
 //   * 4 tokens per warp share every W_g read; the k-tile's W_g pairs are loaded before its
 //     FFMA2s, which run element pair j outermost (independent chains back to back). The
-//     route phase is fp32-FMA bound (T*E*H FMAs in the canonical fmaf order; ~11 us of math
-//     for Mixtral's 134 M FMAs), not HBM bound;
+//     route phase is fp32-FMA bound (T*E*H FMAs in the canonical fmaf order: 128 FFMA2 per
+//     16 LDS.128 per k-tile in SASS; ~12.6 us for Mixtral's 134 M FMAs vs the 7.4 us FMA-pipe
+//     floor at 64 FMA/clk/SM), not HBM bound;
 //   * histogram offsets: each CTA prefix-sums its own units in smem, publishes its totals,
 //     and after a grid barrier (fire-and-forget reductions on a monotonic counter: returning
 //     same-address atomics from 148 SMs serialise to ~10 us) every CTA scans the CTA totals
 //     (~1.2k ints) itself — no serial last-CTA tail;
-//   * permute: each CTA copies its own token rows (x still L2-resident) to their k expert
-//     rows, warp per row, and zeroes a share of the padding rows. This phase is bound by the
-//     write path: 64 MB of x_perm at the measured pure-write rate (scripts/hbm_probe.py,
-//     3.83 TB/s) is ~17 us.
+//   * permute: each CTA copies its own token rows (x L2-resident) to their k expert rows,
+//     warp per row with the whole row's loads in flight, and zeroes a share of the padding
+//     rows. It runs at the write rate of a dirty L2 (the state every real step and the cold-L2
+//     measurement leave): scripts/probes/permute_copy.cu copies 64 MB in 17.4 us with any copy
+//     structure (pipelined rows, quarter rows, smem + bulk stores) against 15.3 us for a pure
+//     64 MB write. Moving the copy onto TMA (one thread: bulk row loads into a ring in the freed
+//     W_g smem, k bulk stores each) was slower, 30 us.
 constexpr int RS_NT = DM_ROUTE_UNIT_TOKENS;
 constexpr int RS_WARPS = 8;
 constexpr int RS_THREADS = RS_WARPS * 32;
@@ -338,7 +344,8 @@ dispatch_stream_kernel(const __grid_constant__ CUtensorMap tmW, const __nv_bfloa
     for (int t = 0; t < RS_NT; ++t) xr[t] = x + (size_t)min(t0 + t, T - 1) * H + lane * 8;
     auto ldx = [&](int it, int4 (&xv)[RS_NT]) {
 #pragma unroll
-      for (int t = 0; t < RS_NT; ++t) xv[t] = it < NI ? ld_nc_v4(xr[t] + it * 256) : make_int4(0, 0, 0, 0);
+      for (int t = 0; t < RS_NT; ++t)
+        xv[t] = it < NI ? ld_nc_v4_hint(xr[t] + it * 256, L2_EVICT_LAST) : make_int4(0, 0, 0, 0);
     };
     int4 x0[RS_NT], x1[RS_NT];
     ldx(0, x0);
@@ -986,9 +993,9 @@ static int dispatch_stream_launch(const void* x, const float* wg, int T, int H, 
   const int upc = (nunit + grid - 1) / grid;
   if (upc > RS_MAX_UPC) return -1;
   grid = (nunit + upc - 1) / upc;
-  // phase 2/3 scratch in the dynamic smem: CTA-total table, positions, >= 2 staging rows
+  // phase 2/3 scratch in the dynamic smem: CTA-total table, positions
   const size_t scratch = (((size_t)grid * E + (size_t)upc * RS_NT * k) * 4 + 1023) & ~(size_t)1023;
-  if (scratch + 2 * (size_t)H * 2 > (size_t)EM * H * 4) return -1;
+  if (scratch > (size_t)EM * H * 4) return -1;
   // W_g as [E*H/32, 32] fp32 rows of 128 B, SWIZZLE_128B boxes of w_box_rows rows
   const int rows_per_expert = H / 32;
   int w_box_rows = 8;

@@ -38,6 +38,17 @@ __device__ __forceinline__ int4 ld_nc_v4(const void* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+// same, with an L2 eviction-priority policy (L2_EVICT_* below)
+__device__ __forceinline__ int4 ld_nc_v4_hint(const void* p, uint64_t policy) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(policy));
+  return r;
+}
+__device__ __forceinline__ void st_v4_hint(void* p, int4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(policy) : "memory");
+}
 __device__ __forceinline__ int4 ld_v4(const void* p) {
   int4 r;
   asm volatile("ld.global.v4.s32 {%0,%1,%2,%3}, [%4];"

@@ -67,8 +67,9 @@ def test_attention_fwd_rejects_bad_shapes():
 
 @pytest.mark.parametrize("s,b,g", [(256, 2, 1), (512, 1, 4)])
 def test_attention_block_own_forward_matches_library(s, b, g):
-    """AttentionBlock with the own forward kernel (+ cuDNN backward on its O / LSE) equals
-    the all-library block: output, input gradient and both weight gradients."""
+    """AttentionBlock on own kernels only (grouped tcgen05 GEMM projections, dm_attention_fwd /
+    _bwd, ragged-K wgrad) equals the all-library block (torch projections + cuDNN SDPA under
+    autograd): output, input gradient and both weight gradients, first call and accumulated."""
     from paper_2605_11005_b200.attention import AttentionBlock
 
     dev = torch.device("cuda", 0)
@@ -82,7 +83,10 @@ def test_attention_block_own_forward_matches_library(s, b, g):
         out = torch.empty_like(x)
         dx = torch.empty_like(x)
         blk.forward(0, x, out, s)
+        assert blk.last_path == ("own" if own else "library")
         blk.backward(0, dh, dx, accumulate=False)
+        blk.forward(1, x, out, s)
+        blk.backward(1, dh, dx, accumulate=True)   # weight grads: 2x
         torch.cuda.synchronize()
         res.append((out.float(), dx.float(), blk.dw_qkv.clone(), blk.dw_o.clone()))
     for a, r in zip(res[0], res[1]):
