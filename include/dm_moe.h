@@ -275,8 +275,9 @@ DM_API int dm_split3(const float* src, int groups, int rows, int cols, int layou
 DM_API int dm_attention_fwd(const void* qkv, int T, int seq_len, int nh, int nkv, int head_dim, void* out,
                             float* lse, void* stream);
 /* Its backward: dqkv [T, (nh + 2*nkv) * 128] bf16 (dQ, dK, dV in the qkv layout) from qkv, the
- * forward's out and lse, and dout [T, nh * 128]; dl_ws is a [batch, nh, seq_len] fp32
- * workspace (rowsum(dout * out)). seq_len must be a multiple of 128. Deterministic. */
+ * forward's out and lse, and dout [T, nh * 128]; dl_ws is a [2, batch, nh, seq_len] fp32
+ * workspace (rowsum(dout * out), then the log2-domain lse). seq_len must be a multiple of 128.
+ * Deterministic (no atomics). */
 DM_API int dm_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, int T,
                             int seq_len, int nh, int nkv, int head_dim, float* dl_ws, void* dqkv, void* stream);
 

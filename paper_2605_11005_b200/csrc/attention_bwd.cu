@@ -29,13 +29,13 @@
 namespace dm {
 
 constexpr int AB_THREADS = 384;
+constexpr float AB_LOG2E = 1.4426950408889634f;
 constexpr int AB_EW = 8;                                  // elementwise warps
 constexpr int AB_T = 64;                                  // streamed tile rows (queries / keys)
 constexpr int AB_STAGES = 3;                              // TMA ring depth of the streamed tiles
 constexpr uint32_t AB_ATOM64 = AB_T * 128;                // 8 KiB: 64 rows x 64 bf16 (SWIZZLE_128B)
 constexpr uint32_t AB_TILE64 = 2 * AB_ATOM64;             // 16 KiB: 64 rows x 128 d
 constexpr uint32_t AB_PT = AT_BM * 128;                   // 16 KiB: 128 rows x 64 bf16 (P / dS)
-constexpr float AB_LOG2E = 1.4426950408889634f;
 
 // K-major [64 rows x 128] tile (two 8 KiB atoms): k16 step kk of the 128-deep reduction
 __device__ __forceinline__ uint64_t ab_kmajor64(uint32_t base, int kk) {
@@ -50,10 +50,11 @@ __device__ __forceinline__ uint64_t ab_kmajor_p(uint32_t base, int kk) {
   return make_sdesc_sw128(base + kk * 32, 16, 1024);
 }
 
-// D[b][h][s] = sum_d dO[t, h, d] * O[t, h, d] (fp32): warp per (token, head)
+// D[b][h][s] = sum_d dO[t, h, d] * O[t, h, d] (fp32) and the log2-domain LSE lse2 = LSE·log2(e)
+// into the workspace [2][b][h][s] (D, then lse2): warp per (token, head)
 __global__ void __launch_bounds__(256)
-attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout, int T, int seq_len,
-                    int nh, float* __restrict__ dl) {
+attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                    const float* __restrict__ lse, int T, int seq_len, int nh, float* __restrict__ dl) {
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < T * nh; q += nw) {
@@ -65,25 +66,38 @@ attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __
     s = __fmaf_rn(bf16lo(a.y), bf16lo(b.y), s);
     s = __fmaf_rn(bf16hi(a.y), bf16hi(b.y), s);
     s = warp_sum_butterfly(s);
-    if (lane == 0) dl[((size_t)(t / seq_len) * nh + h) * seq_len + t % seq_len] = s;
+    if (lane == 0) {
+      const size_t q2 = ((size_t)(t / seq_len) * nh + h) * seq_len + t % seq_len;
+      dl[q2] = s;
+      dl[(size_t)T * nh + q2] = lse[q2] * AB_LOG2E;
+    }
   }
 }
 
 // Elementwise step of one thread = one accumulator row r (TMEM lane) over 32 columns
 // [c0, c0 + 32) of the 64-column S / dP buffers: bf16 P and dS into the row's four 16-byte
 // chunks c0/8 .. c0/8+3 of a [128 x 64] SWIZZLE_128B tile. Key-major kernel (COLS_ARE_QUERIES):
-// row = key, column = query, lse2c / ddc per column; query-major: row = query, one lse2r / ddr.
-// Causal mask: key > query, i.e. (row - col > off) key-major, (col - row > off) query-major,
-// off = the tiles' position difference; only tested when `diag`.
-template <bool COLS_ARE_QUERIES>
-__device__ __forceinline__ void ab_row32(uint32_t tS, uint32_t tP, uint32_t sPt, uint32_t sDS, int r, int c0, bool diag,
-                                         int off, const float* lse2c, const float* ddc, float lse2r, float ddr,
+// row = key, column = query, lse2c / ddc per column (smem, 16-byte aligned); query-major: row =
+// query, one lse2r / ddr. MASK (diagonal tiles only): causal key > query, i.e. (row - col > off)
+// key-major, (col - row > off) query-major, off = the tiles' position difference.
+template <bool COLS_ARE_QUERIES, bool MASK>
+__device__ __forceinline__ void ab_row32(uint32_t tS, uint32_t tP, uint32_t sPt, uint32_t sDS, int r, int c0, int off,
+                                         const float* lse2c, const float* ddc, float lse2r, float ddr,
                                          float scale_log2) {
   uint32_t s32[32], d32[32];
   tmem_ld16(tS + c0, *reinterpret_cast<uint32_t(*)[16]>(s32));
   tmem_ld16(tS + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(s32 + 16));
   tmem_ld16(tP + c0, *reinterpret_cast<uint32_t(*)[16]>(d32));
   tmem_ld16(tP + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(d32 + 16));
+  float l2v[COLS_ARE_QUERIES ? 32 : 1], ddv[COLS_ARE_QUERIES ? 32 : 1];
+  if constexpr (COLS_ARE_QUERIES) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 a = reinterpret_cast<const float4*>(lse2c + c0)[q], b = reinterpret_cast<const float4*>(ddc + c0)[q];
+      l2v[4 * q] = a.x; l2v[4 * q + 1] = a.y; l2v[4 * q + 2] = a.z; l2v[4 * q + 3] = a.w;
+      ddv[4 * q] = b.x; ddv[4 * q + 1] = b.y; ddv[4 * q + 2] = b.z; ddv[4 * q + 3] = b.w;
+    }
+  }
   tmem_wait_ld();
   uint32_t pw[16], dw[16];
 #pragma unroll
@@ -91,13 +105,13 @@ __device__ __forceinline__ void ab_row32(uint32_t tS, uint32_t tP, uint32_t sPt,
     float p2[2], ds2[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const int c = c0 + 2 * q + u;
-      const float l2 = COLS_ARE_QUERIES ? lse2c[c] : lse2r;
-      const float dv = COLS_ARE_QUERIES ? ddc[c] : ddr;
-      const bool masked = diag && (COLS_ARE_QUERIES ? (r - c > off) : (c - r > off));
-      const float p = masked ? 0.f : ex2(__fmaf_rn(__uint_as_float(s32[2 * q + u]), scale_log2, -l2));
+      const int cc = 2 * q + u, c = c0 + cc;
+      const float l2 = COLS_ARE_QUERIES ? l2v[cc] : lse2r;
+      const float dv = COLS_ARE_QUERIES ? ddv[cc] : ddr;
+      float p = ex2(__fmaf_rn(__uint_as_float(s32[cc]), scale_log2, -l2));
+      if constexpr (MASK) p = (COLS_ARE_QUERIES ? (r - c > off) : (c - r > off)) ? 0.f : p;
       p2[u] = p;
-      ds2[u] = p * (__uint_as_float(d32[2 * q + u]) - dv);
+      ds2[u] = p * (__uint_as_float(d32[cc]) - dv);
     }
     pw[q] = pack_bf16(p2[0], p2[1]);
     dw[q] = pack_bf16(ds2[0], ds2[1]);
@@ -129,13 +143,17 @@ __device__ __forceinline__ void ab_store_acc(uint32_t tacc, int c0, float sc, bo
 
 // smem carve-up shared by both kernels' host sizing
 constexpr size_t AB_SMEM_DKDV = 1024 + 2 * (size_t)AT_TILE + AB_STAGES * 2 * (size_t)AB_TILE64 + 4 * (size_t)AB_PT +
-                                4 * AB_T * sizeof(float) + 256;
+                                AB_STAGES * 2 * AB_T * sizeof(float) + 256;
 constexpr size_t AB_SMEM_DQ = 1024 + 2 * (size_t)AT_TILE + AB_STAGES * 2 * (size_t)AB_TILE64 + 2 * (size_t)AB_PT + 256;
+
+// smem descriptor + a byte offset (the 14-bit address field holds addr >> 4; tiles sit below
+// 256 KiB, so the add never carries out of it)
+__device__ __forceinline__ uint64_t dsc(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
 
 // dK_j, dV_j: CTA (128-key tile j = blockIdx.x (heaviest first), KV head, sequence)
 __global__ void __launch_bounds__(AB_THREADS, 1)
 attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmkv, const __grid_constant__ CUtensorMap tmq,
-                     const __grid_constant__ CUtensorMap tmdo, const float* __restrict__ lse,
+                     const __grid_constant__ CUtensorMap tmdo, const float* __restrict__ lse2,
                      const float* __restrict__ dl, int seq_len, int nh, int nkv, float scale_log2, float scale,
                      __nv_bfloat16* __restrict__ dqkv) {
   extern __shared__ uint8_t smem_raw[];
@@ -147,11 +165,11 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmkv, const __grid_cons
   uint8_t* sDO = sQ + AB_STAGES * AB_TILE64;                    // [AB_STAGES] x 16 KiB
   uint8_t* sPt = sDO + AB_STAGES * AB_TILE64;                   // [2] x 16 KiB
   uint8_t* sDSt = sPt + 2 * AB_PT;                              // [2] x 16 KiB
-  float* s_lse = reinterpret_cast<float*>(sDSt + 2 * AB_PT);    // [2][64]
-  float* s_dd = s_lse + 2 * AB_T;                               // [2][64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dd + 2 * AB_T);
+  float* s_lse = reinterpret_cast<float*>(sDSt + 2 * AB_PT);    // [AB_STAGES][64] log2-domain LSE of Q_i's rows
+  float* s_dd = s_lse + AB_STAGES * AB_T;                       // [AB_STAGES][64] D of Q_i's rows
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dd + AB_STAGES * AB_T);
   uint64_t* kv_full = bars;
-  uint64_t* ld_full = bars + 1;                  // [AB_STAGES]
+  uint64_t* ld_full = bars + 1;                  // [AB_STAGES] Q_i, dO_i, lse2, D landed
   uint64_t* ld_empty = ld_full + AB_STAGES;      // [AB_STAGES]
   uint64_t* st_full = ld_empty + AB_STAGES;      // [2] S^T / dP^T buffer b computed
   uint64_t* tm_empty = st_full + 2;              // [2] ... read out of TMEM
@@ -204,13 +222,16 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmkv, const __grid_cons
         if (it >= AB_STAGES) mbar_wait(&ld_empty[s], (uint32_t)((it / AB_STAGES - 1) & 1));
         const int qh = kvh * g + it / per_head, i = 2 * j + it % per_head;
         const int qrow = row0 + i * AB_T;
+        const size_t lrow = ((size_t)b * nh + qh) * seq_len + (size_t)i * AB_T;
         uint8_t* q = sQ + s * AB_TILE64;
         uint8_t* d = sDO + s * AB_TILE64;
-        mbar_expect_tx(&ld_full[s], 2 * AB_TILE64);
+        mbar_expect_tx(&ld_full[s], 2 * AB_TILE64 + 2 * AB_T * sizeof(float));
         tma_load_2d(q, &tmq, &ld_full[s], qh * AT_D, qrow);
         tma_load_2d(q + AB_ATOM64, &tmq, &ld_full[s], qh * AT_D + 64, qrow);
         tma_load_2d(d, &tmdo, &ld_full[s], qh * AT_D, qrow);
         tma_load_2d(d + AB_ATOM64, &tmdo, &ld_full[s], qh * AT_D + 64, qrow);
+        bulk_load_1d(s_lse + s * AB_T, lse2 + lrow, AB_T * sizeof(float), &ld_full[s]);
+        bulk_load_1d(s_dd + s * AB_T, dl + lrow, AB_T * sizeof(float), &ld_full[s]);
       }
     }
     __syncwarp();
@@ -218,19 +239,22 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmkv, const __grid_cons
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(AT_BN, AB_T, 0, 0);   // M = 128 keys, N = 64 queries
       constexpr uint32_t idesc_a = make_idesc_bf16(AT_BN, AT_D, 0, 1);   // M = 128 keys, N = d, B MN-major
-      const uint32_t ka = smem_u32(sK), va = smem_u32(sV);
+      const uint64_t dk0 = at_kmajor(smem_u32(sK), 0), dv0 = at_kmajor(smem_u32(sV), 0);
+      const uint64_t dq0 = ab_kmajor64(smem_u32(sQ), 0), ddo0 = ab_kmajor64(smem_u32(sDO), 0);
+      const uint64_t mq0 = ab_mnmajor64(smem_u32(sQ), 0), mdo0 = ab_mnmajor64(smem_u32(sDO), 0);
+      const uint64_t dp0 = ab_kmajor_p(smem_u32(sPt), 0), dds0 = ab_kmajor_p(smem_u32(sDSt), 0);
       auto dvdk = [&](int q) {   // dV += P^T dO_q, dK += dS^T Q_q
         const int s = q % AB_STAGES, pb = q & 1;
         mbar_wait(&p_full[pb], (uint32_t)((q >> 1) & 1));
         tc_fence_after();
-        const uint32_t pa = smem_u32(sPt + pb * AB_PT), dsa = smem_u32(sDSt + pb * AB_PT);
-        const uint32_t qa = smem_u32(sQ + s * AB_TILE64), da = smem_u32(sDO + s * AB_TILE64);
+        const uint64_t pa = dsc(dp0, pb * AB_PT), dsa = dsc(dds0, pb * AB_PT);
+        const uint64_t qb = dsc(mq0, s * AB_TILE64), db = dsc(mdo0, s * AB_TILE64);
 #pragma unroll
         for (int kk = 0; kk < AB_T / 16; ++kk)
-          umma_bf16_ss(tmem + 256, ab_kmajor_p(pa, kk), ab_mnmajor64(da, kk), idesc_a, (q | kk) ? 1u : 0u);
+          umma_bf16_ss(tmem + 256, dsc(pa, kk * 32), dsc(db, kk * 2048), idesc_a, (q | kk) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < AB_T / 16; ++kk)
-          umma_bf16_ss(tmem + 384, ab_kmajor_p(dsa, kk), ab_mnmajor64(qa, kk), idesc_a, (q | kk) ? 1u : 0u);
+          umma_bf16_ss(tmem + 384, dsc(dsa, kk * 32), dsc(qb, kk * 2048), idesc_a, (q | kk) ? 1u : 0u);
         umma_commit(&ld_empty[s]);
         umma_commit(&ps_empty[pb]);
       };
@@ -240,14 +264,18 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmkv, const __grid_cons
         mbar_wait(&ld_full[s], (uint32_t)((it / AB_STAGES) & 1));
         if (it >= 2) mbar_wait(&tm_empty[tb], (uint32_t)(((it >> 1) - 1) & 1));
         tc_fence_after();
-        const uint32_t qa = smem_u32(sQ + s * AB_TILE64), da = smem_u32(sDO + s * AB_TILE64);
+        const uint64_t qa = dsc(dq0, s * AB_TILE64), da = dsc(ddo0, s * AB_TILE64);
         const uint32_t ts = tmem + tb * 128;
 #pragma unroll
-        for (int kk = 0; kk < AT_D / 16; ++kk)                             // S^T = K_j Q_i^T
-          umma_bf16_ss(ts, at_kmajor(ka, kk), ab_kmajor64(qa, kk), idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < AT_D / 16; ++kk) {                           // S^T = K_j Q_i^T
+          const uint32_t ko = (kk >> 2) * AT_ATOM + (kk & 3) * 32, qo = (kk >> 2) * AB_ATOM64 + (kk & 3) * 32;
+          umma_bf16_ss(ts, dsc(dk0, ko), dsc(qa, qo), idesc_s, kk > 0 ? 1u : 0u);
+        }
 #pragma unroll
-        for (int kk = 0; kk < AT_D / 16; ++kk)                             // dP^T = V_j dO_i^T
-          umma_bf16_ss(ts + 64, at_kmajor(va, kk), ab_kmajor64(da, kk), idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < AT_D / 16; ++kk) {                           // dP^T = V_j dO_i^T
+          const uint32_t ko = (kk >> 2) * AT_ATOM + (kk & 3) * 32, qo = (kk >> 2) * AB_ATOM64 + (kk & 3) * 32;
+          umma_bf16_ss(ts + 64, dsc(dv0, ko), dsc(da, qo), idesc_s, kk > 0 ? 1u : 0u);
+        }
         umma_commit(&st_full[tb]);
         if (it >= 1) dvdk(it - 1);
       }
@@ -258,25 +286,21 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmkv, const __grid_cons
   } else if (warp >= 4) {
     const int q4 = warp & 3, half = (warp - 4) >> 2;
     const int r = q4 * 32 + lane;                                           // key row = TMEM lane
-    const int et = (warp - 4) * 32 + lane;                                  // 0..255
     const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     for (int it = 0; it < n_it; ++it) {
-      const int qh = kvh * g + it / per_head, i = 2 * j + it % per_head;
-      const int tb = it & 1;
-      float* l2 = s_lse + tb * AB_T;
-      float* dd = s_dd + tb * AB_T;
-      if (et < AB_T) {
-        const size_t lrow = ((size_t)b * nh + qh) * seq_len + (size_t)i * AB_T + et;
-        l2[et] = lse[lrow] * AB_LOG2E;                                      // query et of tile i
-        dd[et] = dl[lrow];
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      mbar_wait(&st_full[tb], (uint32_t)((it >> 1) & 1));
+      const int i = 2 * j + it % per_head;
+      const int tb = it & 1, s = it % AB_STAGES;
+      mbar_wait(&st_full[tb], (uint32_t)((it >> 1) & 1));                  // (implies ld_full of stage s)
       tc_fence_after();
       if (it >= 2) mbar_wait(&ps_empty[tb], (uint32_t)(((it >> 1) - 1) & 1));   // P^T / dS^T smem free
       const int off = i * AB_T - j * AT_BN;                                 // query tile start - key tile start
-      ab_row32<true>(trow + tb * 128, trow + tb * 128 + 64, smem_u32(sPt + tb * AB_PT), smem_u32(sDSt + tb * AB_PT), r,
-                     half * 32, off < AT_BN, off, l2, dd, 0.f, 0.f, scale_log2);
+      const uint32_t tS = trow + tb * 128, pP = smem_u32(sPt + tb * AB_PT), pD = smem_u32(sDSt + tb * AB_PT);
+      if (off < AT_BN)
+        ab_row32<true, true>(tS, tS + 64, pP, pD, r, half * 32, off, s_lse + s * AB_T, s_dd + s * AB_T, 0.f, 0.f,
+                             scale_log2);
+      else
+        ab_row32<true, false>(tS, tS + 64, pP, pD, r, half * 32, off, s_lse + s * AB_T, s_dd + s * AB_T, 0.f, 0.f,
+                              scale_log2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tm_empty[tb]);
@@ -300,7 +324,7 @@ attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmkv, const __grid_cons
 // dQ_i: CTA (128-query tile i = n_t-1-blockIdx.x (heaviest first), query head, sequence)
 __global__ void __launch_bounds__(AB_THREADS, 1)
 attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmdo,
-                   const __grid_constant__ CUtensorMap tmkv, const float* __restrict__ lse,
+                   const __grid_constant__ CUtensorMap tmkv, const float* __restrict__ lse2,
                    const float* __restrict__ dl, int seq_len, int nh, int nkv, float scale_log2, float scale,
                    __nv_bfloat16* __restrict__ dqkv) {
   extern __shared__ uint8_t smem_raw[];
@@ -380,15 +404,17 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(AT_BM, AB_T, 0, 0);   // M = 128 queries, N = 64 keys
       constexpr uint32_t idesc_a = make_idesc_bf16(AT_BM, AT_D, 0, 1);   // dQ: N = d, B (K_j) MN-major
-      const uint32_t qa = smem_u32(sQ), da = smem_u32(sDO);
+      const uint64_t dq0 = at_kmajor(smem_u32(sQ), 0), ddo0 = at_kmajor(smem_u32(sDO), 0);
+      const uint64_t dk0 = ab_kmajor64(smem_u32(sK), 0), dv0 = ab_kmajor64(smem_u32(sV), 0);
+      const uint64_t mk0 = ab_mnmajor64(smem_u32(sK), 0), dds0 = ab_kmajor_p(smem_u32(sDS), 0);
       auto dq_step = [&](int q) {   // dQ += dS K_q
         const int s = q % AB_STAGES, pb = q & 1;
         mbar_wait(&p_full[pb], (uint32_t)((q >> 1) & 1));
         tc_fence_after();
-        const uint32_t dsa = smem_u32(sDS + pb * AB_PT), ka = smem_u32(sK + s * AB_TILE64);
+        const uint64_t dsa = dsc(dds0, pb * AB_PT), kb = dsc(mk0, s * AB_TILE64);
 #pragma unroll
         for (int kk = 0; kk < AB_T / 16; ++kk)
-          umma_bf16_ss(tmem + 256, ab_kmajor_p(dsa, kk), ab_mnmajor64(ka, kk), idesc_a, (q | kk) ? 1u : 0u);
+          umma_bf16_ss(tmem + 256, dsc(dsa, kk * 32), dsc(kb, kk * 2048), idesc_a, (q | kk) ? 1u : 0u);
         umma_commit(&kv_empty[s]);
         umma_commit(&ds_empty[pb]);
       };
@@ -398,14 +424,18 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
         mbar_wait(&kv_full[s], (uint32_t)((jt / AB_STAGES) & 1));
         if (jt >= 2) mbar_wait(&tm_empty[tb], (uint32_t)(((jt >> 1) - 1) & 1));
         tc_fence_after();
-        const uint32_t ka = smem_u32(sK + s * AB_TILE64), va = smem_u32(sV + s * AB_TILE64);
+        const uint64_t ka = dsc(dk0, s * AB_TILE64), va = dsc(dv0, s * AB_TILE64);
         const uint32_t ts = tmem + tb * 128;
 #pragma unroll
-        for (int kk = 0; kk < AT_D / 16; ++kk)                             // S = Q_i K_j^T
-          umma_bf16_ss(ts, at_kmajor(qa, kk), ab_kmajor64(ka, kk), idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < AT_D / 16; ++kk) {                           // S = Q_i K_j^T
+          const uint32_t qo = (kk >> 2) * AT_ATOM + (kk & 3) * 32, ko = (kk >> 2) * AB_ATOM64 + (kk & 3) * 32;
+          umma_bf16_ss(ts, dsc(dq0, qo), dsc(ka, ko), idesc_s, kk > 0 ? 1u : 0u);
+        }
 #pragma unroll
-        for (int kk = 0; kk < AT_D / 16; ++kk)                             // dP = dO_i V_j^T
-          umma_bf16_ss(ts + 64, at_kmajor(da, kk), ab_kmajor64(va, kk), idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < AT_D / 16; ++kk) {                           // dP = dO_i V_j^T
+          const uint32_t qo = (kk >> 2) * AT_ATOM + (kk & 3) * 32, ko = (kk >> 2) * AB_ATOM64 + (kk & 3) * 32;
+          umma_bf16_ss(ts + 64, dsc(ddo0, qo), dsc(va, ko), idesc_s, kk > 0 ? 1u : 0u);
+        }
         umma_commit(&s_full[tb]);
         if (jt >= 1) dq_step(jt - 1);
       }
@@ -418,15 +448,18 @@ attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
     const int r = q4 * 32 + lane;                                           // query row = TMEM lane
     const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     const size_t lrow = ((size_t)b * nh + h) * seq_len + (size_t)i * AT_BM + r;
-    const float l2 = lse[lrow] * AB_LOG2E, dd = dl[lrow];
+    const float l2 = lse2[lrow], dd = dl[lrow];
     for (int jt = 0; jt < nj; ++jt) {
       const int tb = jt & 1;
       mbar_wait(&s_full[tb], (uint32_t)((jt >> 1) & 1));
       tc_fence_after();
       if (jt >= 2) mbar_wait(&ds_empty[tb], (uint32_t)(((jt >> 1) - 1) & 1));   // dS smem free
       const int off = i * AT_BM - jt * AB_T;                                // query tile start - key tile start
-      ab_row32<false>(trow + tb * 128, trow + tb * 128 + 64, 0u, smem_u32(sDS + tb * AB_PT), r, half * 32, off < AB_T,
-                      off, nullptr, nullptr, l2, dd, scale_log2);
+      const uint32_t tS = trow + tb * 128, pD = smem_u32(sDS + tb * AB_PT);
+      if (off < AB_T)
+        ab_row32<false, true>(tS, tS + 64, 0u, pD, r, half * 32, off, nullptr, nullptr, l2, dd, scale_log2);
+      else
+        ab_row32<false, false>(tS, tS + 64, 0u, pD, r, half * 32, off, nullptr, nullptr, l2, dd, scale_log2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tm_empty[tb]);
@@ -486,21 +519,22 @@ int dm_attention_bwd(const void* qkv, const void* out, const void* dout, const f
   int blocks = (T * nh + 7) / 8;
   if (blocks > num_sms_current() * 8) blocks = num_sms_current() * 8;
   attn_bwd_dot_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(out),
-                                              reinterpret_cast<const __nv_bfloat16*>(dout), T, seq_len, nh, dl_ws);
+                                              reinterpret_cast<const __nv_bfloat16*>(dout), lse, T, seq_len, nh, dl_ws);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "attention_bwd dot launch");
   note_launch();
   const float scale = 1.0f / sqrtf((float)AT_D), scale_log2 = AB_LOG2E * scale;
+  const float* lse2 = dl_ws + (size_t)T * nh;   // written by the dot kernel
   if ((rc = ensure_smem_attr((const void*)attn_bwd_dkdv_kernel, (int)AB_SMEM_DKDV, "cudaFuncSetAttribute(attn_bwd_dkdv)")))
     return rc;
   if ((rc = ensure_smem_attr((const void*)attn_bwd_dq_kernel, (int)AB_SMEM_DQ, "cudaFuncSetAttribute(attn_bwd_dq)")))
     return rc;
   __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dqkv);
-  attn_bwd_dkdv_kernel<<<dim3(n_t, nkv, nb), AB_THREADS, AB_SMEM_DKDV, st>>>(tm128, tm64, tmdo64, lse, dl_ws, seq_len,
+  attn_bwd_dkdv_kernel<<<dim3(n_t, nkv, nb), AB_THREADS, AB_SMEM_DKDV, st>>>(tm128, tm64, tmdo64, lse2, dl_ws, seq_len,
                                                                               nh, nkv, scale_log2, scale, d);
   if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "attention_bwd dkdv launch");
   note_launch();
-  attn_bwd_dq_kernel<<<dim3(n_t, nh, nb), AB_THREADS, AB_SMEM_DQ, st>>>(tm128, tmdo128, tm64, lse, dl_ws, seq_len, nh,
+  attn_bwd_dq_kernel<<<dim3(n_t, nh, nb), AB_THREADS, AB_SMEM_DQ, st>>>(tm128, tmdo128, tm64, lse2, dl_ws, seq_len, nh,
                                                                          nkv, scale_log2, scale, d);
   if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "attention_bwd dq launch");
   note_launch();

@@ -309,6 +309,7 @@ def attention_bwd(qkv, out, dout, lse, seq_len, nh, nkv, dqkv, dl_ws=None, strea
     _check(lse, F32, (T // seq_len, nh, seq_len), "lse")
     _check(dqkv, BF16, (T, (nh + 2 * nkv) * 128), "dqkv")
     if dl_ws is None:
-        dl_ws = torch.empty(T // seq_len, nh, seq_len, dtype=F32, device=qkv.device)
+        dl_ws = torch.empty(2, T // seq_len, nh, seq_len, dtype=F32, device=qkv.device)
+    _check(dl_ws, F32, (2, T // seq_len, nh, seq_len), "dl_ws")
     _lib.call("dm_attention_bwd", _ptr(qkv), _ptr(out), _ptr(dout), _ptr(lse), T, seq_len, nh, nkv, 128,
               _ptr(dl_ws), _ptr(dqkv), _stream(stream))

@@ -33,7 +33,7 @@ for s in (2048, 4096, 8192):
     lse = torch.empty(b, nh, s, dtype=torch.float32, device="cuda")
     K.attention_fwd(qkv, s, nh, nkv, out, lse)
     dqkv = torch.empty_like(qkv)
-    dl = torch.empty(b, nh, s, dtype=torch.float32, device="cuda")
+    dl = torch.empty(2, b, nh, s, dtype=torch.float32, device="cuda")
     own = t(lambda: K.attention_bwd(qkv, out, dout, lse, s, nh, nkv, dqkv, dl))
     x = qkv.view(b, s, nh + 2 * nkv, D).transpose(1, 2)
     q, k, v = x[:, :nh], x[:, nh:nh + nkv], x[:, nh + nkv:]
