@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <utility>
 
@@ -73,11 +74,13 @@ int ensure_smem_attr(const void* func, int bytes, const char* what) {
 
 int max_active_blocks(const void* func, int threads, size_t smem) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, int>, int> cache;   // (kernel, device) -> blocks per SM
+  // (kernel, device, threads, dynamic smem) -> blocks per SM. Query after the kernel's
+  // dynamic-smem attribute is raised (ensure_smem_attr): above 48 KB the query fails before.
+  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 1;
   std::lock_guard<std::mutex> lk(mu);
-  auto key = std::make_pair(func, dev);
+  auto key = std::make_tuple(func, dev, threads, smem);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int n = 0;

@@ -49,23 +49,60 @@ combine_fwd_kernel(const __nv_bfloat16* __restrict__ y_perm, const int32_t* __re
     float wt[DM_KT_ARRAY];
 #pragma unroll
     for (int j = 0; j < k; ++j) { pos[j] = row_map[(size_t)t * k + j]; wt[j] = w[(size_t)t * k + j]; }
-#pragma unroll 4
-    for (int ch = lane; ch < nvec; ch += 32) {
-      float acc[8];
-      if (resid) {
-        unpack8(ld_nc_v4(resid + (size_t)t * H + ch * 8), acc);
-      } else {
+    if constexpr (KT > 0) {
+      // U chunks per lane: every gather of the batch is issued before the first store (a
+      // store's memory clobber would otherwise hold the next chunk's loads behind it, leaving
+      // one chunk in flight per lane)
+      constexpr int U = KT >= 8 ? 1 : 8 / KT;
+      for (int c0 = lane; c0 < nvec; c0 += 32 * U) {
+        int4 v[U][KT], rv[U];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+        for (int u = 0; u < U; ++u) {
+          const int ch = c0 + 32 * u;
+          const bool ok = ch < nvec;
+#pragma unroll
+          for (int j = 0; j < KT; ++j)
+            v[u][j] = ok ? ld_nc_v4(y_perm + (size_t)pos[j] * H + ch * 8) : make_int4(0, 0, 0, 0);
+          rv[u] = ok && resid ? ld_nc_v4(resid + (size_t)t * H + ch * 8) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int ch = c0 + 32 * u;
+          if (ch >= nvec) break;
+          float acc[8];
+          if (resid) {
+            unpack8(rv[u], acc);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+          }
+#pragma unroll
+          for (int j = 0; j < KT; ++j) {
+            float f[8];
+            unpack8(v[u][j], f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(wt[j], f[i], acc[i]);
+          }
+          st_v4(y + (size_t)t * H + ch * 8, pack8(acc));
+        }
       }
+    } else {
+      for (int ch = lane; ch < nvec; ch += 32) {
+        float acc[8];
+        if (resid) {
+          unpack8(ld_nc_v4(resid + (size_t)t * H + ch * 8), acc);
+        } else {
 #pragma unroll
-      for (int j = 0; j < k; ++j) {
-        float f[8];
-        unpack8(ld_nc_v4(y_perm + (size_t)pos[j] * H + ch * 8), f);
+          for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+        }
+        for (int j = 0; j < k; ++j) {
+          float f[8];
+          unpack8(ld_nc_v4(y_perm + (size_t)pos[j] * H + ch * 8), f);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(wt[j], f[i], acc[i]);
+          for (int i = 0; i < 8; ++i) acc[i] = __fmaf_rn(wt[j], f[i], acc[i]);
+        }
+        st_v4(y + (size_t)t * H + ch * 8, pack8(acc));
       }
-      st_v4(y + (size_t)t * H + ch * 8, pack8(acc));
     }
   }
 }
@@ -213,14 +250,19 @@ permute_bwd_smem_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t
   constexpr int KK = KT ? KT : 1;   // staged gathers per token (runtime k falls back to a loop)
   for (int t0 = (blockIdx.y * 8 + warp) * PBWD_TG; t0 < T; t0 += nw * PBWD_TG) {
     // stage 1: every token's indices, then all TG * k row gathers in flight at once
-    int pos[PBWD_TG][KK];
+    int pos[PBWD_TG][KK], ex[PBWD_TG][KK];
+    float dlv[PBWD_TG][KK];
     int4 v[PBWD_TG][KK];
     int4 rv[PBWD_TG];
 #pragma unroll
     for (int u = 0; u < PBWD_TG; ++u) {
       const int t = min(t0 + u, T - 1);
 #pragma unroll
-      for (int j = 0; j < KK; ++j) pos[u][j] = KT ? row_map[(size_t)t * k + j] : 0;
+      for (int j = 0; j < KK; ++j) {
+        pos[u][j] = KT ? row_map[(size_t)t * k + j] : 0;
+        ex[u][j] = KT && dlogit ? idx[(size_t)t * k + j] : 0;          // with the row indices, not
+        dlv[u][j] = KT && dlogit ? dlogit[(size_t)t * k + j] : 0.0f;   // after this group's stores
+      }
     }
 #pragma unroll
     for (int u = 0; u < PBWD_TG; ++u) {
@@ -253,8 +295,8 @@ permute_bwd_smem_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t
       }
       if (dlogit) {
         for (int j = 0; j < k; ++j) {
-          const int e = idx[(size_t)t * k + j];
-          const float dl = dlogit[(size_t)t * k + j];
+          const int e = KT ? ex[u][KT ? j : 0] : idx[(size_t)t * k + j];
+          const float dl = KT ? dlv[u][KT ? j : 0] : dlogit[(size_t)t * k + j];
           const float4 a = ws[e * 64 + lane * 2], b = ws[e * 64 + lane * 2 + 1];
           acc[0] = __fmaf_rn(dl, a.x, acc[0]); acc[1] = __fmaf_rn(dl, a.y, acc[1]);
           acc[2] = __fmaf_rn(dl, a.z, acc[2]); acc[3] = __fmaf_rn(dl, a.w, acc[3]);
@@ -293,9 +335,17 @@ router_wgrad_reg_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __re
   const bool live = col < H;
   const int tb = blockIdx.y;
   const int t_beg = tb * tb_tokens, t_end = min(T, t_beg + tb_tokens);
+  // ring of RWR_DEPTH prefetched x vectors (tokens warp, warp+NW, ...), issued before the
+  // idx / dlogit staging so the two load latencies overlap
+  int4 xv[RWR_DEPTH];
+#pragma unroll
+  for (int d = 0; d < RWR_DEPTH; ++d) {
+    const int t = t_beg + warp + d * NW;
+    xv[d] = live && t < t_end ? ld_nc_v4(x + (size_t)t * H + col) : make_int4(0, 0, 0, 0);
+  }
   // the token block's expert ids and dlogits: one coalesced pass into smem
   int* s_idx = reinterpret_cast<int*>(red + NW * EM * 8 * 32);
-  float* s_dl = reinterpret_cast<float*>(s_idx + RWR_MAX_TB * DM_MAX_TOPK);
+  float* s_dl = reinterpret_cast<float*>(s_idx + tb_tokens * k);
   for (int q = threadIdx.x; q < (t_end - t_beg) * k; q += blockDim.x) {
     s_idx[q] = idx[(size_t)t_beg * k + q];
     s_dl[q] = dlogit[(size_t)t_beg * k + q];
@@ -307,13 +357,6 @@ router_wgrad_reg_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __re
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[e][i] = 0.0f;
   if (live) {
-    // ring of RWR_DEPTH prefetched x vectors (tokens warp, warp+NW, ...)
-    int4 xv[RWR_DEPTH];
-#pragma unroll
-    for (int d = 0; d < RWR_DEPTH; ++d) {
-      const int t = t_beg + warp + d * NW;
-      xv[d] = t < t_end ? ld_nc_v4(x + (size_t)t * H + col) : make_int4(0, 0, 0, 0);
-    }
     for (int t0 = t_beg + warp; t0 < t_end; t0 += RWR_DEPTH * NW) {
 #pragma unroll
       for (int d = 0; d < RWR_DEPTH; ++d) {
@@ -636,12 +679,17 @@ int dm_router_wgrad(const void* x, const int32_t* idx, const float* dlogit, int 
     // segment tickets follow the partial blocks in the workspace (after the sorted kernel's)
     unsigned* tickets = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(partial_ws) + (size_t)ntb * E * H * 4) +
                         (size_t)((H + 1023) / 1024) * E;
-    const size_t stage = (size_t)RWR_MAX_TB * DM_MAX_TOPK * 8;   // idx + dlogit of a token block
+    // idx + dlogit of a token block (<= RWR_MAX_TB tokens) after the cross-warp reduction
+    // buffer: sized for this k, so two CTAs fit per SM (the DM_MAX_TOPK-sized stage held the
+    // kernel to one CTA of 8 warps per SM: latency bound)
+    const size_t stage = (size_t)RWR_MAX_TB * k * 8;
     const size_t sm8 = 8 * 8 * 8 * 32 * 4 + stage, sm16 = 4 * 16 * 8 * 32 * 4 + stage;
     const void* k8 = (const void*)router_wgrad_reg_kernel<8, 2>;
     const void* k16 = (const void*)router_wgrad_reg_kernel<16, 2>;
-    const int occ8 = max_active_blocks(k8, 256, sm8);
-    const int occ16 = max_active_blocks(k16, 128, sm16);
+    if (int rc = ensure_smem_attr(E <= 8 ? k8 : k16, (int)(E <= 8 ? sm8 : sm16), "cudaFuncSetAttribute(router_wgrad_reg)"))
+      return rc;
+    const int occ8 = E <= 8 ? max_active_blocks(k8, 256, sm8) : 1;
+    const int occ16 = E <= 8 ? 1 : max_active_blocks(k16, 128, sm16);
     // One wave: as many token blocks as the resident CTA slots allow per column chunk
     // (never more than the workspace's ntb), each a contiguous run of tbt tokens.
     const int gx = (H / 8 + 31) / 32;
