@@ -162,11 +162,15 @@ def cpu_baseline(shape, tokens: int | None = None, layer=None, layers: int = 1, 
     T = min(shape.T, tokens or CPU_SAMPLE_TOKENS)
     x = O.f32_to_bf16_bits(rng.standard_normal((T, H), dtype=np.float32))
     dy = O.round_bf16(rng.standard_normal((T, H), dtype=np.float32))
-    t0 = time.perf_counter()
-    for _ in range(layers):
-        f = O.moe_forward(x, wg, w1, w3, w2, k, dtype=np.float32)
-        O.moe_backward(f, x, wg, w1, w3, w2, dy, dtype=np.float32)
-    dt = time.perf_counter() - t0
+    # every host thread for BLAS, whatever OMP_NUM_THREADS says (torchrun sets it to 1)
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=threads):
+        t0 = time.perf_counter()
+        for _ in range(layers):
+            f = O.moe_forward(x, wg, w1, w3, w2, k, dtype=np.float32)
+            O.moe_backward(f, x, wg, w1, w3, w2, dy, dtype=np.float32)
+        dt = time.perf_counter() - t0
     return {"value": T / dt, "unit": UNIT, "cores": threads, "kind": "port", "tokens": T, "seconds": round(dt, 3),
             "sample": f"{T} of the {shape.T} tokens of one micro-batch, full fwd+bwd of {layers} layer(s) "
                       f"(H={H}, E={E}, k={k}, D_e={De}), numpy fp32 BLAS oracle on {threads} threads, "
@@ -669,7 +673,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                                + ("attention + " if args.attention else "") + "routing/combine, F: EP experts)",
                 "layer": "attention + residual MoE block (attention: own kernels)" if args.attention
                          else "MoE block",
-                "transport": "NCCL send/recv (torch.distributed P2P) over NVLink, one communicator per direction",
+                "transport": "NCCL send/recv (torch.distributed P2P) over NVLink",
                 "launch": ("one CUDA graph per rank per iteration (kernels + NCCL P2P + W pass)" if graph is not None
                            else "eager (data-dependent message sizes: host reads the counts headers)"),
                 "weights": "random-init", "l2": "inputs+weights larger than L2",

@@ -813,7 +813,7 @@ class AFPipeRank:
                         self.tx.all_reduce(g, self.a_group)
 
     def init_groups(self):
-        """Create the transport's two direction communicators and the per-pipeline-group
+        """Set up the transport and create the per-pipeline-group
         A communicators (collective: every rank calls new_group for every group, in the
         same order)."""
         self.tx.setup(self.topo.world)

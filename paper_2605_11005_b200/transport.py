@@ -8,11 +8,11 @@ SPEC.md:362) — and the paper runs them on dedicated send/recv process groups
 (PAPER.md:266). Two implementations share one interface:
 
 * `NcclTransport` (the product, one process per GPU): NCCL point-to-point over
-  NVLink 5 / NVSwitch through torch.distributed. A->F traffic (M2N, M2N_b, the
-  forward residual hop A2A) and F->A traffic (N2M, N2M_b, A2A_b) run on two
-  communicators of their own, so each direction has its own NCCL stream and an
-  N2M receive never queues behind an M2N send that is still waiting for its data
-  (a single communicator serialises both directions on one stream).
+  NVLink 5 / NVSwitch through torch.distributed, both directions on one communicator.
+  (One communicator per direction was tried: it deadlocked the Mixtral-size 1:1
+  exchange, eager and graph-captured alike, and slowed the 2:2 / 1:3 F ranks by
+  ~15%; `scripts/diag_n2.sh`. NCCL progresses one communicator's operations in issue
+  order, which is the order both ends agree on.)
 * `LoopbackTransport` (one process, one GPU): every rank is a host thread with its
   own CUDA streams; a send and its matching receive meet in a `LoopbackHub`, which
   issues the device-to-device copy on a per-(src, dst, direction) lane stream once
@@ -49,17 +49,10 @@ class NcclTransport:
     """torch.distributed P2P (NCCL on CUDA tensors, gloo in the CPU tests)."""
 
     def __init__(self):
-        self._dir_groups: dict[str, object] = {}
         self._fast: dict[int, object] = {}
 
     def setup(self, world: int) -> None:
-        """Create the two direction communicators (collective: every rank calls it, in
-        the same order as its other new_group calls)."""
-        if self._dir_groups or not dist.is_initialized():
-            return
-        ranks = list(range(world))
-        for d in (AF, FA):
-            self._dir_groups[d] = dist.new_group(ranks)
+        """Nothing to create: every exchange runs on the default process group."""
 
     def new_group(self, ranks):
         return dist.new_group(list(ranks))
@@ -77,17 +70,17 @@ class NcclTransport:
     def exchange(self, ops: list[tuple[str, torch.Tensor, int]], direction: str = AF):
         """One coalesced group of P2P ops on the current stream; returns the works.
 
-        On CUDA tensors the group is issued straight on the direction's ProcessGroup
+        On CUDA tensors the group is issued straight on the default ProcessGroup
         (_start_coalescing / send / recv / _end_coalescing — what batch_isend_irecv does,
         without its per-op Python validation, which dominated small-shape iterations);
         other backends use the public batch_isend_irecv."""
         ops = [o for o in ops if o[1].numel() > 0]
         if not ops:
             return []
-        group = self._dir_groups.get(direction)
+        group = None
         dev = ops[0][1].device
         if dev.type == "cuda":
-            pg = group if group is not None else dist.distributed_c10d._get_default_group()
+            pg = dist.distributed_c10d._get_default_group()
             fast = self._coalescing_pg(pg, dev)
             if fast:
                 fast._start_coalescing(dev)
