@@ -9,7 +9,7 @@ runN 2 > $O/bench_mixtral_n2_afpipe.json
 runN 2 --config configs/tiny.yaml > $O/bench_tiny_n2_afpipe_2layers.json
 runN 4 > $O/bench_mixtral_n4_2a2f.json
 runN 4 --n-attn 1 > $O/bench_mixtral_n4_1a3f.json
-runN 2 --impl reference > $O/bench_reference_arm_n2.json
+runN 2 --impl reference --steps 3 --warmup 1 > $O/bench_reference_arm_n2.json
 timeout 900 python -m pytest tests/test_runtime_gpu.py -q 2>&1 | tail -3 > $O/test_runtime_gpu_4gpu.txt
 for f in $O/bench_*n2*.json $O/bench_*n4*.json; do python -c "
 import json
