@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--workload", required=True)
     ap.add_argument("--config", default=None)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--kernel-regex", default="grouped_gemm", help="launches to count (a step's full list also "
+                    "holds the A-side kernels)")
     a = ap.parse_args()
     rows = [r for r in csv.reader(open(a.csv)) if r and not r[0].startswith("==")]
     h = rows[0]
@@ -30,7 +32,11 @@ def main():
     launches: dict = {}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
              "nsecond": 1e-9, "msecond": 1e-3, "ms": 1e-3}
+    import re
+
     for r in rows[1:]:
+        if not re.search(a.kernel_regex, r[ki]):
+            continue
         d = launches.setdefault(r[idi], {"kernel": r[ki].split("(")[0]})
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         d[r[mi]] = v
