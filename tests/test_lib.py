@@ -63,6 +63,15 @@ def test_shape_errors_are_negative_codes_without_gpu(lib):
     assert rc == -1
     with pytest.raises(_lib.DMShapeError):
         _lib.call("dm_combine_fwd", None, None, None, 4, 10, 2, None, None, None)
+    # attention: head_dim 128 only; seq_len a multiple of 128 dividing T; nh a multiple of nkv
+    rc = lib.dm_attention_bwd(None, None, None, None, 256, 256, 4, 2, 64, None, None, None)
+    assert rc == -1 and "head_dim" in _lib.last_error()
+    rc = lib.dm_attention_bwd(None, None, None, None, 300, 200, 4, 2, 128, None, None, None)
+    assert rc == -1 and "seq_len" in _lib.last_error()
+    rc = lib.dm_attention_bwd(None, None, None, None, 256, 256, 6, 4, 128, None, None, None)
+    assert rc == -1
+    rc = lib.dm_attention_fwd(None, 256, 256, 4, 2, 64, None, None, None)
+    assert rc == -1
 
 
 def test_missing_library_fails_loudly(tmp_path):
