@@ -248,22 +248,35 @@ permute_bwd_smem_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t
   if (col >= H) return;
   const int nw = gridDim.y * 8;
   constexpr int KK = KT ? KT : 1;   // staged gathers per token (runtime k falls back to a loop)
-  for (int t0 = (blockIdx.y * 8 + warp) * PBWD_TG; t0 < T; t0 += nw * PBWD_TG) {
-    // stage 1: every token's indices, then all TG * k row gathers in flight at once
+  // a group's indices (row_map, idx, dlogit) are loaded one group ahead, so its row gathers
+  // issue without waiting for them
+  int npos[PBWD_TG][KK], nex[PBWD_TG][KK];
+  float ndl[PBWD_TG][KK];
+  auto load_idx = [&](int g0) {
+#pragma unroll
+    for (int u = 0; u < PBWD_TG; ++u) {
+      const int t = min(g0 + u, T - 1);
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        npos[u][j] = KT ? row_map[(size_t)t * k + j] : 0;
+        nex[u][j] = KT && dlogit ? idx[(size_t)t * k + j] : 0;
+        ndl[u][j] = KT && dlogit ? dlogit[(size_t)t * k + j] : 0.0f;
+      }
+    }
+  };
+  const int t_first = (blockIdx.y * 8 + warp) * PBWD_TG;
+  if (t_first < T) load_idx(t_first);
+  for (int t0 = t_first; t0 < T; t0 += nw * PBWD_TG) {
+    // stage 1: all TG * k row gathers of this group in flight at once, then the next group's
+    // indices (before this group's stores, whose memory clobber would hold them back)
     int pos[PBWD_TG][KK], ex[PBWD_TG][KK];
     float dlv[PBWD_TG][KK];
     int4 v[PBWD_TG][KK];
     int4 rv[PBWD_TG];
 #pragma unroll
-    for (int u = 0; u < PBWD_TG; ++u) {
-      const int t = min(t0 + u, T - 1);
+    for (int u = 0; u < PBWD_TG; ++u)
 #pragma unroll
-      for (int j = 0; j < KK; ++j) {
-        pos[u][j] = KT ? row_map[(size_t)t * k + j] : 0;
-        ex[u][j] = KT && dlogit ? idx[(size_t)t * k + j] : 0;          // with the row indices, not
-        dlv[u][j] = KT && dlogit ? dlogit[(size_t)t * k + j] : 0.0f;   // after this group's stores
-      }
-    }
+      for (int j = 0; j < KK; ++j) { pos[u][j] = npos[u][j]; ex[u][j] = nex[u][j]; dlv[u][j] = ndl[u][j]; }
 #pragma unroll
     for (int u = 0; u < PBWD_TG; ++u) {
       const int t = min(t0 + u, T - 1);
@@ -271,6 +284,7 @@ permute_bwd_smem_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t
 #pragma unroll
       for (int j = 0; j < KK; ++j) v[u][j] = KT ? ld_nc_v4(dx_perm + (size_t)pos[u][j] * H + col) : make_int4(0, 0, 0, 0);
     }
+    if (t0 + nw * PBWD_TG < T) load_idx(t0 + nw * PBWD_TG);
 #pragma unroll
     for (int u = 0; u < PBWD_TG; ++u) {
       const int t = t0 + u;
