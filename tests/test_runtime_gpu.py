@@ -240,3 +240,56 @@ def test_afpipe_iteration_graph_capture_matches_eager(layers):
                     for u, v in zip(a, b):
                         assert np.array_equal(u, v), key
     check_against_oracle([o["graph"] for o in outs], 1, layers)
+
+
+def _large_worker(rank, world, port, outdir):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    from paper_2605_11005_b200.moe import MoEShape
+    from paper_2605_11005_b200.runtime import AFPipeRank, Topology
+
+    shape = MoEShape(4096, 4096, 8, 2, 1024)   # Mixtral-size messages: a 75 MB x_perm per exchange
+    r = AFPipeRank(shape, Topology(world, 1, 8, 1), rank, 4, dev, seed=5)
+    r.init_groups()
+    if r.role == "A":
+        g = torch.Generator(device=dev).manual_seed(11)
+        for i in range(4):
+            r.input(i).normal_(generator=g)
+            r.out_bufs[i].dy.normal_(generator=g)
+    out = {}
+    for it in range(2):   # eager, twice (buffers reused across iterations)
+        r.run_iteration()
+    torch.cuda.synchronize()
+    def pick():
+        return [r.out_bufs[i].y.float().cpu() for i in range(4)] if r.role == "A" else []
+
+    out["eager"] = pick()
+    graph = r.capture()
+    graph.replay()
+    torch.cuda.synchronize()
+    out["graph"] = pick()
+    torch.save(out, os.path.join(outdir, f"rank{rank}.pt"))
+    del graph
+    torch.cuda.synchronize()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_afpipe_large_messages_eager_and_graph_do_not_deadlock():
+    """1 A + 1 F with Mixtral-size exchanges (75 MB per message, larger than NCCL's staging
+    buffers): eager and graph-captured iterations complete and agree. (A communicator per
+    direction deadlocked exactly this case while the small-shape tests passed.)"""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_large_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        outs = [torch.load(os.path.join(d, f"rank{r}.pt"), weights_only=False) for r in range(2)]
+    a = outs[0]
+    assert a["eager"] and len(a["eager"]) == 4
+    for e, g in zip(a["eager"], a["graph"]):
+        assert torch.isfinite(g).all()
+        assert torch.equal(e, g)
