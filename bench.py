@@ -206,7 +206,7 @@ def run_reference(args, shape, exp):
                    "microbatches": exp.workload.num_microbatches, "tokens_per_step": tokens},
         "cpu_baseline": {**{kk: v for kk, v in samples[-1].items() if kk != "seconds"}, "value": round(value, 3)},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "consistency": {"timed_s": round(sum(secs), 2), "run_s": round(t_run, 2)},
+        "consistency": {"timed_s": round(sum(secs), 4), "run_s": round(t_run, 4)},
     }
     print(json.dumps(line), flush=True)
     return 0
