@@ -277,9 +277,37 @@ def run_ours(args, shape, exp):
         def total_ms(self, name):
             return sum(s.elapsed_time(e) for s, e in self.pairs[name])
 
+    batched = stack.batched_supported(mb)
+
     def step(ev=None):
         if ev is None:
             stack.iteration(mb)
+            return
+        if batched:   # the order MoEStack.iteration runs: layer-major, one GEMM launch per stage
+            for l, ly in enumerate(stack.layers):
+                for i in range(mb):
+                    if attn is not None:
+                        x_in = stack.inp[i] if l == 0 else stack.layers[l - 1].buffers[i].y
+                        ev.mark("attention", lambda: attn[l].forward(i, x_in, ly.buffers[i].x, stack.seq_len))
+                for i in range(mb):
+                    ev.mark("dispatch", lambda: ly.stage_dispatch(ly.buffers[i]))
+                ev.mark("gemm", lambda: ly.f_forward_all(mb))
+                for i in range(mb):
+                    ev.mark("combine_fwd", lambda: ly.stage_combine(ly.buffers[i]))
+            for l in reversed(range(L)):
+                ly = stack.layers[l]
+                for i in range(mb):
+                    ev.mark("combine_bwd", lambda: ly.stage_combine_bwd(ly.buffers[i]))
+                ev.mark("gemm", lambda: ly.f_backward_all(mb))
+                for i in range(mb):
+                    ev.mark("permute_bwd", lambda: ly.stage_permute_bwd(ly.buffers[i]))
+                    ev.mark("router_wgrad", lambda: ly.stage_router_wgrad(ly.buffers[i], i > 0))
+                if attn is not None:
+                    for i in range(mb):
+                        dst = stack.dinp[i] if l == 0 else stack.layers[l - 1].buffers[i].dy
+                        ev.mark("attention", lambda: attn[l].backward(i, ly.buffers[i].dx, dst, i > 0))
+            for ly in stack.layers:
+                ev.mark("gemm", lambda: ly.wgrad(mb))
             return
         for i in range(mb):
             acc = i > 0
@@ -373,7 +401,7 @@ def run_ours(args, shape, exp):
     peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     # which roofline binds the GEMMs: tensor FLOPs or the HBM bytes they must move
     # (weights streamed per micro-batch fwd + dgrad, fp32 dW, activations)
-    gemm_bytes = args.steps * L * shape.gemm_hbm_bytes(mb, 4 if fp32 else 2)
+    gemm_bytes = args.steps * L * shape.gemm_hbm_bytes(mb, 4 if fp32 else 2, batched=batched)
     ideal_tensor_ms = gemm_flops / (peak_tf * 1e12) * 1e3
     ideal_hbm_ms = gemm_bytes / (peaks["hbm_gbs"] * 1e9) * 1e3
     hbm_bound = ideal_hbm_ms > ideal_tensor_ms
@@ -428,7 +456,10 @@ def run_ours(args, shape, exp):
             "parallelism": "fused single-device (A+F on one GPU)" if world == 1 else f"replicas x{world}",
             "weights": "random-init", "l2": "inputs+weights (2.8 GB) larger than L2 (126 MB)",
             "wgrad": "fp32, deferred: one grouped GEMM per iteration over all micro-batches (K = mb*T*k rows)",
-            "launch": "eager" if graphs is None else "CUDA graphs (per micro-batch + W pass)",
+            "launch": "eager" if graphs is None else ("CUDA graphs (all micro-batches' fwd + bwd, then the W pass)"
+                                                       if batched else "CUDA graphs (per micro-batch + W pass)"),
+            "f_side": ("batched: each expert GEMM stage is one launch over all micro-batches, expert-major groups "
+                       "(weights streamed once per iteration)" if batched else "per micro-batch"),
             "stage_breakdown": "separate eager pass with CUDA events per stage (not the timed region)",
         },
         "roofline": ({
@@ -803,7 +834,48 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
     hy = [torch.empty(T, H, dtype=dt).pin_memory() for _ in range(mb)]
     hdx = [torch.empty(T, H, dtype=dt).pin_memory() for _ in range(mb)]
 
+    batched = graphs is not None and graphs.batched
+    state = {"free": None}   # batched: event after the previous backward (x / dy buffers free)
+
+    def step_batched():
+        # x and dy of every micro-batch land while the previous step's W pass runs; y leaves
+        # during the backward, dx during this step's W pass
+        g_fwd, g_bwd = graphs.microbatch
+        with torch.cuda.stream(copy):
+            if state["free"] is not None:
+                copy.wait_event(state["free"])
+            else:
+                copy.wait_stream(comp)
+            for i in range(mb):
+                stack.input(i).copy_(hx[i], non_blocking=True)
+            x_in = torch.cuda.Event()
+            x_in.record(copy)
+            for i in range(mb):
+                stack.output_grad(i).copy_(hdy[i], non_blocking=True)
+            dy_in = torch.cuda.Event()
+            dy_in.record(copy)
+        comp.wait_event(x_in)
+        g_fwd.replay()
+        fwd_done = torch.cuda.Event()
+        fwd_done.record(comp)
+        comp.wait_event(dy_in)
+        g_bwd.replay()
+        bwd_done = torch.cuda.Event()
+        bwd_done.record(comp)
+        state["free"] = bwd_done
+        with torch.cuda.stream(copy):
+            copy.wait_event(fwd_done)
+            for i in range(mb):
+                hy[i].copy_(stack.output(i), non_blocking=True)
+            copy.wait_event(bwd_done)
+            for i in range(mb):
+                hdx[i].copy_(stack.input_grad(i), non_blocking=True)
+        graphs.wgrad.replay()
+        comp.wait_stream(copy)
+
     def step():
+        if batched:
+            return step_batched()
         loaded = [torch.cuda.Event() for _ in range(mb)]
         done = [torch.cuda.Event() for _ in range(mb)]
         copy.wait_stream(comp)  # previous step finished with the input buffers
@@ -851,7 +923,7 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
     return {"value": round(args.steps * mb * T * world / (ms / 1e3), 1), "unit": UNIT,
             "h2d_bytes_per_step": 2 * per * mb, "d2h_bytes_per_step": 2 * per * mb,
             "ms_per_step": round(ms / args.steps, 3),
-            "path": ("MoEStack.capture graphs (one per micro-batch + W pass)" if graphs is not None else
+            "path": ("MoEStack.capture graphs (iteration + W pass)" if graphs is not None else
                      "MoEStack.forward_backward") + " with pinned host x/dy in, y/dx out (copy stream overlapped)"}
 
 

@@ -190,6 +190,28 @@ DM_API int dm_grouped_wgrad(const void* a_tok, int M, const void* b_tok, int N, 
                             int nseg, int E, int total_rows, int seg_stride_rows, float* dW, float beta,
                             void* stream);
 
+/* The same four GEMMs over explicit group row ranges: group g = rows [group_start[g], group_end[g])
+ * (device arrays, each start a multiple of 128, each range 128-row padded), multiplying weight
+ * matrix (g / b_div) % E. With dm_batch_group_ranges this runs n micro-batches stacked cap rows
+ * apart as ONE launch, groups ordered expert-major (b_div = n), so each expert's weights stream
+ * once for all micro-batches (fused single-device iteration). 2-SM path only. */
+DM_API int dm_grouped_w13_swiglu_fwd_ranges(const void* x_perm, const void* w13, const int32_t* group_start,
+                                            const int32_t* group_end, int G, int E, int b_div, int cap_rows, int H,
+                                            int De, void* h13, void* act, void* stream);
+DM_API int dm_grouped_w2_fwd_ranges(const void* act, const void* w2, const int32_t* group_start,
+                                    const int32_t* group_end, int G, int E, int b_div, int cap_rows, int H, int De,
+                                    void* y_perm, void* stream);
+DM_API int dm_grouped_w2_dgrad_swiglu_bwd_ranges(const void* dy_perm, const void* w2, const void* h13,
+                                                 const int32_t* group_start, const int32_t* group_end, int G, int E,
+                                                 int b_div, int cap_rows, int H, int De, void* dh13, void* stream);
+DM_API int dm_grouped_w13_dgrad_ranges(const void* dh13, const void* w13, const int32_t* group_start,
+                                       const int32_t* group_end, int G, int E, int b_div, int cap_rows, int H, int De,
+                                       void* dx_perm, void* stream);
+/* group_start / group_end [E * n] (expert-major: g = e * n + i) from the [n, E+1] padded offsets
+ * of n micro-batches stacked cap rows apart. */
+DM_API int dm_batch_group_ranges(const int32_t* pad_off, int n, int E, int cap, int32_t* group_start,
+                                 int32_t* group_end, void* stream);
+
 /* Debug: route 2-SM GEMM wait-cycle counters into a device u64[5] buffer (NULL = off). */
 DM_API int dm_debug_gemm_profile(void* buf);
 /* Debug: per-CTA globaltimer timeline of the streaming router (>= 64 u64 per CTA, zeroed;

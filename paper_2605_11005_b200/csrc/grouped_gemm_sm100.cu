@@ -42,7 +42,10 @@ struct GemmArgs {
                                  //   reads zero-filled / discarded B rows, its stores are clipped)
   int K;                         // ragged-M: reduction length (multiple of 64)
   int b_group_rows;              // ragged-M: rows of the B tensor owned by one weight matrix
-  int b_groups;                  // ragged-M: group g multiplies weight matrix g % b_groups
+  int b_groups;                  // ragged-M: group g multiplies weight matrix (g / b_div) % b_groups
+  int b_div;                     // ragged-M: consecutive groups sharing a weight matrix (>= 1)
+  const int* group_end;          // ragged-M, optional: group g = rows [group_off[g], group_end[g])
+                                 //   (group_off then holds G starts); null: contiguous groups
   void* C;
   long long ldc;
   long long c_group_stride;      // ragged-K: elements between groups' C blocks
@@ -411,15 +414,19 @@ template <int EPI> constexpr int g2_stages() { return EPI == EPI_SWIGLU_BWD ? 4 
 template <int EPI> constexpr uint32_t g2_stg_bytes() {
   return EPI == EPI_SWIGLU_FWD ? 3 * BOX_BYTES : EPI == EPI_SWIGLU_BWD ? 4 * BOX_BYTES : 2 * BOX_BYTES;
 }
-// fixed part; the two [G+1]-int tile tables are appended at launch (G-dependent)
+// fixed part; the three [G+1]-int tables (tile starts, group starts / ends) are appended at launch
 template <int EPI> constexpr size_t g2_smem_bytes() {
   return 1024 + g2_stages<EPI>() * (G2_A_BYTES + G2_B_BYTES) + 4 * g2_stg_bytes<EPI>() + 256;
 }
 
 template <int RAGGED_K>
-__device__ __forceinline__ TileInfo decode_tile_2sm(int t, const int* tile_start, const int* off, int G,
-                                                    const GemmArgs& a, uint32_t rank, bool& active) {
-  int lo = 0, hi = G - 1;
+__device__ __forceinline__ TileInfo decode_tile_2sm(int t, const int* tile_start, const int* off, const int* end,
+                                                    int G, const GemmArgs& a, uint32_t rank, bool& active) {
+  // merged mode (group ranges with b_div > 1): the tile table runs over the G / b_div weight
+  // groups, each the union of its b_div member ranges cut into 128-row chunks
+  const bool merged = !RAGGED_K && a.group_end && a.b_div > 1;
+  const int NG = merged ? G / a.b_div : G;
+  int lo = 0, hi = NG - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
     if (tile_start[mid] <= t) lo = mid; else hi = mid - 1;
@@ -428,9 +435,31 @@ __device__ __forceinline__ TileInfo decode_tile_2sm(int t, const int* tile_start
   ti.g = lo;
   const int local = t - tile_start[lo];
   ti.half = 0;
-  if (!RAGGED_K) {
+  if (merged) {
+    // a pair tile = two 128-row chunks of the weight group in (member, row) order — rank 0
+    // takes the first, rank 1 the second, wherever their rows lie; an odd last chunk runs
+    // as an M = 128 pair MMA (64 rows per CTA)
+    const int g0 = lo * a.b_div;
+    int chunks = 0;
+    for (int i = 0; i < a.b_div; ++i) chunks += (end[g0 + i] - off[g0 + i]) >> 7;
+    const int mt = (chunks + 1) >> 1;
+    const int c0 = 2 * (local % mt);
+    ti.half = c0 + 1 >= chunks;
+    int c = ti.half ? c0 : c0 + (int)rank, row = 0;
+    for (int i = 0; i < a.b_div; ++i) {
+      const int cnt = (end[g0 + i] - off[g0 + i]) >> 7;
+      if (c < cnt) { row = off[g0 + i] + (c << 7); break; }
+      c -= cnt;
+    }
+    ti.g = g0;                                          // weight (g0 / b_div) % b_groups
+    ti.m0 = row + (ti.half ? 64 * (int)rank : 0);
+    ti.n0 = (local / mt) * GBN;
+    ti.kb_count = a.K / GBK;
+    ti.row_base = 0;
+    active = true;
+  } else if (!RAGGED_K) {
     const int row_off = off[lo];
-    const int rows = off[lo + 1] - row_off;
+    const int rows = end[lo] - row_off;
     const int mt = (rows + 255) / 256;
     const int tm0 = row_off + (local % mt) * 256;
     // Groups are 128-row aligned, so a tile has 256 or (the group's tail) 128 valid
@@ -682,7 +711,8 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   uint64_t* ibar = tempty + 2;   // [4] per-epilogue-warp input barriers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ibar + 4);
   int* s_tile = reinterpret_cast<int*>(sStg + 4 * STG + 256);
-  int* s_off = s_tile + (args.num_groups + 1);
+  int* s_off = s_tile + (args.num_groups + 1);     // group starts
+  int* s_end = s_off + (args.num_groups + 1);      // group ends
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -692,8 +722,12 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   const int cluster_id = blockIdx.x >> 1;
   const int num_clusters = gridDim.x >> 1;
 
-  if (!RAGGED_K)
-    for (int i = threadIdx.x; i <= G; i += GEMM_THREADS) s_off[i] = args.group_off[i];
+  if (!RAGGED_K) {
+    for (int i = threadIdx.x; i < G; i += GEMM_THREADS) {
+      s_off[i] = args.group_off[i];
+      s_end[i] = args.group_end ? args.group_end[i] : args.group_off[i + 1];
+    }
+  }
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -710,19 +744,30 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
   __syncthreads();
   if (threadIdx.x == 32 * 3) {
     int acc = 0;
-    for (int g = 0; g < G; ++g) {
-      s_tile[g] = acc;
-      const int rows = RAGGED_K ? 0 : s_off[g + 1] - s_off[g];
-      const int nt = (args.N + GBN - 1) / GBN;   // last column tile may be partial (N % 256 == 128)
-      acc += RAGGED_K ? ((args.M + 255) / 256) * nt : ((rows + 255) / 256) * nt;
+    const int nt = (args.N + GBN - 1) / GBN;   // last column tile may be partial (N % 256 == 128)
+    if (!RAGGED_K && args.group_end && args.b_div > 1) {   // merged: per weight group
+      const int NG = G / args.b_div;
+      for (int w = 0; w < NG; ++w) {
+        s_tile[w] = acc;
+        int chunks = 0;
+        for (int i = 0; i < args.b_div; ++i) chunks += (s_end[w * args.b_div + i] - s_off[w * args.b_div + i]) >> 7;
+        acc += ((chunks + 1) >> 1) * nt;
+      }
+      s_tile[NG] = acc;
+    } else {
+      for (int g = 0; g < G; ++g) {
+        s_tile[g] = acc;
+        const int rows = RAGGED_K ? 0 : s_end[g] - s_off[g];
+        acc += RAGGED_K ? ((args.M + 255) / 256) * nt : ((rows + 255) / 256) * nt;
+      }
+      s_tile[G] = acc;
     }
-    s_tile[G] = acc;
   }
   tc_fence_before();
   cluster_sync_all();   // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total_tiles = s_tile[G];
+  const int total_tiles = s_tile[(!RAGGED_K && args.group_end && args.b_div > 1) ? G / args.b_div : G];
 
   if (warp == 0 || (warp == 3 && args.dual_producer)) {
     // ------------------------------------------- TMA producers (both CTAs)
@@ -740,8 +785,8 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       uint32_t phase = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters) {
         bool active;
-        const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, G, args, rank, active);
-        const int b_gofs = RAGGED_K ? 0 : (ti.g % args.b_groups) * args.b_group_rows;
+        const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, s_end, G, args, rank, active);
+        const int b_gofs = RAGGED_K ? 0 : ((ti.g / args.b_div) % args.b_groups) * args.b_group_rows;
         const int nb0 = ti.n0 + 128 * (int)rank;   // this CTA's half of the N tile
         int seg = 0, seg_kb = 0, seg_nkb = 0, seg_row0 = 0;
         for (int kb = 0; kb < ti.kb_count; ++kb) {
@@ -797,7 +842,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
       int it = 0;
       for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
         bool active;
-        const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, G, args, rank, active);
+        const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, s_end, G, args, rank, active);
         const int as = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         DM_PROF_WAIT(1, mbar_wait(&tempty[as], aphase ^ 1));
@@ -832,7 +877,7 @@ grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_co
     int it = 0;
     for (int t = cluster_id; t < total_tiles; t += num_clusters, ++it) {
       bool active;
-      const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, G, args, rank, active);
+      const TileInfo ti = decode_tile_2sm<RAGGED_K>(t, s_tile, s_off, s_end, G, args, rank, active);
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       DM_PROF_WAIT(3, mbar_wait(&tfull[as], aphase));
@@ -971,11 +1016,12 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const EpiTe
     if ((rc = make_epi_map(&tx, et.aux, ta))) return rc;
     if ((rc = make_epi_map(&ti, et.in, ta))) return rc;
     auto kern = grouped_gemm_2sm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
-    const size_t smem = g2_smem_bytes<EPI>() + 2 * ((size_t)args.num_groups + 1) * sizeof(int);
+    const size_t smem = g2_smem_bytes<EPI>() + 3 * ((size_t)args.num_groups + 1) * sizeof(int);
     if (smem > 232448) return set_error(DM_ERR_SHAPE, "too many groups (%d) for the GEMM smem budget", args.num_groups);
     if ((rc = ensure_smem_attr((const void*)kern, 232448, "cudaFuncSetAttribute(gemm2 smem)"))) return rc;
     grid &= ~1;
     GemmArgs a2 = args;
+    if (a2.b_div < 1) a2.b_div = 1;
     a2.prof = g_gemm_prof;
     static const int diag = env_flag("DM_GEMM_DIAG", '1', 1, 0);
     static const int dual = env_flag("DM_GEMM_DUAL", '0', 0, 1);
@@ -983,6 +1029,8 @@ static int launch_gemm(const GemmOperand& oa, const GemmOperand& ob, const EpiTe
     a2.dual_producer = dual;
     kern<<<grid, GEMM_THREADS, smem, stream>>>(ta, tb, tc, tx, ti, a2);
   } else {
+    if (args.group_end || args.b_div > 1)
+      return set_error(DM_ERR_ARG, "group row ranges need the 2-SM GEMM path (unset DM_GEMM_1SM)");
     if (args.N % GBN || (RAGGED_K && args.M % 256))
       return set_error(DM_ERR_SHAPE, "the 1-SM debug GEMM path needs full 256-wide tiles (N=%d, M=%d)", args.N, args.M);
     auto kern = grouped_gemm_kernel<A_MN, B_MN, RAGGED_K, EPI>;
@@ -1008,7 +1056,7 @@ using namespace dm;
 
 extern "C" {
 
-int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t* group_off, int G,
+static int dm_grouped_w13_swiglu_fwd_impl(const void* x_perm, const void* w13, const int32_t* group_off, const int32_t* group_end, int b_div, int G,
                               int E, int cap_rows, int H, int De, void* h13, void* act, void* stream) {
   int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
@@ -1017,6 +1065,7 @@ int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t
   const GemmOperand A{x_perm, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H, false, false};
   const GemmOperand B{w13, (uint64_t)H, (uint64_t)E * 2 * De, (uint64_t)H, false, true};
   GemmArgs a{};
+  a.group_end = group_end; a.b_div = b_div;
   a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = 2 * De; a.K = H; a.b_group_rows = 2 * De;
   a.C = act; a.ldc = De; a.aux = reinterpret_cast<__nv_bfloat16*>(h13); a.ld_aux = 2 * De;
   EpiTensors et;
@@ -1025,7 +1074,7 @@ int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t
   return launch_gemm<0, 0, 0, EPI_SWIGLU_FWD>(A, B, et, a, (cudaStream_t)stream);
 }
 
-int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* group_off, int G, int E,
+static int dm_grouped_w2_fwd_impl(const void* act, const void* w2, const int32_t* group_off, const int32_t* group_end, int b_div, int G, int E,
                       int cap_rows, int H, int De, void* y_perm, void* stream) {
   int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
@@ -1034,6 +1083,7 @@ int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* group_off,
   const GemmOperand A{act, (uint64_t)De, (uint64_t)cap_rows, (uint64_t)De, false, false};
   const GemmOperand B{w2, (uint64_t)De, (uint64_t)E * H, (uint64_t)De, false, true};
   GemmArgs a{};
+  a.group_end = group_end; a.b_div = b_div;
   a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = H; a.K = De; a.b_group_rows = H;
   a.C = y_perm; a.ldc = H;
   EpiTensors et;
@@ -1041,8 +1091,8 @@ int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* group_off,
   return launch_gemm<0, 0, 0, EPI_BF16>(A, B, et, a, (cudaStream_t)stream);
 }
 
-int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const void* h13,
-                                   const int32_t* group_off, int G, int E, int cap_rows, int H, int De,
+static int dm_grouped_w2_dgrad_swiglu_bwd_impl(const void* dy_perm, const void* w2, const void* h13,
+                                   const int32_t* group_off, const int32_t* group_end, int b_div, int G, int E, int cap_rows, int H, int De,
                                    void* dh13, void* stream) {
   int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
@@ -1051,6 +1101,7 @@ int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const vo
   const GemmOperand A{dy_perm, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H, false, false};
   const GemmOperand B{w2, (uint64_t)De, (uint64_t)E * H, (uint64_t)De, true, true};
   GemmArgs a{};
+  a.group_end = group_end; a.b_div = b_div;
   a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = De; a.K = H; a.b_group_rows = H;
   a.aux = reinterpret_cast<__nv_bfloat16*>(dh13); a.ld_aux = 2 * De;
   a.aux_in = reinterpret_cast<const __nv_bfloat16*>(h13); a.ld_aux_in = 2 * De;
@@ -1060,7 +1111,7 @@ int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const vo
   return launch_gemm<0, 1, 0, EPI_SWIGLU_BWD>(A, B, et, a, (cudaStream_t)stream);
 }
 
-int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* group_off, int G, int E,
+static int dm_grouped_w13_dgrad_impl(const void* dh13, const void* w13, const int32_t* group_off, const int32_t* group_end, int b_div, int G, int E,
                          int cap_rows, int H, int De, void* dx_perm, void* stream) {
   int rc = check_groups(G, E, cap_rows);
   if (rc) return rc;
@@ -1069,11 +1120,57 @@ int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* group
   const GemmOperand A{dh13, (uint64_t)2 * De, (uint64_t)cap_rows, (uint64_t)2 * De, false, false};
   const GemmOperand B{w13, (uint64_t)H, (uint64_t)E * 2 * De, (uint64_t)H, true, true};
   GemmArgs a{};
+  a.group_end = group_end; a.b_div = b_div;
   a.num_groups = G; a.b_groups = E; a.group_off = group_off; a.N = H; a.K = 2 * De; a.b_group_rows = 2 * De;
   a.C = dx_perm; a.ldc = H;
   EpiTensors et;
   et.c = {dx_perm, false, (uint64_t)H, (uint64_t)cap_rows, (uint64_t)H};
   return launch_gemm<0, 1, 0, EPI_BF16>(A, B, et, a, (cudaStream_t)stream);
+}
+
+int dm_grouped_w13_swiglu_fwd(const void* x_perm, const void* w13, const int32_t* group_off, int G,
+                              int E, int cap_rows, int H, int De, void* h13, void* act, void* stream) {
+  return dm_grouped_w13_swiglu_fwd_impl(x_perm, w13, group_off, nullptr, 1, G, E, cap_rows, H, De, h13, act, stream);
+}
+int dm_grouped_w2_fwd(const void* act, const void* w2, const int32_t* group_off, int G, int E,
+                      int cap_rows, int H, int De, void* y_perm, void* stream) {
+  return dm_grouped_w2_fwd_impl(act, w2, group_off, nullptr, 1, G, E, cap_rows, H, De, y_perm, stream);
+}
+int dm_grouped_w2_dgrad_swiglu_bwd(const void* dy_perm, const void* w2, const void* h13,
+                                   const int32_t* group_off, int G, int E, int cap_rows, int H, int De,
+                                   void* dh13, void* stream) {
+  return dm_grouped_w2_dgrad_swiglu_bwd_impl(dy_perm, w2, h13, group_off, nullptr, 1, G, E, cap_rows, H, De, dh13,
+                                             stream);
+}
+int dm_grouped_w13_dgrad(const void* dh13, const void* w13, const int32_t* group_off, int G, int E,
+                         int cap_rows, int H, int De, void* dx_perm, void* stream) {
+  return dm_grouped_w13_dgrad_impl(dh13, w13, group_off, nullptr, 1, G, E, cap_rows, H, De, dx_perm, stream);
+}
+
+int dm_grouped_w13_swiglu_fwd_ranges(const void* x_perm, const void* w13, const int32_t* group_start,
+                                     const int32_t* group_end, int G, int E, int b_div, int cap_rows, int H,
+                                     int De, void* h13, void* act, void* stream) {
+  if (b_div < 1 || G % b_div) return set_error(DM_ERR_ARG, "b_div %d must divide G = %d", b_div, G);
+  return dm_grouped_w13_swiglu_fwd_impl(x_perm, w13, group_start, group_end, b_div, G, E, cap_rows, H, De, h13, act,
+                                        stream);
+}
+int dm_grouped_w2_fwd_ranges(const void* act, const void* w2, const int32_t* group_start, const int32_t* group_end,
+                             int G, int E, int b_div, int cap_rows, int H, int De, void* y_perm, void* stream) {
+  if (b_div < 1 || G % b_div) return set_error(DM_ERR_ARG, "b_div %d must divide G = %d", b_div, G);
+  return dm_grouped_w2_fwd_impl(act, w2, group_start, group_end, b_div, G, E, cap_rows, H, De, y_perm, stream);
+}
+int dm_grouped_w2_dgrad_swiglu_bwd_ranges(const void* dy_perm, const void* w2, const void* h13,
+                                          const int32_t* group_start, const int32_t* group_end, int G, int E,
+                                          int b_div, int cap_rows, int H, int De, void* dh13, void* stream) {
+  if (b_div < 1 || G % b_div) return set_error(DM_ERR_ARG, "b_div %d must divide G = %d", b_div, G);
+  return dm_grouped_w2_dgrad_swiglu_bwd_impl(dy_perm, w2, h13, group_start, group_end, b_div, G, E, cap_rows, H, De,
+                                             dh13, stream);
+}
+int dm_grouped_w13_dgrad_ranges(const void* dh13, const void* w13, const int32_t* group_start,
+                                const int32_t* group_end, int G, int E, int b_div, int cap_rows, int H, int De,
+                                void* dx_perm, void* stream) {
+  if (b_div < 1 || G % b_div) return set_error(DM_ERR_ARG, "b_div %d must divide G = %d", b_div, G);
+  return dm_grouped_w13_dgrad_impl(dh13, w13, group_start, group_end, b_div, G, E, cap_rows, H, De, dx_perm, stream);
 }
 
 int dm_grouped_wgrad_strided(const void* a_tok, int M, int lda, const void* b_tok, int N, int ldb,

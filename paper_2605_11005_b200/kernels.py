@@ -131,6 +131,58 @@ def w13_dgrad(dh13, w13, group_off, dx_perm, stream=None):
               H, two_de // 2, _ptr(dx_perm), _stream(stream))
 
 
+# -------------------------------------------- the same GEMMs over explicit group ranges
+def batch_group_ranges(pad_off, cap, group_start, group_end, stream=None):
+    """Expert-major row ranges (g = e * n + i) of n micro-batches stacked cap rows apart,
+    from their [n, E+1] padded offsets."""
+    n, e1 = pad_off.shape
+    _check(group_start, torch.int32, (n * (e1 - 1),), "group_start")
+    _check(group_end, torch.int32, (n * (e1 - 1),), "group_end")
+    _lib.call("dm_batch_group_ranges", _ptr(pad_off), n, e1 - 1, cap, _ptr(group_start), _ptr(group_end),
+              _stream(stream))
+
+
+def _ranges(gs, ge, E, b_div):
+    if gs.dtype != torch.int32 or ge.dtype != torch.int32 or gs.numel() != ge.numel() or gs.numel() < E:
+        raise ValueError("group_start / group_end must be int32 [G] with G >= number of experts")
+    if b_div < 1:
+        raise ValueError("b_div must be >= 1")
+    return gs.numel()
+
+
+def w13_swiglu_fwd_ranges(x_perm, w13, gs, ge, b_div, h13, act, stream=None):
+    cap, H = x_perm.shape
+    E, two_de, _ = w13.shape
+    De = two_de // 2
+    _check(h13, BF16, (cap, 2 * De), "h13"); _check(act, BF16, (cap, De), "act")
+    _lib.call("dm_grouped_w13_swiglu_fwd_ranges", _ptr(x_perm), _ptr(w13), _ptr(gs), _ptr(ge),
+              _ranges(gs, ge, E, b_div), E, b_div, cap, H, De, _ptr(h13), _ptr(act), _stream(stream))
+
+
+def w2_fwd_ranges(act, w2, gs, ge, b_div, y_perm, stream=None):
+    cap, De = act.shape
+    E, H, _ = w2.shape
+    _check(y_perm, BF16, (cap, H), "y_perm")
+    _lib.call("dm_grouped_w2_fwd_ranges", _ptr(act), _ptr(w2), _ptr(gs), _ptr(ge), _ranges(gs, ge, E, b_div), E,
+              b_div, cap, H, De, _ptr(y_perm), _stream(stream))
+
+
+def w2_dgrad_swiglu_bwd_ranges(dy_perm, w2, h13, gs, ge, b_div, dh13, stream=None):
+    cap, H = dy_perm.shape
+    E, _, De = w2.shape
+    _check(dh13, BF16, (cap, 2 * De), "dh13")
+    _lib.call("dm_grouped_w2_dgrad_swiglu_bwd_ranges", _ptr(dy_perm), _ptr(w2), _ptr(h13), _ptr(gs), _ptr(ge),
+              _ranges(gs, ge, E, b_div), E, b_div, cap, H, De, _ptr(dh13), _stream(stream))
+
+
+def w13_dgrad_ranges(dh13, w13, gs, ge, b_div, dx_perm, stream=None):
+    cap, two_de = dh13.shape
+    E, _, H = w13.shape
+    _check(dx_perm, BF16, (cap, H), "dx_perm")
+    _lib.call("dm_grouped_w13_dgrad_ranges", _ptr(dh13), _ptr(w13), _ptr(gs), _ptr(ge), _ranges(gs, ge, E, b_div),
+              E, b_div, cap, H, two_de // 2, _ptr(dx_perm), _stream(stream))
+
+
 def wgrad(a_tok, b_tok, seg_off, dW, beta=0.0, stream=None, seg_stride_rows=None):
     """dW[e] = sum over segments of a_tok[rows]^T b_tok[rows]. seg_off is [E+1] (one
     segment) or [nseg, E+1]; by default segment i starts at row i * rows/nseg (stacked

@@ -64,18 +64,20 @@ class MoEShape:
     def gemm_flops_bwd(self) -> int:
         return 12 * self.R * self.H * self.De
 
-    def gemm_hbm_bytes(self, microbatches: int, e: int = 2) -> int:
-        """Algorithmic HBM bytes of one iteration's expert GEMMs (unpadded rows): per
-        micro-batch the forward and dgrad passes each stream W13 + W2 and their
-        activation operands/outputs; the deferred W pass reads every micro-batch's
-        operands once and writes dW13 + dW2 in fp32. Fine-grained MoE (DeepSeek-V3:
-        ~128 rows per expert) is bound by this, not by tensor FLOPs."""
+    def gemm_hbm_bytes(self, microbatches: int, e: int = 2, batched: bool = False) -> int:
+        """Algorithmic HBM bytes of one iteration's expert GEMMs (unpadded rows): the
+        forward and dgrad passes stream W13 + W2 (once per micro-batch, or once per
+        iteration when the micro-batches run as one batched GEMM) and their activation
+        operands/outputs; the deferred W pass reads every micro-batch's operands once and
+        writes dW13 + dW2 in fp32. Fine-grained MoE (DeepSeek-V3: ~128 rows per expert) is
+        bound by this, not by tensor FLOPs."""
         T, H, E, De, R = self.T, self.H, self.E, self.De, self.R
         w = E * 3 * H * De * e
-        fwd = w + R * (H + 2 * De + De + De + H) * e          # x_perm, h13, act (w+r), y_perm
-        dgrad = w + R * (H + 2 * De + 2 * De + 2 * De + H) * e  # dy_perm, h13, dh13 (w+r), dx_perm
+        fwd = R * (H + 2 * De + De + De + H) * e          # x_perm, h13, act (w+r), y_perm
+        dgrad = R * (H + 2 * De + 2 * De + 2 * De + H) * e  # dy_perm, h13, dh13 (w+r), dx_perm
         wgrad = microbatches * R * (H + De + 2 * De + H) * e + E * 3 * H * De * 4
-        return microbatches * (fwd + dgrad) + wgrad
+        weights = 2 * w * (1 if batched else microbatches)
+        return microbatches * (fwd + dgrad) + weights + wgrad
 
     def hbm_bytes(self, e: int = 2) -> dict[str, int]:
         T, H, R = self.T, self.H, self.R
@@ -130,6 +132,9 @@ class ExpertParams:
     @property
     def num_experts(self) -> int:
         return self.w13.shape[0]
+
+
+GEMM_MAX_GROUPS = 1024   # grouped_gemm_sm100.cu: groups per launch
 
 
 class ActivationSlab:
@@ -349,12 +354,65 @@ class MoELayer:
     def wgrad(self, n: int | None = None, accumulate: bool = False, stream=None) -> None:
         f_wgrad(self.slab, len(self.buffers) if n is None else n, self.experts, accumulate, stream)
 
-    def iteration(self, n: int | None = None, accumulate: bool = False, stream=None) -> None:
-        """Micro-batches 0..n-1 (inputs already in buffers[i].x / .dy), then the W pass."""
-        n = len(self.buffers) if n is None else n
+    # ---- batched F side: the n micro-batches' expert GEMMs as ONE launch each, groups
+    # ordered expert-major (dm_batch_group_ranges), so each expert's W13 / W2 stream once per
+    # iteration instead of once per micro-batch; per-row results are bit-identical.
+    def batched_supported(self, n: int) -> bool:
+        import os
+
+        return (n >= 2 and self.shape.E * n <= GEMM_MAX_GROUPS and os.environ.get("DM_GEMM_1SM") != "1"
+                and os.environ.get("DM_BATCHED", "1") != "0")
+
+    def _group_ranges(self, n: int, stream=None):
+        key = ("ranges", n)
+        if getattr(self, "_rng_key", None) != key:
+            self._rng = (torch.empty(n * self.shape.E, dtype=I32, device=self.device),
+                         torch.empty(n * self.shape.E, dtype=I32, device=self.device))
+            self._rng_key = key
+        gs, ge = self._rng
+        K.batch_group_ranges(self.slab.pad_off[:n], self.slab.cap, gs, ge, stream)
+        return gs, ge
+
+    def f_forward_all(self, n: int, stream=None) -> None:
+        sl, ex = self.slab, self.experts
+        rows = slice(0, n * sl.cap)
+        gs, ge = self._group_ranges(n, stream)
+        K.w13_swiglu_fwd_ranges(sl.x_perm[rows], ex.w13, gs, ge, n, sl.h13[rows], sl.act[rows], stream)
+        K.w2_fwd_ranges(sl.act[rows], ex.w2, gs, ge, n, sl.y_perm[rows], stream)
+
+    def f_backward_all(self, n: int, stream=None) -> None:
+        sl, ex = self.slab, self.experts
+        rows = slice(0, n * sl.cap)
+        gs, ge = self._rng   # from this iteration's forward
+        K.w2_dgrad_swiglu_bwd_ranges(sl.dy_perm[rows], ex.w2, sl.h13[rows], gs, ge, n, sl.dh13[rows], stream)
+        K.w13_dgrad_ranges(sl.dh13[rows], ex.w13, gs, ge, n, sl.dx_perm[rows], stream)
+
+    def forward_all(self, n: int, stream=None) -> None:
         for i in range(n):
-            self.forward_backward(self.buffers[i], accumulate=accumulate or i > 0, stream=stream,
-                                  defer_wgrad=True)
+            a_dispatch(self.buffers[i], self.router, stream)
+        self.f_forward_all(n, stream)
+        for i in range(n):
+            a_combine(self.buffers[i], stream)
+
+    def backward_all(self, n: int, accumulate: bool, stream=None) -> None:
+        for i in range(n):
+            a_combine_bwd(self.buffers[i], stream)
+        self.f_backward_all(n, stream)
+        for i in range(n):
+            a_dispatch_bwd(self.buffers[i], self.router, accumulate or i > 0, stream)
+
+    def iteration(self, n: int | None = None, accumulate: bool = False, stream=None) -> None:
+        """Micro-batches 0..n-1 (inputs already in buffers[i].x / .dy), then the W pass:
+        batched (all forwards, all backwards, one GEMM launch per stage) when supported,
+        else micro-batch by micro-batch. Same results either way."""
+        n = len(self.buffers) if n is None else n
+        if self.batched_supported(n):
+            self.forward_all(n, stream)
+            self.backward_all(n, accumulate, stream)
+        else:
+            for i in range(n):
+                self.forward_backward(self.buffers[i], accumulate=accumulate or i > 0, stream=stream,
+                                      defer_wgrad=True)
         self.wgrad(n, accumulate, stream)
 
     def zero_grad(self) -> None:
@@ -480,10 +538,35 @@ class MoEStack:
         self.forward(i, stream)
         self.backward(i, accumulate, stream, defer_wgrad)
 
+    def batched_supported(self, n: int) -> bool:
+        return all(getattr(l, "batched_supported", lambda n: False)(n) for l in self.layers)
+
+    def forward_all(self, n: int, stream=None) -> None:
+        """Layer by layer, every micro-batch (the batched form of forward(i) for all i)."""
+        for l, layer in enumerate(self.layers):
+            if self.attn is not None:
+                for i in range(n):
+                    x_in = self.inp[i] if l == 0 else self.layers[l - 1].buffers[i].y
+                    self.attn[l].forward(i, x_in, layer.buffers[i].x, self.seq_len)
+            layer.forward_all(n, stream)
+
+    def backward_all(self, n: int, accumulate: bool = False, stream=None) -> None:
+        for l in reversed(range(len(self.layers))):
+            layer = self.layers[l]
+            layer.backward_all(n, accumulate, stream)
+            if self.attn is not None:
+                for i in range(n):
+                    dst = self.dinp[i] if l == 0 else self.layers[l - 1].buffers[i].dy
+                    self.attn[l].backward(i, layer.buffers[i].dx, dst, accumulate or i > 0)
+
     def iteration(self, n: int | None = None, accumulate: bool = False, stream=None) -> None:
         n = len(self.buffers) if n is None else n
-        for i in range(n):
-            self.forward_backward(i, accumulate or i > 0, stream, defer_wgrad=True)
+        if self.batched_supported(n):
+            self.forward_all(n, stream)
+            self.backward_all(n, accumulate, stream)
+        else:
+            for i in range(n):
+                self.forward_backward(i, accumulate or i > 0, stream, defer_wgrad=True)
         for layer in self.layers:
             layer.wgrad(n, accumulate, stream)
 
@@ -505,7 +588,16 @@ class MoEStack:
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         graphs, launches = [], 0
-        for i in range(n):
+        batched = self.batched_supported(n)
+        if batched:   # two graphs: every micro-batch's forward, then every backward (batched GEMMs)
+            for part in (lambda: self.forward_all(n), lambda: self.backward_all(n, accumulate)):
+                g = torch.cuda.CUDAGraph()
+                c0 = _lib.launch_count()
+                with torch.cuda.graph(g):
+                    part()
+                launches += _lib.launch_count() - c0
+                graphs.append(g)
+        for i in range(0 if batched else n):
             g = torch.cuda.CUDAGraph()
             c0 = _lib.launch_count()
             with torch.cuda.graph(g):
@@ -518,16 +610,18 @@ class MoEStack:
             for layer in self.layers:
                 layer.wgrad(n, accumulate)
         launches += _lib.launch_count() - c0
-        return StackGraphs(graphs, gw, launches)
+        return StackGraphs(graphs, gw, launches, batched)
 
 
 @dataclass
 class StackGraphs:
-    """Captured iteration of a MoEStack: `microbatch[i]` then `wgrad` (MoEStack.capture)."""
+    """Captured iteration of a MoEStack (MoEStack.capture): `microbatch[i]` (fwd + bwd of
+    micro-batch i) then `wgrad`; batched: `microbatch` = [all forwards, all backwards]."""
 
     microbatch: list
     wgrad: object
     launches_per_iteration: int
+    batched: bool = False
 
     def replay(self) -> None:
         for g in self.microbatch:
