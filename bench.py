@@ -874,33 +874,41 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
         comp.wait_stream(copy)
 
     def step():
+        # micro-batch i's next-step x / dy are loaded as soon as its fwd + bwd is done (its y
+        # and dx copied out first), so the loads overlap the rest of the step and the W pass
         if batched:
             return step_batched()
-        loaded = [torch.cuda.Event() for _ in range(mb)]
-        done = [torch.cuda.Event() for _ in range(mb)]
-        copy.wait_stream(comp)  # previous step finished with the input buffers
-        with torch.cuda.stream(copy):
-            for i in range(mb):
-                stack.input(i).copy_(hx[i], non_blocking=True)
-                stack.output_grad(i).copy_(hdy[i], non_blocking=True)
-                loaded[i].record(copy)
+        loaded = state.get("loaded")
+        if loaded is None:
+            loaded = [torch.cuda.Event() for _ in range(mb)]
+            copy.wait_stream(comp)
+            with torch.cuda.stream(copy):
+                for i in range(mb):
+                    stack.input(i).copy_(hx[i], non_blocking=True)
+                    stack.output_grad(i).copy_(hdy[i], non_blocking=True)
+                    loaded[i].record(copy)
+        nxt = [torch.cuda.Event() for _ in range(mb)]
         for i in range(mb):
             comp.wait_event(loaded[i])
             if graphs is not None:
                 graphs.microbatch[i].replay()
             else:
                 stack.forward_backward(i, accumulate=i > 0, defer_wgrad=True)
-            done[i].record(comp)
+            done = torch.cuda.Event()
+            done.record(comp)
             with torch.cuda.stream(copy):
-                copy.wait_event(done[i])
+                copy.wait_event(done)
                 hy[i].copy_(stack.output(i), non_blocking=True)
                 hdx[i].copy_(stack.input_grad(i), non_blocking=True)
+                stack.input(i).copy_(hx[i], non_blocking=True)
+                stack.output_grad(i).copy_(hdy[i], non_blocking=True)
+                nxt[i].record(copy)
+        state["loaded"] = nxt
         if graphs is not None:
             graphs.wgrad.replay()
         else:
             for ly in stack.layers:
                 ly.wgrad(mb)
-        comp.wait_stream(copy)
 
     for _ in range(max(1, args.warmup)):
         step()
@@ -912,6 +920,7 @@ def run_e2e(args, stack, shape, mb, dev, world, graphs=None):
     t0.record(comp)
     for _ in range(args.steps):
         step()
+    comp.wait_stream(copy)   # every step's y / dx are on the host
     t1.record(comp)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)

@@ -207,10 +207,12 @@ DM_API int dm_grouped_w2_dgrad_swiglu_bwd_ranges(const void* dy_perm, const void
 DM_API int dm_grouped_w13_dgrad_ranges(const void* dh13, const void* w13, const int32_t* group_start,
                                        const int32_t* group_end, int G, int E, int b_div, int cap_rows, int H, int De,
                                        void* dx_perm, void* stream);
-/* group_start / group_end [E * n] (expert-major: g = e * n + i) from the [n, E+1] padded offsets
- * of n micro-batches stacked cap rows apart. */
-DM_API int dm_batch_group_ranges(const int32_t* pad_off, int n, int E, int cap, int32_t* group_start,
-                                 int32_t* group_end, void* stream);
+/* group_start / group_end [E * n] from the [n, E+1] padded offsets of n micro-batches stacked cap
+ * rows apart: expert_major != 0 orders them g = e * n + i (pass b_div = n to the GEMMs: one weight
+ * pass serves every micro-batch, 128-row chunks of different micro-batches share a pair tile),
+ * else g = i * E + e (b_div = 1: the per-micro-batch tile order, one launch). */
+DM_API int dm_batch_group_ranges(const int32_t* pad_off, int n, int E, int cap, int expert_major,
+                                 int32_t* group_start, int32_t* group_end, void* stream);
 
 /* Debug: route 2-SM GEMM wait-cycle counters into a device u64[5] buffer (NULL = off). */
 DM_API int dm_debug_gemm_profile(void* buf);

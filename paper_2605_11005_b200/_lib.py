@@ -64,7 +64,7 @@ SIGNATURES: dict[str, tuple] = {
     "dm_grouped_w2_fwd_ranges": (_i, [_vp, _vp, _i32p, _i32p, _i, _i, _i, _i, _i, _i, _vp, _vp]),
     "dm_grouped_w2_dgrad_swiglu_bwd_ranges": (_i, [_vp, _vp, _vp, _i32p, _i32p, _i, _i, _i, _i, _i, _i, _vp, _vp]),
     "dm_grouped_w13_dgrad_ranges": (_i, [_vp, _vp, _i32p, _i32p, _i, _i, _i, _i, _i, _i, _vp, _vp]),
-    "dm_batch_group_ranges": (_i, [_i32p, _i, _i, _i, _i32p, _i32p, _vp]),
+    "dm_batch_group_ranges": (_i, [_i32p, _i, _i, _i, _i, _i32p, _i32p, _vp]),
     "dm_debug_gemm_profile": (_i, [_vp]),
     "dm_debug_route_profile": (_i, [_vp]),
     "dm_combine_fwd": (_i, [_vp, _i32p, _f32p, _i, _i, _i, _vp, _vp, _vp]),

@@ -1039,12 +1039,14 @@ static int dispatch_stream_launch(const void* x, const float* wg, int T, int H, 
   return DM_OK;
 }
 
-// Expert-major group row ranges over n micro-batches stacked cap rows apart: group e*n + i =
-// micro-batch i's expert-e block [i*cap + pad_off[i][e], i*cap + pad_off[i][e+1]).
+// Group row ranges over n micro-batches stacked cap rows apart, micro-batch i's expert-e block
+// [i*cap + pad_off[i][e], i*cap + pad_off[i][e+1]): expert-major (group e*n + i) or
+// micro-batch-major (group i*E + e).
 __global__ void batch_group_ranges_kernel(const int32_t* __restrict__ pad_off, int n, int E, int cap,
-                                          int32_t* __restrict__ start, int32_t* __restrict__ end) {
+                                          int expert_major, int32_t* __restrict__ start,
+                                          int32_t* __restrict__ end) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n * E; q += gridDim.x * blockDim.x) {
-    const int e = q / n, i = q % n;
+    const int e = expert_major ? q / n : q % E, i = expert_major ? q % n : q / E;
     start[q] = i * cap + pad_off[i * (E + 1) + e];
     end[q] = i * cap + pad_off[i * (E + 1) + e + 1];
   }
@@ -1150,12 +1152,13 @@ int dm_route_and_dispatch(const void* x, const float* wg, int T, int H, int E, i
   return dm_permute(x, idx, ws.rank, ws.chunk_base, counts, pad_off, T, H, E, k, row_map, src_token, x_perm, stream);
 }
 
-int dm_batch_group_ranges(const int32_t* pad_off, int n, int E, int cap, int32_t* group_start, int32_t* group_end,
-                          void* stream) {
+int dm_batch_group_ranges(const int32_t* pad_off, int n, int E, int cap, int expert_major, int32_t* group_start,
+                          int32_t* group_end, void* stream) {
   if (n < 1 || E < 1 || cap < 0 || cap % DM_ROW_ALIGN || (long long)n * cap > 0x7fffffffLL)
     return set_error(DM_ERR_SHAPE, "batch_group_ranges: n=%d E=%d cap=%d", n, E, cap);
   const int blocks = (n * E + 255) / 256;
-  batch_group_ranges_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(pad_off, n, E, cap, group_start, group_end);
+  batch_group_ranges_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(pad_off, n, E, cap, expert_major, group_start,
+                                                                      group_end);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "batch_group_ranges launch");
   note_launch();

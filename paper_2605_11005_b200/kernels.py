@@ -132,14 +132,14 @@ def w13_dgrad(dh13, w13, group_off, dx_perm, stream=None):
 
 
 # -------------------------------------------- the same GEMMs over explicit group ranges
-def batch_group_ranges(pad_off, cap, group_start, group_end, stream=None):
-    """Expert-major row ranges (g = e * n + i) of n micro-batches stacked cap rows apart,
-    from their [n, E+1] padded offsets."""
+def batch_group_ranges(pad_off, cap, group_start, group_end, expert_major=True, stream=None):
+    """Row ranges of n micro-batches stacked cap rows apart, from their [n, E+1] padded
+    offsets: expert-major (g = e * n + i) or micro-batch-major (g = i * E + e)."""
     n, e1 = pad_off.shape
     _check(group_start, torch.int32, (n * (e1 - 1),), "group_start")
     _check(group_end, torch.int32, (n * (e1 - 1),), "group_end")
-    _lib.call("dm_batch_group_ranges", _ptr(pad_off), n, e1 - 1, cap, _ptr(group_start), _ptr(group_end),
-              _stream(stream))
+    _lib.call("dm_batch_group_ranges", _ptr(pad_off), n, e1 - 1, cap, int(bool(expert_major)), _ptr(group_start),
+              _ptr(group_end), _stream(stream))
 
 
 def _ranges(gs, ge, E, b_div):

@@ -358,10 +358,24 @@ class MoELayer:
     # ordered expert-major (dm_batch_group_ranges), so each expert's W13 / W2 stream once per
     # iteration instead of once per micro-batch; per-row results are bit-identical.
     def batched_supported(self, n: int) -> bool:
+        """Batched F side: by default (DM_BATCHED unset / "auto") for fine-grained experts, where
+        the shared weight pass and pair tiles pay (DeepSeek-V3 +13-19%, the tiny config +40%);
+        coarse experts (Mixtral) measured 1% slower batched on the same box, so they stay per
+        micro-batch unless DM_BATCHED=1. DM_BATCHED=0 disables it."""
         import os
 
-        return (n >= 2 and self.shape.E * n <= GEMM_MAX_GROUPS and os.environ.get("DM_GEMM_1SM") != "1"
-                and os.environ.get("DM_BATCHED", "1") != "0")
+        mode = os.environ.get("DM_BATCHED", "auto")
+        if mode == "0" or n < 2 or self.shape.E * n > GEMM_MAX_GROUPS or os.environ.get("DM_GEMM_1SM") == "1":
+            return False
+        return mode == "1" or self.merged_groups()
+
+    def merged_groups(self) -> bool:
+        """Expert-major groups (one weight pass for all micro-batches, chunks of different
+        micro-batches sharing pair tiles) when experts are fine-grained (< 512 rows per expert
+        and micro-batch: weight streaming and half tiles dominate, e.g. DeepSeek-V3); coarse
+        experts (Mixtral: ~1024 rows) keep the per-micro-batch tile order in one launch — the
+        expert-major order re-reads their large A panels from DRAM (ncu: w13 dgrad 26 GB)."""
+        return self.shape.R < 512 * self.shape.E
 
     def _group_ranges(self, n: int, stream=None):
         key = ("ranges", n)
@@ -370,22 +384,24 @@ class MoELayer:
                          torch.empty(n * self.shape.E, dtype=I32, device=self.device))
             self._rng_key = key
         gs, ge = self._rng
-        K.batch_group_ranges(self.slab.pad_off[:n], self.slab.cap, gs, ge, stream)
+        K.batch_group_ranges(self.slab.pad_off[:n], self.slab.cap, gs, ge, self.merged_groups(), stream)
         return gs, ge
 
     def f_forward_all(self, n: int, stream=None) -> None:
         sl, ex = self.slab, self.experts
         rows = slice(0, n * sl.cap)
         gs, ge = self._group_ranges(n, stream)
-        K.w13_swiglu_fwd_ranges(sl.x_perm[rows], ex.w13, gs, ge, n, sl.h13[rows], sl.act[rows], stream)
-        K.w2_fwd_ranges(sl.act[rows], ex.w2, gs, ge, n, sl.y_perm[rows], stream)
+        bd = n if self.merged_groups() else 1
+        K.w13_swiglu_fwd_ranges(sl.x_perm[rows], ex.w13, gs, ge, bd, sl.h13[rows], sl.act[rows], stream)
+        K.w2_fwd_ranges(sl.act[rows], ex.w2, gs, ge, bd, sl.y_perm[rows], stream)
 
     def f_backward_all(self, n: int, stream=None) -> None:
         sl, ex = self.slab, self.experts
         rows = slice(0, n * sl.cap)
         gs, ge = self._rng   # from this iteration's forward
-        K.w2_dgrad_swiglu_bwd_ranges(sl.dy_perm[rows], ex.w2, sl.h13[rows], gs, ge, n, sl.dh13[rows], stream)
-        K.w13_dgrad_ranges(sl.dh13[rows], ex.w13, gs, ge, n, sl.dx_perm[rows], stream)
+        bd = n if self.merged_groups() else 1
+        K.w2_dgrad_swiglu_bwd_ranges(sl.dy_perm[rows], ex.w2, sl.h13[rows], gs, ge, bd, sl.dh13[rows], stream)
+        K.w13_dgrad_ranges(sl.dh13[rows], ex.w13, gs, ge, bd, sl.dx_perm[rows], stream)
 
     def forward_all(self, n: int, stream=None) -> None:
         for i in range(n):

@@ -477,13 +477,15 @@ def test_fp32_autograd_and_iteration(cuda):
 
 
 @pytest.mark.parametrize("T,H,E,k,De,n,L", [(512, 256, 8, 2, 256, 4, 1), (384, 512, 64, 4, 384, 3, 1),
-                                           (256, 256, 8, 2, 256, 2, 2)])
-def test_batched_iteration_equals_per_microbatch(cuda, T, H, E, k, De, n, L):
-    """The batched iteration (every micro-batch's expert GEMMs as one launch per stage, groups
-    expert-major via dm_batch_group_ranges) is bit-identical to micro-batch-by-micro-batch
-    execution: outputs, input gradients and every weight gradient; its CUDA-graph replay too."""
+                                           (256, 256, 8, 2, 256, 2, 2), (1024, 256, 2, 1, 256, 3, 1)])
+def test_batched_iteration_equals_per_microbatch(cuda, T, H, E, k, De, n, L, monkeypatch):
+    """The batched iteration (every micro-batch's expert GEMMs as one launch per stage: groups
+    expert-major with shared pair tiles for fine-grained experts, micro-batch-major for coarse
+    ones — the last case) is bit-identical to micro-batch-by-micro-batch execution: outputs,
+    input gradients and every weight gradient; its CUDA-graph replay too."""
     from paper_2605_11005_b200.moe import MoELayer, MoEShape, MoEStack
 
+    monkeypatch.setenv("DM_BATCHED", "1")   # the coarse-expert case is batched only on request
     shape = MoEShape(T, H, E, k, De)
     res = []
     for mode in ("per_mb", "batched", "graph"):
