@@ -24,6 +24,8 @@
 // step it's S/dP rows into P/dS. Warp roles (384 threads): warp 0 TMA, warp 1 MMA issuer (one
 // thread), warp 2 TMEM allocator, warps 4-11 elementwise (warp w: TMEM lanes 32·(w%4).., 32 of
 // the 64 columns by (w-4)/4).
+#include <map>
+
 #include "attention_common.cuh"
 
 namespace dm {
@@ -530,14 +532,36 @@ int dm_attention_bwd(const void* qkv, const void* out, const void* dout, const f
   if ((rc = ensure_smem_attr((const void*)attn_bwd_dq_kernel, (int)AB_SMEM_DQ, "cudaFuncSetAttribute(attn_bwd_dq)")))
     return rc;
   __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dqkv);
+  // dK/dV and dQ are independent: dQ runs on a side stream (per host thread and device) forked
+  // from and joined back into the caller's stream, so each kernel's last partial wave is filled
+  // by the other's CTAs (stream capture records the fork / join as graph edges)
+  int dev = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return set_cuda_error(e, "attention_bwd cudaGetDevice");
+  thread_local std::map<int, cudaStream_t> side_streams;
+  cudaStream_t side = side_streams[dev];
+  if (!side) {
+    if ((e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking)) != cudaSuccess)
+      return set_cuda_error(e, "attention_bwd side stream");
+    side_streams[dev] = side;
+  }
+  cudaEvent_t fork, join;
+  if ((e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming)) != cudaSuccess)
+    return set_cuda_error(e, "attention_bwd events");
+  cudaEventRecord(fork, st);
+  cudaStreamWaitEvent(side, fork, 0);
+  attn_bwd_dq_kernel<<<dim3(n_t, nh, nb), AB_THREADS, AB_SMEM_DQ, side>>>(tm128, tmdo128, tm64, lse2, dl_ws, seq_len,
+                                                                           nh, nkv, scale_log2, scale, d);
+  if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "attention_bwd dq launch");
+  note_launch();
   attn_bwd_dkdv_kernel<<<dim3(n_t, nkv, nb), AB_THREADS, AB_SMEM_DKDV, st>>>(tm128, tm64, tmdo64, lse2, dl_ws, seq_len,
                                                                               nh, nkv, scale_log2, scale, d);
   if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "attention_bwd dkdv launch");
   note_launch();
-  attn_bwd_dq_kernel<<<dim3(n_t, nh, nb), AB_THREADS, AB_SMEM_DQ, st>>>(tm128, tmdo128, tm64, lse2, dl_ws, seq_len, nh,
-                                                                         nkv, scale_log2, scale, d);
-  if ((e = cudaGetLastError()) != cudaSuccess) return set_cuda_error(e, "attention_bwd dq launch");
-  note_launch();
+  cudaEventRecord(join, side);
+  cudaStreamWaitEvent(st, join, 0);
+  cudaEventDestroy(fork);   // destruction is deferred until the recorded work completes
+  cudaEventDestroy(join);
   return DM_OK;
 }
 
