@@ -230,15 +230,27 @@ class GpuStages:
 
         a_dispatch_bwd(buf, router, accumulate)
 
-    def f_forward(self, fb, experts: ExpertParams, group_off: torch.Tensor):
+    def f_forward(self, fb, experts: ExpertParams, group_off: torch.Tensor, ranges=None):
+        """ranges = (start, end, b_div): expert-major row ranges over the A ranks' slices (one
+        weight pass for all of them, 128-row chunks of different A ranks sharing pair tiles)."""
         from . import kernels as K
 
+        if ranges is not None:
+            gs, ge, bd = ranges
+            K.w13_swiglu_fwd_ranges(fb.x_perm, experts.w13, gs, ge, bd, fb.h13, fb.act)
+            K.w2_fwd_ranges(fb.act, experts.w2, gs, ge, bd, fb.y_perm)
+            return
         K.w13_swiglu_fwd(fb.x_perm, experts.w13, group_off, fb.h13, fb.act)
         K.w2_fwd(fb.act, experts.w2, group_off, fb.y_perm)
 
-    def f_backward(self, fb, experts: ExpertParams, group_off: torch.Tensor):
+    def f_backward(self, fb, experts: ExpertParams, group_off: torch.Tensor, ranges=None):
         from . import kernels as K
 
+        if ranges is not None:
+            gs, ge, bd = ranges
+            K.w2_dgrad_swiglu_bwd_ranges(fb.dy_perm, experts.w2, fb.h13, gs, ge, bd, fb.dh13)
+            K.w13_dgrad_ranges(fb.dh13, experts.w13, gs, ge, bd, fb.dx_perm)
+            return
         K.w2_dgrad_swiglu_bwd(fb.dy_perm, experts.w2, fb.h13, group_off, fb.dh13)
         K.w13_dgrad(fb.dh13, experts.w13, group_off, fb.dx_perm)
 
@@ -682,6 +694,16 @@ class AFPipeRank:
                 go, seg = go.pin_memory(), seg.pin_memory()
             fm.group_off = torch.empty(len(offs), dtype=I32, device=self.device)
             fm.group_off.copy_(go, non_blocking=self.st.cuda)
+            fm.ranges = None
+            if n_a > 1 and self.st.cuda and base < 512 * self.E_loc * n_a and self.E_loc * n_a <= 1024:
+                # fine-grained experts (< 512 rows per expert): expert-major ranges over the A
+                # ranks' slices, so one weight pass serves all of them (moe.MoELayer.merged_groups)
+                st_ = [fm.slices[a][0] + hdr[a][e] - hdr[a][0] for e in range(self.E_loc) for a in range(n_a)]
+                en_ = [fm.slices[a][0] + hdr[a][e + 1] - hdr[a][0] for e in range(self.E_loc) for a in range(n_a)]
+                rg = torch.tensor([st_, en_], dtype=I32).pin_memory()
+                dev_rg = torch.empty(2, len(st_), dtype=I32, device=self.device)
+                dev_rg.copy_(rg, non_blocking=True)
+                fm.ranges = (dev_rg[0], dev_rg[1], n_a)
             self.seg_offs[layer][i * n_a:(i + 1) * n_a].copy_(seg, non_blocking=self.st.cuda)
             with self.st.ctx("recv"):
                 ops = [("recv", fm.x_perm[b0:b0 + r], src_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
@@ -722,12 +744,12 @@ class AFPipeRank:
         if name == "F_f":
             for w in fm.works.get("M2N", []):
                 w.wait()
-            self.stages.f_forward(fm, experts, fm.group_off)
+            self.stages.f_forward(fm, experts, fm.group_off, getattr(fm, "ranges", None))
             fm.works["N2M_ready"] = self.st.event("compute")
         elif name == "F_b":
             for w in fm.works.get("M2N_b", []):
                 w.wait()
-            self.stages.f_backward(fm, experts, fm.group_off)
+            self.stages.f_backward(fm, experts, fm.group_off, getattr(fm, "ranges", None))
             fm.works["N2M_b_ready"] = self.st.event("compute")
 
     # ------------------------------------------------------------ iteration

@@ -91,7 +91,7 @@ class CpuStages:
         go = group_off.tolist()
         return [(g % E, go[g], go[g + 1]) for g in range(len(go) - 1) if go[g + 1] > go[g]]
 
-    def f_forward(self, fb, experts, group_off):
+    def f_forward(self, fb, experts, group_off, ranges=None):
         E = experts.w13.shape[0]
         for e, a, b in self._groups(group_off, E):
             h = fb.x_perm[a:b].float() @ experts.w13[e].float().t()
@@ -101,7 +101,7 @@ class CpuStages:
             fb.act[a:b] = act.to(BF16)
             fb.y_perm[a:b] = (fb.act[a:b].float() @ experts.w2[e].float().t()).to(BF16)
 
-    def f_backward(self, fb, experts, group_off):
+    def f_backward(self, fb, experts, group_off, ranges=None):
         E = experts.w13.shape[0]
         for e, a, b in self._groups(group_off, E):
             d_act = fb.dy_perm[a:b].float() @ experts.w2[e].float()
