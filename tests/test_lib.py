@@ -72,6 +72,11 @@ def test_shape_errors_are_negative_codes_without_gpu(lib):
     assert rc == -1
     rc = lib.dm_attention_fwd(None, 256, 256, 4, 2, 64, None, None, None)
     assert rc == -1
+    # batched GEMM ranges: cap must be 128-aligned; b_div must divide G
+    rc = lib.dm_batch_group_ranges(None, 4, 8, 100, 1, None, None, None)
+    assert rc == -1 and "batch_group_ranges" in _lib.last_error()
+    rc = lib.dm_grouped_w2_fwd_ranges(None, None, None, None, 10, 5, 3, 1024, 4096, 1024, None, None)
+    assert rc == -4 and "b_div" in _lib.last_error()
 
 
 def test_missing_library_fails_loudly(tmp_path):
