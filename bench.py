@@ -733,6 +733,7 @@ def run_afpipe(args, shape, exp, world, rank, local, dev):
                      "max_GB/s": round(max(link), 1) if link else None,
                      "peak_GB/s": 900.0, "note": "bytes / (data ready -> send complete), per transfer group"},
             "reference_model": _reference_model(exp, topo, shape, mb, L, f_flops, link, peaks, achieved),
+            "schedule_model": _schedule_model(gathered, mb, L, topo.depth, it_end),
             "gpu_launches": int(lsum.item()),
             "clocks": clocks,
             "memory": {
@@ -794,6 +795,40 @@ def isolated_stage_ms(fns: dict, dev, reps: int = 31) -> dict:
         g.replay()
         out[name] = max(median_replay(g) - base, 1e-6)
     return out
+
+
+def _schedule_model(gathered, mb, L, depth, measured_ms):
+    """The reference's schedule (afpipe.plan_layer: the same DAG, credits and list-scheduling
+    priority as the reference build_task_graph + simulate, pinned by tests/golden) fed THIS
+    run's measured task durations (medians over ranks and micro-batches of the instrumented
+    iteration), next to the measured iteration: how far the runtime is from the schedule the
+    reference model predicts for the same stage times (SURVEY §8(d) CPU-A)."""
+    import statistics
+
+    from paper_2605_11005_b200.afpipe import LayerDurations, plan_layer
+
+    dur: dict = {}
+    for g in gathered:
+        for n, i, lane, s, e, b in g["ivs"]:
+            dur.setdefault(n, []).append(e - s)
+    med = lambda k: statistics.median(dur[k]) if dur.get(k) else 0.0  # noqa: E731
+    comm = [x for k in ("M2N", "N2M", "M2N_b", "N2M_b") for x in dur.get(k, [])]
+    ns = lambda ms_: max(1, int(ms_ * 1e6))  # noqa: E731
+    d = LayerDurations(a_fwd=ns(med("A_f")), a_turn=ns(med("A_t")), a_bwd=ns(med("A_b")), f_fwd=ns(med("F_f")),
+                       f_bwd=ns(med("F_b")), m2n=ns(statistics.median(comm) if comm else 0.0))
+    try:
+        plan = plan_layer(mb, d, layers=L, depth=depth)
+    except Exception as ex:  # noqa: BLE001 - a model failure must not fail the bench line
+        return {"error": str(ex)[:200]}
+    w_ms = max(dur.get("W", [0.0]))
+    pred = plan.iteration_ns / 1e6 + w_ms
+    return {"predicted_iteration_ms": round(pred, 3), "measured_iteration_ms": round(measured_ms, 3),
+            "measured_over_predicted": round(measured_ms / pred, 3) if pred > 0 else None,
+            "durations_ms": {"A_f": round(med("A_f"), 4), "A_t": round(med("A_t"), 4), "A_b": round(med("A_b"), 4),
+                             "F_f": round(med("F_f"), 4), "F_b": round(med("F_b"), 4),
+                             "exchange": round(statistics.median(comm), 4) if comm else None, "W": round(w_ms, 4)},
+            "note": "afpipe.plan_layer (the reference schedule restated) on this run's median task times; "
+                    "measured = the instrumented iteration"}
 
 
 def _reference_model(exp, topo, shape, mb, L, f_flops, link, peaks, achieved_tf):

@@ -58,3 +58,17 @@ def test_gpus_must_match_world_size():
                          env=env, cwd=ROOT)
     assert res.returncode != 0
     assert "WORLD_SIZE" in res.stderr
+
+
+def test_schedule_model_reproduces_a_serial_chain():
+    """bench._schedule_model: the restated reference schedule on measured task times — for one
+    micro-batch the chain is serial, so the prediction is the sum of the task times + W."""
+    import bench
+
+    ivs = [("A_f", 0, "compute", 0.0, 1.0, 0), ("M2N", 0, "send", 1.0, 1.2, 8), ("F_f", 0, "compute", 1.2, 3.0, 0),
+           ("N2M", 0, "send", 3.0, 3.2, 8), ("A_t", 0, "compute", 3.2, 3.6, 0), ("M2N_b", 0, "send", 3.6, 3.8, 8),
+           ("F_b", 0, "compute", 3.8, 7.0, 0), ("N2M_b", 0, "send", 7.0, 7.2, 8), ("A_b", 0, "compute", 7.2, 7.5, 0),
+           ("W", -1, "compute", 7.5, 9.0, 0)]
+    m = bench._schedule_model([{"ivs": ivs}], 1, 1, 1, 9.0)
+    assert abs(m["predicted_iteration_ms"] - 9.0) < 1e-3
+    assert m["measured_over_predicted"] == 1.0
