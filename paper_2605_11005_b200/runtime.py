@@ -410,6 +410,7 @@ class AFPipeRank:
         self.t0 = None
         self.host_io = None
         self.x_free, self.dy_free = [], []   # per micro-batch: last reader of x / dy done (e2e)
+        self._start_override = None          # tracing: compute-interval start after a task's waits
 
     # ----------------------------------------------------------------- plan
     def _default_durations(self) -> LayerDurations:
@@ -442,10 +443,18 @@ class AFPipeRank:
         return works
 
     def _compute(self, name: str, i: int, fn):
+        """Run a compute task; with tracing, its interval starts after the task's stream waits on
+        incoming data (`_mark_waited`), so time the compute engine spends waiting for a transfer
+        is not counted as compute (it would hide exposed communication)."""
         ev0 = self.st.event("compute", True) if self.record_events else None
+        self._start_override = None
         fn()
         if ev0 is not None:
-            self.trace.append((name, i, COMPUTE, ev0, self.st.event("compute", True), 0))
+            self.trace.append((name, i, COMPUTE, self._start_override or ev0, self.st.event("compute", True), 0))
+
+    def _mark_waited(self):
+        if self.record_events:
+            self._start_override = self.st.event("compute", True)
 
     # ------------------------------------------------------------- A side
     def _a_pad(self, layer: int, i: int) -> list[int]:
@@ -518,6 +527,7 @@ class AFPipeRank:
             if layer == 0:
                 if self.host_io is not None:
                     self.st.wait("compute", self.x_ready[i])
+                    self._mark_waited()
             elif self.p == 1:   # previous layer's combine writes this layer's input (residual fused)
                 prev = self.lbufs[layer - 1][i]
                 self._wait_works(prev, "N2M")
@@ -542,6 +552,7 @@ class AFPipeRank:
             self._wait_works(b, "N2M")
             if layer == self.L - 1 and self.host_io is not None:
                 self.st.wait("compute", self.dy_ready[i])
+                self._mark_waited()
             self.stages.a_combine(b)
             self.stages.a_combine_bwd(b)
             b.turn_done = self.st.event("compute")
@@ -549,6 +560,7 @@ class AFPipeRank:
             self._wait_works(b, "A2A_b")
             if layer == self.L - 1 and self.host_io is not None:
                 self.st.wait("compute", self.dy_ready[i])
+                self._mark_waited()
             self.stages.a_combine_bwd(b)
             b.turn_done = self.st.event("compute")
         elif name == "A_b":
@@ -652,8 +664,11 @@ class AFPipeRank:
                     b.works_A2A_b = self.tx.exchange([("recv", b.dy, peer)], direction_of(name))
 
     def _wait_works(self, obj, name):
-        for w in getattr(obj, "works_" + name, []) or []:
+        works = getattr(obj, "works_" + name, []) or []
+        for w in works:
             w.wait()  # CUDA: the current (compute) stream waits on the NCCL stream
+        if works:
+            self._mark_waited()
 
     # ------------------------------------------------------------- F side
     def f_comm(self, name: str, i: int, layer: int):
@@ -744,11 +759,13 @@ class AFPipeRank:
         if name == "F_f":
             for w in fm.works.get("M2N", []):
                 w.wait()
+            self._mark_waited()
             self.stages.f_forward(fm, experts, fm.group_off, getattr(fm, "ranges", None))
             fm.works["N2M_ready"] = self.st.event("compute")
         elif name == "F_b":
             for w in fm.works.get("M2N_b", []):
                 w.wait()
+            self._mark_waited()
             self.stages.f_backward(fm, experts, fm.group_off, getattr(fm, "ranges", None))
             fm.works["N2M_b_ready"] = self.st.event("compute")
 
