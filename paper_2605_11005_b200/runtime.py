@@ -715,10 +715,18 @@ class AFPipeRank:
                 # ranks' slices, so one weight pass serves all of them (moe.MoELayer.merged_groups)
                 st_ = [fm.slices[a][0] + hdr[a][e] - hdr[a][0] for e in range(self.E_loc) for a in range(n_a)]
                 en_ = [fm.slices[a][0] + hdr[a][e + 1] - hdr[a][0] for e in range(self.E_loc) for a in range(n_a)]
-                rg = torch.tensor([st_, en_], dtype=I32).pin_memory()
-                dev_rg = torch.empty(2, len(st_), dtype=I32, device=self.device)
-                dev_rg.copy_(rg, non_blocking=True)
-                fm.ranges = (dev_rg[0], dev_rg[1], n_a)
+                if getattr(fm, "_rg_host", None) is None:   # pinned / device staging, allocated once
+                    fm._rg_host = torch.empty(2, len(st_), dtype=I32).pin_memory()
+                    fm._rg_dev = torch.empty(2, len(st_), dtype=I32, device=self.device)
+                # the previous iteration's copy out of the pinned buffer must be done before it
+                # is rewritten (the host already synchronised on this micro-batch's header)
+                if getattr(fm, "_rg_copied", None) is not None:
+                    fm._rg_copied.synchronize()
+                fm._rg_host[0] = torch.tensor(st_, dtype=I32)
+                fm._rg_host[1] = torch.tensor(en_, dtype=I32)
+                fm._rg_dev.copy_(fm._rg_host, non_blocking=True)
+                fm._rg_copied = self.st.event("compute")
+                fm.ranges = (fm._rg_dev[0], fm._rg_dev[1], n_a)
             self.seg_offs[layer][i * n_a:(i + 1) * n_a].copy_(seg, non_blocking=self.st.cuda)
             with self.st.ctx("recv"):
                 ops = [("recv", fm.x_perm[b0:b0 + r], src_rank(a)) for a, (b0, r) in enumerate(fm.slices)]
