@@ -476,9 +476,10 @@ def test_fp32_autograd_and_iteration(cuda):
         assert O.normwise_rel_err(f32(b_), f32(a)) < 1e-5
 
 
-@pytest.mark.parametrize("T,H,E,k,De,n,L", [(512, 256, 8, 2, 256, 4, 1), (384, 512, 64, 4, 384, 3, 1),
-                                           (256, 256, 8, 2, 256, 2, 2), (1024, 256, 2, 1, 256, 3, 1)])
-def test_batched_iteration_equals_per_microbatch(cuda, T, H, E, k, De, n, L, monkeypatch):
+@pytest.mark.parametrize("T,H,E,k,De,n,L,skew", [(512, 256, 8, 2, 256, 4, 1, 0.0), (384, 512, 64, 4, 384, 3, 1, 0.0),
+                                                (256, 256, 8, 2, 256, 2, 2, 0.0), (1024, 256, 2, 1, 256, 3, 1, 0.0),
+                                                (512, 256, 32, 2, 256, 4, 1, 1.0)])
+def test_batched_iteration_equals_per_microbatch(cuda, T, H, E, k, De, n, L, skew, monkeypatch):
     """The batched iteration (every micro-batch's expert GEMMs as one launch per stage: groups
     expert-major with shared pair tiles for fine-grained experts, micro-batch-major for coarse
     ones — the last case) is bit-identical to micro-batch-by-micro-batch execution: outputs,
@@ -491,6 +492,9 @@ def test_batched_iteration_equals_per_microbatch(cuda, T, H, E, k, De, n, L, mon
     for mode in ("per_mb", "batched", "graph"):
         stack = MoEStack([MoELayer.random(shape, cuda, seed=40 + l, num_buffers=n, residual=L > 1)
                           for l in range(L)])
+        if skew:   # about half the tokens pick experts 0 and 1: ragged and empty (expert, mb) ranges
+            for ly in stack.layers:
+                ly.router.wg[:2] += skew
         g = torch.Generator(device="cpu").manual_seed(5)
         for i in range(n):
             stack.input(i).copy_(torch.randn(T, H, generator=g).to(torch.bfloat16))
